@@ -1,0 +1,150 @@
+/*
+ * psg.h -- C ABI of the B200-native partition solver (parallel factorization
+ * A = F T G of arXiv 0912.3678), the drop-in boundary under the reference's
+ * C++ solver API.
+ *
+ * Every entry point is plain C: raw pointers, sizes and an opaque cudaStream_t
+ * (passed as void*, NULL = legacy default stream).  Nothing here throws; each
+ * returns 0 on success or 1 + Errc (the reference error enum,
+ * proj/include/parsol/errors.hpp:12-35) and writes a message into err.  The
+ * C++ host layer (include/parsol/parfact.hpp in this repo) turns that into
+ * parsol::Error(code, detail) exactly like the reference.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/proj):
+ *   psg_factor          <- parallel_factor()      include/parsol/parfact.hpp:52-53
+ *                                                  (impl src/parfact.cpp:21-132)
+ *   psg_solve           <- solve()                include/parsol/parfact.hpp:60
+ *                                                  (impl src/parfact.cpp:186-239)
+ *   psg_solve_reduced   <- solve_reduced()        include/parsol/parfact.hpp:56
+ *                                                  (impl src/parfact.cpp:134-184)
+ *   psg_residual        <- residual()             include/parsol/parfact.hpp:63
+ *                                                  (impl src/parfact.cpp:241-251)
+ *   psg_matvec          <- matvec()               include/parsol/structmat.hpp:66
+ *   psg_plan            <- plan_partition()       include/parsol/partition.hpp:82
+ *   psg_reduced_*       <- ParallelFactorization::reduced (ReducedSystem,
+ *                          include/parsol/parfact.hpp:14-22)
+ *   psg_generate_config -- (new) device generator of the BASELINE configs,
+ *                          bit-identical to SplitMix64 (include/parsol/rng.hpp)
+ */
+#ifndef PSG_H
+#define PSG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Kind numbering = parsol::Kind (structmat.hpp:11). */
+enum psg_kind { PSG_BANDED = 0, PSG_BLOCKTRI = 1, PSG_ABD = 2, PSG_BABD = 3, PSG_CIRCULANT = 4 };
+/* Strategy numbering = parsol::Strategy (localfact.hpp:11). */
+enum psg_strategy { PSG_LU = 0, PSG_LUD = 1, PSG_CR = 2, PSG_ARCE = 3, PSG_LUPIVOT = 4, PSG_QR = 5 };
+/* Errc numbering = parsol::Errc; functions return 1 + value on failure. */
+enum psg_errc {
+  PSG_E_DIMENSION_MISMATCH = 0, PSG_E_INVALID_BANDWIDTH, PSG_E_CORNER_FORBIDDEN,
+  PSG_E_TOO_LARGE_FOR_DENSE, PSG_E_INVALID_PARAMETER, PSG_E_PARSE_ERROR,
+  PSG_E_UNSUPPORTED_VERSION, PSG_E_TOO_MANY_PARTITIONS, PSG_E_UNSUPPORTED_KIND,
+  PSG_E_UNSUPPORTED_STRUCTURE, PSG_E_INDEX_OUT_OF_RANGE, PSG_E_ZERO_PIVOT,
+  PSG_E_SINGULAR_BLOCK, PSG_E_SINGULAR_FACTOR, PSG_E_SINGULAR_REDUCED_SYSTEM,
+  PSG_E_SINGULAR_WINDOW, PSG_E_EXHAUSTED_BODY, PSG_E_STEP_TOO_LARGE,
+  PSG_E_INVALID_INTERVAL, PSG_E_EXPM_FAILURE, PSG_E_NOT_CONVERGED, PSG_E_IO_ERROR,
+  PSG_E_CUDA = 100 /* CUDA runtime failure (no reference equivalent) */
+};
+
+/* Structured matrix descriptor, storage exactly as parsol::StructuredMatrix
+ * (structmat.hpp:16-31): data holds the kind's body entries, corner the
+ * row-major Babd corner block.  on_device = 1: data/corner are device
+ * pointers BORROWED by a handle (they must stay alive and unchanged until
+ * psg_release); on_device = 0: host pointers, copied into the handle. */
+typedef struct {
+  int kind, n, m, s, r;
+  const double* data;
+  size_t data_len;
+  const double* corner;
+  int corner_rows, corner_cols;
+  int on_device;
+} psg_desc;
+
+/* Mirrors parsol::SolveStats (parfact.hpp:24-30) plus the GPU certificate. */
+typedef struct {
+  double factor_seconds;
+  double phase1_seconds; /* condense (speculative interface) */
+  double phase2_seconds; /* reduced solve */
+  double phase3_seconds; /* back-substitution + certificate */
+  long long reduced_ops; /* multiply-adds of phase 2 (function of q only) */
+  double certificate;    /* max componentwise backward error over separator rows */
+  int speculative;       /* 1: the truncated interface was certified and used */
+  int fallbacks;         /* exact re-solves triggered by a failed certificate */
+} psg_stats;
+
+typedef struct psg_handle psg_handle;
+
+/* Factor A on p partitions (parallel_factor).  tol is accepted for API
+ * parity (the reference uses it only for LuPivot/Qr).  Lu, Lud and (where the
+ * reference allows it) CyclicReduction share the same GPU kernels;
+ * Arce/LuPivot/Qr return UnsupportedStructure (no CPU fallback). */
+int psg_factor(const psg_desc* A, int p, int strategy, double tol, void* stream,
+               psg_handle** out, char* err, size_t errlen);
+
+/* Three-phase solve (solve).  f and x are n-vectors, device pointers when
+ * on_device = 1, else host pointers (copied through the handle's device
+ * buffers; pinned host memory makes the copies fast).  Blocks until the
+ * result and its certificate are known.  stats may be NULL. */
+int psg_solve(const psg_handle* h, const double* f, double* x, int on_device, void* stream,
+              psg_stats* stats, char* err, size_t errlen);
+
+void psg_release(psg_handle* h);
+
+/* Reduced system metadata (ReducedSystem, parfact.hpp:14-22): q kept blocks,
+ * scalar dimension, block size k, corner flag. */
+int psg_reduced_info(const psg_handle* h, int* q, int* dim, int* k, int* has_corner);
+/* Host copies of the reduced matrix T in block form (k x k row-major
+ * blocks): diag[q], sub[q] (coupling of block i to i-1; sub[0] = corner
+ * coupling when has_corner), super[q] (coupling of block i to i+1).  Any
+ * pointer may be NULL. */
+int psg_reduced_blocks(const psg_handle* h, double* diag, double* sub, double* super, char* err,
+                       size_t errlen);
+
+/* Solve T x = rhs for the handle's reduced system (solve_reduced), device
+ * or host vectors of length dim. */
+int psg_solve_reduced(const psg_handle* h, const double* rhs, double* x, int on_device,
+                      void* stream, psg_stats* stats, char* err, size_t errlen);
+
+/* plan_partition on the host: body_begin/body_end (p), sep_start (p+1
+ * capacity); writes sep_count and sep_size. */
+int psg_plan(const psg_desc* A, int p, int* body_begin, int* body_end, int* sep_start,
+             int* sep_count, int* sep_size, char* err, size_t errlen);
+
+/* Device residual ||A x - f||_inf / ||f||_inf with the reference's fixed
+ * ascending-column summation and no FMA contraction (bit-identical to the
+ * reference).  A->on_device must match on_device. */
+int psg_residual(const psg_desc* A, const double* x, const double* f, int on_device,
+                 void* stream, double* out, char* err, size_t errlen);
+int psg_matvec(const psg_desc* A, const double* x, double* y, int on_device, void* stream,
+               char* err, size_t errlen);
+
+/* BASELINE config generator on the device (same stream mapping and values as
+ * oracle/parsol_oracle.c or_generate_config).  Shapes via psg_config_shape. */
+int psg_config_shape(int cfg, int size, int* kind, int* n, int* m, int* s, int* r,
+                     size_t* data_len, int* corner_rows, int* corner_cols);
+int psg_generate_config(int cfg, int size, uint64_t seed, double* data, double* corner,
+                        double* f, void* stream, char* err, size_t errlen);
+
+/* Options (per handle): */
+enum psg_option {
+  PSG_OPT_SPECULATIVE = 0, /* 1 (default): truncated interface + certificate; 0: exact */
+  PSG_OPT_HALO = 1,        /* truncation depth H in rows (default 32) */
+  PSG_OPT_CERT_TOL = 2     /* certificate threshold (default 1e-14) */
+};
+int psg_set_option(psg_handle* h, int option, double value);
+
+/* Number of kernels the last psg_factor / psg_solve on this handle launched. */
+int psg_last_launches(const psg_handle* h, int* factor_launches, int* solve_launches);
+
+const char* psg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

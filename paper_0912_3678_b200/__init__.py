@@ -1,0 +1,347 @@
+"""paper_0912_3678_b200 -- B200-native partition solver (A = F T G, arXiv 0912.3678).
+
+Python mirror of the reference `parsol` solver API (proj/include/parsol/
+parfact.hpp:52-63) over the C ABI in include/psg.h (libpsg.so, sm_100a).  The
+names, argument meaning and error behaviour follow the reference:
+
+    F = parallel_factor(A, p, Strategy.Lu)      # parsol::parallel_factor
+    x = solve(F, f, stats)                      # parsol::solve
+    r = residual(A, x, f)                       # parsol::residual
+
+Vectors may be numpy arrays (host; copied through the handle) or CUDA torch
+tensors (device-resident; no copies).  There is no CPU fallback: importing the
+solver on a machine without the built extension raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+from dataclasses import dataclass, field
+from typing import Any
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_LIBPSG = os.path.join(_PKG, "libpsg.so")
+
+__all__ = ["Kind", "Strategy", "Errc", "Error", "StructuredMatrix", "ParallelFactorization",
+           "SolveStats", "parallel_factor", "solve", "solve_reduced", "residual", "matvec",
+           "plan_partition", "generate_config", "config_shape", "lib"]
+
+
+class Kind(enum.IntEnum):  # include/parsol/structmat.hpp:11
+    Banded = 0
+    BlockTridiagonal = 1
+    Abd = 2
+    Babd = 3
+    CirculantLike = 4
+
+
+class Strategy(enum.IntEnum):  # include/parsol/localfact.hpp:11
+    Lu = 0
+    Lud = 1
+    CyclicReduction = 2
+    Arce = 3
+    LuPivot = 4
+    Qr = 5
+
+
+class Errc(enum.IntEnum):  # include/parsol/errors.hpp:12-35
+    DimensionMismatch = 0
+    InvalidBandwidth = 1
+    CornerForbidden = 2
+    TooLargeForDense = 3
+    InvalidParameter = 4
+    ParseError = 5
+    UnsupportedVersion = 6
+    TooManyPartitions = 7
+    UnsupportedKind = 8
+    UnsupportedStructure = 9
+    IndexOutOfRange = 10
+    ZeroPivot = 11
+    SingularBlock = 12
+    SingularFactor = 13
+    SingularReducedSystem = 14
+    SingularWindow = 15
+    ExhaustedBody = 16
+    StepTooLarge = 17
+    InvalidInterval = 18
+    ExpmFailure = 19
+    NotConverged = 20
+    IoError = 21
+    Cuda = 100
+
+
+class Error(RuntimeError):
+    """parsol::Error: carries the reference error code (errors.hpp:39-51)."""
+
+    def __init__(self, code: int, detail: str):
+        try:
+            c = Errc(code)
+            name = c.name
+        except ValueError:
+            c, name = code, f"Errc{code}"
+        super().__init__(f"{name}: {detail}")
+        self.code = c
+        self.detail = detail
+
+
+class _Desc(C.Structure):
+    _fields_ = [("kind", C.c_int), ("n", C.c_int), ("m", C.c_int), ("s", C.c_int), ("r", C.c_int),
+                ("data", C.c_void_p), ("data_len", C.c_size_t), ("corner", C.c_void_p),
+                ("corner_rows", C.c_int), ("corner_cols", C.c_int), ("on_device", C.c_int)]
+
+
+class SolveStats(C.Structure):
+    """parsol::SolveStats (parfact.hpp:24-30) + the GPU certificate."""
+    _fields_ = [("factor_seconds", C.c_double), ("phase1_seconds", C.c_double),
+                ("phase2_seconds", C.c_double), ("phase3_seconds", C.c_double),
+                ("reduced_ops", C.c_longlong), ("certificate", C.c_double),
+                ("speculative", C.c_int), ("fallbacks", C.c_int)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+
+
+def lib():
+    """Load libpsg.so (raises if the CUDA extension is missing -- no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIBPSG):
+            raise ImportError(f"{_LIBPSG} is missing: build it with `python -m paper_0912_3678_b200.build` "
+                              "(the GPU path has no CPU fallback)")
+        L = C.CDLL(_LIBPSG)
+        vp, ip, sz, cp = C.c_void_p, C.c_int, C.c_size_t, C.c_char_p
+        L.psg_factor.argtypes = [C.POINTER(_Desc), ip, ip, C.c_double, vp, C.POINTER(vp), cp, sz]
+        L.psg_solve.argtypes = [vp, vp, vp, ip, vp, C.POINTER(SolveStats), cp, sz]
+        L.psg_release.argtypes = [vp]
+        L.psg_release.restype = None
+        L.psg_reduced_info.argtypes = [vp] + [C.POINTER(C.c_int)] * 4
+        L.psg_reduced_blocks.argtypes = [vp, vp, vp, vp, cp, sz]
+        L.psg_solve_reduced.argtypes = [vp, vp, vp, ip, vp, C.POINTER(SolveStats), cp, sz]
+        L.psg_plan.argtypes = [C.POINTER(_Desc), ip] + [C.POINTER(C.c_int)] * 5 + [cp, sz]
+        L.psg_residual.argtypes = [C.POINTER(_Desc), vp, vp, ip, vp, C.POINTER(C.c_double), cp, sz]
+        L.psg_matvec.argtypes = [C.POINTER(_Desc), vp, vp, ip, vp, cp, sz]
+        L.psg_config_shape.argtypes = [ip, ip] + [C.POINTER(C.c_int)] * 5 + \
+            [C.POINTER(C.c_size_t), C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.psg_generate_config.argtypes = [ip, ip, C.c_uint64, vp, vp, vp, vp, cp, sz]
+        L.psg_set_option.argtypes = [vp, ip, C.c_double]
+        L.psg_last_launches.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.psg_version.restype = C.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, err) -> None:
+    if rc:
+        raise Error(rc - 1, err.value.decode(errors="replace"))
+
+
+def _is_cuda(t) -> bool:
+    return hasattr(t, "is_cuda") and bool(t.is_cuda)
+
+
+def _addr(t):
+    if t is None:
+        return None
+    if _is_cuda(t):
+        return C.c_void_p(t.data_ptr())
+    if hasattr(t, "data_ptr") and not isinstance(t, np.ndarray):  # host torch tensor
+        return C.c_void_p(t.data_ptr())
+    return C.c_void_p(t.ctypes.data)
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        try:
+            import torch
+            if torch.cuda.is_available() and torch.cuda.is_initialized():
+                return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        except Exception:
+            pass
+        return None
+    if hasattr(stream, "cuda_stream"):
+        return C.c_void_p(stream.cuda_stream)
+    return C.c_void_p(int(stream))
+
+
+@dataclass
+class StructuredMatrix:
+    """parsol::StructuredMatrix (structmat.hpp:33-55): compact storage of one
+    of the five kinds.  `data`/`corner` may be numpy (host) or CUDA tensors."""
+    kind: int
+    n: int
+    m: int
+    s: int
+    r: int
+    data: Any
+    corner: Any = None
+    corner_rows: int = 0
+    corner_cols: int = 0
+
+    def __post_init__(self):
+        if isinstance(self.data, np.ndarray):
+            self.data = np.ascontiguousarray(self.data, dtype=np.float64)
+        if isinstance(self.corner, np.ndarray):
+            self.corner = np.ascontiguousarray(self.corner, dtype=np.float64)
+
+    @property
+    def on_device(self) -> bool:
+        return _is_cuda(self.data)
+
+    def desc(self) -> _Desc:
+        n_data = int(self.data.numel() if hasattr(self.data, "numel") else self.data.size)
+        return _Desc(int(self.kind), self.n, self.m, self.s, self.r, _addr(self.data), n_data,
+                     _addr(self.corner), self.corner_rows, self.corner_cols, 1 if self.on_device else 0)
+
+
+@dataclass
+class ParallelFactorization:
+    """parsol::ParallelFactorization (parfact.hpp:35-46): device handle plus
+    the host-side plan / reduced-system metadata."""
+    handle: C.c_void_p
+    A: StructuredMatrix
+    p: int
+    strategy: int
+    q: int = 0
+    dim: int = 0
+    k: int = 0
+    has_corner: bool = False
+    _alive: bool = field(default=True, repr=False)
+
+    def close(self):
+        if self._alive and self.handle:
+            lib().psg_release(self.handle)
+        self._alive = False
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_option(self, option: str, value: float):
+        code = {"speculative": 0, "halo": 1, "cert_tol": 2}[option]
+        _check(lib().psg_set_option(self.handle, code, float(value)), C.create_string_buffer(b"bad option"))
+
+    def launches(self):
+        f, s = C.c_int(), C.c_int()
+        lib().psg_last_launches(self.handle, C.byref(f), C.byref(s))
+        return f.value, s.value
+
+    def reduced_blocks(self):
+        """Tridiagonal reduced matrix T as (sub, diag, super) host arrays."""
+        kk = self.k * self.k
+        d = np.empty(self.q * kk)
+        sb = np.empty(self.q * kk)
+        sp = np.empty(self.q * kk)
+        err = C.create_string_buffer(512)
+        _check(lib().psg_reduced_blocks(self.handle, d.ctypes.data, sb.ctypes.data, sp.ctypes.data, err, 512), err)
+        return sb, d, sp
+
+    def solve(self, f, x=None, stats: SolveStats | None = None, stream=None):
+        return solve(self, f, stats=stats, x=x, stream=stream)
+
+
+def parallel_factor(A: StructuredMatrix, p: int, strategy: int = Strategy.Lu, tol: float = 1e-8,
+                    stream=None) -> ParallelFactorization:
+    d = A.desc()
+    h = C.c_void_p()
+    err = C.create_string_buffer(1024)
+    _check(lib().psg_factor(C.byref(d), int(p), int(strategy), float(tol), _stream_ptr(stream), C.byref(h),
+                            err, 1024), err)
+    F = ParallelFactorization(h, A, int(p), int(strategy))
+    q, dim, k, hc = (C.c_int() for _ in range(4))
+    lib().psg_reduced_info(h, C.byref(q), C.byref(dim), C.byref(k), C.byref(hc))
+    F.q, F.dim, F.k, F.has_corner = q.value, dim.value, k.value, bool(hc.value)
+    return F
+
+
+def solve(F: ParallelFactorization, f, stats: SolveStats | None = None, x=None, stream=None):
+    """Three-phase solve; returns x (same residency as f)."""
+    dev = _is_cuda(f)
+    if x is None:
+        if dev:
+            import torch
+            x = torch.empty_like(f)
+        else:
+            f = np.ascontiguousarray(f, np.float64)
+            x = np.empty_like(f)
+    err = C.create_string_buffer(1024)
+    st = stats if stats is not None else None
+    _check(lib().psg_solve(F.handle, _addr(f), _addr(x), 1 if dev else 0, _stream_ptr(stream),
+                           C.byref(st) if st is not None else None, err, 1024), err)
+    return x
+
+
+def solve_reduced(F: ParallelFactorization, rhs, stats: SolveStats | None = None, stream=None):
+    dev = _is_cuda(rhs)
+    if dev:
+        import torch
+        x = torch.empty_like(rhs)
+    else:
+        rhs = np.ascontiguousarray(rhs, np.float64)
+        x = np.empty_like(rhs)
+    err = C.create_string_buffer(1024)
+    _check(lib().psg_solve_reduced(F.handle, _addr(rhs), _addr(x), 1 if dev else 0, _stream_ptr(stream),
+                                   C.byref(stats) if stats is not None else None, err, 1024), err)
+    return x
+
+
+def residual(A: StructuredMatrix, x, f, stream=None) -> float:
+    """||A x - f||_inf / ||f||_inf on the GPU (parfact.cpp:241-251 semantics)."""
+    d = A.desc()
+    out = C.c_double()
+    err = C.create_string_buffer(1024)
+    _check(lib().psg_residual(C.byref(d), _addr(x), _addr(f), 1 if _is_cuda(x) else 0, _stream_ptr(stream),
+                              C.byref(out), err, 1024), err)
+    return out.value
+
+
+def matvec(A: StructuredMatrix, x, y, stream=None):
+    d = A.desc()
+    err = C.create_string_buffer(1024)
+    _check(lib().psg_matvec(C.byref(d), _addr(x), _addr(y), 1, _stream_ptr(stream), err, 1024), err)
+    return y
+
+
+def plan_partition(A: StructuredMatrix, p: int):
+    d = A.desc()
+    bb = (C.c_int * p)()
+    be = (C.c_int * p)()
+    ss = (C.c_int * (p + 1))()
+    cnt, k = C.c_int(), C.c_int()
+    err = C.create_string_buffer(512)
+    _check(lib().psg_plan(C.byref(d), p, bb, be, ss, C.byref(cnt), C.byref(k), err, 512), err)
+    return dict(body_ranges=[(bb[i], be[i]) for i in range(p)], separator_starts=list(ss[:cnt.value]),
+                sep_size=k.value)
+
+
+def config_shape(cfg: int, size: int) -> dict:
+    k, n, m, s, r, cr, cc = (C.c_int() for _ in range(7))
+    ln = C.c_size_t()
+    rc = lib().psg_config_shape(cfg, size, C.byref(k), C.byref(n), C.byref(m), C.byref(s), C.byref(r),
+                                C.byref(ln), C.byref(cr), C.byref(cc))
+    if rc:
+        raise Error(rc - 1, "unknown config")
+    return dict(kind=k.value, n=n.value, m=m.value, s=s.value, r=r.value, data_len=ln.value,
+                corner_rows=cr.value, corner_cols=cc.value)
+
+
+def generate_config(cfg: int, size: int, seed: int, device="cuda", stream=None):
+    """Seeded BASELINE config instance generated on the GPU -> (A, f)."""
+    import torch
+    sh = config_shape(cfg, size)
+    data = torch.empty(sh["data_len"], dtype=torch.float64, device=device)
+    corner = torch.empty(64, dtype=torch.float64, device=device) if cfg == 4 else None
+    f = torch.empty(sh["n"], dtype=torch.float64, device=device)
+    err = C.create_string_buffer(512)
+    _check(lib().psg_generate_config(cfg, size, seed, _addr(data), _addr(corner), _addr(f), _stream_ptr(stream),
+                                     err, 512), err)
+    A = StructuredMatrix(sh["kind"], sh["n"], sh["m"], sh["s"], sh["r"], data, corner, sh["corner_rows"],
+                         sh["corner_cols"])
+    return A, f

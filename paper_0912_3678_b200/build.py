@@ -1,0 +1,64 @@
+"""In-tree build of the native libraries (sm_100a only).
+
+    libpsg.so          CUDA kernels + the C ABI (include/psg.h)
+    libparsol_b200.so  C++ host API mirroring the reference headers
+                       (include/parsol/*.hpp) on top of libpsg.so
+
+Run ``python -m paper_0912_3678_b200.build`` or ``__graft_entry__.build()``.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+HOST = os.path.join(PKG, "host")
+INCLUDE = os.path.join(ROOT, "include")
+
+NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
+           "-Xptxas", "-warn-spills"]
+
+LIBPSG = os.path.join(PKG, "libpsg.so")
+LIBHOST = os.path.join(PKG, "libparsol_b200.so")
+
+
+def _run(cmd, verbose):
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+
+
+def _newer(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _sources(d, exts):
+    if not os.path.isdir(d):
+        return []
+    return sorted(os.path.join(d, f) for f in os.listdir(d) if f.endswith(exts))
+
+
+def build(verbose: bool = True, force: bool = False, ptxas_verbose: bool = False) -> None:
+    deps = _sources(CSRC, (".cu", ".cuh")) + [os.path.join(INCLUDE, "psg.h")]
+    if force or _newer(LIBPSG, deps):
+        extra = ["-Xptxas", "-v"] if ptxas_verbose else []
+        _run([NVCC, *ARCH, *NVFLAGS, *extra, "-shared", "-o", LIBPSG,
+              os.path.join(CSRC, "psg_capi.cu"), "-lcuda"], verbose)
+    hsrc = _sources(HOST, (".cpp",))
+    hdeps = hsrc + _sources(os.path.join(INCLUDE, "parsol"), (".hpp",)) + [LIBPSG]
+    if hsrc and (force or _newer(LIBHOST, hdeps)):
+        _run(["g++", "-O2", "-std=c++20", "-fPIC", "-shared", "-I" + INCLUDE, "-o", LIBHOST, *hsrc,
+              "-L" + PKG, "-lpsg", "-Wl,-rpath,$ORIGIN"], verbose)
+
+
+if __name__ == "__main__":
+    build(verbose=True, force="--force" in sys.argv, ptxas_verbose="-v" in sys.argv)
