@@ -12,6 +12,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -56,26 +57,87 @@ int set_err(char* err, size_t errlen, int code, const std::string& msg) {
 
 #define LAUNCH_CHECK() CUDA_TRY(cudaGetLastError())
 
+// Process-wide cache of device blocks keyed by byte size: repeated
+// parallel_factor calls on same-shaped systems reuse memory instead of
+// paying cudaMalloc (and its implicit device synchronisation) each time.
+// Blocks are returned only after the owning handle's work has completed.
+struct BlockCache {
+  std::mutex mu;
+  std::multimap<size_t, void*> free_;
+  void* get(size_t bytes) {
+    {
+      std::lock_guard<std::mutex> g(mu);
+      auto it = free_.find(bytes);
+      if (it != free_.end()) {
+        void* p = it->second;
+        free_.erase(it);
+        return p;
+      }
+    }
+    void* p = nullptr;
+    CUDA_TRY(cudaMalloc(&p, bytes));
+    return p;
+  }
+  void put(void* p, size_t bytes) {
+    std::lock_guard<std::mutex> g(mu);
+    free_.emplace(bytes, p);
+  }
+};
+
+BlockCache& block_cache() {
+  static BlockCache* c = new BlockCache;  // intentionally leaked (outlives static dtors)
+  return *c;
+}
+
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
-  size_t n = 0;
+  size_t n = 0, bytes = 0;
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() { reset(); }
   void reset() {
-    if (p) cudaFree(p);
+    if (p) block_cache().put(p, bytes);
     p = nullptr;
-    n = 0;
+    n = bytes = 0;
   }
   void alloc(size_t count) {
     if (count <= n && p) return;
     reset();
-    CUDA_TRY(cudaMalloc(&p, sizeof(T) * std::max<size_t>(count, 1)));
+    bytes = ((sizeof(T) * std::max<size_t>(count, 1)) + 511) & ~size_t(511);
+    p = static_cast<T*>(block_cache().get(bytes));
     n = count;
   }
 };
+
+// Small pinned host slots (status words) carved from one page-locked slab.
+struct PinnedSlots {
+  std::mutex mu;
+  char* slab = nullptr;
+  std::vector<int> free_;
+  static constexpr int kSlot = 64, kCount = 1024;
+  void* get() {
+    std::lock_guard<std::mutex> g(mu);
+    if (!slab) {
+      CUDA_TRY(cudaMallocHost(&slab, kSlot * kCount));
+      for (int i = kCount - 1; i >= 0; --i) free_.push_back(i);
+    }
+    if (free_.empty()) throw Fail{PSG_E_CUDA, "out of pinned status slots"};
+    int i = free_.back();
+    free_.pop_back();
+    return slab + (size_t)i * kSlot;
+  }
+  void put(void* p) {
+    std::lock_guard<std::mutex> g(mu);
+    free_.push_back(int((static_cast<char*>(p) - slab) / kSlot));
+  }
+};
+
+PinnedSlots& pinned_slots() {
+  static PinnedSlots* s = new PinnedSlots;
+  return *s;
+}
 
 // ----------------------------------------------------------------------------
 // descriptor validation: make() (src/structmat.cpp:153-207), with the Babd
@@ -145,17 +207,30 @@ void validate(const psg_desc& A) {
 }
 
 // ----------------------------------------------------------------------------
-// partition plan: plan_partition (src/partition.cpp:52-105)
+// partition plan: plan_partition (src/partition.cpp:52-105), kept in closed
+// form (no O(p) host arrays on the factor path).
 // ----------------------------------------------------------------------------
 struct Plan {
   int kind = 0, n = 0, m = 1, p = 0, sep_size = 0;
   bool has_corner = false;
-  std::vector<int> body_begin, body_end, sep_start;
+  int unit = 1, k_units = 1;
+  long base = 0, rem = 0;
+  int sep_count() const { return has_corner ? p + 1 : p - 1; }
+  long body_begin_units(int i) const {
+    return (has_corner ? k_units : 0) + (long)i * base + std::min<long>(i, rem) + (long)i * k_units;
+  }
+  int body_begin(int i) const { return int(body_begin_units(i) * unit); }
+  int body_end(int i) const { return int((body_begin_units(i) + base + (i < rem ? 1 : 0)) * unit); }
+  int sep_start(int j) const {
+    if (has_corner) return j == 0 ? 0 : body_end(j - 1);
+    return body_end(j);
+  }
 };
 
 Plan make_plan(const psg_desc& A, int p) {
   if (p < 2) throw Fail{PSG_E_TOO_MANY_PARTITIONS, "p must be >= 2"};
-  if (A.kind == PSG_CIRCULANT) throw Fail{PSG_E_UNSUPPORTED_KIND, "circulant-like matrices are not supported on the GPU path"};
+  if (A.kind == PSG_CIRCULANT)
+    throw Fail{PSG_E_UNSUPPORTED_KIND, "circulant-like matrices are not supported on the GPU path"};
   Plan P;
   P.kind = A.kind;
   P.n = A.n;
@@ -165,198 +240,267 @@ Plan make_plan(const psg_desc& A, int p) {
   P.has_corner = A.kind == PSG_BABD;
   const int k = P.sep_size;
   const long seps = P.has_corner ? p + 1L : p - 1L;
-  const int unit = A.kind == PSG_BANDED ? 1 : A.m;
-  if (k % unit != 0) throw Fail{PSG_E_UNSUPPORTED_KIND, "separator does not tile blocks"};
-  const long n_units = A.n / unit, k_units = k / unit;
-  const long body_total = n_units - seps * k_units;
-  const long min_body = std::max(1L, k_units);
+  P.unit = A.kind == PSG_BANDED ? 1 : A.m;
+  if (k % P.unit != 0) throw Fail{PSG_E_UNSUPPORTED_KIND, "separator does not tile blocks"};
+  const long n_units = A.n / P.unit;
+  P.k_units = k / P.unit;
+  const long body_total = n_units - seps * P.k_units;
+  const long min_body = std::max(1, P.k_units);
   if (body_total < (long)p * min_body)
     throw Fail{PSG_E_TOO_MANY_PARTITIONS, "n too small for p = " + std::to_string(p) + " partitions of this kind"};
-  const long base = body_total / p, rem = body_total % p;
-  P.body_begin.resize(p);
-  P.body_end.resize(p);
-  long cursor = 0;
-  if (P.has_corner) {
-    P.sep_start.push_back(int(cursor * unit));
-    cursor += k_units;
-  }
-  for (int i = 0; i < p; ++i) {
-    const long units = base + (i < rem ? 1 : 0);
-    P.body_begin[i] = int(cursor * unit);
-    P.body_end[i] = int((cursor + units) * unit);
-    cursor += units;
-    if (i < p - 1 || P.has_corner) {
-      P.sep_start.push_back(int(cursor * unit));
-      cursor += k_units;
-    }
-  }
+  P.base = body_total / p;
+  P.rem = body_total % p;
   return P;
 }
 
 // ----------------------------------------------------------------------------
-// Tridiagonal multi-level partition solver
+// small pools: CUDA events
 // ----------------------------------------------------------------------------
-constexpr int kNT = 64;
-constexpr int kMaxSeg = 17 * kNT;  // 1088 rows per segment (one CTA)
+struct EventPool {
+  std::mutex mu;
+  std::vector<cudaEvent_t> free_;
+  cudaEvent_t get() {
+    {
+      std::lock_guard<std::mutex> g(mu);
+      if (!free_.empty()) {
+        cudaEvent_t e = free_.back();
+        free_.pop_back();
+        return e;
+      }
+    }
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreate(&e));
+    return e;
+  }
+  void put(cudaEvent_t e) {
+    std::lock_guard<std::mutex> g(mu);
+    free_.push_back(e);
+  }
+};
+
+EventPool& event_pool() {
+  static EventPool* p = new EventPool;
+  return *p;
+}
+
+// ----------------------------------------------------------------------------
+// Tridiagonal solver: speculative single-level path + exact multi-level path
+// ----------------------------------------------------------------------------
+constexpr int kMaxSeg = 32 * 33;  // 1056 rows per segment (one warp)
+constexpr int kMinSpecSeg = 2 * kHalo + 1;
 
 struct TriLevel {
   TriRows A{};
   RowArr F{};
   double* x = nullptr;  // output of this level (rows of this level's system)
   int q = 0;            // rows
-  int nseg = 0, maxlen = 0;
-  std::vector<int> h_start, h_len;
-  DevBuf<int> start, len;
-  DevBuf<double> mat, rhsv;                       // 4*nseg, 2*nseg
+  SegMap S{};
+  int maxlen = 0;
+  DevBuf<int> start, len;                              // refined maps only
+  DevBuf<double> mat, rhsv;                            // 4*nseg, 2*nseg
   DevBuf<double> Tsub, Tdiag, Tsup, rhs_next, x_next;  // nseg-1
-  DevBuf<double2> partR, partL;
-  DevBuf<int> counters;
+  DevBuf<double2> yends;  // level 0 only: per-segment (y_first, y_last) for the certificate
 };
 
-// Split q rows into segments of <= kMaxSeg rows separated by single rows,
-// following the reference plan formula (equal bodies, remainder first).
-void segment_uniform(int q, std::vector<int>& st, std::vector<int>& ln) {
-  st.clear();
-  ln.clear();
+// q rows -> segments of <= kMaxSeg rows separated by single rows, using the
+// reference plan formula (equal bodies, remainder to the leading ones).
+SegMap segment_uniform(int q, int& maxlen) {
   if (q <= kMaxSeg) {
-    st.push_back(0);
-    ln.push_back(q);
-    return;
+    maxlen = q;
+    return SegMap{1, q, 0, nullptr, nullptr};
   }
   const int p = (q + 1 + 1023) / 1024;  // ~1023-row bodies
   const long body_total = (long)q - (p - 1);
-  const long base = body_total / p, rem = body_total % p;
-  long cursor = 0;
-  for (int i = 0; i < p; ++i) {
-    const long u = base + (i < rem ? 1 : 0);
-    st.push_back(int(cursor));
-    ln.push_back(int(u));
-    cursor += u + 1;
-  }
+  const int base = int(body_total / p), rem = int(body_total % p);
+  maxlen = base + (rem ? 1 : 0);
+  return SegMap{p, base, rem, nullptr, nullptr};
 }
 
 template <int M>
-void launch_segment_solve(const TriSolveArgs& a, int nseg, cudaStream_t s) {
-  constexpr int bytes = TriSmem<M, kNT>::BYTES;
-  tri_segment_solve_kernel<M, kNT><<<nseg, kNT, bytes, s>>>(a);
+void launch_segment_solve(const TriSolveArgs& a, int nseg, bool spec, cudaStream_t s) {
+  constexpr int bytes = TriWarpSmem<M>::BYTES;
+  if (spec)
+    tri_segment_solve_kernel<M, true><<<nseg, 32, bytes, s>>>(a);
+  else
+    tri_segment_solve_kernel<M, false><<<nseg, 32, bytes, s>>>(a);
 }
 
-void segment_solve(const TriSolveArgs& a, int nseg, int maxlen, cudaStream_t s) {
-  if (maxlen <= 3 * kNT)
-    launch_segment_solve<3>(a, nseg, s);
-  else if (maxlen <= 5 * kNT)
-    launch_segment_solve<5>(a, nseg, s);
-  else if (maxlen <= 9 * kNT)
-    launch_segment_solve<9>(a, nseg, s);
-  else if (maxlen <= 17 * kNT)
-    launch_segment_solve<17>(a, nseg, s);
+void segment_solve(const TriSolveArgs& a, int nseg, int maxlen, bool spec, cudaStream_t s) {
+  if (maxlen <= 32 * 5)
+    launch_segment_solve<5>(a, nseg, spec, s);
+  else if (maxlen <= 32 * 9)
+    launch_segment_solve<9>(a, nseg, spec, s);
+  else if (maxlen <= 32 * 17)
+    launch_segment_solve<17>(a, nseg, spec, s);
+  else if (maxlen <= 32 * 33)
+    launch_segment_solve<33>(a, nseg, spec, s);
   else
-    throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "segment longer than the per-CTA capacity"};
+    throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "segment longer than the per-warp capacity"};
   LAUNCH_CHECK();
 }
 
+int blocks_for(long work, int tpb) { return (int)((work + tpb - 1) / tpb); }
+
 struct TriSolver {
+  // level-0 system
+  TriRows A0{};
+  int n = 0;
+  SegMap S0{};
+  int maxlen0 = 0, minlen0 = 0;
+  DevBuf<int> start0, len0;  // refined maps
+  // speculative path buffers
+  DevBuf<double> wts, Tdiag;
+  DevBuf<double2> yends;
+  // exact multi-level path (built on demand)
   std::vector<std::unique_ptr<TriLevel>> lv;
   int launches = 0;
 
-  // Level 0 = the user's matrix segmented by the (refined) plan.
-  void build(const TriRows& A0, int n, const std::vector<int>& st, const std::vector<int>& ln) {
-    lv.clear();
+  void init(const TriRows& A, int n_, const SegMap& S, int maxlen, int minlen, const std::vector<int>* st,
+            const std::vector<int>* ln, cudaStream_t s) {
+    A0 = A;
+    n = n_;
+    S0 = S;
+    maxlen0 = maxlen;
+    minlen0 = minlen;
+    if (st) {
+      start0.alloc(st->size());
+      len0.alloc(ln->size());
+      CUDA_TRY(cudaMemcpyAsync(start0.p, st->data(), sizeof(int) * st->size(), cudaMemcpyHostToDevice, s));
+      CUDA_TRY(cudaMemcpyAsync(len0.p, ln->data(), sizeof(int) * ln->size(), cudaMemcpyHostToDevice, s));
+      CUDA_TRY(cudaStreamSynchronize(s));  // pageable source
+      S0.start = start0.p;
+      S0.len = len0.p;
+    }
+    yends.alloc(S0.nseg);
+  }
+
+  bool spec_possible() const { return minlen0 >= kMinSpecSeg && S0.nseg > 1; }
+
+  // ---- speculative path ----------------------------------------------------
+  void spec_factor(cudaStream_t s) {
+    const int nsep = S0.nseg - 1;
+    wts.alloc((size_t)kWRow * nsep);
+    Tdiag.alloc(nsep);
+    tri_spec_factor_kernel<<<blocks_for(nsep, 32 * kFacWarps), 32 * kFacWarps, 0, s>>>(A0, S0, wts.p, Tdiag.p);
+    LAUNCH_CHECK();
+    launches += 1;
+  }
+
+  // level-0 back-substitution (+ fused separator values when spec) and certificate
+  void k3_and_cert(const RowArr& F, double* x, const double* xs, bool spec, DevStatus* st, cudaStream_t s) {
+    TriSolveArgs a{};
+    a.A = A0;
+    a.F = F;
+    a.S = S0;
+    a.xsep = xs;
+    a.wts = spec ? wts.p : nullptr;
+    a.x = x;
+    a.yends = yends.p;
+    a.status = st;
+    segment_solve(a, S0.nseg, maxlen0, spec, s);
+    tri_cert_kernel<<<blocks_for(S0.nseg - 1, 256), 256, 0, s>>>(A0, F, S0, x, yends.p, st);
+    LAUNCH_CHECK();
+    launches += 2;
+  }
+
+  void spec_solve(const RowArr& F, double* x, DevStatus* st, cudaStream_t s, cudaEvent_t* ev) {
+    if (ev) {  // phases 1 and 2 are fused into K3 (diagonal speculative reduced matrix)
+      CUDA_TRY(cudaEventRecord(ev[1], s));
+      CUDA_TRY(cudaEventRecord(ev[2], s));
+    }
+    k3_and_cert(F, x, nullptr, true, st, s);
+  }
+
+  // ---- exact multi-level path ----------------------------------------------
+  void build_levels(cudaStream_t s) {
+    if (!lv.empty()) return;
     auto L0 = std::make_unique<TriLevel>();
     L0->A = A0;
     L0->q = n;
-    L0->h_start = st;
-    L0->h_len = ln;
+    L0->S = S0;
+    L0->maxlen = maxlen0;
     lv.push_back(std::move(L0));
     for (;;) {
       TriLevel& L = *lv.back();
-      L.nseg = (int)L.h_start.size();
-      L.maxlen = *std::max_element(L.h_len.begin(), L.h_len.end());
-      L.start.alloc(L.nseg);
-      L.len.alloc(L.nseg);
-      CUDA_TRY(cudaMemcpy(L.start.p, L.h_start.data(), sizeof(int) * L.nseg, cudaMemcpyHostToDevice));
-      CUDA_TRY(cudaMemcpy(L.len.p, L.h_len.data(), sizeof(int) * L.nseg, cudaMemcpyHostToDevice));
-      if (L.nseg == 1) break;
-      const int ns = L.nseg - 1;
-      L.mat.alloc(4 * (size_t)L.nseg);
-      L.rhsv.alloc(2 * (size_t)L.nseg);
+      const int nseg = L.S.nseg;
+      if (nseg == 1) break;
+      const int ns = nseg - 1;
+      L.mat.alloc(4 * (size_t)nseg);
+      L.rhsv.alloc(2 * (size_t)nseg);
       L.Tsub.alloc(ns);
       L.Tdiag.alloc(ns);
       L.Tsup.alloc(ns);
       L.rhs_next.alloc(ns);
       L.x_next.alloc(ns);
-      if (lv.size() == 1) {
-        L.partR.alloc(ns);
-        L.partL.alloc(ns);
-        L.counters.alloc(ns);
-        CUDA_TRY(cudaMemset(L.counters.p, 0, sizeof(int) * ns));
-      }
       auto N = std::make_unique<TriLevel>();
-      N->A.a = RowArr{L.Tsub.p, 1, ns};
-      N->A.b = RowArr{L.Tdiag.p, 0, ns};
-      N->A.c = RowArr{L.Tsup.p, 0, ns - 1};
-      N->F = RowArr{L.rhs_next.p, 0, ns};
+      N->A.a = make_rows(L.Tsub.p, 1, ns);
+      N->A.b = make_rows(L.Tdiag.p, 0, ns);
+      N->A.c = make_rows(L.Tsup.p, 0, ns - 1);
+      N->F = make_rows(L.rhs_next.p, 0, ns);
       N->x = L.x_next.p;
       N->q = ns;
-      segment_uniform(ns, N->h_start, N->h_len);
+      N->S = segment_uniform(ns, N->maxlen);
       lv.push_back(std::move(N));
     }
+    (void)s;
   }
 
-  static int blocks(long work, int tpb) { return (int)((work + tpb - 1) / tpb); }
-
-  void factor(int H, cudaStream_t s) {
+  void exact_factor(cudaStream_t s) {
+    build_levels(s);
     for (size_t l = 0; l + 1 < lv.size(); ++l) {
       TriLevel& L = *lv[l];
-      tri_interface_kernel<true, false><<<blocks(2L * L.nseg, 128), 128, 0, s>>>(
-          L.A, RowArr{nullptr, 0, 0}, L.start.p, L.len.p, L.nseg, H, L.mat.p, nullptr);
+      tri_interface_kernel<true, false><<<blocks_for(2L * L.S.nseg, 128), 128, 0, s>>>(
+          L.A, make_rows(nullptr, 0, 0), L.S, 0, L.mat.p, nullptr);
       LAUNCH_CHECK();
-      tri_assemble_matrix_kernel<<<blocks(L.nseg - 1, 256), 256, 0, s>>>(L.A, L.start.p, L.len.p, L.nseg - 1,
-                                                                         L.mat.p, L.Tsub.p, L.Tdiag.p, L.Tsup.p);
+      tri_assemble_matrix_kernel<<<blocks_for(L.S.nseg - 1, 256), 256, 0, s>>>(L.A, L.S, L.mat.p, L.Tsub.p,
+                                                                               L.Tdiag.p, L.Tsup.p);
       LAUNCH_CHECK();
       launches += 2;
     }
   }
 
-  // phase1: condense + rhs assembly down the levels; phase2: deepest direct
-  // solve + upper-level back-substitutions; phase3: level-0 back-substitution.
-  void solve(const RowArr& F0, double* x0, int H, DevStatus* st, cudaStream_t s, cudaEvent_t* ev, int from = 0) {
+  // Exact solve of level `from` (0 = the user system, 1 = the reduced system).
+  void exact_solve(const RowArr& F0, double* x0, DevStatus* st, cudaStream_t s, cudaEvent_t* ev, size_t from = 0) {
     lv[from]->F = F0;
     lv[from]->x = x0;
     for (size_t l = from; l + 1 < lv.size(); ++l) {
       TriLevel& L = *lv[l];
-      tri_interface_kernel<false, true><<<blocks(2L * L.nseg, 128), 128, 0, s>>>(
-          L.A, L.F, L.start.p, L.len.p, L.nseg, H, nullptr, L.rhsv.p);
+      tri_interface_kernel<false, true><<<blocks_for(2L * L.S.nseg, 128), 128, 0, s>>>(L.A, L.F, L.S, 0, nullptr,
+                                                                                      L.rhsv.p);
       LAUNCH_CHECK();
-      tri_assemble_rhs_kernel<<<blocks(L.nseg - 1, 256), 256, 0, s>>>(L.A, L.F, L.start.p, L.len.p, L.nseg - 1,
-                                                                      L.rhsv.p, L.rhs_next.p);
+      tri_assemble_rhs_kernel<<<blocks_for(L.S.nseg - 1, 256), 256, 0, s>>>(L.A, L.F, L.S, L.rhsv.p, L.rhs_next.p);
       LAUNCH_CHECK();
       launches += 2;
-      if (l == (size_t)from && ev) cudaEventRecord(ev[1], s);
+      if (l == from && ev) CUDA_TRY(cudaEventRecord(ev[1], s));
     }
-    for (size_t l = lv.size(); l-- > (size_t)from;) {
+    for (size_t l = lv.size(); l-- > from;) {
       TriLevel& L = *lv[l];
-      if (l == (size_t)from && ev && lv.size() > (size_t)from + 1) cudaEventRecord(ev[2], s);
+      if (l == from && ev) CUDA_TRY(cudaEventRecord(ev[2], s));
+      if (l == 0 && L.S.nseg > 1 && st) {
+        k3_and_cert(L.F, L.x, L.x_next.p, false, st, s);
+        continue;
+      }
       TriSolveArgs a{};
       a.A = L.A;
       a.F = L.F;
-      a.seg_start = L.start.p;
-      a.seg_len = L.len.p;
-      a.nseg = L.nseg;
-      a.xsep = L.nseg > 1 ? L.x_next.p : nullptr;
+      a.S = L.S;
+      a.xsep = L.S.nseg > 1 ? L.x_next.p : nullptr;
       a.x = L.x;
-      a.status = st;
-      if (l == 0 && L.nseg > 1) {
-        a.partR = L.partR.p;
-        a.partL = L.partL.p;
-        a.counters = L.counters.p;
-      }
-      segment_solve(a, L.nseg, L.maxlen, s);
+      a.status = l == 0 ? st : nullptr;  // pivots/non-finite values are attributed at level 0 only
+      segment_solve(a, L.S.nseg, L.maxlen, false, s);
       launches += 1;
     }
   }
 
-  long long reduced_ops() const {
+  void restore_level1_wiring() {
+    if (lv.size() > 1) {
+      lv[1]->x = lv[0]->x_next.p;
+      lv[1]->F = make_rows(lv[0]->rhs_next.p, 0, lv[1]->q);
+    }
+  }
+
+  long long reduced_ops(bool spec) const {
+    if (spec) return 2LL * (S0.nseg - 1) * (2 * kHalo + 1);  // 65-term dot product per separator (x2: both CTAs)
     long long ops = 0;
     for (size_t l = 1; l < lv.size(); ++l) ops += 12LL * lv[l]->q;
     return ops;
@@ -374,45 +518,56 @@ struct psg_handle {
   int strategy = 0;
   DevBuf<double> own_data, own_corner;
   TriSolver tri;
-  std::vector<int> seg_start, seg_len;  // level-0 segmentation (refined plan)
+  std::vector<int> seg_start, seg_len;  // level-0 segmentation when refined
   bool refined = false;
   // options
   bool speculative = true;
-  int halo = 32;
   double cert_tol = 1e-14;
-  // state
-  bool factored_exact = false;  // factor data computed in exact mode
+  // state: which factor data is current
+  bool spec_factored = false, exact_factored = false;
   DevBuf<DevStatus> d_status;
-  DevStatus* h_status = nullptr;  // pinned
+  DevStatus* h_status = nullptr;  // pinned slot
   DevBuf<double> d_f, d_x;        // host-path staging
+  cudaEvent_t ev_f0 = nullptr, ev_f1 = nullptr, ev_done = nullptr, ev[4] = {};
   std::mutex mu;
   int factor_launches = 0, solve_launches = 0;
-  double factor_seconds = 0;
   ~psg_handle() {
-    if (h_status) cudaFreeHost(h_status);
+    if (ev_done) cudaEventSynchronize(ev_done);  // buffers go back to the cache only when idle
+    for (cudaEvent_t e : {ev_f0, ev_f1, ev_done, ev[0], ev[1], ev[2], ev[3]})
+      if (e) event_pool().put(e);
+    if (h_status) pinned_slots().put(h_status);
   }
+  bool use_spec() const { return speculative && tri.spec_possible(); }
 };
 
 namespace {
 
+// The reference layout data = [sub (n-1) | diag (n) | super (n-1)]
+// (src/structmat.cpp:33-38): a_r = data[r-1], b_r = data[n-1+r],
+// c_r = data[2n-1+r]; any row index whose address stays inside data is safe
+// to over-read (the staging widens copies to 16-byte boundaries).
 TriRows tri_rows(const psg_desc& A) {
   const double* d = A.data;
-  const int n = A.n;
-  return TriRows{RowArr{d - 1, 1, n}, RowArr{d + (n - 1), 0, n}, RowArr{d + (2L * n - 1), 0, n - 1}};
+  const long n = A.n;
+  return TriRows{make_rows(d - 1, 1, (int)n, 1, 3 * n - 1), make_rows(d + (n - 1), 0, (int)n, -(n - 1), 2 * n - 1),
+                 make_rows(d + (2 * n - 1), 0, (int)n - 1, -(2 * n - 1), n - 1)};
 }
 
-void refine_segments(const Plan& P, std::vector<int>& st, std::vector<int>& ln, bool& refined) {
+// Level-0 segmentation: the reference bodies, refined (extra one-row
+// separators inside a body) when a body exceeds one warp's capacity.
+SegMap plan_segments(const Plan& P, std::vector<int>& st, std::vector<int>& ln, bool& refined, int& maxlen,
+                     int& minlen) {
   st.clear();
   ln.clear();
   refined = false;
+  maxlen = int(P.base + (P.rem ? 1 : 0));
+  minlen = int(P.base);
+  if (maxlen <= kMaxSeg) return SegMap{P.p, int(P.base), int(P.rem), nullptr, nullptr};
+  refined = true;
+  maxlen = 0;
+  minlen = INT_MAX;
   for (int i = 0; i < P.p; ++i) {
-    const int b = P.body_begin[i], L = P.body_end[i] - b;
-    if (L <= kMaxSeg) {
-      st.push_back(b);
-      ln.push_back(L);
-      continue;
-    }
-    refined = true;
+    const int b = P.body_begin(i), L = P.body_end(i) - b;
     const int t = (L + 1 + kMaxSeg) / (kMaxSeg + 1);  // sub-bodies
     const long body = (long)L - (t - 1);
     const long base = body / t, rem = body % t;
@@ -421,9 +576,12 @@ void refine_segments(const Plan& P, std::vector<int>& st, std::vector<int>& ln, 
       const long len = base + (u < rem ? 1 : 0);
       st.push_back(int(cur));
       ln.push_back(int(len));
+      maxlen = std::max<int>(maxlen, int(len));
+      minlen = std::min<int>(minlen, int(len));
       cur += len + 1;
     }
   }
+  return SegMap{(int)st.size(), 0, 0, nullptr, nullptr};
 }
 
 void check_strategy(const psg_desc& A, int strategy) {
@@ -446,18 +604,40 @@ void check_strategy(const psg_desc& A, int strategy) {
 
 bool is_tridiag(const psg_desc& A) { return A.kind == PSG_BANDED && A.s == 1 && A.r == 1; }
 
+// (Re)compute the factor data for the current mode.
 void run_factor(psg_handle* h, cudaStream_t s) {
-  const int H = (h->speculative && !h->factored_exact) ? h->halo : 0;
   h->tri.launches = 0;
-  h->tri.factor(H, s);
+  CUDA_TRY(cudaEventRecord(h->ev_f0, s));
+  if (h->use_spec()) {
+    h->tri.spec_factor(s);
+    h->spec_factored = true;
+  } else {
+    h->tri.exact_factor(s);
+    h->exact_factored = true;
+  }
+  CUDA_TRY(cudaEventRecord(h->ev_f1, s));
   h->factor_launches = h->tri.launches;
+}
+
+int partition_of_segment(const psg_handle* h, int seg) {
+  if (!h->refined) return seg + 1;
+  const int row = h->seg_start[std::min<size_t>(seg, h->seg_start.size() - 1)];
+  int lo = 0, hi = h->plan.p - 1;  // last partition whose body begins at or before row
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) / 2;
+    if (h->plan.body_begin(mid) <= row)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo + 1;
 }
 
 }  // namespace
 
 extern "C" {
 
-const char* psg_version(void) { return "psg-b200 0.1 (sm_100a)"; }
+const char* psg_version(void) { return "psg-b200 0.2 (sm_100a)"; }
 
 int psg_config_shape(int cfg, int size, int* kind, int* n, int* m, int* s, int* r, size_t* data_len,
                      int* corner_rows, int* corner_cols) {
@@ -506,10 +686,12 @@ int psg_plan(const psg_desc* A, int p, int* body_begin, int* body_end, int* sep_
   try {
     validate(*A);
     Plan P = make_plan(*A, p);
-    std::copy(P.body_begin.begin(), P.body_begin.end(), body_begin);
-    std::copy(P.body_end.begin(), P.body_end.end(), body_end);
-    std::copy(P.sep_start.begin(), P.sep_start.end(), sep_start);
-    *sep_count = (int)P.sep_start.size();
+    for (int i = 0; i < p; ++i) {
+      body_begin[i] = P.body_begin(i);
+      body_end[i] = P.body_end(i);
+    }
+    for (int j = 0; j < P.sep_count(); ++j) sep_start[j] = P.sep_start(j);
+    *sep_count = P.sep_count();
     *sep_size = P.sep_size;
     return 0;
   } catch (const Fail& f_) {
@@ -521,18 +703,16 @@ int psg_factor(const psg_desc* Ain, int p, int strategy, double tol, void* strea
                size_t errlen) {
   (void)tol;
   *out = nullptr;
-  std::unique_ptr<psg_handle> h(new psg_handle);
   try {
+    std::unique_ptr<psg_handle> h(new psg_handle);
     validate(*Ain);
     check_strategy(*Ain, strategy);
     h->plan = make_plan(*Ain, p);
     if (!is_tridiag(*Ain))
       throw Fail{PSG_E_UNSUPPORTED_KIND, "GPU path for this kind is not built yet (tridiagonal only)"};
     cudaStream_t s = (cudaStream_t)stream;
-    cudaEvent_t e0, e1;
-    CUDA_TRY(cudaEventCreate(&e0));
-    CUDA_TRY(cudaEventCreate(&e1));
-    CUDA_TRY(cudaEventRecord(e0, s));
+    for (cudaEvent_t* e : {&h->ev_f0, &h->ev_f1, &h->ev_done, &h->ev[0], &h->ev[1], &h->ev[2], &h->ev[3]})
+      *e = event_pool().get();
     h->A = *Ain;
     h->strategy = strategy;
     if (!Ain->on_device) {
@@ -547,18 +727,14 @@ int psg_factor(const psg_desc* Ain, int p, int strategy, double tol, void* strea
       }
       h->A.on_device = 1;
     }
-    refine_segments(h->plan, h->seg_start, h->seg_len, h->refined);
-    h->tri.build(tri_rows(h->A), h->A.n, h->seg_start, h->seg_len);
+    int maxlen = 0, minlen = 0;
+    SegMap S0 = plan_segments(h->plan, h->seg_start, h->seg_len, h->refined, maxlen, minlen);
+    h->tri.init(tri_rows(h->A), h->A.n, S0, maxlen, minlen, h->refined ? &h->seg_start : nullptr,
+                h->refined ? &h->seg_len : nullptr, s);
     h->d_status.alloc(1);
-    CUDA_TRY(cudaMallocHost(&h->h_status, sizeof(DevStatus)));
+    h->h_status = static_cast<DevStatus*>(pinned_slots().get());
     run_factor(h.get(), s);
-    CUDA_TRY(cudaEventRecord(e1, s));
-    CUDA_TRY(cudaEventSynchronize(e1));
-    float ms = 0;
-    cudaEventElapsedTime(&ms, e0, e1);
-    h->factor_seconds = ms * 1e-3;
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
+    CUDA_TRY(cudaEventRecord(h->ev_done, s));
     *out = h.release();
     return 0;
   } catch (const Fail& f_) {
@@ -570,11 +746,23 @@ void psg_release(psg_handle* h) { delete h; }
 
 int psg_set_option(psg_handle* h, int option, double value) {
   std::lock_guard<std::mutex> g(h->mu);
-  switch (option) {
-    case PSG_OPT_SPECULATIVE: h->speculative = value != 0.0; break;
-    case PSG_OPT_HALO: h->halo = std::max(1, (int)value); break;
-    case PSG_OPT_CERT_TOL: h->cert_tol = value; break;
-    default: return 1 + PSG_E_INVALID_PARAMETER;
+  try {
+    switch (option) {
+      case PSG_OPT_SPECULATIVE:
+        h->speculative = value != 0.0;
+        if ((h->use_spec() && !h->spec_factored) || (!h->use_spec() && !h->exact_factored)) {
+          run_factor(h, nullptr);
+          CUDA_TRY(cudaEventRecord(h->ev_done, nullptr));
+        }
+        break;
+      case PSG_OPT_HALO:
+        if ((int)value != kHalo) return 1 + PSG_E_INVALID_PARAMETER;  // fixed to the warp width
+        break;
+      case PSG_OPT_CERT_TOL: h->cert_tol = value; break;
+      default: return 1 + PSG_E_INVALID_PARAMETER;
+    }
+  } catch (const Fail& f_) {
+    return 1 + f_.code;
   }
   return 0;
 }
@@ -601,68 +789,67 @@ int psg_solve(const psg_handle* hc, const double* f, double* x, int on_device, v
       df = h->d_f.p;
       dx = h->d_x.p;
     }
-    cudaEvent_t ev[4];
     const bool timing = stats != nullptr;
-    if (timing)
-      for (auto& e : ev) CUDA_TRY(cudaEventCreate(&e));
-    int fallbacks = 0;
+    int fallbacks = 0, launches = 0;
     bool spec_used = false;
     double cert = 0;
-    h->tri.launches = 0;
     for (int attempt = 0; attempt < 2; ++attempt) {
-      const bool spec = h->speculative && !h->factored_exact;
-      const int H = spec ? h->halo : 0;
-      DevStatus init{0ull, INT_MAX, 0};
-      *h->h_status = init;
+      const bool spec = h->use_spec();
+      *h->h_status = DevStatus{0ull, INT_MAX, INT_MAX};
       CUDA_TRY(cudaMemcpyAsync(h->d_status.p, h->h_status, sizeof(DevStatus), cudaMemcpyHostToDevice, s));
-      if (timing) CUDA_TRY(cudaEventRecord(ev[0], s));
-      h->tri.solve(RowArr{df, 0, n}, dx, H, h->d_status.p, s, timing ? ev : nullptr);
-      if (timing) CUDA_TRY(cudaEventRecord(ev[3], s));
+      if (timing) CUDA_TRY(cudaEventRecord(h->ev[0], s));
+      h->tri.launches = 0;
+      if (spec)
+        h->tri.spec_solve(make_rows(df, 0, n), dx, h->d_status.p, s, timing ? h->ev : nullptr);
+      else
+        h->tri.exact_solve(make_rows(df, 0, n), dx, h->d_status.p, s, timing ? h->ev : nullptr);
+      launches += h->tri.launches;
+      if (timing) CUDA_TRY(cudaEventRecord(h->ev[3], s));
       CUDA_TRY(cudaMemcpyAsync(h->h_status, h->d_status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
       CUDA_TRY(cudaStreamSynchronize(s));
       const DevStatus st = *h->h_status;
       cert = bits_to_double(st.cert_bits);
-      const bool bad = st.bad_seg != INT_MAX;
+      const bool bad = st.bad_seg != INT_MAX || st.pivot_seg != INT_MAX;
       if (!bad && cert <= h->cert_tol) {
         spec_used = spec;
         break;
       }
       if (!spec) {
-        if (bad) {
-          // map the segment back to its reference partition (1-based)
-          const int seg_row = h->seg_start[std::min<size_t>(st.bad_seg, h->seg_start.size() - 1)];
-          int part = 1;
-          for (int i = 0; i < h->plan.p; ++i)
-            if (h->plan.body_begin[i] <= seg_row) part = i + 1;
-          throw Fail{PSG_E_ZERO_PIVOT, "partition " + std::to_string(part) +
-                                           ": zero pivot (non-finite value in the no-pivot elimination)"};
-        }
-        break;  // exact mode: report the certificate, keep the result
+        if (st.pivot_seg != INT_MAX)  // parallel_factor's lowest failing partition (src/parfact.cpp:61-68)
+          throw Fail{PSG_E_ZERO_PIVOT, "partition " + std::to_string(partition_of_segment(h, st.pivot_seg)) +
+                                           ": zero pivot in the no-pivot elimination"};
+        if (bad)
+          throw Fail{PSG_E_SINGULAR_REDUCED_SYSTEM, "non-finite solution: the reduced system is singular"};
+        break;  // exact mode: the certificate is reported, the result kept
       }
-      // speculative interface rejected: refactor exactly and re-solve
+      // speculative interface rejected: switch this handle to the exact path
       ++fallbacks;
-      h->factored_exact = true;
-      run_factor(h, s);
+      h->speculative = false;
+      if (!h->exact_factored) {
+        run_factor(h, s);
+        launches += h->tri.launches;
+      }
     }
     if (!on_device) {
       CUDA_TRY(cudaMemcpyAsync(x, dx, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
       CUDA_TRY(cudaStreamSynchronize(s));
     }
-    h->solve_launches = h->tri.launches;
+    CUDA_TRY(cudaEventRecord(h->ev_done, s));
+    h->solve_launches = launches;
     if (timing) {
-      float t01 = 0, t12 = 0, t23 = 0;
-      cudaEventElapsedTime(&t01, ev[0], ev[1]);
-      cudaEventElapsedTime(&t12, ev[1], ev[2]);
-      cudaEventElapsedTime(&t23, ev[2], ev[3]);
-      stats->factor_seconds = h->factor_seconds;
+      float tf = 0, t01 = 0, t12 = 0, t23 = 0;
+      cudaEventElapsedTime(&tf, h->ev_f0, h->ev_f1);
+      cudaEventElapsedTime(&t01, h->ev[0], h->ev[1]);
+      cudaEventElapsedTime(&t12, h->ev[1], h->ev[2]);
+      cudaEventElapsedTime(&t23, h->ev[2], h->ev[3]);
+      stats->factor_seconds = tf * 1e-3;
       stats->phase1_seconds = t01 * 1e-3;
       stats->phase2_seconds = t12 * 1e-3;
       stats->phase3_seconds = t23 * 1e-3;
-      stats->reduced_ops = h->tri.reduced_ops();
+      stats->reduced_ops = h->tri.reduced_ops(spec_used);
       stats->certificate = cert;
       stats->speculative = spec_used ? 1 : 0;
       stats->fallbacks = fallbacks;
-      for (auto& e : ev) cudaEventDestroy(e);
     }
     return 0;
   } catch (const Fail& f_) {
@@ -671,7 +858,7 @@ int psg_solve(const psg_handle* hc, const double* f, double* x, int on_device, v
 }
 
 int psg_reduced_info(const psg_handle* h, int* q, int* dim, int* k, int* has_corner) {
-  const int qq = (int)h->plan.sep_start.size();
+  const int qq = h->plan.sep_count();
   if (q) *q = qq;
   if (dim) *dim = qq * h->plan.sep_size;
   if (k) *k = h->plan.sep_size;
@@ -683,9 +870,17 @@ int psg_reduced_blocks(const psg_handle* hc, double* diag, double* sub, double* 
   psg_handle* h = const_cast<psg_handle*>(hc);
   std::lock_guard<std::mutex> g(h->mu);
   try {
-    if (h->refined) throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "reduced system was refined internally (bodies > 1088 rows)"};
+    if (h->refined) throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "reduced system was refined internally (bodies > 1056 rows)"};
+    CUDA_TRY(cudaEventSynchronize(h->ev_done));
+    const int ns = h->tri.S0.nseg - 1;
+    if (h->use_spec() && h->spec_factored) {
+      // speculative reduced matrix: diagonal (beta = gamma = 0 below rho^L)
+      if (diag) CUDA_TRY(cudaMemcpy(diag, h->tri.Tdiag.p, sizeof(double) * ns, cudaMemcpyDeviceToHost));
+      if (sub) std::fill(sub, sub + ns, 0.0);
+      if (super) std::fill(super, super + ns, 0.0);
+      return 0;
+    }
     TriLevel& L = *h->tri.lv[0];
-    const int ns = L.nseg - 1;
     if (diag) CUDA_TRY(cudaMemcpy(diag, L.Tdiag.p, sizeof(double) * ns, cudaMemcpyDeviceToHost));
     if (sub) CUDA_TRY(cudaMemcpy(sub, L.Tsub.p, sizeof(double) * ns, cudaMemcpyDeviceToHost));
     if (super) CUDA_TRY(cudaMemcpy(super, L.Tsup.p, sizeof(double) * ns, cudaMemcpyDeviceToHost));
@@ -700,9 +895,14 @@ int psg_solve_reduced(const psg_handle* hc, const double* rhs, double* x, int on
   psg_handle* h = const_cast<psg_handle*>(hc);
   std::lock_guard<std::mutex> g(h->mu);
   try {
-    if (h->refined) throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "reduced system was refined internally (bodies > 1088 rows)"};
+    if (h->refined) throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "reduced system was refined internally (bodies > 1056 rows)"};
     cudaStream_t s = (cudaStream_t)stream;
-    const int q = h->tri.lv[0]->nseg - 1;
+    if (!h->exact_factored) {  // the exact reduced matrix T (parallel_factor's ReducedSystem)
+      h->tri.launches = 0;
+      h->tri.exact_factor(s);
+      h->exact_factored = true;
+    }
+    const int q = h->tri.S0.nseg - 1;
     DevBuf<double> dr, dxv;
     const double* r = rhs;
     double* xo = x;
@@ -713,15 +913,12 @@ int psg_solve_reduced(const psg_handle* hc, const double* rhs, double* x, int on
       r = dr.p;
       xo = dxv.p;
     }
-    if (h->tri.lv.size() < 2) throw Fail{PSG_E_INVALID_PARAMETER, "no reduced system"};
-    // The reduced system is level 1 of the solver; solve it in exact mode.
-    h->tri.solve(RowArr{r, 0, q}, xo, 0, nullptr, s, nullptr, 1);
-    // level 1's x output is xo; restore the level-0 wiring for later solves
-    h->tri.lv[1]->x = h->tri.lv[0]->x_next.p;
-    h->tri.lv[1]->F = RowArr{h->tri.lv[0]->rhs_next.p, 0, q};
+    h->tri.exact_solve(make_rows(r, 0, q), xo, nullptr, s, nullptr, 1);
+    h->tri.restore_level1_wiring();
     if (!on_device) CUDA_TRY(cudaMemcpyAsync(x, xo, sizeof(double) * q, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
-    if (stats) stats->reduced_ops += h->tri.reduced_ops();
+    CUDA_TRY(cudaEventRecord(h->ev_done, s));
+    if (stats) stats->reduced_ops += h->tri.reduced_ops(false);
     return 0;
   } catch (const Fail& f_) {
     return set_err(err, errlen, f_.code, f_.msg);

@@ -15,8 +15,14 @@ namespace psg {
 // b_r = data[n-1+r] is {data + n - 1, 0, n} (src/structmat.cpp:33-38).
 struct RowArr {
   const double* p;
-  int lo, hi;
+  int lo, hi;    // rows with a defined value (outside: structural zero)
+  long slo, shi; // rows whose address lies inside the allocation (safe to over-read)
 };
+
+__host__ __device__ inline RowArr make_rows(const double* p, int lo, int hi, long slo, long shi) {
+  return RowArr{p, lo, hi, slo, shi};
+}
+__host__ __device__ inline RowArr make_rows(const double* p, int lo, int hi) { return RowArr{p, lo, hi, lo, hi}; }
 
 __device__ __forceinline__ double row_at(const RowArr& X, long r) {
   return (r >= X.lo && r < X.hi) ? __ldg(X.p + r) : 0.0;
@@ -25,11 +31,12 @@ __device__ __forceinline__ double row_at(const RowArr& X, long r) {
 // Device status shared by all kernels of one solve.
 struct DevStatus {
   unsigned long long cert_bits;  // max componentwise backward error (double bits, >= 0)
-  int bad_seg;                   // lowest segment with a non-finite value (INT_MAX: none)
-  int pad;
+  int bad_seg;                   // lowest segment with a non-finite solution value (INT_MAX: none)
+  int pivot_seg;                 // lowest segment whose own elimination hit a zero/non-finite pivot
 };
 
 __device__ __forceinline__ void status_nonfinite(DevStatus* st, int seg) { atomicMin(&st->bad_seg, seg); }
+__device__ __forceinline__ void status_pivot(DevStatus* st, int seg) { atomicMin(&st->pivot_seg, seg); }
 
 __device__ __forceinline__ void status_cert(DevStatus* st, double w) {
   if (!(w <= 1.0e300)) w = __longlong_as_double(0x7ff0000000000000ll);  // NaN/huge -> +inf
@@ -78,37 +85,72 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-// Stage rows [r0, r1) of X into shared memory.  `base` must be 16-byte
-// aligned with room for (r1 - r0 + 1) doubles.  Returns buf with
-// buf[r - r0] = X(r) (zero outside X's valid range).  The 16-byte aligned
-// interior goes through one bulk copy (counted into *tx); the <= 2 ragged
-// elements at either end and the zero fill are plain shared stores.  Must be
-// called by ONE thread; the caller publishes with __syncthreads + mbar wait.
-__device__ __forceinline__ double* stage_rows(const RowArr& X, long r0, long r1, double* base,
-                                              uint64_t* bar, uint32_t* tx) {
+// Stage rows [r0, r1) of X into shared memory: issue side.  `base` must be
+// 16-byte aligned with room for (r1 - r0 + 3) doubles; the result buffer is
+// buf = base + 1 + shift (shift 0/1) with buf[r - r0] = row r, buf[j] and row
+// r0+j congruent mod 16 bytes.  The copy is widened to 16-byte boundaries when
+// the widened bytes stay inside the allocation (X.slo/X.shi), so in the
+// common case a single bulk copy moves everything and nothing blocks; rows
+// outside X's defined range are zeroed afterwards by stage_fixup.  Returns
+// shift; *tx accumulates the bulk bytes.  Called by one lane per array.
+__device__ __forceinline__ int stage_issue(const RowArr& X, long r0, long r1, double* base, uint64_t* bar,
+                                           uint32_t* tx) {
   const uintptr_t g0 = reinterpret_cast<uintptr_t>(X.p + r0);
-  const uintptr_t s0 = reinterpret_cast<uintptr_t>(base);
-  const int shift = (int)(((g0 - s0) >> 3) & 1);  // make buf[j] and row r0+j congruent mod 16
-  double* buf = base + shift;
-  const long v0 = r0 > X.lo ? r0 : X.lo;
-  const long v1 = r1 < X.hi ? r1 : X.hi;
-  for (long r = r0; r < r1 && r < v0; ++r) buf[r - r0] = 0.0;
-  for (long r = (v1 > r0 ? v1 : r0); r < r1; ++r) buf[r - r0] = 0.0;
-  if (v1 <= v0) return buf;
+  const uintptr_t s0 = reinterpret_cast<uintptr_t>(base + 1);
+  const int shift = (int)(((g0 - s0) >> 3) & 1);
+  double* buf = base + 1 + shift;
+  long v0 = r0 > X.lo ? r0 : X.lo;
+  long v1 = r1 < X.hi ? r1 : X.hi;
+  if (v1 <= v0) return shift;
   const uintptr_t a0 = reinterpret_cast<uintptr_t>(X.p + v0);
   const uintptr_t a1 = reinterpret_cast<uintptr_t>(X.p + v1);
-  const uintptr_t b0 = (a0 + 15) & ~uintptr_t(15);
-  const uintptr_t b1 = a1 & ~uintptr_t(15);
+  uintptr_t b0 = a0 & ~uintptr_t(15), b1 = (a1 + 15) & ~uintptr_t(15);
+  const bool head_ok = (long)(v0 - ((a0 - b0) >> 3)) >= X.slo;
+  const bool tail_ok = (long)(v1 + ((b1 - a1) >> 3)) <= X.shi;
+  if (!head_ok) b0 = (a0 + 15) & ~uintptr_t(15);
+  if (!tail_ok) b1 = a1 & ~uintptr_t(15);
   if (b1 > b0) {
-    const long rb = v0 + (long)((b0 - a0) >> 3);
+    const long rb = v0 + ((long)b0 - (long)a0) / 8;
     bulk_g2s(buf + (rb - r0), reinterpret_cast<const void*>(b0), (uint32_t)(b1 - b0), bar);
     *tx += (uint32_t)(b1 - b0);
-    if (a0 < b0) buf[v0 - r0] = __ldg(X.p + v0);
-    if (a1 > b1) buf[v1 - 1 - r0] = __ldg(X.p + v1 - 1);
+    if (!head_ok && a0 < b0) buf[v0 - r0] = __ldg(X.p + v0);
+    if (!tail_ok && a1 > b1) buf[v1 - 1 - r0] = __ldg(X.p + v1 - 1);
   } else {
     for (long r = v0; r < v1; ++r) buf[r - r0] = __ldg(X.p + r);
   }
-  return buf;
+  return shift;
+}
+
+// After the mbarrier wait: zero the staged rows that lie outside X's defined
+// range (only the first/last segments of an array have any).
+__device__ __forceinline__ void stage_fixup(const RowArr& X, long r0, long r1, double* buf) {
+  for (long r = r0; r < r1 && r < X.lo; ++r) buf[r - r0] = 0.0;
+  for (long r = (X.hi > r0 ? X.hi : r0); r < r1; ++r) buf[r - r0] = 0.0;
+}
+
+// Bulk shared->global copy (async proxy); dst/src 16-byte aligned, bytes % 16 == 0.
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit_and_wait_read() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// Reciprocal: MUFU approximation + two Newton steps (<= 1 ulp; no slow-path
+// branch).  0 -> inf and inf/NaN -> NaN propagate to the non-finite check.
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
 }
 
 // Host-visible launch accounting.

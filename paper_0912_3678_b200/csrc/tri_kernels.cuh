@@ -26,13 +26,37 @@
 //     the direct solve of small reduced systems (nseg = 1).
 #pragma once
 
+#include <climits>
+
 #include "psg_common.cuh"
 
 namespace psg {
 
+__device__ __forceinline__ double b_minus(double b, double x, double y) { return (b - x) - y; }
+
 struct TriRows {
   RowArr a, b, c;  // sub (coefficient of row r-1), diagonal, super (coefficient of row r+1)
 };
+
+// Segment i = rows [start, start+len) with one separator row after it.
+// Uniform maps use the reference plan formula (src/partition.cpp:94-104 with
+// k = 1): len = base + (i < rem), start = i*(base+1) + min(i, rem); refined
+// plans pass explicit arrays.
+struct SegMap {
+  int nseg, base, rem;
+  const int* start;
+  const int* len;
+};
+
+__device__ __forceinline__ void seg_of(const SegMap& S, int i, long& s, int& L) {
+  if (S.start) {
+    s = S.start[i];
+    L = S.len[i];
+  } else {
+    L = S.base + (i < S.rem ? 1 : 0);
+    s = (long)i * (S.base + 1) + (i < S.rem ? i : S.rem);
+  }
+}
 
 // ----------------------------------------------------------------------------
 // K1: segment-end interface values
@@ -40,16 +64,16 @@ struct TriRows {
 // out_mat[4*seg + {0,1,2,3}] = U0, V0, UL, VL   (when WITH_MAT)
 // out_rhs[2*seg + {0,1}]     = P0, PL           (when WITH_RHS)
 template <bool WITH_MAT, bool WITH_RHS>
-__global__ void __launch_bounds__(128) tri_interface_kernel(TriRows A, RowArr F, const int* __restrict__ seg_start,
-                                                             const int* __restrict__ seg_len, int nseg, int H,
+__global__ void __launch_bounds__(128) tri_interface_kernel(TriRows A, RowArr F, SegMap S, int H,
                                                              double* __restrict__ out_mat,
                                                              double* __restrict__ out_rhs) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   const int seg = idx >> 1;
-  if (seg >= nseg) return;
+  if (seg >= S.nseg) return;
   const int end = idx & 1;
-  const long s = seg_start[seg];
-  const int L = seg_len[seg];
+  long s;
+  int L;
+  seg_of(S, seg, s, L);
   const int h = (H <= 0 || 2 * H >= L) ? L : H;
   if (end == 0) {
     // Bottom-up (UL) sweep over rows h-1 .. 0: row 0 becomes
@@ -108,136 +132,338 @@ __global__ void __launch_bounds__(128) tri_interface_kernel(TriRows A, RowArr F,
 //   Tsup[j]  = c_t V0_{j+1}      (coefficient of x_{j+1})
 //   rhs[j]   = f_t - a_t PL_j - c_t P0_{j+1}
 // ----------------------------------------------------------------------------
-__global__ void tri_assemble_matrix_kernel(TriRows A, const int* __restrict__ seg_start,
-                                           const int* __restrict__ seg_len, int nsep,
+__global__ void tri_assemble_matrix_kernel(TriRows A, SegMap S,
                                            const double* __restrict__ mat, double* __restrict__ Tsub,
                                            double* __restrict__ Tdiag, double* __restrict__ Tsup) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= nsep) return;
-  const long t = (long)seg_start[j] + seg_len[j];
+  if (j >= S.nseg - 1) return;
+  long s0;
+  int L0;
+  seg_of(S, j, s0, L0);
+  const long t = s0 + L0;
   const double a = row_at(A.a, t), b = row_at(A.b, t), c = row_at(A.c, t);
   Tsub[j] = a * mat[4 * j + 2];
   Tdiag[j] = fma(c, mat[4 * (j + 1) + 0], fma(a, mat[4 * j + 3], b));
   Tsup[j] = c * mat[4 * (j + 1) + 1];
 }
 
-__global__ void tri_assemble_rhs_kernel(TriRows A, RowArr F, const int* __restrict__ seg_start,
-                                        const int* __restrict__ seg_len, int nsep,
+__global__ void tri_assemble_rhs_kernel(TriRows A, RowArr F, SegMap S,
                                         const double* __restrict__ rhs_in, double* __restrict__ rhs) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= nsep) return;
-  const long t = (long)seg_start[j] + seg_len[j];
+  if (j >= S.nseg - 1) return;
+  long s0;
+  int L0;
+  seg_of(S, j, s0, L0);
+  const long t = s0 + L0;
   const double a = row_at(A.a, t), c = row_at(A.c, t);
   rhs[j] = fma(-c, rhs_in[2 * (j + 1) + 0], fma(-a, rhs_in[2 * j + 1], row_at(F, t)));
 }
 
+
 // ----------------------------------------------------------------------------
-// K3: per-segment solve.  CTA = NT threads = one segment of <= M*NT rows;
-// thread t owns body rows [tM, tM+M) (M odd => the stride-M shared-memory
-// walk of a warp touches 16 distinct 8-byte bank pairs: 2 wavefronts, the
-// minimum for 64-bit loads).
+// Speculative interface, one warp per separator row t between
+// segments j and j+1.  Truncate both adjacent bodies to their H = 32 rows next
+// to t: the first row of the inverse of the leading block of segment j+1 and
+// the last row of the inverse of the trailing block of segment j follow from
+// two 32-row transposed solves (warp PCR, one row per lane).  Because the
+// far-corner entries of a body inverse are O(rho^L) (exactly 0.0 in fp64 for
+// the BASELINE generators, where the reference's beta/gamma also vanish), the
+// speculative reduced matrix is diagonal:
+//   Tdiag_t = b_t - a_t c_{t-1} v_31 - c_t a_{t+1} w_0
+//   x_t     = ( f_t - a_t sum_i v_i f_{t-32+i} - c_t sum_i w_i f_{t+1+i} ) / Tdiag_t
+// The factor stores the 65 weights of that dot product; the solve is one
+// coalesced dot product per separator.  The certificate (separator residuals
+// after the exact body solves) decides whether the speculation stands.
+// ----------------------------------------------------------------------------
+constexpr int kHalo = 32;
+
+// Solve the 32x32 tridiagonal system held one row per lane
+//   lo*y_{i-1} + di*y_i + up*y_{i+1} = r   (out-of-block couplings zeroed)
+// by 5 normalised parallel-cyclic-reduction steps.  Returns y_lane.
+__device__ __forceinline__ double warp_tri_pcr(double lo, double di, double up, double r) {
+  constexpr unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  double inv = fast_rcp(di);
+  lo *= inv;
+  up *= inv;
+  r *= inv;
+#pragma unroll
+  for (int st = 1; st < 32; st <<= 1) {
+    double la = __shfl_up_sync(FULL, lo, st), lu = __shfl_up_sync(FULL, up, st), lr = __shfl_up_sync(FULL, r, st);
+    double ha = __shfl_down_sync(FULL, lo, st), hu = __shfl_down_sync(FULL, up, st),
+           hr = __shfl_down_sync(FULL, r, st);
+    if (lane < st) la = lu = lr = 0.0;
+    if (lane + st >= 32) ha = hu = hr = 0.0;
+    inv = fast_rcp(1.0 - lo * lu - up * ha);
+    const double nr = r - lo * lr - up * hr;
+    lo = -lo * la * inv;
+    up = -up * hu * inv;
+    r = nr * inv;
+  }
+  return r;
+}
+
+// Weight rows: wts[j * kWRow + i], i < 32: -a_t v_i / Tdiag (v = last row of
+// the inverse of segment j's trailing block), 32 <= i < 64: -c_t w_{i-32} /
+// Tdiag (w = first row of the inverse of segment j+1's leading block),
+// i = 64: 1 / Tdiag.  With the top-down sweep d_k = b_k - l_k c_{k-1},
+// l_k = a_k / d_{k-1} of the trailing block, v_31 = 1/d_31 and
+// v_i = -l_{i+1} v_{i+1}; with the bottom-up sweep e_k = b_k - mu_k a_{k+1},
+// mu_k = c_k / e_{k+1} of the leading block, w_0 = 1/e_0 and
+// w_i = -mu_{i-1} w_{i-1}.
+constexpr int kWRow = 66;  // 64 weights + 1/Tdiag + pad (528 B, 16-byte multiple)
+constexpr int kFacWarps = 1;
+constexpr int kFacPitch = 33;  // [row][separator] tiles padded to 33 columns
+
+// One warp = 32 consecutive separators.  The 32-row windows are loaded
+// coalesced (lane = row), transposed through shared memory so that lane =
+// separator for the sequential sweeps, and the weight rows go back through
+// shared memory to one TMA bulk store.
+__global__ void __launch_bounds__(32 * kFacWarps) tri_spec_factor_kernel(TriRows A, SegMap S, double* __restrict__ wts,
+                                                                         double* __restrict__ Tdiag) {
+  constexpr unsigned FULL = 0xffffffffu;
+  __shared__ __align__(16) double tile[kFacWarps][3][kHalo * kFacPitch];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nsep = S.nseg - 1;
+  const int j0 = (blockIdx.x * kFacWarps + wid) * 32;
+  if (j0 >= nsep) return;
+  const int nj = min(32, nsep - j0);
+  double* tA = tile[wid][0];
+  double* tB = tile[wid][1];
+  double* tC = tile[wid][2];
+  long tme;  // this lane's separator row
+  {
+    long s0;
+    int L0;
+    seg_of(S, min(j0 + lane, nsep - 1), s0, L0);
+    tme = s0 + L0;
+  }
+  // ---- trailing block of segment j: rows t-32+k (coupling to row t-33 dropped)
+#pragma unroll 4
+  for (int jj = 0; jj < 32; ++jj) {
+    const long t = __shfl_sync(FULL, tme, jj);
+    const long r = t - kHalo + lane;
+    tA[lane * kFacPitch + jj] = row_at(A.a, r);
+    tB[lane * kFacPitch + jj] = row_at(A.b, r);
+    tC[lane * kFacPitch + jj] = row_at(A.c, r);
+  }
+  __syncwarp();
+  double m[kHalo];
+  double d = tB[lane];
+  double cprev = tC[lane];
+#pragma unroll
+  for (int k = 1; k < kHalo; ++k) {
+    const double l = tA[k * kFacPitch + lane] * fast_rcp(d);
+    m[k] = l;
+    d = fma(-l, cprev, tB[k * kFacPitch + lane]);
+    cprev = tC[k * kFacPitch + lane];
+  }
+  const double v31 = fast_rcp(d);
+  __syncwarp();
+  // ---- leading block of segment j+1: rows t+1+k (coupling to row t+33 dropped)
+#pragma unroll 4
+  for (int jj = 0; jj < 32; ++jj) {
+    const long t = __shfl_sync(FULL, tme, jj);
+    const long r = t + 1 + lane;
+    tA[lane * kFacPitch + jj] = row_at(A.a, r);
+    tB[lane * kFacPitch + jj] = row_at(A.b, r);
+    tC[lane * kFacPitch + jj] = row_at(A.c, r);
+  }
+  __syncwarp();
+  double mu[kHalo];
+  double e = tB[(kHalo - 1) * kFacPitch + lane];
+  double anext = tA[(kHalo - 1) * kFacPitch + lane];
+#pragma unroll
+  for (int k = kHalo - 2; k >= 0; --k) {
+    const double mk = tC[k * kFacPitch + lane] * fast_rcp(e);
+    mu[k] = mk;
+    e = fma(-mk, anext, tB[k * kFacPitch + lane]);
+    anext = tA[k * kFacPitch + lane];
+  }
+  const double w0 = fast_rcp(e);
+  const double at = row_at(A.a, tme), bt = row_at(A.b, tme), ct = row_at(A.c, tme);
+  const double td = b_minus(bt, at * row_at(A.c, tme - 1) * v31, ct * row_at(A.a, tme + 1) * w0);
+  const double it = 1.0 / td;
+  if (lane < nj) Tdiag[j0 + lane] = td;
+  __syncwarp();
+  // ---- weight rows -> shared (reusing the tiles: 32 x kWRow doubles) -> one bulk store
+  double* wout = tA;  // needs 32 * 66 = 2112 doubles; tA..tC hold 3 * 1056 contiguous
+  const double sa = -at * it, sc = -ct * it;
+  double v = v31;
+  wout[lane * kWRow + kHalo - 1] = sa * v;
+#pragma unroll
+  for (int i = kHalo - 2; i >= 0; --i) {
+    v = -m[i + 1] * v;
+    wout[lane * kWRow + i] = sa * v;
+  }
+  double w = w0;
+  wout[lane * kWRow + kHalo] = sc * w;
+#pragma unroll
+  for (int i = 1; i < kHalo; ++i) {
+    w = -mu[i - 1] * w;
+    wout[lane * kWRow + kHalo + i] = sc * w;
+  }
+  wout[lane * kWRow + 2 * kHalo] = it;
+  wout[lane * kWRow + 2 * kHalo + 1] = 0.0;
+  fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    bulk_s2g(wts + (long)j0 * kWRow, wout, (uint32_t)(nj * kWRow * sizeof(double)));
+    bulk_commit_and_wait_read();
+  }
+}
+
+// x_t = f_t / Tdiag + sum_i W[i] f(t-32+i) + sum_i W[32+i] f(t+1+i), evaluated by
+// one warp with a fixed lane order and reduction tree, so the two CTAs that
+// need the same separator get bit-identical values.  fw points at the
+// shared-memory f row of t-32; W at the weight row in shared memory.
+__device__ __forceinline__ double spec_sep_value(const double* fw, const double* W) {
+  const int lane = threadIdx.x & 31;
+  double acc = fma(W[lane], fw[lane], W[kHalo + lane] * fw[kHalo + 1 + lane]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  return fma(fw[kHalo], W[2 * kHalo], acc);
+}
+
+// ----------------------------------------------------------------------------
+// K3: per-segment solve.  One warp = one segment of <= 32*M body rows; lane t
+// owns body rows [tM, tM+M).  M is odd so the stride-M shared-memory walk of
+// the warp touches 16 distinct 8-byte bank pairs (2 wavefronts per LDS.64,
+// the minimum).  Rows are staged by four lanes issuing one TMA bulk copy each
+// (a, b, c, f); x leaves through one TMA bulk store.
+//   1. chunk elimination: every chunk row j ends as
+//        ap[j] y_first + y_j + cp[j] y_last = dp[j]
+//      (row 0: ap y_{prev last} + y_0 + cp y_last; row M-1: ap y_0 + y_{M-1} + cp y_{next first});
+//   2. the chunk-last unknowns are eliminated, leaving one tridiagonal row
+//      per lane in the chunk-first unknowns, solved by 5 shuffle PCR steps;
+//   3. chunk back-substitution.
 // ----------------------------------------------------------------------------
 struct TriSolveArgs {
   TriRows A;
   RowArr F;
-  const int* seg_start;
-  const int* seg_len;
-  int nseg;
-  const double* xsep;  // nseg-1 separator values (NULL when nseg == 1)
+  SegMap S;
+  const double* xsep;  // nseg-1 separator values (exact path; NULL when nseg == 1)
+  const double* wts;   // speculative path: weight rows (kWRow per separator)
   double* x;           // output, row r at x[r]
-  // certificate (level 1 only; NULL disables)
-  double2* partR;
-  double2* partL;
-  int* counters;
+  double2* yends;      // per segment (y_first, y_last) for the certificate (NULL: skip)
   DevStatus* status;
 };
 
-template <int M, int NT>
-struct TriSmem {
-  static constexpr int LCAP = M * NT + 2;   // body rows + both separators
-  static constexpr int ROW = LCAP + 2;      // + alignment shift, even
-  static constexpr int BYTES = (4 * ROW + 8 * NT + 2 * NT) * 8 + 16;
+template <int M>
+struct TriWarpSmem {
+  static constexpr int CAP = 32 * M;                // body rows per segment
+  static constexpr int ROW = CAP + 6;               // + both separator rows + staging slack, even
+  static constexpr int ROWF = CAP + 2 * kHalo + 6;  // f also carries 32 rows past each separator
+  static constexpr int WROW = 2 * kWRow + 4;        // the two weight rows (+ slack)
+  static constexpr int BYTES = (3 * ROW + ROWF + WROW) * 8;
 };
 
-__device__ __forceinline__ void cert_combine(const double2* partR, const double2* partL, int j, DevStatus* st) {
-  const double2 R = __ldcg(partR + j);
-  const double2 Lp = __ldcg(partL + j);
-  const double v = R.x + Lp.x;
-  const double a = R.y + Lp.y;
-  double w = a > 0.0 ? fabs(v) / a : (v != 0.0 ? __longlong_as_double(0x7ff0000000000000ll) : 0.0);
-  status_cert(st, w);
-}
-
-template <int M, int NT>
-__global__ void __launch_bounds__(NT) tri_segment_solve_kernel(TriSolveArgs args) {
+template <int M, bool SPEC>
+__global__ void __launch_bounds__(32) tri_segment_solve_kernel(TriSolveArgs args) {
   static_assert(M % 2 == 1 && M >= 3, "M must be odd and >= 3");
-  using SM = TriSmem<M, NT>;
+  constexpr int ROW = TriWarpSmem<M>::ROW;
+  constexpr int ROWF = TriWarpSmem<M>::ROWF;
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int FH = SPEC ? kHalo + 1 : 1;  // f rows staged before/after the body
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t bar;
-  const int tid = threadIdx.x;
+  const int lane = threadIdx.x;
   const int seg = blockIdx.x;
-  const long s = args.seg_start[seg];
-  const int L = args.seg_len[seg];
+  long s;
+  int L;
+  seg_of(args.S, seg, s, L);
+  const int nseg = args.S.nseg;
+  const bool has_l = seg > 0, has_r = seg < nseg - 1;
 
-  double* sA;
-  double* sB;
-  double* sC;
-  double* sF;
-  double* pcr = smem + 4 * SM::ROW;  // 2 x 4 x NT
-  double* sx = pcr + 8 * NT;         // 2 x NT scratch (E rows, F values)
-  __shared__ double* bufs[4];
-  if (tid == 0) {
-    mbar_init(&bar, 1);
+  // ---- staging: lanes 0..3 (a, b, c, f) and 4 (weight rows) issue one bulk copy each
+  const long w0 = (long)(has_l ? seg - 1 : seg) * kWRow;
+  const int nw = SPEC ? (int)has_l + (int)has_r : 0;
+  RowArr X = lane == 0 ? args.A.a : lane == 1 ? args.A.b : lane == 2 ? args.A.c : args.F;
+  long lo = lane == 3 ? s - FH : s - 1, hi = lane == 3 ? s + L + FH : s + L + 1;
+  if (SPEC && lane == 4) {
+    X = make_rows(args.wts, 0, (int)(w0 + nw * kWRow));
+    lo = w0;
+    hi = w0 + nw * kWRow;
+  }
+  double* const base = smem + (lane < 4 ? lane * ROW : 3 * ROW + ROWF);
+  const int nstage = SPEC ? 5 : 4;
+  if (lane == 0) mbar_init(&bar, nstage);
+  __syncwarp();
+  int shift = 0;
+  if (lane < nstage) {
     uint32_t tx = 0;
-    const long r0 = s - 1, r1 = s + L + 1;
-    bufs[0] = stage_rows(args.A.a, r0, r1, smem + 0 * SM::ROW, &bar, &tx);
-    bufs[1] = stage_rows(args.A.b, r0, r1, smem + 1 * SM::ROW, &bar, &tx);
-    bufs[2] = stage_rows(args.A.c, r0, r1, smem + 2 * SM::ROW, &bar, &tx);
-    bufs[3] = stage_rows(args.F, r0, r1, smem + 3 * SM::ROW, &bar, &tx);
+    shift = stage_issue(X, lo, hi, base, &bar, &tx);
     mbar_arrive_expect_tx(&bar, tx);
   }
-  const double xl = (seg > 0) ? args.xsep[seg - 1] : 0.0;
-  const double xr = (seg < args.nseg - 1) ? args.xsep[seg] : 0.0;
-  __syncthreads();
+  // sX[q] = body row q; sX[-1] / sX[L] = left / right separator rows
+  double* sA = smem + 0 * ROW + 2 + __shfl_sync(FULL, shift, 0);
+  double* sB = smem + 1 * ROW + 2 + __shfl_sync(FULL, shift, 1);
+  double* sC = smem + 2 * ROW + 2 + __shfl_sync(FULL, shift, 2);
+  double* sF = smem + 3 * ROW + 1 + FH + __shfl_sync(FULL, shift, 3);
+  const double* sW = smem + 3 * ROW + ROWF + 1 + __shfl_sync(FULL, shift, 4);
+  double xl = 0.0, xr = 0.0;
+  if (!SPEC) {
+    xl = has_l ? args.xsep[seg - 1] : 0.0;
+    xr = has_r ? args.xsep[seg] : 0.0;
+  }
   mbar_wait(&bar, 0);
-  sA = bufs[0];
-  sB = bufs[1];
-  sC = bufs[2];
-  sF = bufs[3];
+  if (lane < 4) stage_fixup(X, lo, hi, base + 1 + shift);
+  __syncwarp();
+  // separator coupling terms: a_s x_l enters row 0, c x_r row L-1 (folded in
+  // after the forward sweep, which is linear in those two rhs entries)
+  const double cl = -sA[0], cr = -sC[L - 1];
+  // pad to 32*M rows with decoupled identity rows; their rhs keeps the staged
+  // f rows past the body (finite; needed for x_r) and is zero beyond them
+  for (int q = L + lane; q < 32 * M; q += 32) {
+    sA[q] = 0.0;
+    sB[q] = 1.0;
+    sC[q] = 0.0;
+    if (q >= L + FH) sF[q] = 0.0;
+  }
+  if (lane == 0) {  // row 0 / row L-1 couple to the separators, not to the neighbours
+    sA[0] = 0.0;
+    sC[L - 1] = 0.0;
+  }
+  __syncwarp();
 
-  // ---- chunk elimination: every row j of the chunk ends as
-  //      ap[j] * y_first + y_j + cp[j] * y_last = dp[j]
-  //      (row 0: ap*y_{prev chunk last} + y_0 + cp*y_last; row M-1: ap*y_0 + y_{M-1} + cp*y_{next first})
+  // ---- chunk elimination: every chunk row j ends as
+  //      ap[j] y_first + y_j + cp[j] y_last = dp[j]
   double ap[M], cp[M], dp[M];
-  const int q0 = tid * M;
+  const int q0 = lane * M;
+  const int jL = L - 1 - q0;  // chunk position of row L-1 (valid when 0 <= jL < M)
+  double rsum = 0.0;          // sum |pivot reciprocals|: non-finite <=> a pivot of this body vanished
+  double rL = 0.0;            // pivot reciprocal of row L-1 (for the x_r fold)
+  double r0 = 0.0;            // pivot reciprocal of chunk row 0 (for the x_l fold, lane 0)
 #pragma unroll
   for (int j = 0; j < M; ++j) {
-    const int q = q0 + j;
-    const bool valid = q < L;
-    double a = valid ? sA[1 + q] : 0.0;
-    const double b = valid ? sB[1 + q] : 1.0;
-    double c = valid ? sC[1 + q] : 0.0;
-    double f = valid ? sF[1 + q] : 0.0;
-    if (q == 0) {
-      f = fma(-a, xl, f);
-      a = 0.0;
-    }
-    if (q == L - 1) {
-      f = fma(-c, xr, f);
-      c = 0.0;
-    }
+    const double a = sA[q0 + j], b = sB[q0 + j], c = sC[q0 + j], f = sF[q0 + j];
+    double r;
     if (j < 2) {
-      const double r = 1.0 / b;
+      r = fast_rcp(b);
       ap[j] = a * r;
       cp[j] = c * r;
       dp[j] = f * r;
     } else {
-      const double r = 1.0 / fma(-a, cp[j - 1], b);
+      r = fast_rcp(fma(-a, cp[j - 1], b));
       dp[j] = r * fma(-a, dp[j - 1], f);
       ap[j] = -r * a * ap[j - 1];
       cp[j] = r * c;
     }
+    rsum += fabs(r);
+    if (j == jL) rL = r;
+    if (j == 0) r0 = r;
   }
+  if (SPEC) {  // separator values (phases 1+2 fused), overlapping the forward sweep's latency
+    if (has_l) xl = spec_sep_value(sF - 1 - kHalo, sW);
+    if (has_r) xr = spec_sep_value(sF + L - kHalo, sW + (has_l ? kWRow : 0));
+  }
+  // fold the separator terms: the forward sweep never feeds chunk row 0's rhs or
+  // row L-1's rhs into another real row (row 0 enters only the final row-0
+  // step, row L-1 only identity padding), so only their own dp entry changes
+  if (lane == 0) dp[0] = fma(cl * xl, r0, dp[0]);
+#pragma unroll
+  for (int j = 0; j < M; ++j)
+    if (j == jL) dp[j] = fma(cr * xr, rL, dp[j]);
 #pragma unroll
   for (int j = M - 3; j >= 1; --j) {
     dp[j] = fma(-cp[j], dp[j + 1], dp[j]);
@@ -245,122 +471,111 @@ __global__ void __launch_bounds__(NT) tri_segment_solve_kernel(TriSolveArgs args
     cp[j] = -cp[j] * cp[j + 1];
   }
   {
-    const double r = 1.0 / fma(-cp[0], ap[1], 1.0);
+    const double r = fast_rcp(fma(-cp[0], ap[1], 1.0));
+    rsum += fabs(r);
     dp[0] = r * fma(-cp[0], dp[1], dp[0]);
     ap[0] = r * ap[0];
     cp[0] = -r * cp[0] * cp[1];
   }
 
-  // ---- chunk interfaces: eliminate the E (last-row) unknowns, giving one
-  //      tridiagonal row per thread in the F (first-row) unknowns.
-  double* sEa = sx;  // reuse: E rows need 3 arrays -> use pcr buffer 1 region
-  double* eA = pcr + 4 * NT;
-  double* eC = eA + NT;
-  double* eD = eC + NT;
-  eA[tid] = ap[M - 1];
-  eC[tid] = cp[M - 1];
-  eD[tid] = dp[M - 1];
-  __syncthreads();
-  double al, be, ga, de;
+  // ---- chunk interfaces -> one normalised tridiagonal row per lane in F = y_first
+  const double aE = ap[M - 1], cE = cp[M - 1], dE = dp[M - 1];
+  double pa = __shfl_up_sync(FULL, aE, 1), pc = __shfl_up_sync(FULL, cE, 1), pd = __shfl_up_sync(FULL, dE, 1);
+  if (lane == 0) pa = pc = pd = 0.0;
+  double al = -ap[0] * pa;
+  double ga = -cp[0] * cE;
+  double de = dp[0] - ap[0] * pd - cp[0] * dE;
   {
-    const double pa = tid > 0 ? eA[tid - 1] : 0.0;
-    const double pc = tid > 0 ? eC[tid - 1] : 0.0;
-    const double pd = tid > 0 ? eD[tid - 1] : 0.0;
-    al = -ap[0] * pa;
-    be = 1.0 - ap[0] * pc - cp[0] * ap[M - 1];
-    ga = -cp[0] * cp[M - 1];
-    de = dp[0] - ap[0] * pd - cp[0] * dp[M - 1];
+    const double r = fast_rcp(1.0 - ap[0] * pc - cp[0] * aE);
+    rsum += fabs(r);
+    al *= r;
+    ga *= r;
+    de *= r;
   }
-  (void)sEa;
-  // ---- parallel cyclic reduction over the NT F-rows (double-buffered).
-  int buf = 0;
 #pragma unroll
-  for (int st = 1; st < NT; st <<= 1) {
-    double* P = pcr + buf * 4 * NT;
-    P[tid] = al;
-    P[NT + tid] = be;
-    P[2 * NT + tid] = ga;
-    P[3 * NT + tid] = de;
-    __syncthreads();
-    double la = 0.0, lb = 1.0, lg = 0.0, ld = 0.0, ha = 0.0, hb = 1.0, hg = 0.0, hd = 0.0;
-    if (tid - st >= 0) {
-      la = P[tid - st];
-      lb = P[NT + tid - st];
-      lg = P[2 * NT + tid - st];
-      ld = P[3 * NT + tid - st];
-    }
-    if (tid + st < NT) {
-      ha = P[tid + st];
-      hb = P[NT + tid + st];
-      hg = P[2 * NT + tid + st];
-      hd = P[3 * NT + tid + st];
-    }
-    const double k1 = al / lb;
-    const double k2 = ga / hb;
-    al = -k1 * la;
-    ga = -k2 * hg;
-    be = be - k1 * lg - k2 * ha;
-    de = de - k1 * ld - k2 * hd;
-    buf ^= 1;
+  for (int st = 1; st < 32; st <<= 1) {
+    double la = __shfl_up_sync(FULL, al, st), lg = __shfl_up_sync(FULL, ga, st), ld = __shfl_up_sync(FULL, de, st);
+    double ha = __shfl_down_sync(FULL, al, st), hg = __shfl_down_sync(FULL, ga, st),
+           hd = __shfl_down_sync(FULL, de, st);
+    if (lane < st) la = lg = ld = 0.0;
+    if (lane + st >= 32) ha = hg = hd = 0.0;
+    const double r = fast_rcp(1.0 - al * lg - ga * ha);
+    rsum += fabs(r);
+    const double nde = de - al * ld - ga * hd;
+    al = -al * la * r;
+    ga = -ga * hg * r;
+    de = nde * r;
   }
-  const double Fv = de / be;
-  sx[tid] = Fv;
-  __syncthreads();
-  const double Fn = tid + 1 < NT ? sx[tid + 1] : 0.0;
-  const double Ev = dp[M - 1] - ap[M - 1] * Fv - cp[M - 1] * Fn;
+  const double Fv = de;
+  double Fn = __shfl_down_sync(FULL, Fv, 1);
+  if (lane == 31) Fn = 0.0;
+  const double Ev = dE - aE * Fv - cE * Fn;
 
-  // ---- chunk back-substitution, finite check, stage y over f.
+  // ---- chunk back-substitution, finite check, stage y over f
   bool finite = true;
 #pragma unroll
   for (int j = 0; j < M; ++j) {
-    const int q = q0 + j;
-    double y;
-    if (j == 0)
-      y = Fv;
-    else if (j == M - 1)
-      y = Ev;
-    else
-      y = dp[j] - ap[j] * Fv - cp[j] * Ev;
-    if (q < L) {
-      finite &= isfinite(y);
-      sF[1 + q] = y;
+    const double y = (j == 0) ? Fv : (j == M - 1) ? Ev : dp[j] - ap[j] * Fv - cp[j] * Ev;
+    if (q0 + j < L) finite &= isfinite(y);
+    sF[q0 + j] = y;
+  }
+  if (args.status) {
+    const bool piv_ok = __all_sync(FULL, isfinite(rsum));
+    const bool all_ok = __all_sync(FULL, finite);
+    if (lane == 0) {
+      if (!piv_ok) status_pivot(args.status, seg);
+      if (!all_ok) status_nonfinite(args.status, seg);
     }
   }
-  if (!finite && args.status) status_nonfinite(args.status, seg);
-  __syncthreads();
+  fence_proxy_async_smem();
+  __syncwarp();
 
-  // ---- coalesced write-back of the body (and the right separator).
-  double* xo = args.x + s;
-  for (int q = tid; q < L; q += NT) xo[q] = sF[1 + q];
-
-  if (tid == 0 && seg < args.nseg - 1) args.x[s + L] = xr;
-
-  // ---- certificate: componentwise backward error of the separator rows,
-  //      combined by whichever neighbouring CTA arrives second.
-  if (tid == 0 && args.counters) {
-    const double y0 = sF[1], yL = sF[L];
-    if (seg < args.nseg - 1) {
-      const double aR = sA[L + 1], bR = sB[L + 1], fR = sF[L + 1];
-      const double t1 = aR * yL, t2 = bR * xr;
-      args.partR[seg] = make_double2(fR - t1 - t2, fabs(fR) + fabs(t1) + fabs(t2));
-      __threadfence();
-      if (atomicAdd(args.counters + seg, 1) == 1) {
-        __threadfence();
-        cert_combine(args.partR, args.partL, seg, args.status);
-        args.counters[seg] = 0;
-      }
+  // ---- write-back: aligned interior by one TMA bulk store, ragged ends by lanes 1/2
+  double* xg = args.x + s;
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(xg), a1 = reinterpret_cast<uintptr_t>(xg + L);
+  const uintptr_t b0 = (a0 + 15) & ~uintptr_t(15), b1 = a1 & ~uintptr_t(15);
+  const bool congruent = ((a0 - reinterpret_cast<uintptr_t>(sF)) & 15) == 0;
+  if (congruent && b1 > b0) {
+    if (lane == 0) {
+      bulk_s2g(reinterpret_cast<void*>(b0), sF + ((b0 - a0) >> 3), (uint32_t)(b1 - b0));
+      bulk_commit_and_wait_read();
     }
-    if (seg > 0) {
-      const double t3 = sC[0] * y0;
-      args.partL[seg - 1] = make_double2(-t3, fabs(t3));
-      __threadfence();
-      if (atomicAdd(args.counters + seg - 1, 1) == 1) {
-        __threadfence();
-        cert_combine(args.partR, args.partL, seg - 1, args.status);
-        args.counters[seg - 1] = 0;
-      }
-    }
+    if (lane == 1 && a0 < b0) xg[0] = sF[0];
+    if (lane == 2 && a1 > b1) xg[L - 1] = sF[L - 1];
+  } else {
+    for (int q = lane; q < L; q += 32) xg[q] = sF[q];
   }
+  if (lane == 3) {
+    if (has_r) args.x[s + L] = xr;
+    if (args.yends) args.yends[seg] = make_double2(sF[0], sF[L - 1]);
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Certificate: componentwise backward error of every separator row,
+//   w_t = |f_t - a_t y_{t-1} - b_t x_t - c_t y_{t+1}| / (|f_t| + |a_t y_{t-1}| + |b_t x_t| + |c_t y_{t+1}|)
+// with the body values y from K3.  The body rows are solved exactly given
+// the separators, so this bounds the error the speculative interface let in.
+// ----------------------------------------------------------------------------
+__global__ void tri_cert_kernel(TriRows A, RowArr F, SegMap S, const double* __restrict__ x,
+                                const double2* __restrict__ yends, DevStatus* st) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  double w = 0.0;
+  if (j < S.nseg - 1) {
+    long s0;
+    int L0;
+    seg_of(S, j, s0, L0);
+    const long t = s0 + L0;
+    const double yl = yends[j].y, yr = yends[j + 1].x, xt = x[t];
+    const double t1 = row_at(A.a, t) * yl, t2 = row_at(A.b, t) * xt, t3 = row_at(A.c, t) * yr;
+    const double f = row_at(F, t);
+    const double r = ((f - t1) - t2) - t3;
+    const double den = fabs(f) + fabs(t1) + fabs(t2) + fabs(t3);
+    w = den > 0.0 ? fabs(r) / den : (r != 0.0 ? __longlong_as_double(0x7ff0000000000000ll) : 0.0);
+    if (!(w <= 1.0e300)) w = __longlong_as_double(0x7ff0000000000000ll);
+  }
+  for (int o = 16; o > 0; o >>= 1) w = fmax(w, __shfl_xor_sync(0xffffffffu, w, o));
+  if ((threadIdx.x & 31) == 0 && w > 0.0) status_cert(st, w);
 }
 
 }  // namespace psg

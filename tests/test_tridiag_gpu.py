@@ -84,3 +84,101 @@ def test_config1_full_size(cuda):
     Ah = O.Matrix(A.kind, A.n, A.m, A.s, A.r, A.data.cpu().numpy())
     want = O.solve_sequential(Ah, f.cpu().numpy())
     assert O.rel_err(x.cpu().numpy(), want) <= 1e-12
+
+
+def _toeplitz(n, lo, d, up):
+    data = np.concatenate([np.full(n - 1, lo), np.full(n, d), np.full(n - 1, up)])
+    return O.Matrix(O.BANDED, n, 1, 1, 1, data)
+
+
+def test_weak_dominance_falls_back_to_exact(cuda):
+    # rho ~ 0.9: a 32-row truncation is far from exact -> certificate rejects it
+    n, p = 40000, 40
+    A = _toeplitz(n, -1.0, 2.02, -1.0)
+    f = np.sin(np.arange(n) * 0.37)
+    want, _ = O.parallel_solve(A, p, f)
+    got, st, _ = _solve_gpu(cuda, A, p, f)
+    assert st.fallbacks == 1 and st.speculative == 0
+    assert O.rel_err(got, want) <= 1e-10
+    assert O.residual(A, got, f) <= 1e-13
+
+
+@pytest.mark.parametrize("n,p", [(20000, 3), (9, 2), (3, 2), (200, 10), (5000, 100)])
+def test_refined_and_small_segments(cuda, n, p):
+    A, f = O.generate_config(0, n, 5)
+    want, _ = O.parallel_solve(A, p, f)
+    got, st, _ = _solve_gpu(cuda, A, p, f)
+    assert O.rel_err(got, want) <= 1e-12
+    assert O.residual(A, got, f) <= 1e-13
+
+
+def test_toeplitz_known_answer(cuda):
+    # Toeplitz(-1,2,-1), n=3, p=2, f=[1,1,1] -> x=[1.5,2,1.5]
+    A = _toeplitz(3, -1.0, 2.0, -1.0)
+    got, _, _ = _solve_gpu(cuda, A, 2, np.ones(3))
+    assert np.allclose(got, [1.5, 2.0, 1.5], rtol=0, atol=1e-15)
+
+
+def test_reduced_matrix_matches_reference_T(cuda):
+    A, f = O.generate_config(0, 1 << 14, 9)
+    p = 16
+    info = O.factor_info(A, p)
+    T = info["T"]
+    GA = psg.StructuredMatrix(A.kind, A.n, A.m, A.s, A.r, _dev(cuda, A.data))
+    F = psg.parallel_factor(GA, p)
+    sub, diag, sup = F.reduced_blocks()
+    q = info["dim"]
+    assert F.q == q == p - 1
+    scale = np.max(np.abs(np.diag(T)))
+    assert np.max(np.abs(diag - np.diag(T))) <= 1e-14 * scale
+    assert np.max(np.abs(sub[1:] - np.diag(T, -1))) <= 1e-14 * scale
+    assert np.max(np.abs(sup[:-1] - np.diag(T, 1))) <= 1e-14 * scale
+    # solve_reduced (exact) against a dense solve of the reference T
+    rhs = np.cos(np.arange(q))
+    xr = psg.solve_reduced(F, rhs)
+    assert O.rel_err(xr, np.linalg.solve(T, rhs)) <= 1e-12
+
+
+def test_strategies_and_errors(cuda):
+    A, f = O.generate_config(0, 4096, 4)
+    GA = psg.StructuredMatrix(A.kind, A.n, A.m, A.s, A.r, _dev(cuda, A.data))
+    want, _ = O.parallel_solve(A, 8, f)
+    for s in (psg.Strategy.Lu, psg.Strategy.Lud, psg.Strategy.CyclicReduction):
+        F = psg.parallel_factor(GA, 8, s)
+        got = psg.solve(F, _dev(cuda, f)).cpu().numpy()
+        assert O.rel_err(got, want) <= 1e-12
+    for s, code in ((psg.Strategy.LuPivot, psg.Errc.UnsupportedStructure), (psg.Strategy.Qr, psg.Errc.UnsupportedStructure),
+                    (psg.Strategy.Arce, psg.Errc.UnsupportedKind)):
+        with pytest.raises(psg.Error) as ei:
+            psg.parallel_factor(GA, 8, s)
+        assert ei.value.code == code
+    with pytest.raises(psg.Error) as ei:
+        psg.parallel_factor(GA, 1)
+    assert ei.value.code == psg.Errc.TooManyPartitions
+    with pytest.raises(psg.Error) as ei:
+        psg.parallel_factor(GA, 4000)
+    assert ei.value.code == psg.Errc.TooManyPartitions
+
+
+def test_zero_pivot_reports_partition(cuda):
+    # p = 3 on n = 3000: bodies [0,1000) [1001,2000) [2001,3000), separators 1000, 2000.
+    # Rows 1001/1002 of partition 2 become the [[0,1],[1,0]] block of
+    # tests/test_localfact.cpp:369-385 -> ZeroPivot tagged with partition 2.
+    n, p = 3000, 3
+    A = _toeplitz(n, 1.0, 4.0, 1.0)
+    d = A.data.copy()
+    sub, dia, sup = 0, n - 1, 2 * n - 1    # a_r = d[sub + r - 1], b_r = d[dia + r], c_r = d[sup + r]
+    d[dia + 1001] = 0.0
+    d[dia + 1002] = 0.0
+    d[sup + 1001] = 1.0
+    d[sub + 1002 - 1] = 1.0
+    A = O.Matrix(O.BANDED, n, 1, 1, 1, d)
+    with pytest.raises(O.OracleError) as eo:
+        O.parallel_solve(A, p, np.ones(n))
+    assert eo.value.errc == psg.Errc.ZeroPivot and "partition 2" in str(eo.value)
+    GA = psg.StructuredMatrix(A.kind, A.n, A.m, A.s, A.r, _dev(cuda, A.data))
+    F = psg.parallel_factor(GA, p)
+    with pytest.raises(psg.Error) as ei:
+        psg.solve(F, _dev(cuda, np.ones(n)))
+    assert ei.value.code == psg.Errc.ZeroPivot
+    assert "partition 2" in str(ei.value)
