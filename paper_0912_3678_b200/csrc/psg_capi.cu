@@ -116,7 +116,7 @@ struct PinnedSlots {
   std::mutex mu;
   char* slab = nullptr;
   std::vector<int> free_;
-  static constexpr int kSlot = 64, kCount = 1024;
+  static constexpr int kSlot = 512, kCount = 256;
   void* get() {
     std::lock_guard<std::mutex> g(mu);
     if (!slab) {
@@ -299,7 +299,6 @@ struct TriLevel {
   DevBuf<int> start, len;                              // refined maps only
   DevBuf<double> mat, rhsv;                            // 4*nseg, 2*nseg
   DevBuf<double> Tsub, Tdiag, Tsup, rhs_next, x_next;  // nseg-1
-  DevBuf<double2> yends;  // level 0 only: per-segment (y_first, y_last) for the certificate
 };
 
 // q rows -> segments of <= kMaxSeg rows separated by single rows, using the
@@ -317,23 +316,20 @@ SegMap segment_uniform(int q, int& maxlen) {
 }
 
 template <int M>
-void launch_segment_solve(const TriSolveArgs& a, int nseg, bool spec, cudaStream_t s) {
+void launch_segment_solve(const TriSolveArgs& a, int nseg, cudaStream_t s) {
   constexpr int bytes = TriWarpSmem<M>::BYTES;
-  if (spec)
-    tri_segment_solve_kernel<M, true><<<nseg, 32, bytes, s>>>(a);
-  else
-    tri_segment_solve_kernel<M, false><<<nseg, 32, bytes, s>>>(a);
+  tri_segment_solve_kernel<M><<<nseg, 32, bytes, s>>>(a);
 }
 
-void segment_solve(const TriSolveArgs& a, int nseg, int maxlen, bool spec, cudaStream_t s) {
+void segment_solve(const TriSolveArgs& a, int nseg, int maxlen, cudaStream_t s) {
   if (maxlen <= 32 * 5)
-    launch_segment_solve<5>(a, nseg, spec, s);
+    launch_segment_solve<5>(a, nseg, s);
   else if (maxlen <= 32 * 9)
-    launch_segment_solve<9>(a, nseg, spec, s);
+    launch_segment_solve<9>(a, nseg, s);
   else if (maxlen <= 32 * 17)
-    launch_segment_solve<17>(a, nseg, spec, s);
+    launch_segment_solve<17>(a, nseg, s);
   else if (maxlen <= 32 * 33)
-    launch_segment_solve<33>(a, nseg, spec, s);
+    launch_segment_solve<33>(a, nseg, s);
   else
     throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "segment longer than the per-warp capacity"};
   LAUNCH_CHECK();
@@ -349,8 +345,8 @@ struct TriSolver {
   int maxlen0 = 0, minlen0 = 0;
   DevBuf<int> start0, len0;  // refined maps
   // speculative path buffers
-  DevBuf<double> wts, Tdiag;
-  DevBuf<double2> yends;
+  DevBuf<double> wts, Tdiag, xsep;
+  DevBuf<double4> crec;  // per-segment certificate records
   // exact multi-level path (built on demand)
   std::vector<std::unique_ptr<TriLevel>> lv;
   int launches = 0;
@@ -371,7 +367,8 @@ struct TriSolver {
       S0.start = start0.p;
       S0.len = len0.p;
     }
-    yends.alloc(S0.nseg);
+    crec.alloc(S0.nseg);
+    if (S0.nseg > 1) xsep.alloc(S0.nseg - 1);
   }
 
   bool spec_possible() const { return minlen0 >= kMinSpecSeg && S0.nseg > 1; }
@@ -381,34 +378,38 @@ struct TriSolver {
     const int nsep = S0.nseg - 1;
     wts.alloc((size_t)kWRow * nsep);
     Tdiag.alloc(nsep);
-    tri_spec_factor_kernel<<<blocks_for(nsep, 32 * kFacWarps), 32 * kFacWarps, 0, s>>>(A0, S0, wts.p, Tdiag.p);
+    tri_spec_factor_kernel<<<blocks_for(nsep, kFacSeps), 32, 0, s>>>(A0, S0, wts.p, Tdiag.p);
     LAUNCH_CHECK();
     launches += 1;
   }
 
-  // level-0 back-substitution (+ fused separator values when spec) and certificate
-  void k3_and_cert(const RowArr& F, double* x, const double* xs, bool spec, DevStatus* st, cudaStream_t s) {
+  // level-0 back-substitution and separator certificate
+  void k3_and_cert(const RowArr& F, double* x, const double* xs, DevStatus* st, cudaStream_t s) {
     TriSolveArgs a{};
     a.A = A0;
     a.F = F;
     a.S = S0;
     a.xsep = xs;
-    a.wts = spec ? wts.p : nullptr;
     a.x = x;
-    a.yends = yends.p;
+    a.crec = crec.p;
     a.status = st;
-    segment_solve(a, S0.nseg, maxlen0, spec, s);
-    tri_cert_kernel<<<blocks_for(S0.nseg - 1, 256), 256, 0, s>>>(A0, F, S0, x, yends.p, st);
+    segment_solve(a, S0.nseg, maxlen0, s);
+    tri_cert_kernel<<<blocks_for(S0.nseg - 1, 256), 256, 0, s>>>(S0.nseg - 1, crec.p, st);
     LAUNCH_CHECK();
     launches += 2;
   }
 
   void spec_solve(const RowArr& F, double* x, DevStatus* st, cudaStream_t s, cudaEvent_t* ev) {
-    if (ev) {  // phases 1 and 2 are fused into K3 (diagonal speculative reduced matrix)
+    const int nsep = S0.nseg - 1;
+    tri_spec_sep_kernel<<<blocks_for((long)blocks_for(nsep, kSepPerWarp) * 32, 256), 256, 0, s>>>(F, S0, wts.p,
+                                                                                                   xsep.p);
+    LAUNCH_CHECK();
+    launches += 1;
+    if (ev) {  // the speculative reduced matrix is diagonal: phase 2 is fused into phase 1
       CUDA_TRY(cudaEventRecord(ev[1], s));
       CUDA_TRY(cudaEventRecord(ev[2], s));
     }
-    k3_and_cert(F, x, nullptr, true, st, s);
+    k3_and_cert(F, x, xsep.p, st, s);
   }
 
   // ---- exact multi-level path ----------------------------------------------
@@ -477,7 +478,7 @@ struct TriSolver {
       TriLevel& L = *lv[l];
       if (l == from && ev) CUDA_TRY(cudaEventRecord(ev[2], s));
       if (l == 0 && L.S.nseg > 1 && st) {
-        k3_and_cert(L.F, L.x, L.x_next.p, false, st, s);
+        k3_and_cert(L.F, L.x, L.x_next.p, st, s);
         continue;
       }
       TriSolveArgs a{};
@@ -487,7 +488,7 @@ struct TriSolver {
       a.xsep = L.S.nseg > 1 ? L.x_next.p : nullptr;
       a.x = L.x;
       a.status = l == 0 ? st : nullptr;  // pivots/non-finite values are attributed at level 0 only
-      segment_solve(a, L.S.nseg, L.maxlen, false, s);
+      segment_solve(a, L.S.nseg, L.maxlen, s);
       launches += 1;
     }
   }
@@ -500,7 +501,7 @@ struct TriSolver {
   }
 
   long long reduced_ops(bool spec) const {
-    if (spec) return 2LL * (S0.nseg - 1) * (2 * kHalo + 1);  // 65-term dot product per separator (x2: both CTAs)
+    if (spec) return (long long)(S0.nseg - 1) * (2 * kHalo + 1);  // one 65-term dot product per separator
     long long ops = 0;
     for (size_t l = 1; l < lv.size(); ++l) ops += 12LL * lv[l]->q;
     return ops;
@@ -795,7 +796,9 @@ int psg_solve(const psg_handle* hc, const double* f, double* x, int on_device, v
     double cert = 0;
     for (int attempt = 0; attempt < 2; ++attempt) {
       const bool spec = h->use_spec();
-      *h->h_status = DevStatus{0ull, INT_MAX, INT_MAX};
+      for (int i = 0; i < kCertSlots; ++i) h->h_status->cert_bits[i] = 0ull;
+      h->h_status->bad_seg = INT_MAX;
+      h->h_status->pivot_seg = INT_MAX;
       CUDA_TRY(cudaMemcpyAsync(h->d_status.p, h->h_status, sizeof(DevStatus), cudaMemcpyHostToDevice, s));
       if (timing) CUDA_TRY(cudaEventRecord(h->ev[0], s));
       h->tri.launches = 0;
@@ -808,7 +811,8 @@ int psg_solve(const psg_handle* hc, const double* f, double* x, int on_device, v
       CUDA_TRY(cudaMemcpyAsync(h->h_status, h->d_status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
       CUDA_TRY(cudaStreamSynchronize(s));
       const DevStatus st = *h->h_status;
-      cert = bits_to_double(st.cert_bits);
+      cert = 0.0;
+      for (int i = 0; i < kCertSlots; ++i) cert = std::max(cert, bits_to_double(st.cert_bits[i]));
       const bool bad = st.bad_seg != INT_MAX || st.pivot_seg != INT_MAX;
       if (!bad && cert <= h->cert_tol) {
         spec_used = spec;
@@ -923,6 +927,20 @@ int psg_solve_reduced(const psg_handle* hc, const double* rhs, double* x, int on
   } catch (const Fail& f_) {
     return set_err(err, errlen, f_.code, f_.msg);
   }
+}
+
+// Debug/inspection: copy an internal buffer to the host.  what = 0: speculative
+// weight rows (nsep x 68), 1: speculative Tdiag (nsep).  Returns the count.
+long psg_debug_buffer(const psg_handle* hc, int what, double* out, long cap) {
+  psg_handle* h = const_cast<psg_handle*>(hc);
+  std::lock_guard<std::mutex> g(h->mu);
+  if (cudaEventSynchronize(h->ev_done) != cudaSuccess) return -1;
+  const DevBuf<double>& b = what == 0 ? h->tri.wts : h->tri.Tdiag;
+  const long nsep = h->tri.S0.nseg - 1;
+  const long cnt = what == 0 ? nsep * kWRow : nsep;
+  if (!b.p || cnt > cap) return -cnt;
+  if (cudaMemcpy(out, b.p, sizeof(double) * cnt, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  return cnt;
 }
 
 int psg_matvec(const psg_desc* A, const double* x, double* y, int on_device, void* stream, char* err, size_t errlen) {

@@ -28,11 +28,18 @@ __device__ __forceinline__ double row_at(const RowArr& X, long r) {
   return (r >= X.lo && r < X.hi) ? __ldg(X.p + r) : 0.0;
 }
 
-// Device status shared by all kernels of one solve.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Device status shared by all kernels of one solve.  The certificate max is
+// spread over kCertSlots words (by block index) to keep same-address atomic
+// traffic low when every CTA reports; the host takes the max of the slots.
+constexpr int kCertSlots = 32;
 struct DevStatus {
-  unsigned long long cert_bits;  // max componentwise backward error (double bits, >= 0)
-  int bad_seg;                   // lowest segment with a non-finite solution value (INT_MAX: none)
-  int pivot_seg;                 // lowest segment whose own elimination hit a zero/non-finite pivot
+  unsigned long long cert_bits[kCertSlots];  // max componentwise backward error (double bits, >= 0)
+  int bad_seg;                               // lowest segment with a non-finite solution value (INT_MAX: none)
+  int pivot_seg;                             // lowest segment whose own elimination hit a zero/non-finite pivot
 };
 
 __device__ __forceinline__ void status_nonfinite(DevStatus* st, int seg) { atomicMin(&st->bad_seg, seg); }
@@ -40,16 +47,22 @@ __device__ __forceinline__ void status_pivot(DevStatus* st, int seg) { atomicMin
 
 __device__ __forceinline__ void status_cert(DevStatus* st, double w) {
   if (!(w <= 1.0e300)) w = __longlong_as_double(0x7ff0000000000000ll);  // NaN/huge -> +inf
-  atomicMax(&st->cert_bits, (unsigned long long)__double_as_longlong(w));
+  atomicMax(&st->cert_bits[blockIdx.x % kCertSlots], (unsigned long long)__double_as_longlong(w));
+}
+
+// cp.async (LDGSTS) 8-byte copy global -> shared, no register staging.
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------
 // mbarrier + bulk async copy (TMA engine, non-tensor form)
 // ---------------------------------------------------------------------------
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));

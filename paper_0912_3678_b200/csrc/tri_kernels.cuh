@@ -203,108 +203,100 @@ __device__ __forceinline__ double warp_tri_pcr(double lo, double di, double up, 
   return r;
 }
 
-// Weight rows: wts[j * kWRow + i], i < 32: -a_t v_i / Tdiag (v = last row of
-// the inverse of segment j's trailing block), 32 <= i < 64: -c_t w_{i-32} /
-// Tdiag (w = first row of the inverse of segment j+1's leading block),
-// i = 64: 1 / Tdiag.  With the top-down sweep d_k = b_k - l_k c_{k-1},
-// l_k = a_k / d_{k-1} of the trailing block, v_31 = 1/d_31 and
-// v_i = -l_{i+1} v_{i+1}; with the bottom-up sweep e_k = b_k - mu_k a_{k+1},
-// mu_k = c_k / e_{k+1} of the leading block, w_0 = 1/e_0 and
-// w_i = -mu_{i-1} w_{i-1}.
-constexpr int kWRow = 66;  // 64 weights + 1/Tdiag + pad (528 B, 16-byte multiple)
-constexpr int kFacWarps = 1;
-constexpr int kFacPitch = 33;  // [row][separator] tiles padded to 33 columns
+// Weight row of separator j (kWRow doubles):
+//   [0, 32)  -a_t v_i / Tdiag   v = last row of the inverse of segment j's trailing 32-row block
+//   [32, 64) -c_t w_i / Tdiag   w = first row of the inverse of segment j+1's leading block
+//   64: 1/Tdiag   65: Tdiag   66: kR = a_t c_{t-1} v_31   67: kL = c_t a_{t+1} w_0
+// (Tdiag = b_t - kR - kL).  Trailing block: top-down sweep d_k = b_k - l_k c_{k-1},
+// l_k = a_k / d_{k-1}, v_31 = 1/d_31, v_i = -l_{i+1} v_{i+1}.  Leading block:
+// bottom-up sweep e_k = b_k - mu_k a_{k+1}, mu_k = c_k / e_{k+1}, w_0 = 1/e_0,
+// w_i = -mu_{i-1} w_{i-1}.  Both are the same recurrence read in opposite row
+// orders, which is how one warp runs them on its two half-warps at once.
+constexpr int kWRow = 68;
+constexpr int kFacSeps = 16;             // separators per warp (one per half-warp lane pair)
+constexpr int kWin = 2 * kHalo + 1;      // window rows t-32 .. t+32
+constexpr int kFacPitch = kFacSeps + 1;  // [row][separator] tile pitch (odd: conflict-free)
 
-// One warp = 32 consecutive separators.  The 32-row windows are loaded
-// coalesced (lane = row), transposed through shared memory so that lane =
-// separator for the sequential sweeps, and the weight rows go back through
-// shared memory to one TMA bulk store.
-__global__ void __launch_bounds__(32 * kFacWarps) tri_spec_factor_kernel(TriRows A, SegMap S, double* __restrict__ wts,
-                                                                         double* __restrict__ Tdiag) {
+__global__ void __launch_bounds__(32) tri_spec_factor_kernel(TriRows A, SegMap S, double* __restrict__ wts,
+                                                             double* __restrict__ Tdiag) {
   constexpr unsigned FULL = 0xffffffffu;
-  __shared__ __align__(16) double tile[kFacWarps][3][kHalo * kFacPitch];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __shared__ __align__(16) double tile[3][kWin * kFacPitch];
+  const int lane = threadIdx.x;
   const int nsep = S.nseg - 1;
-  const int j0 = (blockIdx.x * kFacWarps + wid) * 32;
-  if (j0 >= nsep) return;
-  const int nj = min(32, nsep - j0);
-  double* tA = tile[wid][0];
-  double* tB = tile[wid][1];
-  double* tC = tile[wid][2];
-  long tme;  // this lane's separator row
+  const int j0 = blockIdx.x * kFacSeps;
+  const int nj = min(kFacSeps, nsep - j0);
+  const int jj = lane & (kFacSeps - 1);
+  long tme;
   {
     long s0;
     int L0;
-    seg_of(S, min(j0 + lane, nsep - 1), s0, L0);
+    seg_of(S, min(j0 + jj, nsep - 1), s0, L0);
     tme = s0 + L0;
   }
-  // ---- trailing block of segment j: rows t-32+k (coupling to row t-33 dropped)
-#pragma unroll 4
-  for (int jj = 0; jj < 32; ++jj) {
-    const long t = __shfl_sync(FULL, tme, jj);
-    const long r = t - kHalo + lane;
-    tA[lane * kFacPitch + jj] = row_at(A.a, r);
-    tB[lane * kFacPitch + jj] = row_at(A.b, r);
-    tC[lane * kFacPitch + jj] = row_at(A.c, r);
+  // ---- windows -> shared, transposed ([row][separator]), all copies in flight
+#pragma unroll 1
+  for (int q = 0; q < kFacSeps; ++q) {
+    const long t = __shfl_sync(FULL, tme, q);
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      const int k = ch * 32 + lane;
+      if (k < kWin) {
+        const long r = t - kHalo + k;
+        cp_async8(&tile[0][k * kFacPitch + q], A.a.p + r);
+        cp_async8(&tile[1][k * kFacPitch + q], A.b.p + r);
+        cp_async8(&tile[2][k * kFacPitch + q], A.c.p + r);
+      }
+    }
   }
+  cp_async_wait_all();
   __syncwarp();
+  // ---- one sweep per lane: lanes < 16 trailing block (rows 0..31, downwards in
+  //      the matrix = upwards in k), lanes >= 16 leading block (rows 64..33)
+  const bool trail = lane < kFacSeps;
+  const double* Nm = trail ? tile[0] : tile[2];  // multiplier numerator (a | c)
+  const double* Qc = trail ? tile[2] : tile[0];  // coupling to the previous row (c | a)
+  const double* Bd = tile[1];
+  const int w0r = trail ? 0 : kWin - 1;
+  const int dw = trail ? kFacPitch : -kFacPitch;
+  int off = w0r * kFacPitch + jj;
+  double piv = Bd[off];
+  double qprev = Qc[off];
   double m[kHalo];
-  double d = tB[lane];
-  double cprev = tC[lane];
 #pragma unroll
   for (int k = 1; k < kHalo; ++k) {
-    const double l = tA[k * kFacPitch + lane] * fast_rcp(d);
+    off += dw;
+    const double l = Nm[off] * fast_rcp(piv);
     m[k] = l;
-    d = fma(-l, cprev, tB[k * kFacPitch + lane]);
-    cprev = tC[k * kFacPitch + lane];
+    piv = fma(-l, qprev, Bd[off]);
+    qprev = Qc[off];
   }
-  const double v31 = fast_rcp(d);
+  const double u31 = fast_rcp(piv);  // v_31 (trailing) or w_0 (leading)
+  const double other = __shfl_xor_sync(FULL, u31, kFacSeps);
+  const double v31 = trail ? u31 : other, w0 = trail ? other : u31;
+  const int ts = kHalo * kFacPitch + jj;  // separator row t in the tile
+  const double at = tile[0][ts], bt = tile[1][ts], ct = tile[2][ts];
+  const double kR = at * tile[2][ts - kFacPitch] * v31;
+  const double kL = ct * tile[0][ts + kFacPitch] * w0;
+  const double td = b_minus(bt, kR, kL);
+  const double it = 1.0 / td;
   __syncwarp();
-  // ---- leading block of segment j+1: rows t+1+k (coupling to row t+33 dropped)
-#pragma unroll 4
-  for (int jj = 0; jj < 32; ++jj) {
-    const long t = __shfl_sync(FULL, tme, jj);
-    const long r = t + 1 + lane;
-    tA[lane * kFacPitch + jj] = row_at(A.a, r);
-    tB[lane * kFacPitch + jj] = row_at(A.b, r);
-    tC[lane * kFacPitch + jj] = row_at(A.c, r);
-  }
-  __syncwarp();
-  double mu[kHalo];
-  double e = tB[(kHalo - 1) * kFacPitch + lane];
-  double anext = tA[(kHalo - 1) * kFacPitch + lane];
+  // ---- weight rows -> shared (reusing the tile) -> one bulk store
+  double* wout = &tile[0][0];
+  const double sc = (trail ? -at : -ct) * it;
+  double u = u31;
+  wout[jj * kWRow + (trail ? kHalo - 1 : kHalo)] = sc * u;
 #pragma unroll
   for (int k = kHalo - 2; k >= 0; --k) {
-    const double mk = tC[k * kFacPitch + lane] * fast_rcp(e);
-    mu[k] = mk;
-    e = fma(-mk, anext, tB[k * kFacPitch + lane]);
-    anext = tA[k * kFacPitch + lane];
+    u = -m[k + 1] * u;
+    wout[jj * kWRow + (trail ? k : 2 * kHalo - 1 - k)] = sc * u;
   }
-  const double w0 = fast_rcp(e);
-  const double at = row_at(A.a, tme), bt = row_at(A.b, tme), ct = row_at(A.c, tme);
-  const double td = b_minus(bt, at * row_at(A.c, tme - 1) * v31, ct * row_at(A.a, tme + 1) * w0);
-  const double it = 1.0 / td;
-  if (lane < nj) Tdiag[j0 + lane] = td;
-  __syncwarp();
-  // ---- weight rows -> shared (reusing the tiles: 32 x kWRow doubles) -> one bulk store
-  double* wout = tA;  // needs 32 * 66 = 2112 doubles; tA..tC hold 3 * 1056 contiguous
-  const double sa = -at * it, sc = -ct * it;
-  double v = v31;
-  wout[lane * kWRow + kHalo - 1] = sa * v;
-#pragma unroll
-  for (int i = kHalo - 2; i >= 0; --i) {
-    v = -m[i + 1] * v;
-    wout[lane * kWRow + i] = sa * v;
+  if (trail) {
+    wout[jj * kWRow + 64] = it;
+    wout[jj * kWRow + 65] = td;
+    wout[jj * kWRow + 66] = kR;
+    wout[jj * kWRow + 67] = kL;
+    if (jj < nj) Tdiag[j0 + jj] = td;
   }
-  double w = w0;
-  wout[lane * kWRow + kHalo] = sc * w;
-#pragma unroll
-  for (int i = 1; i < kHalo; ++i) {
-    w = -mu[i - 1] * w;
-    wout[lane * kWRow + kHalo + i] = sc * w;
-  }
-  wout[lane * kWRow + 2 * kHalo] = it;
-  wout[lane * kWRow + 2 * kHalo + 1] = 0.0;
   fence_proxy_async_smem();
   __syncwarp();
   if (lane == 0) {
@@ -313,16 +305,51 @@ __global__ void __launch_bounds__(32 * kFacWarps) tri_spec_factor_kernel(TriRows
   }
 }
 
-// x_t = f_t / Tdiag + sum_i W[i] f(t-32+i) + sum_i W[32+i] f(t+1+i), evaluated by
-// one warp with a fixed lane order and reduction tree, so the two CTAs that
-// need the same separator get bit-identical values.  fw points at the
-// shared-memory f row of t-32; W at the weight row in shared memory.
-__device__ __forceinline__ double spec_sep_value(const double* fw, const double* W) {
+// Speculative separator values (phase 1 + phase 2 fused): with the weight row
+// W of separator j and the f rows t-32 .. t+32 around its row t,
+//   x_t = f_t / Tdiag + sum_i W[i] f(t-32+i) + sum_i W[32+i] f(t+1+i).
+// One warp evaluates kSepPerWarp separators; all their loads are issued
+// before the first reduction so each warp keeps ~16 coalesced 256-byte
+// requests in flight.
+constexpr int kSepPerWarp = 4;
+__global__ void __launch_bounds__(256) tri_spec_sep_kernel(RowArr F, SegMap S, const double* __restrict__ wts,
+                                                            double* __restrict__ xsep) {
   const int lane = threadIdx.x & 31;
-  double acc = fma(W[lane], fw[lane], W[kHalo + lane] * fw[kHalo + 1 + lane]);
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nsep = S.nseg - 1;
+  const int j0 = warp * kSepPerWarp;
+  if (j0 >= nsep) return;
+  double w1[kSepPerWarp], w2[kSepPerWarp], f1[kSepPerWarp], f2[kSepPerWarp];
+  long tt[kSepPerWarp];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  return fma(fw[kHalo], W[2 * kHalo], acc);
+  for (int k = 0; k < kSepPerWarp; ++k) {
+    const int j = min(j0 + k, nsep - 1);
+    long s0;
+    int L0;
+    seg_of(S, j, s0, L0);
+    tt[k] = s0 + L0;
+    const double* W = wts + (long)j * kWRow;
+    w1[k] = __ldg(W + lane);
+    w2[k] = __ldg(W + kHalo + lane);
+    f1[k] = row_at(F, tt[k] - kHalo + lane);
+    f2[k] = row_at(F, tt[k] + 1 + lane);
+  }
+  double mine = 0.0, ft = 0.0, it = 0.0;
+  if (lane < kSepPerWarp && j0 + lane < nsep) {
+    long s0;
+    int L0;
+    seg_of(S, j0 + lane, s0, L0);
+    ft = row_at(F, s0 + L0);
+    it = __ldg(wts + (long)(j0 + lane) * kWRow + 2 * kHalo);
+  }
+#pragma unroll
+  for (int k = 0; k < kSepPerWarp; ++k) {
+    double acc = fma(w1[k], f1[k], w2[k] * f2[k]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == k) mine = acc;
+  }
+  if (lane < kSepPerWarp && j0 + lane < nsep) xsep[j0 + lane] = fma(ft, it, mine);
 }
 
 // ----------------------------------------------------------------------------
@@ -342,31 +369,27 @@ struct TriSolveArgs {
   TriRows A;
   RowArr F;
   SegMap S;
-  const double* xsep;  // nseg-1 separator values (exact path; NULL when nseg == 1)
-  const double* wts;   // speculative path: weight rows (kWRow per separator)
+  const double* xsep;  // nseg-1 separator values (NULL when nseg == 1)
   double* x;           // output, row r at x[r]
-  double2* yends;      // per segment (y_first, y_last) for the certificate (NULL: skip)
+  double4* crec;       // per-segment certificate record (NULL: skip), see tri_cert_kernel
   DevStatus* status;
 };
 
 template <int M>
 struct TriWarpSmem {
-  static constexpr int CAP = 32 * M;                // body rows per segment
-  static constexpr int ROW = CAP + 6;               // + both separator rows + staging slack, even
-  static constexpr int ROWF = CAP + 2 * kHalo + 6;  // f also carries 32 rows past each separator
-  static constexpr int WROW = 2 * kWRow + 4;        // the two weight rows (+ slack)
-  static constexpr int BYTES = (3 * ROW + ROWF + WROW) * 8;
+  static constexpr int CAP = 32 * M;   // body rows per segment
+  static constexpr int ROW = CAP + 6;  // + both separator rows + staging slack, even
+  static constexpr int BYTES = 4 * ROW * 8;
 };
 
-template <int M, bool SPEC>
+template <int M>
 __global__ void __launch_bounds__(32) tri_segment_solve_kernel(TriSolveArgs args) {
   static_assert(M % 2 == 1 && M >= 3, "M must be odd and >= 3");
   constexpr int ROW = TriWarpSmem<M>::ROW;
-  constexpr int ROWF = TriWarpSmem<M>::ROWF;
   constexpr unsigned FULL = 0xffffffffu;
-  constexpr int FH = SPEC ? kHalo + 1 : 1;  // f rows staged before/after the body
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t bar;
+  __shared__ double sepv[4];
   const int lane = threadIdx.x;
   const int seg = blockIdx.x;
   long s;
@@ -375,22 +398,14 @@ __global__ void __launch_bounds__(32) tri_segment_solve_kernel(TriSolveArgs args
   const int nseg = args.S.nseg;
   const bool has_l = seg > 0, has_r = seg < nseg - 1;
 
-  // ---- staging: lanes 0..3 (a, b, c, f) and 4 (weight rows) issue one bulk copy each
-  const long w0 = (long)(has_l ? seg - 1 : seg) * kWRow;
-  const int nw = SPEC ? (int)has_l + (int)has_r : 0;
-  RowArr X = lane == 0 ? args.A.a : lane == 1 ? args.A.b : lane == 2 ? args.A.c : args.F;
-  long lo = lane == 3 ? s - FH : s - 1, hi = lane == 3 ? s + L + FH : s + L + 1;
-  if (SPEC && lane == 4) {
-    X = make_rows(args.wts, 0, (int)(w0 + nw * kWRow));
-    lo = w0;
-    hi = w0 + nw * kWRow;
-  }
-  double* const base = smem + (lane < 4 ? lane * ROW : 3 * ROW + ROWF);
-  const int nstage = SPEC ? 5 : 4;
-  if (lane == 0) mbar_init(&bar, nstage);
+  // ---- staging: lanes 0..3 issue one bulk copy each (a, b, c, f rows s-1 .. s+L)
+  const RowArr X = lane == 0 ? args.A.a : lane == 1 ? args.A.b : lane == 2 ? args.A.c : args.F;
+  const long lo = s - 1, hi = s + L + 1;
+  double* const base = smem + (lane & 3) * ROW;
+  if (lane == 0) mbar_init(&bar, 4);
   __syncwarp();
   int shift = 0;
-  if (lane < nstage) {
+  if (lane < 4) {
     uint32_t tx = 0;
     shift = stage_issue(X, lo, hi, base, &bar, &tx);
     mbar_arrive_expect_tx(&bar, tx);
@@ -399,41 +414,36 @@ __global__ void __launch_bounds__(32) tri_segment_solve_kernel(TriSolveArgs args
   double* sA = smem + 0 * ROW + 2 + __shfl_sync(FULL, shift, 0);
   double* sB = smem + 1 * ROW + 2 + __shfl_sync(FULL, shift, 1);
   double* sC = smem + 2 * ROW + 2 + __shfl_sync(FULL, shift, 2);
-  double* sF = smem + 3 * ROW + 1 + FH + __shfl_sync(FULL, shift, 3);
-  const double* sW = smem + 3 * ROW + ROWF + 1 + __shfl_sync(FULL, shift, 4);
-  double xl = 0.0, xr = 0.0;
-  if (!SPEC) {
-    xl = has_l ? args.xsep[seg - 1] : 0.0;
-    xr = has_r ? args.xsep[seg] : 0.0;
-  }
+  double* sF = smem + 3 * ROW + 2 + __shfl_sync(FULL, shift, 3);
+  const double xl = has_l ? args.xsep[seg - 1] : 0.0;
+  const double xr = has_r ? args.xsep[seg] : 0.0;
   mbar_wait(&bar, 0);
   if (lane < 4) stage_fixup(X, lo, hi, base + 1 + shift);
   __syncwarp();
-  // separator coupling terms: a_s x_l enters row 0, c x_r row L-1 (folded in
-  // after the forward sweep, which is linear in those two rhs entries)
-  const double cl = -sA[0], cr = -sC[L - 1];
-  // pad to 32*M rows with decoupled identity rows; their rhs keeps the staged
-  // f rows past the body (finite; needed for x_r) and is zero beyond them
-  for (int q = L + lane; q < 32 * M; q += 32) {
+  if (lane == 0) {
+    sepv[0] = sA[L];  // separator-row entries for the certificate record
+    sepv[1] = sB[L];
+    sepv[2] = sF[L];
+    sepv[3] = sC[-1];
+    sF[0] = fma(-sA[0], xl, sF[0]);  // fold the separator couplings into the rhs
+    sA[0] = 0.0;
+    sF[L - 1] = fma(-sC[L - 1], xr, sF[L - 1]);
+    sC[L - 1] = 0.0;
+  }
+  for (int q = L + lane; q < 32 * M; q += 32) {  // decoupled identity padding
     sA[q] = 0.0;
     sB[q] = 1.0;
     sC[q] = 0.0;
-    if (q >= L + FH) sF[q] = 0.0;
-  }
-  if (lane == 0) {  // row 0 / row L-1 couple to the separators, not to the neighbours
-    sA[0] = 0.0;
-    sC[L - 1] = 0.0;
+    sF[q] = 0.0;
   }
   __syncwarp();
 
   // ---- chunk elimination: every chunk row j ends as
   //      ap[j] y_first + y_j + cp[j] y_last = dp[j]
+  //      (row 0: ap y_{prev last} + y_0 + cp y_last; row M-1: ap y_0 + y_{M-1} + cp y_{next first})
   double ap[M], cp[M], dp[M];
   const int q0 = lane * M;
-  const int jL = L - 1 - q0;  // chunk position of row L-1 (valid when 0 <= jL < M)
-  double rsum = 0.0;          // sum |pivot reciprocals|: non-finite <=> a pivot of this body vanished
-  double rL = 0.0;            // pivot reciprocal of row L-1 (for the x_r fold)
-  double r0 = 0.0;            // pivot reciprocal of chunk row 0 (for the x_l fold, lane 0)
+  double rsum = 0.0;  // sum of |pivot reciprocals|: non-finite <=> a pivot of this body vanished
 #pragma unroll
   for (int j = 0; j < M; ++j) {
     const double a = sA[q0 + j], b = sB[q0 + j], c = sC[q0 + j], f = sF[q0 + j];
@@ -450,20 +460,7 @@ __global__ void __launch_bounds__(32) tri_segment_solve_kernel(TriSolveArgs args
       cp[j] = r * c;
     }
     rsum += fabs(r);
-    if (j == jL) rL = r;
-    if (j == 0) r0 = r;
   }
-  if (SPEC) {  // separator values (phases 1+2 fused), overlapping the forward sweep's latency
-    if (has_l) xl = spec_sep_value(sF - 1 - kHalo, sW);
-    if (has_r) xr = spec_sep_value(sF + L - kHalo, sW + (has_l ? kWRow : 0));
-  }
-  // fold the separator terms: the forward sweep never feeds chunk row 0's rhs or
-  // row L-1's rhs into another real row (row 0 enters only the final row-0
-  // step, row L-1 only identity padding), so only their own dp entry changes
-  if (lane == 0) dp[0] = fma(cl * xl, r0, dp[0]);
-#pragma unroll
-  for (int j = 0; j < M; ++j)
-    if (j == jL) dp[j] = fma(cr * xr, rL, dp[j]);
 #pragma unroll
   for (int j = M - 3; j >= 1; --j) {
     dp[j] = fma(-cp[j], dp[j + 1], dp[j]);
@@ -547,7 +544,11 @@ __global__ void __launch_bounds__(32) tri_segment_solve_kernel(TriSolveArgs args
   }
   if (lane == 3) {
     if (has_r) args.x[s + L] = xr;
-    if (args.yends) args.yends[seg] = make_double2(sF[0], sF[L - 1]);
+    // certificate record: right separator t = s+L: (a_t y_{t-1}, b_t x_t, f_t),
+    // left separator: c_{s-1} y_s
+    if (args.crec)
+      args.crec[seg] = make_double4(has_r ? sepv[0] * sF[L - 1] : 0.0, has_r ? sepv[1] * xr : 0.0,
+                                    has_r ? sepv[2] : 0.0, has_l ? sepv[3] * sF[0] : 0.0);
   }
 }
 
@@ -557,20 +558,13 @@ __global__ void __launch_bounds__(32) tri_segment_solve_kernel(TriSolveArgs args
 // with the body values y from K3.  The body rows are solved exactly given
 // the separators, so this bounds the error the speculative interface let in.
 // ----------------------------------------------------------------------------
-__global__ void tri_cert_kernel(TriRows A, RowArr F, SegMap S, const double* __restrict__ x,
-                                const double2* __restrict__ yends, DevStatus* st) {
+__global__ void tri_cert_kernel(int nsep, const double4* __restrict__ crec, DevStatus* st) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   double w = 0.0;
-  if (j < S.nseg - 1) {
-    long s0;
-    int L0;
-    seg_of(S, j, s0, L0);
-    const long t = s0 + L0;
-    const double yl = yends[j].y, yr = yends[j + 1].x, xt = x[t];
-    const double t1 = row_at(A.a, t) * yl, t2 = row_at(A.b, t) * xt, t3 = row_at(A.c, t) * yr;
-    const double f = row_at(F, t);
-    const double r = ((f - t1) - t2) - t3;
-    const double den = fabs(f) + fabs(t1) + fabs(t2) + fabs(t3);
+  if (j < nsep) {
+    const double4 R = crec[j], N = crec[j + 1];
+    const double r = ((R.z - R.x) - R.y) - N.w;  // f_t - a_t y_{t-1} - b_t x_t - c_t y_{t+1}
+    const double den = fabs(R.z) + fabs(R.x) + fabs(R.y) + fabs(N.w);
     w = den > 0.0 ? fabs(r) / den : (r != 0.0 ? __longlong_as_double(0x7ff0000000000000ll) : 0.0);
     if (!(w <= 1.0e300)) w = __longlong_as_double(0x7ff0000000000000ll);
   }
