@@ -173,6 +173,25 @@ class Clocks:
 
 
 # ---------------------------------------------------------------------------
+# multi-rank aggregation: max over ranks of the device-timed total, sum of the
+# units all ranks processed (weak scaling: each rank owns its own system)
+# ---------------------------------------------------------------------------
+def aggregate(ms_total_local, units_local, steps, dist=None, device="cpu"):
+    import torch
+    t = torch.tensor([ms_total_local, float(units_local)], dtype=torch.float64, device=device)
+    if dist is not None:
+        mx = t[:1].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = t[1:].clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        ms_total, units = float(mx.item()), float(sm.item())
+    else:
+        ms_total, units = float(t[0].item()), float(t[1].item())
+    ms_step = ms_total / steps
+    return ms_step, units, units / (ms_step / 1e3)
+
+
+# ---------------------------------------------------------------------------
 # our GPU path
 # ---------------------------------------------------------------------------
 def impl_ours(args, rank, world, local_rank):
@@ -221,10 +240,7 @@ def impl_ours(args, rank, world, local_rank):
     ms_total = ev0.elapsed_time(ev1)
     clk = clocks.stop() if clocks else None
 
-    t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_step = float(t.item()) / args.steps
+    ms_step, units, _ = aggregate(ms_total, n, args.steps, dist if world > 1 else None, dev)
 
     # correctness of the timed run (outside the timed region)
     res = psg.residual(A, x, f)
@@ -290,7 +306,7 @@ def impl_ours(args, rank, world, local_rank):
         except Exception as e:  # baseline is informative only
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable", "sample": str(e)}
 
-    value = world * n / (ms_step / 1e3)
+    value = units / (ms_step / 1e3)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",

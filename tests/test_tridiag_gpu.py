@@ -182,3 +182,20 @@ def test_zero_pivot_reports_partition(cuda):
         psg.solve(F, _dev(cuda, np.ones(n)))
     assert ei.value.code == psg.Errc.ZeroPivot
     assert "partition 2" in str(ei.value)
+
+
+import glob as _glob
+import os as _os
+
+_GOLD = sorted(_glob.glob(_os.path.join(_os.path.dirname(__file__), "golden", "cfg[01]_*.npz")))
+
+
+@pytest.mark.parametrize("path", _GOLD, ids=[_os.path.basename(c)[:-4] for c in _GOLD])
+def test_cuda_matches_reference_golden(cuda, path):
+    g = np.load(path)
+    A, f = O.generate_config(int(g["cfg"]), int(g["size"]), int(g["seed"]))
+    got, st, F = _solve_gpu(cuda, A, int(g["p"]), f)
+    assert O.rel_err(got, g["x"]) <= 1e-12        # vs reference parallel_factor+solve
+    assert O.rel_err(got, g["x_seq"]) <= 1e-12    # vs reference solve_sequential
+    assert O.residual(A, got, f) <= 1e-13
+    assert F.q == int(g["q"]) and F.dim == int(g["dim"])
