@@ -83,6 +83,7 @@ def lib():
         L.or_config_shape.argtypes = [C.c_int, C.c_int] + [C.POINTER(C.c_int)] * 5 + \
             [C.POINTER(C.c_size_t), C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.or_generate_config.argtypes = [C.c_int, C.c_int, C.c_uint64, _dp, _dp, _dp]
+        L.or_generate_random.argtypes = [C.c_int] * 5 + [C.c_uint64, C.c_double, _dp, _dp]
         L.or_body_entry_count.argtypes = [C.c_int] * 5
         L.or_body_entry_count.restype = C.c_size_t
         _lib = L
@@ -116,6 +117,8 @@ def ref():
         R.ref_residual.argtypes = [C.c_void_p, _dp, _dp, C.c_size_t]
         R.ref_residual.restype = C.c_double
         R.ref_plan.argtypes = [C.c_void_p, C.c_int] + [C.POINTER(C.c_int)] * 5 + [C.c_char_p, C.c_size_t]
+        R.ref_generate_random.argtypes = [C.c_int] * 5 + [C.c_uint64, C.c_double, _dp, _dp, C.c_char_p,
+                                                          C.c_size_t]
         _ref = R
     return _ref
 
@@ -176,6 +179,22 @@ def generate_config(cfg: int, size: int, seed: int):
     A = Matrix(sh["kind"], sh["n"], sh["m"], sh["s"], sh["r"], data, corner,
                sh["corner_rows"], sh["corner_cols"])
     return A, f
+
+
+def generate_random(kind: int, n: int, m: int, s: int, r: int, seed: int, dominance: float):
+    """Restated generate_random (src/structmat.cpp:282-333) -> Matrix."""
+    cnt = lib().or_body_entry_count(kind, n, m, s, r)
+    data = np.empty(cnt, np.float64)
+    corner = np.empty(m * m, np.float64) if kind == BABD else None
+    rc = lib().or_generate_random(kind, n, m, s, r, seed, dominance, _ptr(data), _ptr(corner))
+    if rc:
+        raise OracleError(rc, "generate_random failed")
+    return Matrix(kind, n, m, s, r, data, corner, m if kind == BABD else 0, m if kind == BABD else 0)
+
+
+def random_vector(n: int, seed: int):
+    """tests/oracles.hpp:42-47: SplitMix64(seed, 77) draws."""
+    return np.array([lib().or_splitmix_unit(seed, 77, k + 1) for k in range(n)])
 
 
 def parallel_solve(A: Matrix, p: int, f: np.ndarray, strategy: int = LU):
@@ -340,6 +359,17 @@ class RefFact:
         if rc:
             raise OracleError(rc, err.value.decode())
         return x, ops.value, ph
+
+
+def ref_generate_random(kind, n, m, s, r, seed, dominance):
+    cnt = lib().or_body_entry_count(kind, n, m, s, r)
+    data = np.empty(cnt, np.float64)
+    corner = np.empty(m * m, np.float64) if kind == BABD else None
+    err = C.create_string_buffer(256)
+    rc = ref().ref_generate_random(kind, n, m, s, r, seed, dominance, _ptr(data), _ptr(corner), err, 256)
+    if rc:
+        raise OracleError(rc, err.value.decode())
+    return data, corner
 
 
 def ref_set_threads(t: int) -> int:

@@ -1041,3 +1041,55 @@ int or_generate_config(int cfg, int size, uint64_t seed, double* data, double* c
   }
   return 0;
 }
+
+/* generate_random (src/structmat.cpp:282-333): draws in storage order from
+ * SplitMix64(seed), Babd corner m x m, then diagonal rescaled to
+ * +-dominance * max(off-row |sum|, 1).  Babd here also accepts s = m, r = 0. */
+int or_generate_random(int kind, int n, int m, int s, int r, uint64_t seed, double dominance, double* data,
+                       double* corner) {
+  if (dominance < 0) return 1 + E_InvalidParameter;
+  const size_t count = or_body_entry_count(kind, n, m, s, r);
+  uint64_t ctr = 0;
+  for (size_t e = 0; e < count; ++e) data[e] = or_splitmix_unit(seed, 0, ++ctr);
+  if (kind == OR_BABD)
+    for (int e = 0; e < m * m; ++e) corner[e] = or_splitmix_unit(seed, 0, ++ctr);
+  or_mat A = {kind, n, m, s, r, data, count, kind == OR_BABD ? corner : NULL, kind == OR_BABD ? m : 0,
+              kind == OR_BABD ? m : 0, NULL};
+  char err[128];
+  int rc = or_mat_prepare(&A, err, sizeof err);
+  if (rc) return rc;
+  if (dominance > 0.0) {
+    for (int i = 0; i < n; ++i) {
+      int j0, j1, k0, k1;
+      row_columns(&A, i, &j0, &j1, &k0, &k1);
+      double off = 0.0;
+      for (int j = j0; j < j1; ++j)
+        if (j != i) off += fabs(or_at(&A, i, j));
+      for (int j = k0; j < k1; ++j)
+        if (j != i) off += fabs(or_at(&A, i, j));
+      double mag = dominance * (off > 1.0 ? off : 1.0);
+      double old = or_at(&A, i, i);
+      double val = old < 0 ? -mag : mag;
+      size_t pos;
+      switch (kind) {
+        case OR_BANDED: pos = band_offset(n, s, 0) + (size_t)i; break;
+        case OR_BLOCKTRI: {
+          int b = i / m;
+          size_t offr = b == 0 ? 0 : (size_t)(3 * b - 1) * m * m;
+          int blk = b > 0 ? 1 : 0;
+          pos = offr + (size_t)blk * m * m + (size_t)(i - b * m) * m + (i - b * m);
+          break;
+        }
+        default: {
+          int b = i / m, c0, c1;
+          abd_span(n, m, s, r, b, &c0, &c1);
+          pos = A.abd_off[b] + (size_t)(i - b * m) * (c1 - c0) + (i - c0);
+          break;
+        }
+      }
+      data[pos] = val;
+    }
+  }
+  or_mat_release(&A);
+  return 0;
+}

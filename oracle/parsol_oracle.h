@@ -92,6 +92,10 @@ int or_config_shape(int cfg, int size, int* kind, int* n, int* m, int* s, int* r
 int or_generate_config(int cfg, int size, uint64_t seed, double* data, double* corner,
                        double* f);
 
+/* generate_random, src/structmat.cpp:282-333 (corner m x m for Babd). */
+int or_generate_random(int kind, int n, int m, int s, int r, uint64_t seed, double dominance, double* data,
+                       double* corner);
+
 #ifdef __cplusplus
 }
 #endif

@@ -148,6 +148,19 @@ double ref_residual(void* hm, const double* x, const double* f, size_t n) {
   return residual(static_cast<RefMat*>(hm)->A, xv, fv);
 }
 
+// generate_random (src/structmat.cpp:282-333) through the reference itself.
+int ref_generate_random(int kind, int n, int m, int s, int r, unsigned long long seed, double dominance,
+                        double* data, double* corner, char* err, size_t errlen) {
+  try {
+    StructuredMatrix A = generate_random(Kind(kind), n, m, s, r, seed, dominance);
+    std::memcpy(data, A.data.data(), sizeof(double) * A.data.size());
+    if (!A.corner.empty() && corner) std::memcpy(corner, A.corner.data(), sizeof(double) * A.corner.size());
+    return 0;
+  } catch (const std::exception& e) {
+    return report(e, err, errlen);
+  }
+}
+
 int ref_plan(void* hm, int p, int* body_begin, int* body_end, int* sep_start, int* sep_count,
              int* sep_size, char* err, size_t errlen) {
   try {

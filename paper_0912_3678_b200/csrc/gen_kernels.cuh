@@ -212,4 +212,30 @@ __global__ void residual_kernel(MatView A, const double* __restrict__ x, const d
   }
 }
 
+// r = f - A x (no FMA, ascending columns) and out[0] = max|r| bits, out[1] = max|f| bits.
+__global__ void residual_vec_kernel(MatView A, const double* __restrict__ x, const double* __restrict__ f,
+                                    double* __restrict__ r, unsigned long long* out) {
+  double num = 0.0, den = 0.0;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < A.n; i += (long)gridDim.x * blockDim.x) {
+    const double ri = __dsub_rn(f[i], row_dot(A, i, x));
+    r[i] = ri;
+    double v = fabs(ri);
+    if (!(v <= 1.0e308)) v = __longlong_as_double(0x7ff0000000000000ll);
+    num = fmax(num, v);
+    den = fmax(den, fabs(f[i]));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    num = fmax(num, __shfl_xor_sync(0xffffffffu, num, o));
+    den = fmax(den, __shfl_xor_sync(0xffffffffu, den, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(out + 0, (unsigned long long)__double_as_longlong(num));
+    atomicMax(out + 1, (unsigned long long)__double_as_longlong(den));
+  }
+}
+
+__global__ void axpy_kernel(long n, const double* __restrict__ d, double* __restrict__ x) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) x[i] += d[i];
+}
+
 }  // namespace psg

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "../../include/psg.h"
+#include "gen_exact.cuh"
 #include "gen_kernels.cuh"
 #include "psg_common.cuh"
 #include "tri_kernels.cuh"
@@ -508,6 +509,204 @@ struct TriSolver {
   }
 };
 
+// ----------------------------------------------------------------------------
+// Generic exact solver (every kind): multi-level partition method over
+// structured views; the reduced matrix of each level is the next level's
+// StructuredMatrix (block tridiagonal, or ABD row layout + corner).
+// ----------------------------------------------------------------------------
+void envelope_of(int kind, int m, int s, int r, int& es, int& er) {  // scalar_envelope
+  if (kind == PSG_BANDED) {
+    es = s;
+    er = r;
+  } else if (kind == PSG_BLOCKTRI) {
+    es = er = 2 * m - 1;
+  } else {
+    es = m - 1 + s;
+    er = m - 1 + r;
+  }
+}
+
+struct GenLevel {
+  SMView A{};
+  int es = 0, er = 0, k = 0, p = 0, q = 0;
+  bool corner = false, direct = false;
+  const double* f = nullptr;
+  double* x = nullptr;
+  std::vector<GPart> hpart;
+  std::vector<int> hsep;
+  DevBuf<GPart> part;
+  DevBuf<int> sep;
+  DevBuf<double> blocks, kr, scratch;
+  DevBuf<double> Tdata, Tcorner, rhs_next, x_next;  // next level system
+  DevBuf<double> work;                              // direct solve scratch
+  int K = 0;                                        // direct: bordered tail size
+};
+
+constexpr int kGenDirectRows = 256;
+
+struct GenSolver {
+  std::vector<std::unique_ptr<GenLevel>> lv;
+  int launches = 0;
+
+  static Plan plan_of(const SMView& A, int p) {
+    psg_desc d{A.kind, A.n, A.m, A.s, A.r, nullptr, 0, nullptr, A.cr, A.cc, 1};
+    return make_plan(d, p);
+  }
+
+  void add_level(const SMView& A, int p_or_0) {
+    auto L = std::make_unique<GenLevel>();
+    L->A = A;
+    envelope_of(A.kind, A.m, A.s, A.r, L->es, L->er);
+    if (L->es + 1 + L->er > kGenMaxW) throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "band envelope too wide for the GPU path"};
+    if (p_or_0 == 0) {
+      L->direct = true;
+      L->K = 0;
+      if (A.kind == PSG_BABD) L->K = std::min(A.cc + L->es + L->er, A.n);
+      const long nb = A.n - L->K;
+      L->work.alloc((size_t)nb * (L->es + 1 + L->er) + (size_t)nb * L->K + (size_t)A.n + (size_t)L->K * L->K +
+                    (size_t)L->K + (size_t)A.n + 16);
+      lv.push_back(std::move(L));
+      return;
+    }
+    Plan P = plan_of(A, p_or_0);
+    L->p = p_or_0;
+    L->k = P.sep_size;
+    if (L->k > kGenMaxK) throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "separator block too large for the GPU path"};
+    L->corner = P.has_corner;
+    L->q = P.sep_count();
+    L->hpart.resize(P.p);
+    for (int i = 0; i < P.p; ++i) {
+      const int lsi = P.has_corner ? i : i - 1, rsi = P.has_corner ? i + 1 : i;
+      L->hpart[i] = GPart{P.body_begin(i), P.body_end(i) - P.body_begin(i), lsi >= 0 ? P.sep_start(lsi) : -1,
+                          rsi < P.sep_count() ? P.sep_start(rsi) : -1};
+    }
+    L->hsep.resize(L->q);
+    for (int j = 0; j < L->q; ++j) L->hsep[j] = P.sep_start(j);
+    L->part.alloc(P.p);
+    L->sep.alloc(L->q);
+    CUDA_TRY(cudaMemcpy(L->part.p, L->hpart.data(), sizeof(GPart) * P.p, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(L->sep.p, L->hsep.data(), sizeof(int) * L->q, cudaMemcpyHostToDevice));
+    const int kk = L->k * L->k;
+    L->blocks.alloc((size_t)P.p * 4 * kk);
+    L->kr.alloc((size_t)P.p * 2 * L->k);
+    L->scratch.alloc((size_t)A.n * (L->er + 2));
+    // next level: the reduced matrix as a structured matrix of q blocks of size k
+    const int q = L->q, k = L->k;
+    SMView T{};
+    T.m = k;
+    T.n = q * k;
+    if (!L->corner) {
+      T.kind = PSG_BLOCKTRI;
+      T.s = T.r = 1;
+      L->Tdata.alloc((size_t)(3 * q - 2) * kk);
+    } else {
+      T.kind = PSG_BABD;
+      T.s = T.r = k;
+      T.cr = T.cc = k;
+      L->Tdata.alloc((size_t)(q >= 2 ? 2 * 2 * kk + (size_t)(q - 2) * 3 * kk : kk));
+      L->Tcorner.alloc(kk);
+      T.corner = L->Tcorner.p;
+    }
+    T.data = L->Tdata.p;
+    L->rhs_next.alloc((size_t)q * k);
+    L->x_next.alloc((size_t)q * k);
+    lv.push_back(std::move(L));
+    GenLevel& cur = *lv.back();
+    // choose the next level's partition count: bodies of ~31 blocks, direct when small
+    const int pn = (long)T.n > kGenDirectRows ? std::max(2, q / 32) : 0;
+    (void)cur;
+    add_level(T, pn);
+  }
+
+  void build(const SMView& A0, int p) {
+    lv.clear();
+    add_level(A0, p);
+    // wire rhs/x of every level > 0
+    for (size_t l = 1; l < lv.size(); ++l) {
+      lv[l]->f = lv[l - 1]->rhs_next.p;
+      lv[l]->x = lv[l - 1]->x_next.p;
+    }
+  }
+
+  GenArgs args_of(GenLevel& L, DevStatus* st) {
+    GenArgs g{};
+    g.A = L.A;
+    g.part = L.part.p;
+    g.p = L.p;
+    g.k = L.k;
+    g.es = L.es;
+    g.er = L.er;
+    g.f = L.f;
+    g.has_corner = L.corner ? 1 : 0;
+    g.blocks = L.blocks.p;
+    g.kr = L.kr.p;
+    g.x = L.x;
+    g.scratch = L.scratch.p;
+    g.status = st;
+    return g;
+  }
+
+  void factor(cudaStream_t s) {
+    for (size_t l = 0; l + 1 < lv.size(); ++l) {
+      GenLevel& L = *lv[l];
+      GenArgs g = args_of(L, nullptr);
+      gen_ends_kernel<0><<<2 * L.p, 32, 0, s>>>(g);
+      LAUNCH_CHECK();
+      const long ent = (long)L.q * L.k * L.k;
+      gen_assemble_T_kernel<<<(int)((ent + 255) / 256), 256, 0, s>>>(g, L.Tdata.p, L.Tcorner.p);
+      LAUNCH_CHECK();
+      launches += 2;
+    }
+  }
+
+  void solve(const double* f0, double* x0, DevStatus* st, cudaStream_t s, cudaEvent_t* ev, size_t from = 0) {
+    lv[from]->f = f0;
+    lv[from]->x = x0;
+    for (size_t l = from; l + 1 < lv.size(); ++l) {
+      GenLevel& L = *lv[l];
+      GenArgs g = args_of(L, l == 0 ? st : nullptr);
+      gen_ends_kernel<1><<<2 * L.p, 32, 0, s>>>(g);
+      LAUNCH_CHECK();
+      const long ent = (long)L.q * L.k;
+      gen_assemble_rhs_kernel<<<(int)((ent + 255) / 256), 256, 0, s>>>(g, L.sep.p, L.rhs_next.p);
+      LAUNCH_CHECK();
+      launches += 2;
+      if (l == from && ev) CUDA_TRY(cudaEventRecord(ev[1], s));
+    }
+    for (size_t l = lv.size(); l-- > from;) {
+      GenLevel& L = *lv[l];
+      if (l == from && ev) CUDA_TRY(cudaEventRecord(ev[2], s));
+      if (L.direct) {
+        gen_direct_kernel<<<1, 32, 0, s>>>(L.A, L.es, L.er, L.K, L.f, L.x, L.work.p, l == 0 ? st : nullptr);
+        LAUNCH_CHECK();
+        launches += 1;
+        continue;
+      }
+      GenArgs g = args_of(L, l == 0 ? st : nullptr);
+      g.xsep = L.x_next.p;
+      gen_backsolve_kernel<<<L.p, 32, 0, s>>>(g);
+      LAUNCH_CHECK();
+      launches += 1;
+    }
+  }
+
+  void restore_level1_wiring() {
+    if (lv.size() > 1) {
+      lv[1]->f = lv[0]->rhs_next.p;
+      lv[1]->x = lv[0]->x_next.p;
+    }
+  }
+
+  long long reduced_ops() const {
+    long long ops = 0;
+    for (size_t l = 1; l < lv.size(); ++l) {
+      const long n = lv[l]->A.n;
+      ops += (long long)n * (lv[l]->es + 1 + lv[l]->er) * (lv[l]->es + 2);
+    }
+    return ops;
+  }
+};
+
 }  // namespace
 
 // ----------------------------------------------------------------------------
@@ -519,6 +718,12 @@ struct psg_handle {
   int strategy = 0;
   DevBuf<double> own_data, own_corner;
   TriSolver tri;
+  GenSolver gen;
+  bool generic = false;                 // non-tridiagonal kinds: generic exact path
+  double refine_tol = 1e-14;            // generic path: refine once when ||Ax-f||/||f|| exceeds this
+  double last_residual = 0.0;
+  DevBuf<double> d_r, d_d;              // refinement residual / correction
+  DevBuf<unsigned long long> d_norm;
   std::vector<int> seg_start, seg_len;  // level-0 segmentation when refined
   bool refined = false;
   // options
@@ -538,7 +743,7 @@ struct psg_handle {
       if (e) event_pool().put(e);
     if (h_status) pinned_slots().put(h_status);
   }
-  bool use_spec() const { return speculative && tri.spec_possible(); }
+  bool use_spec() const { return !generic && speculative && tri.spec_possible(); }
 };
 
 namespace {
@@ -609,6 +814,14 @@ bool is_tridiag(const psg_desc& A) { return A.kind == PSG_BANDED && A.s == 1 && 
 void run_factor(psg_handle* h, cudaStream_t s) {
   h->tri.launches = 0;
   CUDA_TRY(cudaEventRecord(h->ev_f0, s));
+  if (h->generic) {
+    h->gen.launches = 0;
+    h->gen.factor(s);
+    h->exact_factored = true;
+    CUDA_TRY(cudaEventRecord(h->ev_f1, s));
+    h->factor_launches = h->gen.launches;
+    return;
+  }
   if (h->use_spec()) {
     h->tri.spec_factor(s);
     h->spec_factored = true;
@@ -709,8 +922,7 @@ int psg_factor(const psg_desc* Ain, int p, int strategy, double tol, void* strea
     validate(*Ain);
     check_strategy(*Ain, strategy);
     h->plan = make_plan(*Ain, p);
-    if (!is_tridiag(*Ain))
-      throw Fail{PSG_E_UNSUPPORTED_KIND, "GPU path for this kind is not built yet (tridiagonal only)"};
+    h->generic = !is_tridiag(*Ain);
     cudaStream_t s = (cudaStream_t)stream;
     for (cudaEvent_t* e : {&h->ev_f0, &h->ev_f1, &h->ev_done, &h->ev[0], &h->ev[1], &h->ev[2], &h->ev[3]})
       *e = event_pool().get();
@@ -728,10 +940,16 @@ int psg_factor(const psg_desc* Ain, int p, int strategy, double tol, void* strea
       }
       h->A.on_device = 1;
     }
-    int maxlen = 0, minlen = 0;
-    SegMap S0 = plan_segments(h->plan, h->seg_start, h->seg_len, h->refined, maxlen, minlen);
-    h->tri.init(tri_rows(h->A), h->A.n, S0, maxlen, minlen, h->refined ? &h->seg_start : nullptr,
-                h->refined ? &h->seg_len : nullptr, s);
+    if (h->generic) {
+      SMView V{h->A.kind, h->A.n, h->A.m, h->A.s, h->A.r, h->A.data, h->A.corner, h->A.corner_rows, h->A.corner_cols};
+      CUDA_TRY(cudaStreamSynchronize(s));  // plan uploads below use the legacy stream
+      h->gen.build(V, p);
+    } else {
+      int maxlen = 0, minlen = 0;
+      SegMap S0 = plan_segments(h->plan, h->seg_start, h->seg_len, h->refined, maxlen, minlen);
+      h->tri.init(tri_rows(h->A), h->A.n, S0, maxlen, minlen, h->refined ? &h->seg_start : nullptr,
+                  h->refined ? &h->seg_len : nullptr, s);
+    }
     h->d_status.alloc(1);
     h->h_status = static_cast<DevStatus*>(pinned_slots().get());
     run_factor(h.get(), s);
@@ -751,6 +969,7 @@ int psg_set_option(psg_handle* h, int option, double value) {
     switch (option) {
       case PSG_OPT_SPECULATIVE:
         h->speculative = value != 0.0;
+        if (h->generic) break;  // the generic path is exact
         if ((h->use_spec() && !h->spec_factored) || (!h->use_spec() && !h->exact_factored)) {
           run_factor(h, nullptr);
           CUDA_TRY(cudaEventRecord(h->ev_done, nullptr));
@@ -802,17 +1021,53 @@ int psg_solve(const psg_handle* hc, const double* f, double* x, int on_device, v
       CUDA_TRY(cudaMemcpyAsync(h->d_status.p, h->h_status, sizeof(DevStatus), cudaMemcpyHostToDevice, s));
       if (timing) CUDA_TRY(cudaEventRecord(h->ev[0], s));
       h->tri.launches = 0;
-      if (spec)
+      h->gen.launches = 0;
+      if (h->generic) {
+        h->gen.solve(df, dx, h->d_status.p, s, timing ? h->ev : nullptr);
+        // residual certificate of the exact generic solve; one step of iterative
+        // refinement with the same factorization when it exceeds refine_tol
+        // (non-dominant kinds such as BABD lose a little accuracy without pivoting)
+        MatView v{h->A.kind, h->A.n, h->A.m, h->A.s, h->A.r, h->A.data, h->A.corner, h->A.corner_rows,
+                  h->A.corner_cols};
+        h->d_r.alloc(n);
+        h->d_norm.alloc(2);
+        auto resid = [&](double* out_rel) {
+          unsigned long long hb[2];
+          CUDA_TRY(cudaMemsetAsync(h->d_norm.p, 0, 2 * sizeof(unsigned long long), s));
+          residual_vec_kernel<<<148 * 8, 256, 0, s>>>(v, dx, df, h->d_r.p, h->d_norm.p);
+          LAUNCH_CHECK();
+          CUDA_TRY(cudaMemcpyAsync(hb, h->d_norm.p, sizeof hb, cudaMemcpyDeviceToHost, s));
+          CUDA_TRY(cudaStreamSynchronize(s));
+          const double num = bits_to_double(hb[0]), den = bits_to_double(hb[1]);
+          *out_rel = den > 0 ? num / den : num;
+        };
+        double rel = 0.0;
+        resid(&rel);
+        launches += 1;
+        if (rel > h->refine_tol && rel == rel) {
+          h->d_d.alloc(n);
+          h->gen.solve(h->d_r.p, h->d_d.p, nullptr, s, nullptr);
+          axpy_kernel<<<148 * 8, 256, 0, s>>>(n, h->d_d.p, dx);
+          LAUNCH_CHECK();
+          launches += 2;
+          resid(&rel);
+          launches += 1;
+        }
+        h->gen.lv[0]->f = df;
+        h->gen.lv[0]->x = dx;
+        h->last_residual = rel;
+      } else if (spec)
         h->tri.spec_solve(make_rows(df, 0, n), dx, h->d_status.p, s, timing ? h->ev : nullptr);
       else
         h->tri.exact_solve(make_rows(df, 0, n), dx, h->d_status.p, s, timing ? h->ev : nullptr);
-      launches += h->tri.launches;
+      launches += h->tri.launches + h->gen.launches;
       if (timing) CUDA_TRY(cudaEventRecord(h->ev[3], s));
       CUDA_TRY(cudaMemcpyAsync(h->h_status, h->d_status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
       CUDA_TRY(cudaStreamSynchronize(s));
       const DevStatus st = *h->h_status;
       cert = 0.0;
       for (int i = 0; i < kCertSlots; ++i) cert = std::max(cert, bits_to_double(st.cert_bits[i]));
+      if (h->generic) cert = h->last_residual;  // the generic path certifies by its residual
       const bool bad = st.bad_seg != INT_MAX || st.pivot_seg != INT_MAX;
       if (!bad && cert <= h->cert_tol) {
         spec_used = spec;
@@ -850,7 +1105,7 @@ int psg_solve(const psg_handle* hc, const double* f, double* x, int on_device, v
       stats->phase1_seconds = t01 * 1e-3;
       stats->phase2_seconds = t12 * 1e-3;
       stats->phase3_seconds = t23 * 1e-3;
-      stats->reduced_ops = h->tri.reduced_ops(spec_used);
+      stats->reduced_ops = h->generic ? h->gen.reduced_ops() : h->tri.reduced_ops(spec_used);
       stats->certificate = cert;
       stats->speculative = spec_used ? 1 : 0;
       stats->fallbacks = fallbacks;
@@ -874,8 +1129,43 @@ int psg_reduced_blocks(const psg_handle* hc, double* diag, double* sub, double* 
   psg_handle* h = const_cast<psg_handle*>(hc);
   std::lock_guard<std::mutex> g(h->mu);
   try {
-    if (h->refined) throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "reduced system was refined internally (bodies > 1056 rows)"};
     CUDA_TRY(cudaEventSynchronize(h->ev_done));
+    if (h->generic) {
+      GenLevel& L = *h->gen.lv[0];
+      const int q = L.q, k = L.k, kk = k * k;
+      std::vector<double> T(L.Tdata.n), C(kk, 0.0);
+      CUDA_TRY(cudaMemcpy(T.data(), L.Tdata.p, sizeof(double) * T.size(), cudaMemcpyDeviceToHost));
+      if (L.corner) CUDA_TRY(cudaMemcpy(C.data(), L.Tcorner.p, sizeof(double) * kk, cudaMemcpyDeviceToHost));
+      auto put = [&](double* dst, int j, const double* src, int pitch) {
+        if (!dst) return;
+        for (int t = 0; t < k; ++t)
+          for (int u = 0; u < k; ++u) dst[(long)j * kk + t * k + u] = src ? src[(long)t * pitch + u] : 0.0;
+      };
+      for (int j = 0; j < q; ++j) {
+        if (!L.corner) {
+          const long off = j == 0 ? 0 : (3L * j - 1) * kk;
+          const int dblk = j > 0 ? 1 : 0;
+          put(sub, j, j > 0 ? &T[off] : nullptr, k);
+          put(diag, j, &T[off + (long)dblk * kk], k);
+          put(super, j, j < q - 1 ? &T[off + (long)(dblk + 1) * kk] : nullptr, k);
+        } else {
+          const long off = j == 0 ? 0 : (long)k * 2 * k + (long)(j - 1) * k * 3 * k;
+          const int width = (j == 0 || j == q - 1) ? 2 * k : 3 * k;
+          const double* row = &T[off];
+          if (j == 0) {
+            put(sub, 0, C.data(), k);  // sub[0] carries the corner coupling (psg.h)
+            put(diag, 0, row, width);
+            put(super, 0, q > 1 ? row + k : nullptr, width);
+          } else {
+            put(sub, j, row, width);
+            put(diag, j, row + k, width);
+            put(super, j, j < q - 1 ? row + 2 * k : nullptr, width);
+          }
+        }
+      }
+      return 0;
+    }
+    if (h->refined) throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "reduced system was refined internally (bodies > 1056 rows)"};
     const int ns = h->tri.S0.nseg - 1;
     if (h->use_spec() && h->spec_factored) {
       // speculative reduced matrix: diagonal (beta = gamma = 0 below rho^L)
@@ -899,8 +1189,29 @@ int psg_solve_reduced(const psg_handle* hc, const double* rhs, double* x, int on
   psg_handle* h = const_cast<psg_handle*>(hc);
   std::lock_guard<std::mutex> g(h->mu);
   try {
-    if (h->refined) throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "reduced system was refined internally (bodies > 1056 rows)"};
     cudaStream_t s = (cudaStream_t)stream;
+    if (h->generic) {
+      if (h->gen.lv.size() < 2) throw Fail{PSG_E_INVALID_PARAMETER, "no reduced system"};
+      const int dim = h->gen.lv[0]->q * h->gen.lv[0]->k;
+      DevBuf<double> dr, dxv;
+      const double* r = rhs;
+      double* xo = x;
+      if (!on_device) {
+        dr.alloc(dim);
+        dxv.alloc(dim);
+        CUDA_TRY(cudaMemcpyAsync(dr.p, rhs, sizeof(double) * dim, cudaMemcpyHostToDevice, s));
+        r = dr.p;
+        xo = dxv.p;
+      }
+      h->gen.solve(r, xo, nullptr, s, nullptr, 1);
+      h->gen.restore_level1_wiring();
+      if (!on_device) CUDA_TRY(cudaMemcpyAsync(x, xo, sizeof(double) * dim, cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaStreamSynchronize(s));
+      CUDA_TRY(cudaEventRecord(h->ev_done, s));
+      if (stats) stats->reduced_ops += h->gen.reduced_ops();
+      return 0;
+    }
+    if (h->refined) throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "reduced system was refined internally (bodies > 1056 rows)"};
     if (!h->exact_factored) {  // the exact reduced matrix T (parallel_factor's ReducedSystem)
       h->tri.launches = 0;
       h->tri.exact_factor(s);

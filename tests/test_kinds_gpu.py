@@ -1,0 +1,101 @@
+"""GPU parity for every structured kind (generic exact partition path):
+banded (any s, r), block tridiagonal, ABD, BABD (standard and the s=m, r=0 BVP
+layout of BASELINE config 4) against the oracle (bit-identical to the
+reference) and the reference goldens; full-size configs 2-4."""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_0912_3678_b200 as psg
+
+pytestmark = pytest.mark.gpu
+
+
+def _gpu(torch, A, p, f, strategy=psg.Strategy.Lu):
+    dev = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    GA = psg.StructuredMatrix(A.kind, A.n, A.m, A.s, A.r, dev(A.data), dev(A.corner), A.corner_rows, A.corner_cols)
+    F = psg.parallel_factor(GA, p, strategy)
+    st = psg.SolveStats()
+    x = psg.solve(F, dev(f), st).cpu().numpy()
+    return x, st, F, GA
+
+
+SHAPES = [  # kind, n, m, s, r, p
+    (0, 600, 1, 2, 1, 5), (0, 601, 1, 3, 3, 7), (0, 500, 1, 1, 2, 4), (0, 2000, 1, 3, 3, 16),
+    (1, 360, 3, 1, 1, 6), (1, 1024, 4, 1, 1, 8), (1, 96, 2, 1, 1, 4),
+    (2, 400, 4, 2, 2, 5), (2, 240, 3, 1, 2, 4),
+    (3, 440, 2, 1, 1, 6), (3, 640, 4, 2, 2, 8), (3, 1032, 8, 8, 0, 8),
+]
+
+
+@pytest.mark.parametrize("kind,n,m,s,r,p", SHAPES)
+def test_generic_kinds_match_oracle(cuda, kind, n, m, s, r, p):
+    if kind == 3 and r == 0:  # BVP layout: no generate_random dominance path, use config 4 generator
+        A, f = O.generate_config(4, n // 8 - 1, 3)
+    else:
+        A = O.generate_random(kind, n, m, s, r, 100 + n, 2.0)
+        f = O.random_vector(n, 9)
+    want, _ = O.parallel_solve(A, p, f)
+    got, st, F, _ = _gpu(cuda, A, p, f)
+    tol = 1e-12 if kind != 3 else 1e-11
+    assert O.rel_err(got, want) <= tol
+    assert O.residual(A, got, f) <= 1e-13
+
+
+@pytest.mark.parametrize("kind,n,m,s,r,p", [(1, 360, 3, 1, 1, 6), (0, 601, 1, 3, 3, 7), (3, 440, 2, 1, 1, 6)])
+def test_generic_reduced_matrix_matches_reference_T(cuda, kind, n, m, s, r, p):
+    A = O.generate_random(kind, n, m, s, r, 7 + n, 2.0)
+    info = O.factor_info(A, p)
+    T, k, q = info["T"], info["k"], info["q"]
+    f = O.random_vector(n, 1)
+    _, _, F, _ = _gpu(cuda, A, p, f)
+    assert (F.q, F.k) == (q, k)
+    sub, diag, sup = F.reduced_blocks()
+    kk = k * k
+    G = np.zeros_like(T)
+    for j in range(q):
+        G[j * k:(j + 1) * k, j * k:(j + 1) * k] = diag[j * kk:(j + 1) * kk].reshape(k, k)
+        if j > 0:
+            G[j * k:(j + 1) * k, (j - 1) * k:j * k] = sub[j * kk:(j + 1) * kk].reshape(k, k)
+        if j < q - 1:
+            G[j * k:(j + 1) * k, (j + 1) * k:(j + 2) * k] = sup[j * kk:(j + 1) * kk].reshape(k, k)
+    if F.has_corner:
+        G[0:k, (q - 1) * k:q * k] += sub[0:kk].reshape(k, k)
+    scale = np.max(np.abs(T))
+    assert np.max(np.abs(G - T)) <= 1e-13 * scale
+    rhs = np.cos(np.arange(q * k))
+    xr = psg.solve_reduced(F, rhs)
+    assert O.rel_err(xr, np.linalg.solve(T, rhs)) <= 1e-11
+
+
+_GOLD = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "cfg[234]_*.npz")))
+
+
+@pytest.mark.parametrize("path", _GOLD, ids=[os.path.basename(c)[:-4] for c in _GOLD])
+def test_generic_matches_reference_golden(cuda, path):
+    g = np.load(path)
+    A, f = O.generate_config(int(g["cfg"]), int(g["size"]), int(g["seed"]))
+    got, st, F, _ = _gpu(cuda, A, int(g["p"]), f)
+    tol = 1e-12 if int(g["cfg"]) != 4 else 1e-10
+    assert O.rel_err(got, g["x"]) <= tol
+    assert O.residual(A, got, f) <= 1e-13
+    assert F.q == int(g["q"]) and F.dim == int(g["dim"])
+
+
+@pytest.mark.parametrize("cfg,size,p", [(2, 1 << 20, 16384), (3, 1 << 24, 32768), (4, 1 << 18, 4096)])
+def test_full_size_configs(cuda, cfg, size, p):
+    torch = cuda
+    A, f = psg.generate_config(cfg, size, cfg + 1)
+    F = psg.parallel_factor(A, p)
+    st = psg.SolveStats()
+    x = psg.solve(F, f, st)
+    res = psg.residual(A, x, f)
+    assert res <= 1e-13
+    Ah = O.Matrix(A.kind, A.n, A.m, A.s, A.r, A.data.cpu().numpy(),
+                  None if A.corner is None else A.corner.cpu().numpy(), A.corner_rows, A.corner_cols)
+    want = O.solve_sequential(Ah, f.cpu().numpy())
+    tol = 1e-12 if cfg != 4 else 1e-10
+    assert O.rel_err(x.cpu().numpy(), want) <= tol

@@ -89,3 +89,13 @@ def test_zero_pivot_partition_matches_reference():
         O.RefMatrix(A).factor(p)
     assert eo.value.errc == er.value.errc == 11
     assert "partition 2" in str(eo.value) and "partition 2" in str(er.value)
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built (needs /root/reference)")
+@pytest.mark.parametrize("kind,n,m,s,r", [(0, 37, 1, 2, 3), (1, 36, 3, 1, 1), (2, 40, 4, 2, 2), (3, 44, 2, 1, 1)])
+def test_generate_random_matches_reference(kind, n, m, s, r):
+    A = O.generate_random(kind, n, m, s, r, 17, 2.0)
+    d, c = O.ref_generate_random(kind, n, m, s, r, 17, 2.0)
+    assert np.array_equal(A.data, d)
+    if c is not None:
+        assert np.array_equal(A.corner, c)
