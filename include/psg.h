@@ -96,6 +96,27 @@ int psg_solve(const psg_handle* h, const double* f, double* x, int on_device, vo
 
 void psg_release(psg_handle* h);
 
+/* Asynchronous solve (device pointers only; the tridiagonal path; other kinds
+ * run blocking).  Enqueues the speculative solve on `stream` and returns; x is
+ * final in stream order unless its certificate fails, in which case psg_sync
+ * re-solves that right-hand side exactly.  Call psg_sync before reading x on
+ * the host or reusing f.  timing != 0 records phase events for psg_sync's
+ * stats.  Up to 64 solves may be pending; more drain the oldest. */
+int psg_solve_async(const psg_handle* h, const double* f, double* x, int timing, void* stream, char* err,
+                    size_t errlen);
+/* Wait for every pending asynchronous solve, repair failed certificates, and
+ * accumulate their statistics (SolveStats semantics: phases add up). */
+int psg_sync(const psg_handle* h, psg_stats* stats, char* err, size_t errlen);
+
+/* New matrix values with the structure the handle was factored for (kind, n,
+ * m, s, r, corner shape, p): recompute the factorization in place, without
+ * re-planning or re-allocating.  The equivalent of parallel_factor on a
+ * matrix whose sparsity pattern is unchanged.  Pending asynchronous solves are
+ * not drained (stream order keeps them on the old factor data) but are
+ * certified at psg_sync against the values current then: call psg_sync before
+ * overwriting A's values in place. */
+int psg_refactor(psg_handle* h, const psg_desc* A, void* stream, char* err, size_t errlen);
+
 /* Reduced system metadata (ReducedSystem, parfact.hpp:14-22): q kept blocks,
  * scalar dimension, block size k, corner flag. */
 int psg_reduced_info(const psg_handle* h, int* q, int* dim, int* k, int* has_corner);

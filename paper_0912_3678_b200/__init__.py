@@ -118,6 +118,9 @@ def lib():
         vp, ip, sz, cp = C.c_void_p, C.c_int, C.c_size_t, C.c_char_p
         L.psg_factor.argtypes = [C.POINTER(_Desc), ip, ip, C.c_double, vp, C.POINTER(vp), cp, sz]
         L.psg_solve.argtypes = [vp, vp, vp, ip, vp, C.POINTER(SolveStats), cp, sz]
+        L.psg_solve_async.argtypes = [vp, vp, vp, ip, vp, cp, sz]
+        L.psg_sync.argtypes = [vp, C.POINTER(SolveStats), cp, sz]
+        L.psg_refactor.argtypes = [vp, C.POINTER(_Desc), vp, cp, sz]
         L.psg_release.argtypes = [vp]
         L.psg_release.restype = None
         L.psg_reduced_info.argtypes = [vp] + [C.POINTER(C.c_int)] * 4
@@ -245,6 +248,26 @@ class ParallelFactorization:
 
     def solve(self, f, x=None, stats: SolveStats | None = None, stream=None):
         return solve(self, f, stats=stats, x=x, stream=stream)
+
+    def refactor(self, A: "StructuredMatrix | None" = None, stream=None):
+        """New values, same structure (psg_refactor): refactor in place."""
+        A = self.A if A is None else A
+        d = A.desc()
+        err = C.create_string_buffer(512)
+        _check(lib().psg_refactor(self.handle, C.byref(d), _stream_ptr(stream), err, 512), err)
+        self.A = A
+        return self
+
+    def solve_async(self, f, x, timing: bool = False, stream=None):
+        """Enqueue a device solve; x is final after sync() (psg_solve_async)."""
+        err = C.create_string_buffer(512)
+        _check(lib().psg_solve_async(self.handle, _addr(f), _addr(x), 1 if timing else 0, _stream_ptr(stream),
+                                     err, 512), err)
+        return x
+
+    def sync(self, stats: SolveStats | None = None):
+        err = C.create_string_buffer(512)
+        _check(lib().psg_sync(self.handle, C.byref(stats) if stats is not None else None, err, 512), err)
 
 
 def parallel_factor(A: StructuredMatrix, p: int, strategy: int = Strategy.Lu, tol: float = 1e-8,

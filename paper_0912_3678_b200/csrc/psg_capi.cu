@@ -403,7 +403,7 @@ struct TriSolver {
   void spec_solve(const RowArr& F, double* x, DevStatus* st, cudaStream_t s, cudaEvent_t* ev) {
     const int nsep = S0.nseg - 1;
     tri_spec_sep_kernel<<<blocks_for((long)blocks_for(nsep, kSepPerWarp) * 32, 256), 256, 0, s>>>(F, S0, wts.p,
-                                                                                                   xsep.p);
+                                                                                                   xsep.p, st);
     LAUNCH_CHECK();
     launches += 1;
     if (ev) {  // the speculative reduced matrix is diagonal: phase 2 is fused into phase 1
@@ -737,11 +737,33 @@ struct psg_handle {
   cudaEvent_t ev_f0 = nullptr, ev_f1 = nullptr, ev_done = nullptr, ev[4] = {};
   std::mutex mu;
   int factor_launches = 0, solve_launches = 0;
+  // asynchronous solves: per-solve status slots, repaired at psg_sync
+  static constexpr int kRing = 64;
+  struct Pending {
+    int slot;
+    const double* f;
+    double* x;
+    cudaStream_t s;
+    bool spec, timing;
+    int launches;
+  };
+  std::vector<Pending> pending;
+  DevBuf<DevStatus> d_ring;
+  DevStatus* h_ring = nullptr;               // pinned mirror
+  cudaEvent_t ring_done[kRing] = {}, ring_t[kRing][4] = {};
+  long async_count = 0;
   ~psg_handle() {
     if (ev_done) cudaEventSynchronize(ev_done);  // buffers go back to the cache only when idle
+    for (auto& pd : pending) cudaEventSynchronize(ring_done[pd.slot]);
     for (cudaEvent_t e : {ev_f0, ev_f1, ev_done, ev[0], ev[1], ev[2], ev[3]})
       if (e) event_pool().put(e);
+    for (int i = 0; i < kRing; ++i) {
+      if (ring_done[i]) event_pool().put(ring_done[i]);
+      for (int j = 0; j < 4; ++j)
+        if (ring_t[i][j]) event_pool().put(ring_t[i][j]);
+    }
     if (h_status) pinned_slots().put(h_status);
+    if (h_ring) cudaFreeHost(h_ring);
   }
   bool use_spec() const { return !generic && speculative && tri.spec_possible(); }
 };
@@ -993,6 +1015,145 @@ int psg_last_launches(const psg_handle* h, int* f, int* s) {
   return 0;
 }
 
+namespace {
+
+// Generic (non-tridiagonal) solve: exact, certified by its residual, refined
+// once when the residual exceeds refine_tol.  Blocking.
+int generic_solve(psg_handle* h, const double* df, double* dx, cudaStream_t s, bool timing, double* cert) {
+  const int n = h->A.n;
+  for (int i = 0; i < kCertSlots; ++i) h->h_status->cert_bits[i] = 0ull;
+  h->h_status->bad_seg = INT_MAX;
+  h->h_status->pivot_seg = INT_MAX;
+  CUDA_TRY(cudaMemcpyAsync(h->d_status.p, h->h_status, sizeof(DevStatus), cudaMemcpyHostToDevice, s));
+  if (timing) CUDA_TRY(cudaEventRecord(h->ev[0], s));
+  h->gen.launches = 0;
+  h->gen.solve(df, dx, h->d_status.p, s, timing ? h->ev : nullptr);
+  if (timing) CUDA_TRY(cudaEventRecord(h->ev[3], s));
+  MatView v{h->A.kind, h->A.n, h->A.m, h->A.s, h->A.r, h->A.data, h->A.corner, h->A.corner_rows, h->A.corner_cols};
+  h->d_r.alloc(n);
+  h->d_norm.alloc(2);
+  auto resid = [&]() {
+    unsigned long long hb[2];
+    CUDA_TRY(cudaMemsetAsync(h->d_norm.p, 0, 2 * sizeof(unsigned long long), s));
+    residual_vec_kernel<<<148 * 8, 256, 0, s>>>(v, dx, df, h->d_r.p, h->d_norm.p);
+    LAUNCH_CHECK();
+    CUDA_TRY(cudaMemcpyAsync(hb, h->d_norm.p, sizeof hb, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(h->h_status, h->d_status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    const double num = bits_to_double(hb[0]), den = bits_to_double(hb[1]);
+    return den > 0 ? num / den : num;
+  };
+  double rel = resid();
+  int launches = h->gen.launches + 1;
+  const DevStatus st0 = *h->h_status;
+  if (st0.pivot_seg != INT_MAX)
+    throw Fail{PSG_E_ZERO_PIVOT, "partition " + std::to_string(st0.pivot_seg + 1) + ": zero pivot in the no-pivot elimination"};
+  if (rel > h->refine_tol && rel == rel) {
+    h->d_d.alloc(n);
+    h->gen.launches = 0;
+    h->gen.solve(h->d_r.p, h->d_d.p, nullptr, s, nullptr);
+    axpy_kernel<<<148 * 8, 256, 0, s>>>(n, h->d_d.p, dx);
+    LAUNCH_CHECK();
+    launches += h->gen.launches + 2;
+    rel = resid();
+  }
+  h->gen.lv[0]->f = df;
+  h->gen.lv[0]->x = dx;
+  if (!(rel == rel) || st0.bad_seg != INT_MAX)
+    throw Fail{PSG_E_SINGULAR_REDUCED_SYSTEM, "non-finite solution: the reduced system is singular"};
+  *cert = rel;
+  return launches;
+}
+
+// Tridiagonal: enqueue one solve attempt whose status lands in device slot
+// `st`, copied to host slot `hst` and marked by event `done`.
+int tri_enqueue(psg_handle* h, const double* df, double* dx, cudaStream_t s, DevStatus* st, DevStatus* hst,
+                cudaEvent_t done, cudaEvent_t* ev, bool spec) {
+  const int n = h->A.n;
+  h->tri.launches = 0;
+  if (ev) CUDA_TRY(cudaEventRecord(ev[0], s));
+  if (spec) {
+    h->tri.spec_solve(make_rows(df, 0, n), dx, st, s, ev);  // the first kernel resets the status slot
+  } else {
+    DevStatus init{};
+    for (int i = 0; i < kCertSlots; ++i) init.cert_bits[i] = 0ull;
+    init.bad_seg = INT_MAX;
+    init.pivot_seg = INT_MAX;
+    *hst = init;
+    CUDA_TRY(cudaMemcpyAsync(st, hst, sizeof(DevStatus), cudaMemcpyHostToDevice, s));
+    h->tri.exact_solve(make_rows(df, 0, n), dx, st, s, ev);
+  }
+  if (ev) CUDA_TRY(cudaEventRecord(ev[3], s));
+  CUDA_TRY(cudaMemcpyAsync(hst, st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaEventRecord(done, s));
+  return h->tri.launches;
+}
+
+struct Outcome {
+  double cert = 0;
+  bool bad = false, pivot = false;
+  int pivot_seg = 0;
+};
+
+Outcome read_status(const DevStatus& st) {
+  Outcome o;
+  for (int i = 0; i < kCertSlots; ++i) o.cert = std::max(o.cert, bits_to_double(st.cert_bits[i]));
+  o.pivot = st.pivot_seg != INT_MAX;
+  o.pivot_seg = st.pivot_seg;
+  o.bad = o.pivot || st.bad_seg != INT_MAX || !(o.cert == o.cert);
+  return o;
+}
+
+// Blocking tridiagonal solve with the speculative -> exact fallback.
+void tri_solve_blocking(psg_handle* h, const double* df, double* dx, cudaStream_t s, psg_stats* stats) {
+  const bool timing = stats != nullptr;
+  int fallbacks = 0, launches = 0;
+  bool spec_used = false;
+  double cert = 0;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    const bool spec = h->use_spec();
+    if (!spec && !h->exact_factored) {  // exact mode needs its factor data (levels, reduced T)
+      run_factor(h, s);
+      launches += h->tri.launches;
+    }
+    launches += tri_enqueue(h, df, dx, s, h->d_status.p, h->h_status, h->ev_done, timing ? h->ev : nullptr, spec);
+    CUDA_TRY(cudaEventSynchronize(h->ev_done));
+    const Outcome o = read_status(*h->h_status);
+    cert = o.cert;
+    if (!o.bad && cert <= h->cert_tol) {
+      spec_used = spec;
+      break;
+    }
+    if (!spec) {
+      if (o.pivot)  // parallel_factor's lowest failing partition (src/parfact.cpp:61-68)
+        throw Fail{PSG_E_ZERO_PIVOT, "partition " + std::to_string(partition_of_segment(h, o.pivot_seg)) +
+                                         ": zero pivot in the no-pivot elimination"};
+      if (o.bad) throw Fail{PSG_E_SINGULAR_REDUCED_SYSTEM, "non-finite solution: the reduced system is singular"};
+      break;  // exact mode: the certificate is reported, the result kept
+    }
+    ++fallbacks;  // speculative interface rejected: switch this handle to the exact path
+    h->speculative = false;
+  }
+  h->solve_launches = launches;
+  if (stats) {
+    float tf = 0, t01 = 0, t12 = 0, t23 = 0;
+    cudaEventElapsedTime(&tf, h->ev_f0, h->ev_f1);
+    cudaEventElapsedTime(&t01, h->ev[0], h->ev[1]);
+    cudaEventElapsedTime(&t12, h->ev[1], h->ev[2]);
+    cudaEventElapsedTime(&t23, h->ev[2], h->ev[3]);
+    stats->factor_seconds = tf * 1e-3;
+    stats->phase1_seconds += t01 * 1e-3;  // accumulate like SolveStats (src/parfact.cpp:233-237)
+    stats->phase2_seconds += t12 * 1e-3;
+    stats->phase3_seconds += t23 * 1e-3;
+    stats->reduced_ops += h->tri.reduced_ops(spec_used);
+    stats->certificate = std::max(stats->certificate, cert);
+    stats->speculative = spec_used ? 1 : 0;
+    stats->fallbacks += fallbacks;
+  }
+}
+
+}  // namespace
+
 int psg_solve(const psg_handle* hc, const double* f, double* x, int on_device, void* stream, psg_stats* stats,
               char* err, size_t errlen) {
   psg_handle* h = const_cast<psg_handle*>(hc);
@@ -1009,107 +1170,163 @@ int psg_solve(const psg_handle* hc, const double* f, double* x, int on_device, v
       df = h->d_f.p;
       dx = h->d_x.p;
     }
-    const bool timing = stats != nullptr;
-    int fallbacks = 0, launches = 0;
-    bool spec_used = false;
-    double cert = 0;
-    for (int attempt = 0; attempt < 2; ++attempt) {
-      const bool spec = h->use_spec();
-      for (int i = 0; i < kCertSlots; ++i) h->h_status->cert_bits[i] = 0ull;
-      h->h_status->bad_seg = INT_MAX;
-      h->h_status->pivot_seg = INT_MAX;
-      CUDA_TRY(cudaMemcpyAsync(h->d_status.p, h->h_status, sizeof(DevStatus), cudaMemcpyHostToDevice, s));
-      if (timing) CUDA_TRY(cudaEventRecord(h->ev[0], s));
-      h->tri.launches = 0;
-      h->gen.launches = 0;
-      if (h->generic) {
-        h->gen.solve(df, dx, h->d_status.p, s, timing ? h->ev : nullptr);
-        // residual certificate of the exact generic solve; one step of iterative
-        // refinement with the same factorization when it exceeds refine_tol
-        // (non-dominant kinds such as BABD lose a little accuracy without pivoting)
-        MatView v{h->A.kind, h->A.n, h->A.m, h->A.s, h->A.r, h->A.data, h->A.corner, h->A.corner_rows,
-                  h->A.corner_cols};
-        h->d_r.alloc(n);
-        h->d_norm.alloc(2);
-        auto resid = [&](double* out_rel) {
-          unsigned long long hb[2];
-          CUDA_TRY(cudaMemsetAsync(h->d_norm.p, 0, 2 * sizeof(unsigned long long), s));
-          residual_vec_kernel<<<148 * 8, 256, 0, s>>>(v, dx, df, h->d_r.p, h->d_norm.p);
-          LAUNCH_CHECK();
-          CUDA_TRY(cudaMemcpyAsync(hb, h->d_norm.p, sizeof hb, cudaMemcpyDeviceToHost, s));
-          CUDA_TRY(cudaStreamSynchronize(s));
-          const double num = bits_to_double(hb[0]), den = bits_to_double(hb[1]);
-          *out_rel = den > 0 ? num / den : num;
-        };
-        double rel = 0.0;
-        resid(&rel);
-        launches += 1;
-        if (rel > h->refine_tol && rel == rel) {
-          h->d_d.alloc(n);
-          h->gen.solve(h->d_r.p, h->d_d.p, nullptr, s, nullptr);
-          axpy_kernel<<<148 * 8, 256, 0, s>>>(n, h->d_d.p, dx);
-          LAUNCH_CHECK();
-          launches += 2;
-          resid(&rel);
-          launches += 1;
-        }
-        h->gen.lv[0]->f = df;
-        h->gen.lv[0]->x = dx;
-        h->last_residual = rel;
-      } else if (spec)
-        h->tri.spec_solve(make_rows(df, 0, n), dx, h->d_status.p, s, timing ? h->ev : nullptr);
-      else
-        h->tri.exact_solve(make_rows(df, 0, n), dx, h->d_status.p, s, timing ? h->ev : nullptr);
-      launches += h->tri.launches + h->gen.launches;
-      if (timing) CUDA_TRY(cudaEventRecord(h->ev[3], s));
-      CUDA_TRY(cudaMemcpyAsync(h->h_status, h->d_status.p, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
-      CUDA_TRY(cudaStreamSynchronize(s));
-      const DevStatus st = *h->h_status;
-      cert = 0.0;
-      for (int i = 0; i < kCertSlots; ++i) cert = std::max(cert, bits_to_double(st.cert_bits[i]));
-      if (h->generic) cert = h->last_residual;  // the generic path certifies by its residual
-      const bool bad = st.bad_seg != INT_MAX || st.pivot_seg != INT_MAX;
-      if (!bad && cert <= h->cert_tol) {
-        spec_used = spec;
-        break;
+    if (h->generic) {
+      double cert = 0;
+      const int launches = generic_solve(h, df, dx, s, stats != nullptr, &cert);
+      h->solve_launches = launches;
+      if (stats) {
+        float tf = 0, t01 = 0, t12 = 0, t23 = 0;
+        cudaEventElapsedTime(&tf, h->ev_f0, h->ev_f1);
+        cudaEventElapsedTime(&t01, h->ev[0], h->ev[1]);
+        cudaEventElapsedTime(&t12, h->ev[1], h->ev[2]);
+        cudaEventElapsedTime(&t23, h->ev[2], h->ev[3]);
+        stats->factor_seconds = tf * 1e-3;
+        stats->phase1_seconds += t01 * 1e-3;
+        stats->phase2_seconds += t12 * 1e-3;
+        stats->phase3_seconds += t23 * 1e-3;
+        stats->reduced_ops += h->gen.reduced_ops();
+        stats->certificate = std::max(stats->certificate, cert);
+        stats->speculative = 0;
       }
-      if (!spec) {
-        if (st.pivot_seg != INT_MAX)  // parallel_factor's lowest failing partition (src/parfact.cpp:61-68)
-          throw Fail{PSG_E_ZERO_PIVOT, "partition " + std::to_string(partition_of_segment(h, st.pivot_seg)) +
-                                           ": zero pivot in the no-pivot elimination"};
-        if (bad)
-          throw Fail{PSG_E_SINGULAR_REDUCED_SYSTEM, "non-finite solution: the reduced system is singular"};
-        break;  // exact mode: the certificate is reported, the result kept
-      }
-      // speculative interface rejected: switch this handle to the exact path
-      ++fallbacks;
-      h->speculative = false;
-      if (!h->exact_factored) {
-        run_factor(h, s);
-        launches += h->tri.launches;
-      }
+    } else {
+      tri_solve_blocking(h, df, dx, s, stats);
     }
     if (!on_device) {
       CUDA_TRY(cudaMemcpyAsync(x, dx, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
       CUDA_TRY(cudaStreamSynchronize(s));
     }
     CUDA_TRY(cudaEventRecord(h->ev_done, s));
-    h->solve_launches = launches;
-    if (timing) {
-      float tf = 0, t01 = 0, t12 = 0, t23 = 0;
-      cudaEventElapsedTime(&tf, h->ev_f0, h->ev_f1);
-      cudaEventElapsedTime(&t01, h->ev[0], h->ev[1]);
-      cudaEventElapsedTime(&t12, h->ev[1], h->ev[2]);
-      cudaEventElapsedTime(&t23, h->ev[2], h->ev[3]);
-      stats->factor_seconds = tf * 1e-3;
-      stats->phase1_seconds = t01 * 1e-3;
-      stats->phase2_seconds = t12 * 1e-3;
-      stats->phase3_seconds = t23 * 1e-3;
-      stats->reduced_ops = h->generic ? h->gen.reduced_ops() : h->tri.reduced_ops(spec_used);
-      stats->certificate = cert;
-      stats->speculative = spec_used ? 1 : 0;
-      stats->fallbacks = fallbacks;
+    return 0;
+  } catch (const Fail& f_) {
+    return set_err(err, errlen, f_.code, f_.msg);
+  }
+}
+
+namespace {
+
+// Drain the pending asynchronous solves in order; a solve whose certificate
+// failed is repaired by the exact path (the handle switches to exact mode).
+void drain(psg_handle* h, psg_stats* stats) {
+  std::vector<psg_handle::Pending> todo;
+  todo.swap(h->pending);
+  for (const auto& pd : todo) {
+    CUDA_TRY(cudaEventSynchronize(h->ring_done[pd.slot]));
+    const Outcome o = read_status(h->h_ring[pd.slot]);
+    if (stats && pd.timing) {
+      float t01 = 0, t23 = 0;
+      cudaEventElapsedTime(&t01, h->ring_t[pd.slot][0], h->ring_t[pd.slot][1]);
+      cudaEventElapsedTime(&t23, h->ring_t[pd.slot][2], h->ring_t[pd.slot][3]);
+      stats->phase1_seconds += t01 * 1e-3;
+      stats->phase3_seconds += t23 * 1e-3;
+      stats->reduced_ops += h->tri.reduced_ops(pd.spec);
+      stats->certificate = std::max(stats->certificate, o.cert);
+      stats->speculative = pd.spec ? 1 : 0;
     }
+    if (!o.bad && o.cert <= h->cert_tol) continue;
+    if (stats) stats->fallbacks += 1;
+    h->speculative = false;
+    tri_solve_blocking(h, pd.f, pd.x, pd.s, nullptr);  // exact (throws on a genuine zero pivot)
+  }
+}
+
+}  // namespace
+
+int psg_solve_async(const psg_handle* hc, const double* f, double* x, int timing, void* stream, char* err,
+                    size_t errlen) {
+  psg_handle* h = const_cast<psg_handle*>(hc);
+  std::lock_guard<std::mutex> g(h->mu);
+  try {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (h->generic) {  // the generic path certifies by a residual pass: blocking
+      double cert = 0;
+      h->solve_launches = generic_solve(h, f, x, s, false, &cert);
+      CUDA_TRY(cudaEventRecord(h->ev_done, s));
+      return 0;
+    }
+    if (!h->h_ring) {
+      CUDA_TRY(cudaMallocHost(&h->h_ring, sizeof(DevStatus) * psg_handle::kRing));
+      h->d_ring.alloc(psg_handle::kRing);
+      for (int i = 0; i < psg_handle::kRing; ++i) {
+        h->ring_done[i] = event_pool().get();
+        for (int j = 0; j < 4; ++j) h->ring_t[i][j] = event_pool().get();
+      }
+    }
+    if ((int)h->pending.size() >= psg_handle::kRing) drain(h, nullptr);
+    const int slot = (int)(h->async_count++ % psg_handle::kRing);
+    const bool spec = h->use_spec();
+    const int launches = tri_enqueue(h, f, x, s, h->d_ring.p + slot, h->h_ring + slot, h->ring_done[slot],
+                                     timing ? h->ring_t[slot] : nullptr, spec);
+    h->pending.push_back(psg_handle::Pending{slot, f, x, s, spec, timing != 0, launches});
+    h->solve_launches = launches;
+    CUDA_TRY(cudaEventRecord(h->ev_done, s));
+    return 0;
+  } catch (const Fail& f_) {
+    return set_err(err, errlen, f_.code, f_.msg);
+  }
+}
+
+int psg_sync(const psg_handle* hc, psg_stats* stats, char* err, size_t errlen) {
+  psg_handle* h = const_cast<psg_handle*>(hc);
+  std::lock_guard<std::mutex> g(h->mu);
+  try {
+    if (stats) {
+      float tf = 0;
+      CUDA_TRY(cudaEventSynchronize(h->ev_f1));
+      cudaEventElapsedTime(&tf, h->ev_f0, h->ev_f1);
+      stats->factor_seconds = tf * 1e-3;
+    }
+    drain(h, stats);
+    return 0;
+  } catch (const Fail& f_) {
+    return set_err(err, errlen, f_.code, f_.msg);
+  }
+}
+
+// New matrix values with the same structure (kind, n, m, s, r, corner shape):
+// recompute the factor data on the handle's buffers (no re-planning).
+int psg_refactor(psg_handle* h, const psg_desc* A, void* stream, char* err, size_t errlen) {
+  std::lock_guard<std::mutex> g(h->mu);
+  try {
+    validate(*A);
+    if (A->kind != h->A.kind || A->n != h->A.n || A->m != h->A.m || A->s != h->A.s || A->r != h->A.r ||
+        A->corner_rows != h->A.corner_rows || A->corner_cols != h->A.corner_cols)
+      throw Fail{PSG_E_DIMENSION_MISMATCH, "psg_refactor needs the factored structure"};
+    cudaStream_t s = (cudaStream_t)stream;
+    // Pending asynchronous solves are NOT drained here: the factor kernels run
+    // after them in stream order.  Their certificates are checked at psg_sync
+    // against the matrix values current then, so callers must psg_sync before
+    // changing A's values in place (psg.h).
+    const double* data = A->data;
+    const double* corner = A->corner;
+    if (!A->on_device) {
+      h->own_data.alloc(A->data_len);
+      CUDA_TRY(cudaMemcpyAsync(h->own_data.p, A->data, sizeof(double) * A->data_len, cudaMemcpyHostToDevice, s));
+      data = h->own_data.p;
+      if (A->corner) {
+        const size_t cn = (size_t)A->corner_rows * A->corner_cols;
+        h->own_corner.alloc(cn);
+        CUDA_TRY(cudaMemcpyAsync(h->own_corner.p, A->corner, sizeof(double) * cn, cudaMemcpyHostToDevice, s));
+        corner = h->own_corner.p;
+      }
+    }
+    const bool moved = data != h->A.data || corner != h->A.corner;
+    h->A.data = data;
+    h->A.corner = corner;
+    if (h->generic) {
+      if (moved) {
+        SMView V{h->A.kind, h->A.n, h->A.m, h->A.s, h->A.r, h->A.data, h->A.corner, h->A.corner_rows,
+                 h->A.corner_cols};
+        CUDA_TRY(cudaStreamSynchronize(s));
+        h->gen.build(V, h->plan.p);
+      }
+    } else if (moved) {
+      h->tri.A0 = tri_rows(h->A);
+      if (!h->tri.lv.empty()) h->tri.lv[0]->A = h->tri.A0;
+    }
+    h->spec_factored = h->exact_factored = false;
+    h->speculative = true;  // a new matrix gets a fresh speculation
+    run_factor(h, s);
+    CUDA_TRY(cudaEventRecord(h->ev_done, s));
     return 0;
   } catch (const Fail& f_) {
     return set_err(err, errlen, f_.code, f_.msg);

@@ -313,8 +313,16 @@ __global__ void __launch_bounds__(32) tri_spec_factor_kernel(TriRows A, SegMap S
 // requests in flight.
 constexpr int kSepPerWarp = 4;
 __global__ void __launch_bounds__(256) tri_spec_sep_kernel(RowArr F, SegMap S, const double* __restrict__ wts,
-                                                            double* __restrict__ xsep) {
+                                                            double* __restrict__ xsep, DevStatus* reset) {
   const int lane = threadIdx.x & 31;
+  if (reset && blockIdx.x == 0 && threadIdx.x < kCertSlots + 2) {  // first kernel of the solve: fresh status
+    if (threadIdx.x < kCertSlots)
+      reset->cert_bits[threadIdx.x] = 0ull;
+    else if (threadIdx.x == kCertSlots)
+      reset->bad_seg = 0x7fffffff;
+    else
+      reset->pivot_seg = 0x7fffffff;
+  }
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nsep = S.nseg - 1;
   const int j0 = warp * kSepPerWarp;

@@ -199,3 +199,44 @@ def test_cuda_matches_reference_golden(cuda, path):
     assert O.rel_err(got, g["x_seq"]) <= 1e-12    # vs reference solve_sequential
     assert O.residual(A, got, f) <= 1e-13
     assert F.q == int(g["q"]) and F.dim == int(g["dim"])
+
+
+def test_async_and_refactor(cuda):
+    torch = cuda
+    A, f = psg.generate_config(1, 1 << 20, 3)
+    F = psg.parallel_factor(A, 1024)
+    xs = [torch.empty_like(f) for _ in range(3)]
+    fs = [f, f * 2.0, torch.flip(f, [0]).contiguous()]
+    for fi, xi in zip(fs, xs):
+        F.solve_async(fi, xi, timing=True)
+    st = psg.SolveStats()
+    F.sync(st)
+    assert st.speculative == 1 and st.fallbacks == 0 and st.phase3_seconds > 0
+    for fi, xi in zip(fs, xs):
+        assert psg.residual(A, xi, fi) <= 1e-13
+    # new values, same structure: refactor in place
+    A2, f2 = psg.generate_config(1, 1 << 20, 4)
+    F.refactor(A2)
+    x2 = torch.empty_like(f2)
+    F.solve_async(f2, x2)
+    F.sync()
+    assert psg.residual(A2, x2, f2) <= 1e-13
+    Ah = O.Matrix(A2.kind, A2.n, 1, 1, 1, A2.data.cpu().numpy())
+    assert O.rel_err(x2.cpu().numpy(), O.solve_sequential(Ah, f2.cpu().numpy())) <= 1e-12
+
+
+def test_async_repairs_failed_speculation(cuda):
+    torch = cuda
+    n, p = 40000, 40
+    A = _toeplitz(n, -1.0, 2.02, -1.0)   # weak dominance: the 32-row truncation is rejected
+    f = np.sin(np.arange(n) * 0.37)
+    GA = psg.StructuredMatrix(A.kind, A.n, A.m, A.s, A.r, _dev(cuda, A.data))
+    F = psg.parallel_factor(GA, p)
+    fd = _dev(cuda, f)
+    x = torch.empty_like(fd)
+    F.solve_async(fd, x)
+    st = psg.SolveStats()
+    F.sync(st)
+    assert st.fallbacks == 1
+    want, _ = O.parallel_solve(A, p, f)
+    assert O.rel_err(x.cpu().numpy(), want) <= 1e-10
