@@ -143,7 +143,7 @@ int psg_plan(const psg_desc* A, int p, int* body_begin, int* body_end, int* sep_
 int psg_residual(const psg_desc* A, const double* x, const double* f, int on_device,
                  void* stream, double* out, char* err, size_t errlen);
 int psg_matvec(const psg_desc* A, const double* x, double* y, int on_device, void* stream,
-               char* err, size_t errlen);
+               char* err, size_t errlen); /* host vectors (on_device = 0) are staged through the device */
 
 /* BASELINE config generator on the device (same stream mapping and values as
  * oracle/parsol_oracle.c or_generate_config).  Shapes via psg_config_shape. */
@@ -151,6 +151,11 @@ int psg_config_shape(int cfg, int size, int* kind, int* n, int* m, int* s, int* 
                      size_t* data_len, int* corner_rows, int* corner_cols);
 int psg_generate_config(int cfg, int size, uint64_t seed, double* data, double* corner,
                         double* f, void* stream, char* err, size_t errlen);
+
+/* make() validation (src/structmat.cpp:153-207, plus the Babd s = m, r = 0
+ * layout) and body_entry_count (:64-84) -- host-only, no device work. */
+int psg_validate(const psg_desc* A, char* err, size_t errlen);
+size_t psg_body_entry_count(int kind, int n, int m, int s, int r);
 
 /* Options (per handle): */
 enum psg_option {

@@ -1471,13 +1471,47 @@ long psg_debug_buffer(const psg_handle* hc, int what, double* out, long cap) {
   return cnt;
 }
 
+int psg_validate(const psg_desc* A, char* err, size_t errlen) {
+  try {
+    validate(*A);
+    return 0;
+  } catch (const Fail& f_) {
+    return set_err(err, errlen, f_.code, f_.msg);
+  }
+}
+
+size_t psg_body_entry_count(int kind, int n, int m, int s, int r) { return body_entry_count(kind, n, m, s, r); }
+
 int psg_matvec(const psg_desc* A, const double* x, double* y, int on_device, void* stream, char* err, size_t errlen) {
   try {
     validate(*A);
-    if (!on_device || !A->on_device) throw Fail{PSG_E_INVALID_PARAMETER, "psg_matvec needs device pointers"};
+    cudaStream_t s = (cudaStream_t)stream;
     MatView v{A->kind, A->n, A->m, A->s, A->r, A->data, A->corner, A->corner_rows, A->corner_cols};
-    matvec_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(v, x, y);
+    DevBuf<double> dd, dc, dxv, dyv;
+    if (!A->on_device) {
+      dd.alloc(A->data_len);
+      CUDA_TRY(cudaMemcpyAsync(dd.p, A->data, sizeof(double) * A->data_len, cudaMemcpyHostToDevice, s));
+      v.data = dd.p;
+      if (A->corner) {
+        const size_t cn = (size_t)A->corner_rows * A->corner_cols;
+        dc.alloc(cn);
+        CUDA_TRY(cudaMemcpyAsync(dc.p, A->corner, sizeof(double) * cn, cudaMemcpyHostToDevice, s));
+        v.corner = dc.p;
+      }
+    }
+    const double* xd = x;
+    double* yd = y;
+    if (!on_device) {
+      dxv.alloc(A->n);
+      dyv.alloc(A->n);
+      CUDA_TRY(cudaMemcpyAsync(dxv.p, x, sizeof(double) * A->n, cudaMemcpyHostToDevice, s));
+      xd = dxv.p;
+      yd = dyv.p;
+    }
+    matvec_kernel<<<148 * 8, 256, 0, s>>>(v, xd, yd);
     LAUNCH_CHECK();
+    if (!on_device) CUDA_TRY(cudaMemcpyAsync(y, yd, sizeof(double) * A->n, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
     return 0;
   } catch (const Fail& f_) {
     return set_err(err, errlen, f_.code, f_.msg);

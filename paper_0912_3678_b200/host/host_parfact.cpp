@@ -1,0 +1,143 @@
+// host_parfact.cpp -- parallel_factor / solve / solve_reduced / residual /
+// solve_sequential of the C++ API (reference proj/include/parsol/parfact.hpp,
+// seqref.hpp), each a thin call into the C ABI (psg.h): no CPU fallback.
+#include <algorithm>
+#include <string>
+
+#include "parsol/parfact.hpp"
+#include "parsol/seqref.hpp"
+#include "psg.h"
+
+namespace parsol {
+
+namespace {
+
+psg_desc host_desc(const StructuredMatrix& A) {
+  return psg_desc{int(A.kind), A.n, A.m, A.s, A.r, A.data.data(), A.data.size(),
+                  A.corner.empty() ? nullptr : A.corner.data(), A.corner_rows, A.corner_cols, 0};
+}
+
+void check(int rc, const char* err) {
+  if (rc) fail(Errc(rc - 1), err);
+}
+
+void add_stats(SolveStats* st, const psg_stats& s) {
+  if (!st) return;
+  st->factor_seconds = s.factor_seconds;
+  st->phase1_seconds += s.phase1_seconds;
+  st->phase2_seconds += s.phase2_seconds;
+  st->phase3_seconds += s.phase3_seconds;
+  st->reduced_ops += s.reduced_ops;
+  st->certificate = std::max(st->certificate, s.certificate);
+  st->fallbacks += s.fallbacks;
+}
+
+}  // namespace
+
+ParallelFactorization parallel_factor(const StructuredMatrix& A, int p, Strategy strategy, double tol) {
+  char err[512];
+  ParallelFactorization F;
+  F.strategy = strategy;
+  F.plan = plan_partition(A, p);
+  psg_handle* h = nullptr;
+  const psg_desc d = host_desc(A);
+  check(psg_factor(&d, p, int(strategy), tol, nullptr, &h, err, sizeof err), err);
+  F.device = std::shared_ptr<psg_handle>(h, psg_release);
+  F.n = A.n;
+  int q = 0, dim = 0, k = 0, corner = 0;
+  psg_reduced_info(h, &q, &dim, &k, &corner);
+  ReducedSystem& R = F.reduced;
+  R.q = q;
+  R.dim = dim;
+  R.has_corner = corner != 0;
+  for (int j = 0; j < q; ++j) {
+    R.block_sizes.push_back(k);
+    R.positions.push_back(F.plan.separator_starts[j]);
+    R.offsets.push_back(j * k);
+  }
+  // kept_maps (src/parfact.cpp:106-127): reduced indices of each partition's separators
+  F.kept_maps.assign(p, {});
+  for (int i = 0; i < p; ++i) {
+    const int left = corner ? i : i - 1, right = corner ? i + 1 : i;
+    if (left >= 0)
+      for (int t = 0; t < k; ++t) F.kept_maps[i].push_back(left * k + t);
+    if (right < q)
+      for (int t = 0; t < k; ++t) F.kept_maps[i].push_back(right * k + t);
+  }
+  if (dim <= kDenseReducedLimit) {  // dense image of T for callers and oracles
+    const int kk = k * k;
+    std::vector<double> dg(std::size_t(q) * kk), sb(std::size_t(q) * kk), sp(std::size_t(q) * kk);
+    check(psg_reduced_blocks(h, dg.data(), sb.data(), sp.data(), err, sizeof err), err);
+    R.T = DenseMatrix(dim, dim);
+    for (int j = 0; j < q; ++j)
+      for (int t = 0; t < k; ++t)
+        for (int u = 0; u < k; ++u) {
+          R.T.at(j * k + t, j * k + u) = dg[std::size_t(j) * kk + t * k + u];
+          if (j > 0) R.T.at(j * k + t, (j - 1) * k + u) = sb[std::size_t(j) * kk + t * k + u];
+          if (j + 1 < q) R.T.at(j * k + t, (j + 1) * k + u) = sp[std::size_t(j) * kk + t * k + u];
+        }
+    if (corner)
+      for (int t = 0; t < k; ++t)
+        for (int u = 0; u < k; ++u) R.T.at(t, (q - 1) * k + u) += sb[t * k + u];
+  }
+  psg_stats s{};
+  F.factor_seconds = 0;
+  return F;
+}
+
+Vector solve(const ParallelFactorization& F, const Vector& f, SolveStats* stats) {
+  if (int(f.size()) != F.n) fail(Errc::DimensionMismatch, "rhs length");
+  char err[512];
+  Vector x(f.size());
+  psg_stats s{};
+  check(psg_solve(F.device.get(), f.data(), x.data(), 0, nullptr, stats ? &s : nullptr, err, sizeof err), err);
+  add_stats(stats, s);
+  return x;
+}
+
+void solve_device(const ParallelFactorization& F, const double* f_dev, double* x_dev, SolveStats* stats,
+                  void* stream) {
+  char err[512];
+  psg_stats s{};
+  check(psg_solve(F.device.get(), f_dev, x_dev, 1, stream, stats ? &s : nullptr, err, sizeof err), err);
+  add_stats(stats, s);
+}
+
+Vector solve_reduced(const ParallelFactorization& F, const Vector& rhs, SolveStats* stats) {
+  if (int(rhs.size()) != F.reduced.dim) fail(Errc::DimensionMismatch, "reduced rhs length");
+  char err[512];
+  Vector x(rhs.size());
+  psg_stats s{};
+  check(psg_solve_reduced(F.device.get(), rhs.data(), x.data(), 0, nullptr, stats ? &s : nullptr, err, sizeof err),
+        err);
+  if (stats) stats->reduced_ops += s.reduced_ops;
+  return x;
+}
+
+double residual(const StructuredMatrix& A, const Vector& x, const Vector& f) {
+  if (int(x.size()) != A.n || int(f.size()) != A.n) fail(Errc::DimensionMismatch, "residual lengths");
+  char err[512];
+  double out = 0;
+  const psg_desc d = host_desc(A);
+  check(psg_residual(&d, x.data(), f.data(), 0, nullptr, &out, err, sizeof err), err);
+  return out;
+}
+
+// No CPU solver in this library: the sequential reference entry point runs
+// the GPU partition solver with bodies of ~1023 rows (units of m for blocked kinds).
+Vector solve_sequential(const StructuredMatrix& A, const Vector& f) {
+  const int unit = A.kind == Kind::Banded ? 1 : A.m;
+  const int units = A.n / unit;
+  int p = std::max(2, units / 1024);
+  // keep the plan feasible for small systems (each body at least one separator wide)
+  while (p > 2) {
+    const int k_units = A.kind == Kind::Banded ? std::max(A.s, A.r) : 1;
+    const long seps = A.kind == Kind::Babd ? p + 1 : p - 1;
+    if (units - seps * k_units >= long(p) * std::max(1, k_units)) break;
+    p /= 2;
+  }
+  ParallelFactorization F = parallel_factor(A, p, Strategy::Lu);
+  return solve(F, f);
+}
+
+}  // namespace parsol
