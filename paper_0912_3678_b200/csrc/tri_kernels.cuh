@@ -215,12 +215,20 @@ __device__ __forceinline__ double warp_tri_pcr(double lo, double di, double up, 
 constexpr int kWRow = 68;
 constexpr int kFacSeps = 16;             // separators per warp (one per half-warp lane pair)
 constexpr int kWin = 2 * kHalo + 1;      // window rows t-32 .. t+32
-constexpr int kFacPitch = kFacSeps + 1;  // [row][separator] tile pitch (odd: conflict-free)
+constexpr int kFacPitch = 70;            // per-(array, separator) window slot: 65 rows + staging slack,
+                                         // 16-byte multiple; 70 = 6 mod 16 keeps lane conflicts 2-way
 
+// One warp = 16 consecutive separators.  Every (array, separator) window is
+// one TMA bulk copy (48 per warp, all in flight on one mbarrier); each lane
+// then sweeps its own window in shared memory, lanes < 16 the trailing block
+// (top-down LU) and lanes >= 16 the leading block (bottom-up UL) of the same
+// separator; the weight rows leave through one TMA bulk store.
 __global__ void __launch_bounds__(32) tri_spec_factor_kernel(TriRows A, SegMap S, double* __restrict__ wts,
                                                              double* __restrict__ Tdiag) {
   constexpr unsigned FULL = 0xffffffffu;
-  __shared__ __align__(16) double tile[3][kWin * kFacPitch];
+  __shared__ __align__(16) double tile[3 * kFacSeps * kFacPitch];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ int shifts[3 * kFacSeps];
   const int lane = threadIdx.x;
   const int nsep = S.nseg - 1;
   const int j0 = blockIdx.x * kFacSeps;
@@ -233,33 +241,30 @@ __global__ void __launch_bounds__(32) tri_spec_factor_kernel(TriRows A, SegMap S
     seg_of(S, min(j0 + jj, nsep - 1), s0, L0);
     tme = s0 + L0;
   }
-  // ---- windows -> shared, transposed ([row][separator]), all copies in flight
-#pragma unroll 1
-  for (int q = 0; q < kFacSeps; ++q) {
-    const long t = __shfl_sync(FULL, tme, q);
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-      const int k = ch * 32 + lane;
-      if (k < kWin) {
-        const long r = t - kHalo + k;
-        cp_async8(&tile[0][k * kFacPitch + q], A.a.p + r);
-        cp_async8(&tile[1][k * kFacPitch + q], A.b.p + r);
-        cp_async8(&tile[2][k * kFacPitch + q], A.c.p + r);
-      }
-    }
-  }
-  cp_async_wait_all();
+  // ---- windows -> shared: task = (array x, separator q), one bulk copy each
+  if (lane == 0) mbar_init(&bar, 3 * kFacSeps);
   __syncwarp();
-  // ---- one sweep per lane: lanes < 16 trailing block (rows 0..31, downwards in
-  //      the matrix = upwards in k), lanes >= 16 leading block (rows 64..33)
+  for (int task = lane; task < 3 * kFacSeps; task += 32) {
+    const int x = task / kFacSeps, q = task % kFacSeps;
+    const long t = tme;  // q == lane & 15 for every task this lane issues
+    const RowArr X = x == 0 ? A.a : x == 1 ? A.b : A.c;
+    uint32_t tx = 0;
+    shifts[task] = stage_issue(X, t - kHalo, t + kHalo + 1, tile + task * kFacPitch, &bar, &tx);
+    mbar_arrive_expect_tx(&bar, tx);
+  }
+  __syncwarp();
+  mbar_wait(&bar, 0);
+  const double* wA = tile + (0 * kFacSeps + jj) * kFacPitch + 1 + shifts[0 * kFacSeps + jj];
+  const double* wB = tile + (1 * kFacSeps + jj) * kFacPitch + 1 + shifts[1 * kFacSeps + jj];
+  const double* wC = tile + (2 * kFacSeps + jj) * kFacPitch + 1 + shifts[2 * kFacSeps + jj];
+  // ---- one sweep per lane: lanes < 16 the trailing block (window rows 0..31
+  //      downwards), lanes >= 16 the leading block (rows 64..33 upwards)
   const bool trail = lane < kFacSeps;
-  const double* Nm = trail ? tile[0] : tile[2];  // multiplier numerator (a | c)
-  const double* Qc = trail ? tile[2] : tile[0];  // coupling to the previous row (c | a)
-  const double* Bd = tile[1];
-  const int w0r = trail ? 0 : kWin - 1;
-  const int dw = trail ? kFacPitch : -kFacPitch;
-  int off = w0r * kFacPitch + jj;
-  double piv = Bd[off];
+  const double* Nm = trail ? wA : wC;  // multiplier numerator (a | c)
+  const double* Qc = trail ? wC : wA;  // coupling to the previous row (c | a)
+  const int dw = trail ? 1 : -1;
+  int off = trail ? 0 : kWin - 1;
+  double piv = wB[off];
   double qprev = Qc[off];
   double m[kHalo];
 #pragma unroll
@@ -267,21 +272,20 @@ __global__ void __launch_bounds__(32) tri_spec_factor_kernel(TriRows A, SegMap S
     off += dw;
     const double l = Nm[off] * fast_rcp(piv);
     m[k] = l;
-    piv = fma(-l, qprev, Bd[off]);
+    piv = fma(-l, qprev, wB[off]);
     qprev = Qc[off];
   }
   const double u31 = fast_rcp(piv);  // v_31 (trailing) or w_0 (leading)
   const double other = __shfl_xor_sync(FULL, u31, kFacSeps);
   const double v31 = trail ? u31 : other, w0 = trail ? other : u31;
-  const int ts = kHalo * kFacPitch + jj;  // separator row t in the tile
-  const double at = tile[0][ts], bt = tile[1][ts], ct = tile[2][ts];
-  const double kR = at * tile[2][ts - kFacPitch] * v31;
-  const double kL = ct * tile[0][ts + kFacPitch] * w0;
+  const double at = wA[kHalo], bt = wB[kHalo], ct = wC[kHalo];  // separator row t
+  const double kR = at * wC[kHalo - 1] * v31;
+  const double kL = ct * wA[kHalo + 1] * w0;
   const double td = b_minus(bt, kR, kL);
   const double it = 1.0 / td;
   __syncwarp();
   // ---- weight rows -> shared (reusing the tile) -> one bulk store
-  double* wout = &tile[0][0];
+  double* wout = tile;
   const double sc = (trail ? -at : -ct) * it;
   double u = u31;
   wout[jj * kWRow + (trail ? kHalo - 1 : kHalo)] = sc * u;
