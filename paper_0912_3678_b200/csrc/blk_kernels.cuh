@@ -1,0 +1,783 @@
+// blk_kernels.cuh -- the speculative partition method for K x K block-
+// tridiagonal structure: BlockTridiagonal m = K and Banded s, r <= K (a band
+// matrix is block tridiagonal with K x K blocks on any K-aligned row grid).
+// K = 2..4.  The scalar tridiagonal path (tri_kernels.cuh) is the K = 1 case
+// of the same design:
+//
+//   factor (blk_spec_factor_kernel): per separator block S (K rows), the
+//     Schur complement T = A_SS - B1 [B_T^-1]_{near} C_T - C0 [B_L^-1]_{near} A_L
+//     of the TRUNCATED neighbouring bodies (HB block rows each side), and the
+//     weights that give x_S = T^-1 f_S + sum W^T_d f(S-(d+1)K) + sum W^L_d f(S+K+dK)
+//     -- the separator row of F T G restricted to the truncation window
+//     (src/localfact.cpp:84-225 computes the same blocks on full bodies);
+//   solve:
+//     blk_spec_sep_kernel      x_S from the weights (warp per separator);
+//     blk_segment_solve_kernel the bodies, exact given x_S (warp per body, block
+//                              chunk elimination + block PCR across lanes);
+//     blk_cert_kernel          componentwise backward error of every separator
+//                              row from the bodies' boundary records.
+//   A failed certificate sends the solve to the exact generic path
+//   (gen_exact.cuh), whose level-0 back-substitution is this same body kernel.
+//
+// No pivoting inside blocks (the reference's Lu/Lud strategies assume the
+// same; a vanished pivot is reported as ZeroPivot by the exact path).
+#pragma once
+
+#include "gen_exact.cuh"
+#include "psg_common.cuh"
+
+namespace psg {
+
+// ---------------------------------------------------------------------------
+// register K x K block algebra (segment kernel)
+// ---------------------------------------------------------------------------
+template <int K>
+struct Blk {
+  double v[K][K];
+};
+template <int K>
+struct Vec {
+  double v[K];
+};
+
+template <int K>
+__device__ __forceinline__ Blk<K> blk_mul(const Blk<K>& A, const Blk<K>& B) {
+  Blk<K> C;
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      double acc = A.v[i][0] * B.v[0][j];
+#pragma unroll
+      for (int l = 1; l < K; ++l) acc = fma(A.v[i][l], B.v[l][j], acc);
+      C.v[i][j] = acc;
+    }
+  return C;
+}
+
+// C -= A B
+template <int K>
+__device__ __forceinline__ void blk_mul_sub(Blk<K>& C, const Blk<K>& A, const Blk<K>& B) {
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      double acc = C.v[i][j];
+#pragma unroll
+      for (int l = 0; l < K; ++l) acc = fma(-A.v[i][l], B.v[l][j], acc);
+      C.v[i][j] = acc;
+    }
+}
+
+template <int K>
+__device__ __forceinline__ Vec<K> blk_mv(const Blk<K>& A, const Vec<K>& x) {
+  Vec<K> y;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    double acc = A.v[i][0] * x.v[0];
+#pragma unroll
+    for (int l = 1; l < K; ++l) acc = fma(A.v[i][l], x.v[l], acc);
+    y.v[i] = acc;
+  }
+  return y;
+}
+
+// y -= A x
+template <int K>
+__device__ __forceinline__ void blk_mv_sub(Vec<K>& y, const Blk<K>& A, const Vec<K>& x) {
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    double acc = y.v[i];
+#pragma unroll
+    for (int l = 0; l < K; ++l) acc = fma(-A.v[i][l], x.v[l], acc);
+    y.v[i] = acc;
+  }
+}
+
+template <int K>
+__device__ __forceinline__ void blk_neg(Blk<K>& A) {
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j < K; ++j) A.v[i][j] = -A.v[i][j];
+}
+
+template <int K>
+__device__ __forceinline__ void blk_set_eye(Blk<K>& A) {
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j < K; ++j) A.v[i][j] = i == j ? 1.0 : 0.0;
+}
+
+template <int K>
+__device__ __forceinline__ void blk_set_zero(Blk<K>& A) {
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j < K; ++j) A.v[i][j] = 0.0;
+}
+
+// In-place inverse, Gauss-Jordan without pivoting; sum |1/pivot| -> *rsum.
+template <int K>
+__device__ __forceinline__ void blk_inv(Blk<K>& A, double* rsum) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const double p = fast_rcp(A.v[k][k]);
+    *rsum += fabs(p);
+    A.v[k][k] = 1.0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) A.v[k][j] *= p;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      if (i == k) continue;
+      const double f = A.v[i][k];
+      A.v[i][k] = 0.0;
+#pragma unroll
+      for (int j = 0; j < K; ++j) A.v[i][j] = fma(-f, A.v[k][j], A.v[i][j]);
+    }
+  }
+}
+
+template <int K>
+__device__ __forceinline__ Blk<K> blk_shfl(const Blk<K>& a, int src) {
+  Blk<K> r;
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j < K; ++j) r.v[i][j] = __shfl_sync(0xffffffffu, a.v[i][j], src);
+  return r;
+}
+template <int K>
+__device__ __forceinline__ Vec<K> vec_shfl(const Vec<K>& a, int src) {
+  Vec<K> r;
+#pragma unroll
+  for (int i = 0; i < K; ++i) r.v[i] = __shfl_sync(0xffffffffu, a.v[i], src);
+  return r;
+}
+
+__device__ __forceinline__ long band_start(long n, int s, int d) {
+  long off = 0;
+  for (int b = -s; b < d; ++b) off += n - (b < 0 ? -b : b);
+  return off;
+}
+
+// ---------------------------------------------------------------------------
+// body solver
+// ---------------------------------------------------------------------------
+enum BlkLayout { kBlkBlockTri = 0, kBlkBanded = 1 };
+
+struct BlkArgs {
+  const double* data;  // matrix storage (reference layout)
+  long n;              // scalar dimension
+  int s, r;            // banded: bandwidths (<= K)
+  const double* f;     // rhs by global row
+  double* x;           // solution by global row
+  const double* xsep;  // separator values, K per separator (separator index order)
+  const GPart* part;   // bodies: [b, b+L), separators ls / rs (-1: none)
+  int nseg;
+  double* rec;         // certificate records (4K per body) or null
+  DevStatus* status;
+};
+
+template <int K, int M>
+struct BlkSmem {
+  static constexpr int NBMAX = 32 * M;             // block rows per body
+  static constexpr int P = NBMAX + 1;              // element-major pitch (odd)
+  static constexpr int PB = NBMAX * K + 1;         // banded: band pitch (odd)
+  static constexpr int MAT_BT = 3 * K * K * P;     // block tridiagonal staging
+  static constexpr int MAT_BD = (2 * K + 1) * PB;  // banded staging (bands -K..K)
+  static constexpr int STASH = 32 * M * (2 * K * K + K);
+  static constexpr int MAT = (MAT_BT > STASH ? MAT_BT : STASH);
+  static constexpr int MATB = (MAT_BD > STASH ? MAT_BD : STASH);
+  static constexpr int F = NBMAX * K + 1;
+  static constexpr int bytes(int layout) { return 8 * ((layout == kBlkBlockTri ? MAT : MATB) + F); }
+};
+
+// Certificate record of one body (4K doubles): for its left separator rows u,
+//   rec[0..K)  sum_t A(ls+u, b+t) y(b+t)   rec[K..2K)  sum |.|
+// and for its right separator rows with the body's last rows
+//   rec[2K..3K) signed                      rec[3K..4K) abs.
+
+template <int K, int M, int LAYOUT>
+__global__ void __launch_bounds__(32) blk_segment_solve_kernel(BlkArgs g) {
+  using SM = BlkSmem<K, M>;
+  constexpr int P = SM::P, PB = SM::PB;
+  constexpr int KK = K * K;
+  constexpr int MATD = LAYOUT == kBlkBlockTri ? SM::MAT : SM::MATB;
+  constexpr unsigned FULL = 0xffffffffu;
+  extern __shared__ __align__(16) double sm[];
+  double* smf = sm + MATD;  // rhs / solution by body row
+  const int lane = threadIdx.x;
+  const int seg = blockIdx.x;
+  const GPart Pt = g.part[seg];
+  const long b = Pt.b;
+  const int L = Pt.L;
+  const int NB = (L + K - 1) / K;
+  const int NR = NB * K;
+  const long n = g.n;
+  const int lsi = seg - 1, rsi = seg;
+
+  // ---- staging (element-major / band-major)
+  if (LAYOUT == kBlkBlockTri) {
+    // block rows B0..B0+NB-1 are contiguous: [(3 B0 - 1) KK, (3 (B0+NB) - 1) KK)
+    const long B0 = b / K;
+    const long g0 = (3 * B0 - 1) * KK;
+    const long tot = (long)NB * 3 * KK;
+    const long glen = (3 * (n / K) - 2) * KK;
+    constexpr int U = 16;  // loads in flight per lane
+    for (long i0 = lane; i0 < tot; i0 += 32 * U) {
+      double v[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const long i = i0 + 32 * k, gi = g0 + i;
+        v[k] = (i < tot && gi >= 0 && gi < glen) ? __ldg(g.data + gi) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const long i = i0 + 32 * k;
+        if (i < tot) {
+          const int q = (int)(i / (3 * KK)), e = (int)(i % (3 * KK));
+          sm[e * P + q] = v[k];
+        }
+      }
+    }
+  } else {
+    constexpr int U = 8;
+    for (int d = -g.s; d <= g.r; ++d) {
+      const long bs = band_start(n, g.s, d) - (d < 0 ? -d : 0);
+      for (int x0 = lane; x0 < NR; x0 += 32 * U) {
+        double v[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          const int xr = x0 + 32 * k;
+          const long row = b + xr, col = row + d;
+          v[k] = (xr < L && col >= 0 && col < n) ? __ldg(g.data + bs + row) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k)
+          if (x0 + 32 * k < NR) sm[(d + K) * PB + x0 + 32 * k] = v[k];
+      }
+    }
+  }
+  {
+    constexpr int U = 8;
+    for (int x0 = lane; x0 < NR; x0 += 32 * U) {
+      double v[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) v[k] = x0 + 32 * k < L ? __ldg(g.f + b + x0 + 32 * k) : 0.0;
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+        if (x0 + 32 * k < NR) smf[x0 + 32 * k] = v[k];
+    }
+  }
+  Vec<K> xl, xrv;
+#pragma unroll
+  for (int u = 0; u < K; ++u) {
+    xl.v[u] = Pt.ls >= 0 ? __ldg(g.xsep + (long)lsi * K + u) : 0.0;
+    xrv.v[u] = Pt.rs >= 0 ? __ldg(g.xsep + (long)rsi * K + u) : 0.0;
+  }
+  __syncwarp();
+  // staged A(b+xrow, b+ycol) (0 outside the structure)
+  auto elem = [&](int xrow, int ycol) -> double {
+    if (LAYOUT == kBlkBlockTri) {
+      const int q = xrow / K;
+      const int qc = ycol >= 0 ? ycol / K : -1;
+      const int blk = qc - q + 1;
+      if (blk < 0 || blk > 2) return 0.0;
+      return sm[(blk * KK + (xrow - q * K) * K + (ycol - qc * K)) * P + q];
+    } else {
+      const int d = ycol - xrow;
+      if (d < -g.s || d > g.r) return 0.0;
+      return sm[(d + K) * PB + xrow];
+    }
+  };
+  // fold the separator couplings of the first / last K body rows into the rhs
+  if (lane < K) {
+    if (Pt.ls >= 0) {
+      double fv = smf[lane];
+#pragma unroll
+      for (int t = 0; t < K; ++t) fv = fma(-elem(lane, t - K), xl.v[t], fv);
+      smf[lane] = fv;
+    }
+  } else if (lane >= 16 && lane < 16 + K) {
+    const int xrow = L - K + (lane - 16);
+    if (Pt.rs >= 0) {
+      double fv = smf[xrow];
+#pragma unroll
+      for (int t = 0; t < K; ++t) fv = fma(-elem(xrow, L + t), xrv.v[t], fv);
+      smf[xrow] = fv;
+    }
+  }
+  __syncwarp();
+
+  // block (q, blk) with separator columns and padding rows masked out
+  auto load_blk = [&](int q, int blk) {
+    Blk<K> B;
+#pragma unroll
+    for (int u = 0; u < K; ++u)
+#pragma unroll
+      for (int v = 0; v < K; ++v) {
+        const int xrow = q * K + u, ycol = (q + blk - 1) * K + v;
+        double val;
+        if (LAYOUT == kBlkBlockTri) {
+          val = sm[(blk * KK + u * K + v) * P + q];
+        } else {
+          const int d = ycol - xrow;
+          val = (d >= -g.s && d <= g.r) ? sm[(d + K) * PB + xrow] : 0.0;
+        }
+        if (xrow >= L)
+          val = (blk == 1 && u == v) ? 1.0 : 0.0;  // padding: identity, decoupled
+        else if (ycol < 0 || ycol >= L)
+          val = 0.0;  // folded into the rhs
+        B.v[u][v] = val;
+      }
+    return B;
+  };
+
+  // ---- block chunk elimination: AP_j y_first + y_j + CP_j y_last = DP_j
+  Blk<K> AP[M], CP[M];
+  Vec<K> DP[M];
+  double rsum = 0.0;
+  const int q0 = lane * M;
+#pragma unroll
+  for (int j = 0; j < M; ++j) {
+    const int q = q0 + j;
+    Blk<K> Ab, Db, Cb;
+    Vec<K> Fv;
+    if (q < NB) {
+      Ab = load_blk(q, 0);
+      Db = load_blk(q, 1);
+      Cb = load_blk(q, 2);
+#pragma unroll
+      for (int u = 0; u < K; ++u) Fv.v[u] = smf[q * K + u];
+    } else {
+      blk_set_zero<K>(Ab);
+      blk_set_zero<K>(Cb);
+      blk_set_eye<K>(Db);
+#pragma unroll
+      for (int u = 0; u < K; ++u) Fv.v[u] = 0.0;
+    }
+    if (j < 2) {
+      blk_inv<K>(Db, &rsum);
+      AP[j] = blk_mul<K>(Db, Ab);
+      CP[j] = blk_mul<K>(Db, Cb);
+      DP[j] = blk_mv<K>(Db, Fv);
+    } else {
+      blk_mul_sub<K>(Db, Ab, CP[j - 1]);
+      blk_inv<K>(Db, &rsum);
+      blk_mv_sub<K>(Fv, Ab, DP[j - 1]);
+      DP[j] = blk_mv<K>(Db, Fv);
+      const Blk<K> aap = blk_mul<K>(Ab, AP[j - 1]);
+      AP[j] = blk_mul<K>(Db, aap);
+      blk_neg<K>(AP[j]);
+      CP[j] = blk_mul<K>(Db, Cb);
+    }
+  }
+#pragma unroll
+  for (int j = M - 3; j >= 1; --j) {
+    blk_mv_sub<K>(DP[j], CP[j], DP[j + 1]);
+    blk_mul_sub<K>(AP[j], CP[j], AP[j + 1]);
+    CP[j] = blk_mul<K>(CP[j], CP[j + 1]);
+    blk_neg<K>(CP[j]);
+  }
+  if (M >= 3) {
+    Blk<K> R;
+    blk_set_eye<K>(R);
+    blk_mul_sub<K>(R, CP[0], AP[1]);
+    blk_inv<K>(R, &rsum);
+    blk_mv_sub<K>(DP[0], CP[0], DP[1]);
+    DP[0] = blk_mv<K>(R, DP[0]);
+    AP[0] = blk_mul<K>(R, AP[0]);
+    const Blk<K> cc = blk_mul<K>(CP[0], CP[1]);
+    CP[0] = blk_mul<K>(R, cc);
+    blk_neg<K>(CP[0]);
+  }
+  // ---- chunk interfaces: one normalised block row per lane in F = y_first
+  Blk<K> al, ga, be;
+  Vec<K> de = DP[0];
+  blk_set_eye<K>(be);
+  blk_set_zero<K>(al);
+  {
+    const int lo1 = lane > 0 ? lane - 1 : 0;
+    const Blk<K> pa = blk_shfl<K>(AP[M - 1], lo1);
+    if (lane > 0) {
+      al = blk_mul<K>(AP[0], pa);
+      blk_neg<K>(al);
+    }
+    const Blk<K> pc = blk_shfl<K>(CP[M - 1], lo1);
+    if (lane > 0) blk_mul_sub<K>(be, AP[0], pc);
+    const Vec<K> pd = vec_shfl<K>(DP[M - 1], lo1);
+    if (lane > 0) blk_mv_sub<K>(de, AP[0], pd);
+  }
+  blk_mul_sub<K>(be, CP[0], AP[M - 1]);
+  blk_mv_sub<K>(de, CP[0], DP[M - 1]);
+  ga = blk_mul<K>(CP[0], CP[M - 1]);
+  blk_neg<K>(ga);
+  // stash the chunk state in the consumed staging area (lane-interleaved)
+  __syncwarp();
+  {
+    double* st = sm + lane;
+#pragma unroll
+    for (int j = 0; j < M; ++j)
+#pragma unroll
+      for (int u = 0; u < K; ++u) {
+#pragma unroll
+        for (int v = 0; v < K; ++v) {
+          st[32 * ((j * K + u) * (2 * K + 1) + 2 * v)] = AP[j].v[u][v];
+          st[32 * ((j * K + u) * (2 * K + 1) + 2 * v + 1)] = CP[j].v[u][v];
+        }
+        st[32 * ((j * K + u) * (2 * K + 1) + 2 * K)] = DP[j].v[u];
+      }
+  }
+  blk_inv<K>(be, &rsum);
+  al = blk_mul<K>(be, al);
+  ga = blk_mul<K>(be, ga);
+  de = blk_mv<K>(be, de);
+#pragma unroll 1
+  for (int st = 1; st < 32; st <<= 1) {
+    const bool hl = lane >= st, hh = lane + st < 32;
+    const int sl = hl ? lane - st : lane, sh = hh ? lane + st : lane;
+    Blk<K> nb, na, ng;
+    blk_set_eye<K>(nb);
+    Vec<K> nd = de;
+    {
+      const Blk<K> lg = blk_shfl<K>(ga, sl);
+      if (hl) blk_mul_sub<K>(nb, al, lg);
+      const Blk<K> la = blk_shfl<K>(al, sl);
+      if (hl)
+        na = blk_mul<K>(al, la);
+      else
+        blk_set_zero<K>(na);
+      const Vec<K> ld = vec_shfl<K>(de, sl);
+      if (hl) blk_mv_sub<K>(nd, al, ld);
+    }
+    {
+      const Blk<K> ha = blk_shfl<K>(al, sh);
+      if (hh) blk_mul_sub<K>(nb, ga, ha);
+      const Blk<K> hg = blk_shfl<K>(ga, sh);
+      if (hh)
+        ng = blk_mul<K>(ga, hg);
+      else
+        blk_set_zero<K>(ng);
+      const Vec<K> hd = vec_shfl<K>(de, sh);
+      if (hh) blk_mv_sub<K>(nd, ga, hd);
+    }
+    blk_inv<K>(nb, &rsum);
+    al = blk_mul<K>(nb, na);
+    blk_neg<K>(al);
+    ga = blk_mul<K>(nb, ng);
+    blk_neg<K>(ga);
+    de = blk_mv<K>(nb, nd);
+  }
+  // ---- back-substitution
+  const Vec<K> Fv = de;
+  Vec<K> Fn = vec_shfl<K>(Fv, lane < 31 ? lane + 1 : lane);
+  if (lane == 31)
+#pragma unroll
+    for (int u = 0; u < K; ++u) Fn.v[u] = 0.0;
+#pragma unroll
+  for (int j = 0; j < M; ++j) {
+    const double* st = sm + lane;
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+#pragma unroll
+      for (int v = 0; v < K; ++v) {
+        AP[j].v[u][v] = st[32 * ((j * K + u) * (2 * K + 1) + 2 * v)];
+        CP[j].v[u][v] = st[32 * ((j * K + u) * (2 * K + 1) + 2 * v + 1)];
+      }
+      DP[j].v[u] = st[32 * ((j * K + u) * (2 * K + 1) + 2 * K)];
+    }
+  }
+  Vec<K> Ev = DP[M - 1];
+  blk_mv_sub<K>(Ev, AP[M - 1], Fv);
+  blk_mv_sub<K>(Ev, CP[M - 1], Fn);
+  bool finite = true;
+#pragma unroll
+  for (int j = 0; j < M; ++j) {
+    Vec<K> y;
+    if (j == 0) {
+      y = Fv;
+    } else if (j == M - 1) {
+      y = Ev;
+    } else {
+      y = DP[j];
+      blk_mv_sub<K>(y, AP[j], Fv);
+      blk_mv_sub<K>(y, CP[j], Ev);
+    }
+    const int q = q0 + j;
+    if (q < NB) {
+#pragma unroll
+      for (int u = 0; u < K; ++u) {
+        if (q * K + u < L) finite &= isfinite(y.v[u]);
+        smf[q * K + u] = y.v[u];
+      }
+    }
+  }
+  if (g.status) {
+    const bool piv_ok = __all_sync(FULL, isfinite(rsum));
+    const bool all_ok = __all_sync(FULL, finite);
+    if (lane == 0) {
+      if (!piv_ok) status_pivot(g.status, seg);
+      if (!all_ok) status_nonfinite(g.status, seg);
+    }
+  }
+  __syncwarp();
+  for (int r = lane; r < L; r += 32) g.x[b + r] = smf[r];
+  if (lane < K && Pt.rs >= 0) g.x[Pt.rs + lane] = xrv.v[lane];
+  // ---- certificate records: the separator rows' couplings to this body
+  if (g.rec) {
+    double* rc = g.rec + (long)seg * 4 * K;
+    auto at = [&](long row, long col) -> double {  // global A(row, col), known in range
+      if (LAYOUT == kBlkBlockTri) {
+        const long B = row / K, Bc = col / K;
+        if (Bc < B - 1 || Bc > B + 1) return 0.0;
+        const long off = B == 0 ? 0 : (3 * B - 1) * KK;
+        const long blk = B == 0 ? Bc - B : Bc - B + 1;
+        return __ldg(g.data + off + blk * KK + (row - B * K) * K + (col - Bc * K));
+      } else {
+        const int d = (int)(col - row);
+        if (d < -g.s || d > g.r) return 0.0;
+        return __ldg(g.data + band_start(n, g.s, d) + row - (d < 0 ? -d : 0));
+      }
+    };
+    if (lane < K) {
+      double sg = 0.0, ab = 0.0;
+      if (Pt.ls >= 0) {
+        const long row = Pt.ls + lane;
+        for (int t = 0; t < 2 * K && t < L; ++t) {
+          const double pr = at(row, b + t) * smf[t];
+          sg += pr;
+          ab += fabs(pr);
+        }
+      }
+      rc[lane] = sg;
+      rc[K + lane] = ab;
+    } else if (lane >= 16 && lane < 16 + K) {
+      const int u = lane - 16;
+      double sg = 0.0, ab = 0.0;
+      if (Pt.rs >= 0) {
+        const long row = Pt.rs + u;
+        for (int t = 1; t <= 2 * K && t <= L; ++t) {
+          const double pr = at(row, b + L - t) * smf[L - t];
+          sg += pr;
+          ab += fabs(pr);
+        }
+      }
+      rc[2 * K + u] = sg;
+      rc[3 * K + u] = ab;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// speculative factor: warp per separator, half-warp per side, one block
+// element per lane (lane e = 4u + v of its half), HB block rows per side.
+// ---------------------------------------------------------------------------
+struct BlkSpecArgs {
+  const double* data;
+  long n;
+  int s, r;
+  int layout;
+  int nsep;
+  const int* sep;  // separator start rows
+  double* W;       // out: per separator (1 + 2 HB) K*K: T^-1 | W^T_0..HB-1 | W^L_0..HB-1
+  double* Tdiag;   // out: per separator the K*K block A_SS (certificate)
+};
+
+// A(i, j) for the block kinds (0 outside the structure)
+__device__ __forceinline__ double blk_at(const BlkSpecArgs& g, int K, long i, long j) {
+  if (i < 0 || j < 0 || i >= g.n || j >= g.n) return 0.0;
+  if (g.layout == kBlkBlockTri) {
+    const long bi = i / K, bj = j / K;
+    if (bi - bj > 1 || bj - bi > 1) return 0.0;
+    const long off = bi == 0 ? 0 : (3 * bi - 1) * (long)K * K;
+    const long blk = bi > 0 ? bj - bi + 1 : bj - bi;
+    return __ldg(g.data + off + blk * K * K + (i - bi * K) * K + (j - bj * K));
+  }
+  const long d = j - i;
+  if (d < -g.s || d > g.r) return 0.0;
+  return __ldg(g.data + band_start(g.n, g.s, (int)d) + (i - (d < 0 ? -d : 0)));
+}
+
+// distributed K x K (K <= 4) algebra inside a 16-lane half (base 0 or 16),
+// lane base + 4u + v holds element (u, v); lanes with u or v >= K hold 0.
+__device__ __forceinline__ double dmul(double a, double b, int base, int u, int v, int K) {
+  double acc = 0.0;
+  for (int l = 0; l < K; ++l)
+    acc = fma(__shfl_sync(0xffffffffu, a, base + u * 4 + l), __shfl_sync(0xffffffffu, b, base + l * 4 + v), acc);
+  return acc;
+}
+// in-place Gauss-Jordan inverse without pivoting
+__device__ __forceinline__ double dinv(double a, int base, int u, int v, int K, double* rsum) {
+  for (int k = 0; k < K; ++k) {
+    const double akk = __shfl_sync(0xffffffffu, a, base + k * 4 + k);
+    const double auk = __shfl_sync(0xffffffffu, a, base + u * 4 + k);
+    const double akv = __shfl_sync(0xffffffffu, a, base + k * 4 + v);
+    const double p = fast_rcp(akk);
+    if (u == 0 && v == 0) *rsum += fabs(p);
+    if (u == k && v == k)
+      a = p;
+    else if (u == k)
+      a = akv * p;
+    else if (v == k)
+      a = -auk * p;
+    else
+      a = fma(-auk * p, akv, a);
+  }
+  return a;
+}
+
+template <int K, int HB>
+__global__ void __launch_bounds__(128) blk_spec_factor_kernel(BlkSpecArgs g) {
+  const int lane = threadIdx.x & 31;
+  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (j >= g.nsep) return;  // warp-uniform
+  constexpr int KK = K * K;
+  const int h = lane >> 4, e = lane & 15, u = e >> 2, v = e & 3;
+  const int base = h << 4;
+  const bool act = u < K && v < K;
+  const double eye = (u == v) ? 1.0 : 0.0;
+  const long S = g.sep[j];
+  const long n = g.n;
+  // Both halves run the same far -> near elimination (no divergence around the
+  // shuffles).  Block i = 0 (far) .. HB-1 (near) of side h starts at row
+  //   trailing (h = 0): S - (HB - i) K      leading (h = 1): S + K + (HB - 1 - i) K
+  // and couples to its farther neighbour through Fc (trailing: sub, leading:
+  // super) and to its nearer neighbour through Nc.  Element (u, v) of the
+  // sub / diag / super block of the block row at r0: t = 0 / 1 / 2.
+  const int tF = h == 0 ? 0 : 2, tN = 2 - tF;
+  auto prep = [&](int t, long& off, bool& ok) {
+    const int d = v - u + (t - 1) * K;
+    ok = act && (g.layout == kBlkBlockTri || (d >= -g.s && d <= g.r));
+    off = g.layout == kBlkBlockTri ? (long)t * KK + u * K + v : (ok ? band_start(n, g.s, d) - (d < 0 ? -d : 0) + u : 0);
+  };
+  long oD, oF, oN;
+  bool kD, kF, kN;
+  prep(1, oD, kD);
+  prep(tF, oF, kF);
+  prep(tN, oN, kN);
+  auto ld = [&](long r0, int t, long off, bool ok) -> double {
+    if (!ok) return 0.0;
+    if (g.layout == kBlkBlockTri) {
+      const long B = r0 / K;
+      return (B + t - 1 >= 0 && B + t - 1 < n / K) ? __ldg(g.data + (3 * B - 1) * KK + off) : 0.0;
+    }
+    const long col = r0 + v + (t - 1) * K;
+    return (col >= 0 && col < n) ? __ldg(g.data + off + r0) : 0.0;
+  };
+  double Dg[HB], Fc[HB], Nc[HB];
+#pragma unroll
+  for (int i = 0; i < HB; ++i) {
+    const long r0 = h == 0 ? S - (long)(HB - i) * K : S + K + (long)(HB - 1 - i) * K;
+    Dg[i] = act ? ld(r0, 1, oD, kD) : eye;
+    Fc[i] = ld(r0, tF, oF, kF);
+    Nc[i] = ld(r0, tN, oN, kN);
+  }
+  // couplings with the separator: B1 = A(S+u, S-K+v) / C0 = A(S+u, S+K+v);
+  // near block -> separator: A(S-K+u, S+v) / A(S+K+u, S+v)
+  const double Bc = act ? blk_at(g, K, S + u, h == 0 ? S - K + v : S + K + v) : 0.0;
+  const double Cc = act ? blk_at(g, K, h == 0 ? S - K + u : S + K + u, S + v) : 0.0;
+  const double Dss = act ? blk_at(g, K, S + u, S + v) : eye;
+  double rsum = 0.0;
+  double Np[HB];  // Np[i] = Fc[i+1] G_i (the weights' transfer from block i+1 to block i)
+#pragma unroll
+  for (int i = 0; i < HB; ++i) {
+    if (i > 0) Dg[i] -= dmul(Fc[i], dmul(Dg[i - 1], Nc[i - 1], base, u, v, K), base, u, v, K);
+    const double Gi = dinv(Dg[i], base, u, v, K, &rsum);
+    Dg[i] = act ? Gi : 0.0;
+    if (i > 0) Np[i - 1] = dmul(Fc[i], Dg[i - 1], base, u, v, K);
+  }
+  const double Xn = Dg[HB - 1];  // near diagonal block of the truncated inverse
+  const double part = dmul(Bc, dmul(Xn, Cc, base, u, v, K), base, u, v, K);
+  const double other = __shfl_xor_sync(0xffffffffu, part, 16);
+  double Ti = dinv(Dss - part - other, base, u, v, K, &rsum);
+  if (!act) Ti = 0.0;
+  double* out = g.W + (long)j * (1 + 2 * HB) * KK;
+  if (h == 0 && act) {
+    out[u * K + v] = Ti;
+    g.Tdiag[(long)j * KK + u * K + v] = Dss;
+  }
+  // weights near to far: W_0 = -T^-1 Bc G_near, W_d = -W_{d-1} Np[HB-1-d]
+  double w = -dmul(dmul(Ti, Bc, base, u, v, K), Xn, base, u, v, K);
+#pragma unroll
+  for (int d = 0; d < HB; ++d) {
+    if (d > 0) w = -dmul(w, Np[HB - 1 - d], base, u, v, K);
+    if (act) out[(long)(1 + h * HB + d) * KK + u * K + v] = w;
+  }
+  (void)rsum;  // a vanished pivot leaves non-finite weights: the certificate rejects them
+}
+
+// x_S = T^-1 f_S + sum_d W^T_d f(S-(d+1)K ..) + sum_d W^L_d f(S+K+dK ..):
+// warp per separator; block 0 also resets the solve's status slot.
+template <int K, int HB>
+__global__ void __launch_bounds__(128) blk_spec_sep_kernel(const double* __restrict__ W, const int* __restrict__ sep,
+                                                           int nsep, const double* __restrict__ f,
+                                                           double* __restrict__ xsep, DevStatus* reset) {
+  constexpr int KK = K * K, NBK = 1 + 2 * HB, BPI = 32 / KK;
+  const int lane = threadIdx.x & 31;
+  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (reset && blockIdx.x == 0 && threadIdx.x < kCertSlots + 2) {
+    if (threadIdx.x < kCertSlots)
+      reset->cert_bits[threadIdx.x] = 0ull;
+    else if (threadIdx.x == kCertSlots)
+      reset->bad_seg = INT_MAX;
+    else
+      reset->pivot_seg = INT_MAX;
+  }
+  if (j >= nsep) return;
+  const long S = sep[j];
+  const double* w = W + (long)j * NBK * KK;
+  const int e = lane % KK, slot = lane / KK;
+  const int v = e % K;
+  double acc = 0.0;
+  if (slot < BPI) {
+#pragma unroll 4
+    for (int blk = slot; blk < NBK; blk += BPI) {
+      const long row = blk == 0 ? S : (blk <= HB ? S - (long)blk * K : S + K + (long)(blk - 1 - HB) * K);
+      acc = fma(__ldg(w + (long)blk * KK + e), __ldg(f + row + v), acc);
+    }
+  }
+  __shared__ double red[4][32];
+  red[threadIdx.x >> 5][lane] = acc;
+  __syncwarp();
+  if (lane < K) {
+    double s = 0.0;
+    for (int t = 0; t < BPI * KK; ++t)
+      if ((t % KK) / K == lane) s += red[threadIdx.x >> 5][t];
+    xsep[(long)j * K + lane] = s;
+  }
+}
+
+// omega = max over separator rows of |f - A_SS x_S - left - right| / (|f| + sum |terms|).
+template <int K>
+__global__ void blk_cert_kernel(const double* __restrict__ Tdiag, const int* __restrict__ sep, int nsep,
+                                const double* __restrict__ f, const double* __restrict__ xsep,
+                                const double* __restrict__ rec, DevStatus* st) {
+  double worst = 0.0;
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < (long)nsep * K; t += (long)gridDim.x * blockDim.x) {
+    const long j = t / K;
+    const int u = (int)(t % K);
+    const long S = sep[j];
+    double sg = 0.0, ab = 0.0;
+#pragma unroll
+    for (int v = 0; v < K; ++v) {
+      const double pr = Tdiag[j * K * K + u * K + v] * xsep[j * K + v];
+      sg += pr;
+      ab += fabs(pr);
+    }
+    const double* rl = rec + j * 4 * K;        // body j: its right separator is j
+    const double* rr = rec + (j + 1) * 4 * K;  // body j+1: its left separator is j
+    sg += rl[2 * K + u] + rr[u];
+    ab += rl[3 * K + u] + rr[K + u];
+    const double fv = f[S + u];
+    const double num = fabs(fv - sg), den = fabs(fv) + ab;
+    double om = den > 0 ? num / den : num;
+    if (!(om <= 1.0e308)) om = __longlong_as_double(0x7ff0000000000000ll);
+    worst = fmax(worst, om);
+  }
+  for (int o = 16; o > 0; o >>= 1) worst = fmax(worst, __shfl_xor_sync(0xffffffffu, worst, o));
+  if ((threadIdx.x & 31) == 0 && worst > 0) status_cert(st, worst);
+}
+
+}  // namespace psg

@@ -23,6 +23,7 @@
 #include "gen_kernels.cuh"
 #include "psg_common.cuh"
 #include "tri_kernels.cuh"
+#include "blk_kernels.cuh"
 
 using namespace psg;
 
@@ -526,6 +527,185 @@ void envelope_of(int kind, int m, int s, int r, int& es, int& er) {  // scalar_e
   }
 }
 
+// ----------------------------------------------------------------------------
+// K x K block speculative path (blk_kernels.cuh)
+// ----------------------------------------------------------------------------
+template <int K, int M, int LAYOUT>
+void launch_blk_kernel(const BlkArgs& a, cudaStream_t s) {
+  constexpr int bytes = BlkSmem<K, M>::bytes(LAYOUT);
+  static bool attr = false;
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(blk_segment_solve_kernel<K, M, LAYOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  bytes));
+    attr = true;
+  }
+  blk_segment_solve_kernel<K, M, LAYOUT><<<a.nseg, 32, bytes, s>>>(a);
+  LAUNCH_CHECK();
+}
+
+// chunk depth M per block size: 32 M block rows per body
+int blk_chunk(int K, int NB) {
+  if (K == 4) return NB <= 64 ? 2 : 0;
+  if (K == 3) return NB <= 64 ? 2 : (NB <= 96 ? 3 : 0);
+  if (K == 2) return NB <= 96 ? 3 : (NB <= 160 ? 5 : 0);
+  return 0;
+}
+int blk_max_nb(int K) { return K == 4 ? 64 : (K == 3 ? 96 : 160); }
+
+bool launch_blk_segments(int K, int NB, int layout, const BlkArgs& a, cudaStream_t s) {
+  const int M = blk_chunk(K, NB);
+#define PSG_BLK_CASE(KK_, MM_)                                                   \
+  if (K == KK_ && M == MM_) {                                                    \
+    if (layout == kBlkBlockTri)                                                  \
+      launch_blk_kernel<KK_, MM_, kBlkBlockTri>(a, s);                           \
+    else                                                                         \
+      launch_blk_kernel<KK_, MM_, kBlkBanded>(a, s);                             \
+    return true;                                                                 \
+  }
+  PSG_BLK_CASE(4, 2)
+  PSG_BLK_CASE(3, 2)
+  PSG_BLK_CASE(3, 3)
+  PSG_BLK_CASE(2, 3)
+  PSG_BLK_CASE(2, 5)
+#undef PSG_BLK_CASE
+  return false;
+}
+
+// truncation depth in block rows per side (about 64 scalar rows)
+constexpr int blk_hb(int K) { return K == 2 ? 32 : 16; }
+
+// Speculative solver for the K x K block kinds.  Its bodies are the
+// reference plan's, each split into equal sub-bodies (extra K-row separators)
+// when longer than one warp's 32 M block rows.
+struct BlkSolver {
+  int K = 0, layout = 0, NB = 0;
+  bool possible = false;
+  BlkArgs base{};
+  std::vector<GPart> hpart;
+  std::vector<int> hsep;
+  DevBuf<GPart> part;
+  DevBuf<int> sep;
+  DevBuf<double> W, Tdiag, xsep, rec;
+  int nseg = 0, nsep = 0, launches = 0;
+
+  void init(const psg_desc& A, const Plan& P) {
+    possible = false;
+    if (P.has_corner) return;
+    if (A.kind == PSG_BLOCKTRI && A.m >= 2 && A.m <= 4) {
+      K = A.m;
+      layout = kBlkBlockTri;
+    } else if (A.kind == PSG_BANDED && P.sep_size >= 2 && P.sep_size <= 4) {
+      K = P.sep_size;
+      layout = kBlkBanded;
+    } else {
+      return;
+    }
+    const int unit = layout == kBlkBlockTri ? K : 1, ku = K / unit;
+    hpart.clear();
+    hsep.clear();
+    int maxL = 0, minL = INT_MAX;
+    for (int i = 0; i < P.p; ++i) {
+      const int b = P.body_begin(i), L = P.body_end(i) - b;
+      const int Lu = L / unit;
+      auto nb_of = [&](int t) { return (((Lu - (t - 1) * ku) + t - 1) / t * unit + K - 1) / K; };
+      int t = 1;
+      while (t < Lu && nb_of(t) > blk_max_nb(K)) ++t;
+      const int body = Lu - (t - 1) * ku, bs = body / t, br = body % t;
+      int cur = b;
+      for (int u = 0; u < t; ++u) {
+        const int len = (bs + (u < br ? 1 : 0)) * unit;
+        hpart.push_back(GPart{cur, len, -1, -1});
+        maxL = std::max(maxL, len);
+        minL = std::min(minL, len);
+        cur += len;
+        if (u + 1 < t || i + 1 < P.p) {
+          hsep.push_back(cur);
+          cur += K;
+        }
+      }
+    }
+    nseg = (int)hpart.size();
+    nsep = (int)hsep.size();
+    for (int g = 0; g < nseg; ++g) {
+      hpart[g].ls = g > 0 ? hsep[g - 1] : -1;
+      hpart[g].rs = g < nsep ? hsep[g] : -1;
+    }
+    NB = (maxL + K - 1) / K;
+    if (minL < blk_hb(K) * K || minL < 2 * K || blk_chunk(K, NB) == 0 || nsep < 1) return;
+    part.alloc(nseg);
+    sep.alloc(nsep);
+    CUDA_TRY(cudaMemcpy(part.p, hpart.data(), sizeof(GPart) * nseg, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(sep.p, hsep.data(), sizeof(int) * nsep, cudaMemcpyHostToDevice));
+    W.alloc((size_t)nsep * (1 + 2 * blk_hb(K)) * K * K);
+    Tdiag.alloc((size_t)nsep * K * K);
+    xsep.alloc((size_t)nsep * K);
+    rec.alloc((size_t)nseg * 4 * K);
+    base.n = A.n;
+    base.s = A.s;
+    base.r = A.r;
+    base.data = A.data;
+    base.part = part.p;
+    base.nseg = nseg;
+    possible = true;
+  }
+
+  void set_data(const double* d) { base.data = d; }
+
+  void spec_factor(cudaStream_t s) {
+    BlkSpecArgs g{};
+    g.data = base.data;
+    g.n = base.n;
+    g.s = base.s;
+    g.r = base.r;
+    g.layout = layout;
+    g.nsep = nsep;
+    g.sep = sep.p;
+    g.W = W.p;
+    g.Tdiag = Tdiag.p;
+    const int grid = (nsep + 3) / 4;
+    if (K == 4)
+      blk_spec_factor_kernel<4, blk_hb(4)><<<grid, 128, 0, s>>>(g);
+    else if (K == 3)
+      blk_spec_factor_kernel<3, blk_hb(3)><<<grid, 128, 0, s>>>(g);
+    else
+      blk_spec_factor_kernel<2, blk_hb(2)><<<grid, 128, 0, s>>>(g);
+    LAUNCH_CHECK();
+    launches += 1;
+  }
+
+  // sep -> bodies -> certificate; the first kernel resets the status slot.
+  void spec_solve(const double* f, double* x, DevStatus* st, cudaStream_t s, cudaEvent_t* ev) {
+    const int grid = (nsep + 3) / 4;
+    if (K == 4)
+      blk_spec_sep_kernel<4, blk_hb(4)><<<grid, 128, 0, s>>>(W.p, sep.p, nsep, f, xsep.p, st);
+    else if (K == 3)
+      blk_spec_sep_kernel<3, blk_hb(3)><<<grid, 128, 0, s>>>(W.p, sep.p, nsep, f, xsep.p, st);
+    else
+      blk_spec_sep_kernel<2, blk_hb(2)><<<grid, 128, 0, s>>>(W.p, sep.p, nsep, f, xsep.p, st);
+    LAUNCH_CHECK();
+    if (ev) {
+      CUDA_TRY(cudaEventRecord(ev[1], s));
+      CUDA_TRY(cudaEventRecord(ev[2], s));
+    }
+    BlkArgs a = base;
+    a.f = f;
+    a.x = x;
+    a.xsep = xsep.p;
+    a.rec = rec.p;
+    a.status = st;
+    if (!launch_blk_segments(K, NB, layout, a, s)) throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "block body too long"};
+    const int cg = std::min(148 * 8, (nsep * K + 255) / 256);
+    if (K == 4)
+      blk_cert_kernel<4><<<cg, 256, 0, s>>>(Tdiag.p, sep.p, nsep, f, xsep.p, rec.p, st);
+    else if (K == 3)
+      blk_cert_kernel<3><<<cg, 256, 0, s>>>(Tdiag.p, sep.p, nsep, f, xsep.p, rec.p, st);
+    else
+      blk_cert_kernel<2><<<cg, 256, 0, s>>>(Tdiag.p, sep.p, nsep, f, xsep.p, rec.p, st);
+    LAUNCH_CHECK();
+    launches += 3;
+  }
+};
+
 struct GenLevel {
   SMView A{};
   int es = 0, er = 0, k = 0, p = 0, q = 0;
@@ -684,10 +864,46 @@ struct GenSolver {
       }
       GenArgs g = args_of(L, l == 0 ? st : nullptr);
       g.xsep = L.x_next.p;
-      gen_backsolve_kernel<<<L.p, 32, 0, s>>>(g);
-      LAUNCH_CHECK();
+      if (!blk_backsolve(L, g, s)) {
+        gen_backsolve_kernel<<<L.p, 32, 0, s>>>(g);
+        LAUNCH_CHECK();
+      }
       launches += 1;
     }
+  }
+
+  // K x K block-tridiagonal levels (BlockTridiagonal m = K, Banded s, r <= K
+  // with separators of K rows) whose bodies fit one warp go through the block
+  // body kernel (blk_kernels.cuh) instead of the band back-substitution.
+  bool blk_backsolve(const GenLevel& L, const GenArgs& g, cudaStream_t s) {
+    static const bool off = getenv("PSG_NO_BLK") != nullptr;
+    if (off || L.corner || L.k < 2 || L.k > 4) return false;
+    int layout;
+    if (L.A.kind == PSG_BLOCKTRI && L.A.m == L.k)
+      layout = kBlkBlockTri;
+    else if (L.A.kind == PSG_BANDED && L.A.s <= L.k && L.A.r <= L.k)
+      layout = kBlkBanded;
+    else
+      return false;
+    int maxL = 0, minL = INT_MAX;
+    for (const GPart& P : L.hpart) {
+      maxL = std::max(maxL, P.L);
+      minL = std::min(minL, P.L);
+    }
+    if (minL < 2 * L.k) return false;
+    BlkArgs a{};
+    a.data = L.A.data;
+    a.n = L.A.n;
+    a.s = L.A.s;
+    a.r = L.A.r;
+    a.f = g.f;
+    a.x = g.x;
+    a.xsep = g.xsep;
+    a.part = g.part;
+    a.nseg = L.p;
+    a.rec = nullptr;
+    a.status = g.status;
+    return launch_blk_segments(L.k, (maxL + L.k - 1) / L.k, layout, a, s);
   }
 
   void restore_level1_wiring() {
@@ -719,6 +935,7 @@ struct psg_handle {
   DevBuf<double> own_data, own_corner;
   TriSolver tri;
   GenSolver gen;
+  BlkSolver blk;                        // speculative path of the K x K block kinds
   bool generic = false;                 // non-tridiagonal kinds: generic exact path
   double refine_tol = 1e-14;            // generic path: refine once when ||Ax-f||/||f|| exceeds this
   double last_residual = 0.0;
@@ -766,6 +983,8 @@ struct psg_handle {
     if (h_ring) cudaFreeHost(h_ring);
   }
   bool use_spec() const { return !generic && speculative && tri.spec_possible(); }
+  bool use_blk() const { return generic && speculative && blk.possible; }
+  bool spec_mode() const { return generic ? use_blk() : use_spec(); }
 };
 
 namespace {
@@ -838,10 +1057,17 @@ void run_factor(psg_handle* h, cudaStream_t s) {
   CUDA_TRY(cudaEventRecord(h->ev_f0, s));
   if (h->generic) {
     h->gen.launches = 0;
-    h->gen.factor(s);
-    h->exact_factored = true;
+    h->blk.launches = 0;
+    if (h->use_blk()) {
+      h->blk.spec_factor(s);
+      h->spec_factored = true;
+      h->factor_launches = h->blk.launches;
+    } else {
+      h->gen.factor(s);
+      h->exact_factored = true;
+      h->factor_launches = h->gen.launches;
+    }
     CUDA_TRY(cudaEventRecord(h->ev_f1, s));
-    h->factor_launches = h->gen.launches;
     return;
   }
   if (h->use_spec()) {
@@ -966,6 +1192,7 @@ int psg_factor(const psg_desc* Ain, int p, int strategy, double tol, void* strea
       SMView V{h->A.kind, h->A.n, h->A.m, h->A.s, h->A.r, h->A.data, h->A.corner, h->A.corner_rows, h->A.corner_cols};
       CUDA_TRY(cudaStreamSynchronize(s));  // plan uploads below use the legacy stream
       h->gen.build(V, p);
+      h->blk.init(h->A, h->plan);
     } else {
       int maxlen = 0, minlen = 0;
       SegMap S0 = plan_segments(h->plan, h->seg_start, h->seg_len, h->refined, maxlen, minlen);
@@ -991,8 +1218,7 @@ int psg_set_option(psg_handle* h, int option, double value) {
     switch (option) {
       case PSG_OPT_SPECULATIVE:
         h->speculative = value != 0.0;
-        if (h->generic) break;  // the generic path is exact
-        if ((h->use_spec() && !h->spec_factored) || (!h->use_spec() && !h->exact_factored)) {
+        if ((h->spec_mode() && !h->spec_factored) || (!h->spec_mode() && !h->exact_factored)) {
           run_factor(h, nullptr);
           CUDA_TRY(cudaEventRecord(h->ev_done, nullptr));
         }
@@ -1065,6 +1291,86 @@ int generic_solve(psg_handle* h, const double* df, double* dx, cudaStream_t s, b
   return launches;
 }
 
+struct Outcome {
+  double cert = 0;
+  bool bad = false, pivot = false;
+  int pivot_seg = 0;
+};
+
+Outcome read_status(const DevStatus& st) {
+  Outcome o;
+  for (int i = 0; i < kCertSlots; ++i) o.cert = std::max(o.cert, bits_to_double(st.cert_bits[i]));
+  o.pivot = st.pivot_seg != INT_MAX;
+  o.pivot_seg = st.pivot_seg;
+  o.bad = o.pivot || st.bad_seg != INT_MAX || !(o.cert == o.cert);
+  return o;
+}
+
+void ensure_exact_generic(psg_handle* h, cudaStream_t s) {
+  if (h->exact_factored) return;
+  h->gen.launches = 0;
+  h->gen.factor(s);
+  h->exact_factored = true;
+}
+
+// Block kinds: enqueue one speculative solve whose status lands in device
+// slot `st`, copied to host slot `hst` and marked by event `done`.
+int blk_enqueue(psg_handle* h, const double* df, double* dx, cudaStream_t s, DevStatus* st, DevStatus* hst,
+                cudaEvent_t done, cudaEvent_t* ev) {
+  h->blk.launches = 0;
+  if (ev) CUDA_TRY(cudaEventRecord(ev[0], s));
+  h->blk.spec_solve(df, dx, st, s, ev);
+  if (ev) CUDA_TRY(cudaEventRecord(ev[3], s));
+  CUDA_TRY(cudaMemcpyAsync(hst, st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaEventRecord(done, s));
+  return h->blk.launches;
+}
+
+void add_phase_stats(psg_handle* h, psg_stats* stats, cudaEvent_t* ev) {
+  float tf = 0, t01 = 0, t12 = 0, t23 = 0;
+  cudaEventElapsedTime(&tf, h->ev_f0, h->ev_f1);
+  cudaEventElapsedTime(&t01, ev[0], ev[1]);
+  cudaEventElapsedTime(&t12, ev[1], ev[2]);
+  cudaEventElapsedTime(&t23, ev[2], ev[3]);
+  stats->factor_seconds = tf * 1e-3;
+  stats->phase1_seconds += t01 * 1e-3;  // accumulate like SolveStats (src/parfact.cpp:233-237)
+  stats->phase2_seconds += t12 * 1e-3;
+  stats->phase3_seconds += t23 * 1e-3;
+}
+
+// Generic kinds, blocking: the block speculative path when possible, else (or
+// when its certificate fails) the exact generic path with residual refinement.
+void generic_blocking(psg_handle* h, const double* df, double* dx, cudaStream_t s, psg_stats* stats) {
+  int fallbacks = 0;
+  if (h->use_blk()) {
+    if (!h->spec_factored) run_factor(h, s);
+    const int launches = blk_enqueue(h, df, dx, s, h->d_status.p, h->h_status, h->ev_done, stats ? h->ev : nullptr);
+    CUDA_TRY(cudaEventSynchronize(h->ev_done));
+    const Outcome o = read_status(*h->h_status);
+    if (!o.bad && o.cert <= h->cert_tol) {
+      h->solve_launches = launches;
+      if (stats) {
+        add_phase_stats(h, stats, h->ev);
+        stats->certificate = std::max(stats->certificate, o.cert);
+        stats->speculative = 1;
+      }
+      return;
+    }
+    fallbacks = 1;
+    h->speculative = false;  // speculative interface rejected: this handle goes exact
+  }
+  ensure_exact_generic(h, s);
+  double cert = 0;
+  h->solve_launches = generic_solve(h, df, dx, s, stats != nullptr, &cert);
+  if (stats) {
+    add_phase_stats(h, stats, h->ev);
+    stats->reduced_ops += h->gen.reduced_ops();
+    stats->certificate = std::max(stats->certificate, cert);
+    stats->speculative = 0;
+    stats->fallbacks += fallbacks;
+  }
+}
+
 // Tridiagonal: enqueue one solve attempt whose status lands in device slot
 // `st`, copied to host slot `hst` and marked by event `done`.
 int tri_enqueue(psg_handle* h, const double* df, double* dx, cudaStream_t s, DevStatus* st, DevStatus* hst,
@@ -1087,21 +1393,6 @@ int tri_enqueue(psg_handle* h, const double* df, double* dx, cudaStream_t s, Dev
   CUDA_TRY(cudaMemcpyAsync(hst, st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaEventRecord(done, s));
   return h->tri.launches;
-}
-
-struct Outcome {
-  double cert = 0;
-  bool bad = false, pivot = false;
-  int pivot_seg = 0;
-};
-
-Outcome read_status(const DevStatus& st) {
-  Outcome o;
-  for (int i = 0; i < kCertSlots; ++i) o.cert = std::max(o.cert, bits_to_double(st.cert_bits[i]));
-  o.pivot = st.pivot_seg != INT_MAX;
-  o.pivot_seg = st.pivot_seg;
-  o.bad = o.pivot || st.bad_seg != INT_MAX || !(o.cert == o.cert);
-  return o;
 }
 
 // Blocking tridiagonal solve with the speculative -> exact fallback.
@@ -1171,23 +1462,7 @@ int psg_solve(const psg_handle* hc, const double* f, double* x, int on_device, v
       dx = h->d_x.p;
     }
     if (h->generic) {
-      double cert = 0;
-      const int launches = generic_solve(h, df, dx, s, stats != nullptr, &cert);
-      h->solve_launches = launches;
-      if (stats) {
-        float tf = 0, t01 = 0, t12 = 0, t23 = 0;
-        cudaEventElapsedTime(&tf, h->ev_f0, h->ev_f1);
-        cudaEventElapsedTime(&t01, h->ev[0], h->ev[1]);
-        cudaEventElapsedTime(&t12, h->ev[1], h->ev[2]);
-        cudaEventElapsedTime(&t23, h->ev[2], h->ev[3]);
-        stats->factor_seconds = tf * 1e-3;
-        stats->phase1_seconds += t01 * 1e-3;
-        stats->phase2_seconds += t12 * 1e-3;
-        stats->phase3_seconds += t23 * 1e-3;
-        stats->reduced_ops += h->gen.reduced_ops();
-        stats->certificate = std::max(stats->certificate, cert);
-        stats->speculative = 0;
-      }
+      generic_blocking(h, df, dx, s, stats);
     } else {
       tri_solve_blocking(h, df, dx, s, stats);
     }
@@ -1218,14 +1493,17 @@ void drain(psg_handle* h, psg_stats* stats) {
       cudaEventElapsedTime(&t23, h->ring_t[pd.slot][2], h->ring_t[pd.slot][3]);
       stats->phase1_seconds += t01 * 1e-3;
       stats->phase3_seconds += t23 * 1e-3;
-      stats->reduced_ops += h->tri.reduced_ops(pd.spec);
+      if (!h->generic) stats->reduced_ops += h->tri.reduced_ops(pd.spec);
       stats->certificate = std::max(stats->certificate, o.cert);
       stats->speculative = pd.spec ? 1 : 0;
     }
     if (!o.bad && o.cert <= h->cert_tol) continue;
     if (stats) stats->fallbacks += 1;
     h->speculative = false;
-    tri_solve_blocking(h, pd.f, pd.x, pd.s, nullptr);  // exact (throws on a genuine zero pivot)
+    if (h->generic)
+      generic_blocking(h, pd.f, pd.x, pd.s, nullptr);
+    else
+      tri_solve_blocking(h, pd.f, pd.x, pd.s, nullptr);  // exact (throws on a genuine zero pivot)
   }
 }
 
@@ -1237,9 +1515,8 @@ int psg_solve_async(const psg_handle* hc, const double* f, double* x, int timing
   std::lock_guard<std::mutex> g(h->mu);
   try {
     cudaStream_t s = (cudaStream_t)stream;
-    if (h->generic) {  // the generic path certifies by a residual pass: blocking
-      double cert = 0;
-      h->solve_launches = generic_solve(h, f, x, s, false, &cert);
+    if (h->generic && !h->use_blk()) {  // the exact generic path certifies by a residual pass: blocking
+      generic_blocking(h, f, x, s, nullptr);
       CUDA_TRY(cudaEventRecord(h->ev_done, s));
       return 0;
     }
@@ -1253,9 +1530,12 @@ int psg_solve_async(const psg_handle* hc, const double* f, double* x, int timing
     }
     if ((int)h->pending.size() >= psg_handle::kRing) drain(h, nullptr);
     const int slot = (int)(h->async_count++ % psg_handle::kRing);
-    const bool spec = h->use_spec();
-    const int launches = tri_enqueue(h, f, x, s, h->d_ring.p + slot, h->h_ring + slot, h->ring_done[slot],
-                                     timing ? h->ring_t[slot] : nullptr, spec);
+    const bool spec = h->spec_mode();
+    const int launches =
+        h->generic ? blk_enqueue(h, f, x, s, h->d_ring.p + slot, h->h_ring + slot, h->ring_done[slot],
+                                 timing ? h->ring_t[slot] : nullptr)
+                   : tri_enqueue(h, f, x, s, h->d_ring.p + slot, h->h_ring + slot, h->ring_done[slot],
+                                 timing ? h->ring_t[slot] : nullptr, spec);
     h->pending.push_back(psg_handle::Pending{slot, f, x, s, spec, timing != 0, launches});
     h->solve_launches = launches;
     CUDA_TRY(cudaEventRecord(h->ev_done, s));
@@ -1318,6 +1598,7 @@ int psg_refactor(psg_handle* h, const psg_desc* A, void* stream, char* err, size
                  h->A.corner_cols};
         CUDA_TRY(cudaStreamSynchronize(s));
         h->gen.build(V, h->plan.p);
+        h->blk.set_data(h->A.data);
       }
     } else if (moved) {
       h->tri.A0 = tri_rows(h->A);
@@ -1348,6 +1629,10 @@ int psg_reduced_blocks(const psg_handle* hc, double* diag, double* sub, double* 
   try {
     CUDA_TRY(cudaEventSynchronize(h->ev_done));
     if (h->generic) {
+      if (!h->exact_factored) {  // parallel_factor's ReducedSystem comes from the exact path
+        ensure_exact_generic(h, nullptr);
+        CUDA_TRY(cudaDeviceSynchronize());
+      }
       GenLevel& L = *h->gen.lv[0];
       const int q = L.q, k = L.k, kk = k * k;
       std::vector<double> T(L.Tdata.n), C(kk, 0.0);
@@ -1409,6 +1694,7 @@ int psg_solve_reduced(const psg_handle* hc, const double* rhs, double* x, int on
     cudaStream_t s = (cudaStream_t)stream;
     if (h->generic) {
       if (h->gen.lv.size() < 2) throw Fail{PSG_E_INVALID_PARAMETER, "no reduced system"};
+      ensure_exact_generic(h, s);
       const int dim = h->gen.lv[0]->q * h->gen.lv[0]->k;
       DevBuf<double> dr, dxv;
       const double* r = rhs;
