@@ -24,6 +24,7 @@
 #include "psg_common.cuh"
 #include "tri_kernels.cuh"
 #include "blk_kernels.cuh"
+#include "chain_kernels.cuh"
 
 using namespace psg;
 
@@ -706,6 +707,173 @@ struct BlkSolver {
   }
 };
 
+// ----------------------------------------------------------------------------
+// BVP-layout BABD chain path (chain_kernels.cuh)
+// ----------------------------------------------------------------------------
+struct ChainLevel {
+  int nb = 0, P = 0;
+  bool direct = false;
+  const double* data = nullptr;
+  const double* f = nullptr;
+  double* x = nullptr;
+  std::vector<int> hcut;
+  DevBuf<int> cut;
+  DevBuf<double> next_data, next_f, next_x, corr_x;
+};
+
+constexpr int kChainDirect = 64;  // levels with at most this many block rows are solved by one warp
+constexpr int kChainChunk = 32;   // chunk length (steps) of the reduced levels
+constexpr int kChainChunk0 = 16;  // chunk length of level 0
+
+struct ChainSolver {
+  int MB = 0;
+  bool possible = false;
+  const double* corner = nullptr;
+  std::vector<std::unique_ptr<ChainLevel>> lv;
+  int launches = 0;
+
+  void init(const psg_desc& A, const Plan& P) {
+    possible = false;
+    lv.clear();
+    if (A.kind != PSG_BABD || A.s != A.m || A.r != 0 || !P.has_corner) return;
+    if (A.corner_rows != A.m || A.corner_cols != A.m) return;
+    if (A.m != 2 && A.m != 4 && A.m != 8) return;
+    MB = A.m;
+    corner = A.corner;
+    auto L = std::make_unique<ChainLevel>();
+    L->nb = A.n / MB;
+    L->data = A.data;
+    // level-0 chunks of ~kChainChunk0 blocks (internal; independent of the
+    // reference plan, whose reduced system the exact path keeps)
+    L->P = (L->nb - 1 + kChainChunk0 - 1) / kChainChunk0;
+    for (int k = 0; k <= L->P; ++k) L->hcut.push_back(int((long)k * (L->nb - 1) / L->P));
+    for (;;) {
+      ChainLevel& c = *L;
+      c.cut.alloc(c.hcut.size());
+      CUDA_TRY(cudaMemcpy(c.cut.p, c.hcut.data(), sizeof(int) * c.hcut.size(), cudaMemcpyHostToDevice));
+      const int nb2 = c.P + 1;
+      c.next_data.alloc((size_t)MB * MB + (size_t)(nb2 - 1) * 2 * MB * MB);
+      c.next_f.alloc((size_t)nb2 * MB);
+      c.next_x.alloc((size_t)nb2 * MB);
+      if (lv.empty()) c.corr_x.alloc((size_t)nb2 * MB);
+      auto N = std::make_unique<ChainLevel>();
+      N->nb = nb2;
+      N->data = c.next_data.p;
+      N->f = c.next_f.p;
+      N->x = c.next_x.p;
+      lv.push_back(std::move(L));
+      if (nb2 <= kChainDirect) {
+        N->direct = true;
+        lv.push_back(std::move(N));
+        break;
+      }
+      N->P = (nb2 - 1 + kChainChunk - 1) / kChainChunk;
+      for (int k = 0; k <= N->P; ++k) N->hcut.push_back(int((long)k * (nb2 - 1) / N->P));
+      L = std::move(N);
+    }
+    possible = true;
+  }
+
+  void set_data(const double* d, const double* c) {
+    if (!lv.empty()) lv[0]->data = d;
+    corner = c;
+  }
+
+  ChainLevelArgs args(ChainLevel& L, DevStatus* st) const {
+    ChainLevelArgs g{};
+    g.data = L.data;
+    g.corner = corner;
+    g.nb = L.nb;
+    g.P = L.P;
+    g.cut = L.cut.p;
+    g.f = L.f;
+    g.x = L.x;
+    g.next_data = L.next_data.p;
+    g.next_f = L.next_f.p;
+    g.next_x = L.next_x.p;
+    g.status = st;
+    return g;
+  }
+
+  template <int M>
+  void factor_t(cudaStream_t s) {
+    for (auto& L : lv) {
+      if (L->direct) break;
+      const int threads = L->P * M;
+      chain_factor_kernel<M><<<(threads + 127) / 128, 128, 0, s>>>(args(*L, nullptr));
+      LAUNCH_CHECK();
+      ++launches;
+    }
+  }
+
+  template <int M>
+  void solve_t(const double* f, double* x, DevStatus* st, cudaStream_t s, cudaEvent_t* ev) {
+    lv[0]->f = f;
+    lv[0]->x = x;
+    for (auto& L : lv) {
+      if (L->direct) break;
+      chain_condense_kernel<M><<<(L->P * M + 127) / 128, 128, 0, s>>>(args(*L, nullptr));
+      LAUNCH_CHECK();
+      ++launches;
+    }
+    if (ev) CUDA_TRY(cudaEventRecord(ev[1], s));
+    upper_t<M>(s, 1);
+    if (ev) CUDA_TRY(cudaEventRecord(ev[2], s));
+    // level 0: final pass, condensing its separator residuals for one correction
+    ChainLevel& L0 = *lv[0];
+    ChainLevelArgs a = args(L0, nullptr);
+    a.corr_f = L0.next_f.p;
+    chain_final_kernel<M><<<(L0.P * M + 127) / 128, 128, 0, s>>>(a);
+    LAUNCH_CHECK();
+    ++launches;
+    // correction: A d = r (separator rows) through the reduced levels, then x += d
+    lv[1]->x = L0.corr_x.p;
+    for (size_t l = 1; l < lv.size(); ++l) {
+      ChainLevel& L = *lv[l];
+      if (L.direct) break;
+      chain_condense_kernel<M><<<(L.P * M + 127) / 128, 128, 0, s>>>(args(L, nullptr));
+      LAUNCH_CHECK();
+      ++launches;
+    }
+    upper_t<M>(s, 1);
+    lv[1]->x = L0.next_x.p;
+    ChainLevelArgs c = args(L0, st);  // certifies the corrected separator rows
+    c.accumulate = 1;
+    c.corr_x = L0.corr_x.p;
+    chain_final_kernel<M><<<(L0.P * M + 127) / 128, 128, 0, s>>>(c);
+    LAUNCH_CHECK();
+    chain_bc_cert_kernel<M><<<1, 32, 0, s>>>(args(L0, st));
+    LAUNCH_CHECK();
+    launches += 2;
+  }
+
+  // direct solve of the last level and final passes of levels >= from (top down)
+  template <int M>
+  void upper_t(cudaStream_t s, size_t from) {
+    chain_direct_kernel<M><<<1, 32, 0, s>>>(args(*lv.back(), nullptr));
+    LAUNCH_CHECK();
+    ++launches;
+    for (size_t l = lv.size() - 1; l-- > from;) {
+      ChainLevel& L = *lv[l];
+      chain_final_kernel<M><<<(L.P * M + 127) / 128, 128, 0, s>>>(args(L, nullptr));
+      LAUNCH_CHECK();
+      ++launches;
+    }
+  }
+
+  void factor(cudaStream_t s) {
+    if (MB == 8) factor_t<8>(s);
+    else if (MB == 4) factor_t<4>(s);
+    else factor_t<2>(s);
+  }
+  // status slot must be reset by the caller
+  void solve(const double* f, double* x, DevStatus* st, cudaStream_t s, cudaEvent_t* ev) {
+    if (MB == 8) solve_t<8>(f, x, st, s, ev);
+    else if (MB == 4) solve_t<4>(f, x, st, s, ev);
+    else solve_t<2>(f, x, st, s, ev);
+  }
+};
+
 struct GenLevel {
   SMView A{};
   int es = 0, er = 0, k = 0, p = 0, q = 0;
@@ -936,6 +1104,7 @@ struct psg_handle {
   TriSolver tri;
   GenSolver gen;
   BlkSolver blk;                        // speculative path of the K x K block kinds
+  ChainSolver chain;                    // BVP-layout BABD chain path
   bool generic = false;                 // non-tridiagonal kinds: generic exact path
   double refine_tol = 1e-14;            // generic path: refine once when ||Ax-f||/||f|| exceeds this
   double last_residual = 0.0;
@@ -984,7 +1153,8 @@ struct psg_handle {
   }
   bool use_spec() const { return !generic && speculative && tri.spec_possible(); }
   bool use_blk() const { return generic && speculative && blk.possible; }
-  bool spec_mode() const { return generic ? use_blk() : use_spec(); }
+  bool use_chain() const { return generic && speculative && chain.possible; }
+  bool spec_mode() const { return generic ? (use_blk() || use_chain()) : use_spec(); }
 };
 
 namespace {
@@ -1062,6 +1232,11 @@ void run_factor(psg_handle* h, cudaStream_t s) {
       h->blk.spec_factor(s);
       h->spec_factored = true;
       h->factor_launches = h->blk.launches;
+    } else if (h->use_chain()) {
+      h->chain.launches = 0;
+      h->chain.factor(s);
+      h->spec_factored = true;
+      h->factor_launches = h->chain.launches;
     } else {
       h->gen.factor(s);
       h->exact_factored = true;
@@ -1193,6 +1368,7 @@ int psg_factor(const psg_desc* Ain, int p, int strategy, double tol, void* strea
       CUDA_TRY(cudaStreamSynchronize(s));  // plan uploads below use the legacy stream
       h->gen.build(V, p);
       h->blk.init(h->A, h->plan);
+      h->chain.init(h->A, h->plan);
     } else {
       int maxlen = 0, minlen = 0;
       SegMap S0 = plan_segments(h->plan, h->seg_start, h->seg_len, h->refined, maxlen, minlen);
@@ -1317,13 +1493,28 @@ void ensure_exact_generic(psg_handle* h, cudaStream_t s) {
 // slot `st`, copied to host slot `hst` and marked by event `done`.
 int blk_enqueue(psg_handle* h, const double* df, double* dx, cudaStream_t s, DevStatus* st, DevStatus* hst,
                 cudaEvent_t done, cudaEvent_t* ev) {
-  h->blk.launches = 0;
-  if (ev) CUDA_TRY(cudaEventRecord(ev[0], s));
-  h->blk.spec_solve(df, dx, st, s, ev);
+  int launches;
+  if (h->use_blk()) {
+    h->blk.launches = 0;
+    if (ev) CUDA_TRY(cudaEventRecord(ev[0], s));
+    h->blk.spec_solve(df, dx, st, s, ev);  // its first kernel resets the status slot
+    launches = h->blk.launches;
+  } else {
+    DevStatus init{};
+    for (int i = 0; i < kCertSlots; ++i) init.cert_bits[i] = 0ull;
+    init.bad_seg = INT_MAX;
+    init.pivot_seg = INT_MAX;
+    *hst = init;
+    CUDA_TRY(cudaMemcpyAsync(st, hst, sizeof(DevStatus), cudaMemcpyHostToDevice, s));
+    h->chain.launches = 0;
+    if (ev) CUDA_TRY(cudaEventRecord(ev[0], s));
+    h->chain.solve(df, dx, st, s, ev);
+    launches = h->chain.launches;
+  }
   if (ev) CUDA_TRY(cudaEventRecord(ev[3], s));
   CUDA_TRY(cudaMemcpyAsync(hst, st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaEventRecord(done, s));
-  return h->blk.launches;
+  return launches;
 }
 
 void add_phase_stats(psg_handle* h, psg_stats* stats, cudaEvent_t* ev) {
@@ -1342,7 +1533,7 @@ void add_phase_stats(psg_handle* h, psg_stats* stats, cudaEvent_t* ev) {
 // when its certificate fails) the exact generic path with residual refinement.
 void generic_blocking(psg_handle* h, const double* df, double* dx, cudaStream_t s, psg_stats* stats) {
   int fallbacks = 0;
-  if (h->use_blk()) {
+  if (h->use_blk() || h->use_chain()) {
     if (!h->spec_factored) run_factor(h, s);
     const int launches = blk_enqueue(h, df, dx, s, h->d_status.p, h->h_status, h->ev_done, stats ? h->ev : nullptr);
     CUDA_TRY(cudaEventSynchronize(h->ev_done));
@@ -1515,7 +1706,7 @@ int psg_solve_async(const psg_handle* hc, const double* f, double* x, int timing
   std::lock_guard<std::mutex> g(h->mu);
   try {
     cudaStream_t s = (cudaStream_t)stream;
-    if (h->generic && !h->use_blk()) {  // the exact generic path certifies by a residual pass: blocking
+    if (h->generic && !h->spec_mode()) {  // the exact generic path certifies by a residual pass: blocking
       generic_blocking(h, f, x, s, nullptr);
       CUDA_TRY(cudaEventRecord(h->ev_done, s));
       return 0;
@@ -1599,6 +1790,7 @@ int psg_refactor(psg_handle* h, const psg_desc* A, void* stream, char* err, size
         CUDA_TRY(cudaStreamSynchronize(s));
         h->gen.build(V, h->plan.p);
         h->blk.set_data(h->A.data);
+        h->chain.set_data(h->A.data, h->A.corner);
       }
     } else if (moved) {
       h->tri.A0 = tri_rows(h->A);

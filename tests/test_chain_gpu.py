@@ -1,0 +1,100 @@
+"""GPU parity of the BVP-layout BABD chain path (chain_kernels.cuh: Babd with
+s = m, r = 0, BASELINE config 4) against the oracle (bit-identical to the
+reference): config-4 instances at several sizes / partition counts, random
+BVP-layout matrices with m = 2, 4, 8, the async API and the exact option."""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_0912_3678_b200 as psg
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev(torch, a):
+    return None if a is None else torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _gpu(torch, A, p, f, opts=None):
+    GA = psg.StructuredMatrix(A.kind, A.n, A.m, A.s, A.r, _dev(torch, A.data), _dev(torch, A.corner),
+                              A.corner_rows, A.corner_cols)
+    F = psg.parallel_factor(GA, p)
+    for k, v in (opts or {}).items():
+        F.set_option(k, v)
+    st = psg.SolveStats()
+    x = psg.solve(F, _dev(torch, f), st).cpu().numpy()
+    return x, st, F, GA
+
+
+def random_bvp(m, nb, seed, h=None):
+    """BVP-layout BABD (block rows: BC [Ba | .. | Bb], then [S_b | R_b]) with
+    trapezoid-like steps S = -(I + h M_b), R = I - h M_{b+1}."""
+    rng = np.random.default_rng(seed)
+    h = h if h is not None else 0.5 / (nb - 1)
+    I = np.eye(m)
+    Ms = rng.uniform(-1, 1, size=(nb, m, m)) / m
+    Ba = I + 0.3 * rng.uniform(-1, 1, size=(m, m))
+    Bb = 0.5 * rng.uniform(-1, 1, size=(m, m))
+    rows = [Ba.ravel()]
+    for b in range(1, nb):
+        S = -(I + h * Ms[b - 1])
+        R = I - h * Ms[b]
+        rows.append(np.hstack([S, R]).ravel())
+    data = np.concatenate(rows)
+    A = O.Matrix(3, m * nb, m, m, 0, data, Bb.ravel().copy(), m, m)
+    f = rng.uniform(-1, 1, size=m * nb)
+    return A, f
+
+
+@pytest.mark.parametrize("size,p", [(1023, 8), (4095, 64), (1 << 14, 256), (1 << 15, 100)])
+def test_chain_config4_matches_oracle(cuda, size, p):
+    A, f = O.generate_config(4, size, 3)
+    want, _ = O.parallel_solve(A, p, f)
+    x, st, F, _ = _gpu(cuda, A, p, f)
+    assert st.speculative == 1, "chain path not taken"
+    assert st.certificate <= 1e-14
+    assert O.rel_err(x, want) <= 1e-10
+    assert O.residual(A, x, f) <= 1e-13
+
+
+@pytest.mark.parametrize("m,nb,p", [(2, 3000, 16), (4, 2000, 40), (8, 1500, 30), (8, 5000, 4)])
+def test_chain_random_bvp_matches_oracle(cuda, m, nb, p):
+    A, f = random_bvp(m, nb, 11 + m)
+    want, _ = O.parallel_solve(A, p, f)
+    x, st, F, _ = _gpu(cuda, A, p, f)
+    assert st.speculative == 1
+    assert O.rel_err(x, want) <= 1e-10
+    assert O.residual(A, x, f) <= 1e-13
+
+
+def test_chain_exact_option_matches(cuda):
+    A, f = O.generate_config(4, 2047, 5)
+    want, _ = O.parallel_solve(A, 16, f)
+    x, st, F, _ = _gpu(cuda, A, 16, f, {"speculative": 0.0})
+    assert st.speculative == 0
+    assert O.rel_err(x, want) <= 1e-10
+
+
+def test_chain_async_and_refactor(cuda):
+    torch = cuda
+    A1, f1 = O.generate_config(4, 4095, 1)
+    A2, f2 = O.generate_config(4, 4095, 2)
+    p = 64
+    GA = psg.StructuredMatrix(A1.kind, A1.n, A1.m, A1.s, A1.r, _dev(torch, A1.data), _dev(torch, A1.corner),
+                              A1.corner_rows, A1.corner_cols)
+    F = psg.parallel_factor(GA, p)
+    xs = [torch.empty(A1.n, dtype=torch.float64, device="cuda") for _ in range(2)]
+    dfs = [_dev(torch, f1), _dev(torch, f2)]
+    for df, dx in zip(dfs, xs):
+        F.solve_async(df, dx)
+    st = psg.SolveStats()
+    F.sync(st)
+    for f, dx in zip((f1, f2), xs):
+        want, _ = O.parallel_solve(A1, p, f)
+        assert O.rel_err(dx.cpu().numpy(), want) <= 1e-10
+    GA.data.copy_(_dev(torch, A2.data))
+    GA.corner.copy_(_dev(torch, A2.corner))
+    F.refactor(GA)
+    x = psg.solve(F, dfs[1]).cpu().numpy()
+    want, _ = O.parallel_solve(A2, p, f2)
+    assert O.rel_err(x, want) <= 1e-10
