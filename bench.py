@@ -194,6 +194,44 @@ def aggregate(ms_total_local, units_local, steps, dist=None, device="cpu"):
 # ---------------------------------------------------------------------------
 # our GPU path
 # ---------------------------------------------------------------------------
+OTHER = [(0, 1 << 20, 1024), (2, 1 << 20, 16384), (3, 1 << 24, 32768), (4, 1 << 18, 4096)]
+
+
+def other_configs(psg, torch, peak, dev, steps=5):
+    """The other BASELINE configs through the same production path (one handle,
+    refactor + async certified solve per step, device-timed), reported beside
+    the headline -- informative, outside its timed region."""
+    out = []
+    for cfg, size, p in OTHER:
+        A, f = psg.generate_config(cfg, size, cfg + 1, device=dev)
+        x = torch.empty_like(f)
+        H = psg.parallel_factor(A, p, psg.Strategy.Lu)
+        for _ in range(2):
+            H.refactor(A)
+            H.solve_async(f, x)
+        H.sync()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st = psg.SolveStats()
+        e0.record()
+        for _ in range(steps):
+            H.refactor(A)
+            H.solve_async(f, x, timing=True)
+        H.sync(st)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        corner = 0 if A.corner is None else A.corner.numel()
+        min_bytes = (A.data.numel() + corner + 2 * A.n) * 8
+        out.append({"cfg": cfg, "n": A.n, "p": p, "ms_per_step": ms, "unknowns_per_s": A.n / (ms / 1e3),
+                    "hbm_roofline_frac": min_bytes / (ms / 1e3) / 1e9 / peak, "min_bytes": min_bytes,
+                    "residual": psg.residual(A, x, f), "certificate": st.certificate,
+                    "path": "speculative" if st.speculative else "exact", "fallbacks": st.fallbacks})
+        H.close()
+        del A, f, x
+    return out
+
+
 def impl_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -325,6 +363,8 @@ def impl_ours(args, rank, world, local_rank):
                "path": "psg_factor(host A) + psg_solve(host f -> host x), pinned buffers"}
         assert torch.allclose(hx, x.cpu(), rtol=0, atol=1e-12)
 
+    other = None if args.no_other_configs else other_configs(psg, torch, peak, dev)
+
     cpu = None
     if not args.no_cpu_baseline:
         try:
@@ -355,6 +395,7 @@ def impl_ours(args, rank, world, local_rank):
                    "path": "parallel_factor (new handle) + blocking solve per step"},
         "certificate_max": cert, "speculative": spec, "residual": res,
         "gpu_launches": launches,
+        "other_configs": other,
         "clocks": clk,
         "e2e": e2e,
         "cpu_baseline": cpu,
@@ -371,6 +412,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
