@@ -40,6 +40,7 @@ struct ChainLevelArgs {
   double* next_f;        // condense: next level's rhs
   const double* next_x;  // final: next level's solution (x at the separators)
   double* corr_f;        // final (optional): condensed separator residuals R_sep^-1 r_sep -> next level rhs
+  double* tm;            // factor output / solve input: per block [T row i | M row i] (T = -R^-1 S, M = R^-1)
   int accumulate;        // final: x += chain of corr_x with zero forcing (the correction pass)
   const double* corr_x;  // accumulate: correction d at the separators (next_x keeps x_sep)
   DevStatus* status;
@@ -93,89 +94,6 @@ __device__ __forceinline__ void load_row(const double* data, int b, int i, doubl
 }
 
 // factor: Phi_j, written as next level row j+1 = [ -Phi_j | I ]; chunk 0 also copies Ba.
-template <int MB>
-__global__ void __launch_bounds__(128) chain_factor_kernel(ChainLevelArgs g) {
-  const int lane = threadIdx.x & 31, i = lane % MB;
-  const int j = (blockIdx.x * blockDim.x + threadIdx.x) / MB;
-  const bool live = j < g.P;
-  const int b0 = live ? g.cut[j] + 1 : 1, b1 = live ? g.cut[j + 1] : 0;
-  int len = b1 - b0 + 1, maxlen = len;
-  for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
-  double phi[MB];
-#pragma unroll
-  for (int c = 0; c < MB; ++c) phi[c] = i == c ? 1.0 : 0.0;
-  for (int t = 0; t < maxlen; ++t) {
-    const bool act = t < len;
-    double S[MB], R[MB], w[MB];
-    if (act) {
-      load_row<MB>(g.data, b0 + t, i, S, R);
-    } else {
-#pragma unroll
-      for (int c = 0; c < MB; ++c) {
-        S[c] = 0.0;
-        R[c] = i == c ? 1.0 : 0.0;
-      }
-    }
-    // w = -S Phi (row i)
-#pragma unroll
-    for (int c = 0; c < MB; ++c) w[c] = 0.0;
-#pragma unroll
-    for (int l = 0; l < MB; ++l)
-#pragma unroll
-      for (int c = 0; c < MB; ++c) w[c] = fma(-S[l], gshfl<MB>(phi[c], l), w[c]);
-    lane_solve<MB, MB>(R, w, i);
-    if (act)
-#pragma unroll
-      for (int c = 0; c < MB; ++c) phi[c] = w[c];
-  }
-  if (live) {
-    double* o = g.next_data + MB * MB + (long)j * 2 * MB * MB + (long)i * 2 * MB;
-#pragma unroll
-    for (int c = 0; c < MB; ++c) {
-      o[c] = -phi[c];
-      o[MB + c] = i == c ? 1.0 : 0.0;
-    }
-    if (j == 0)
-#pragma unroll
-      for (int c = 0; c < MB; ++c) g.next_data[i * MB + c] = __ldg(g.data + i * MB + c);
-  }
-}
-
-// condense: phi_j = the chain from zero with f; next_f[j+1] = phi_j, next_f[0] = f[0].
-template <int MB>
-__global__ void __launch_bounds__(128) chain_condense_kernel(ChainLevelArgs g) {
-  const int lane = threadIdx.x & 31, i = lane % MB;
-  const int j = (blockIdx.x * blockDim.x + threadIdx.x) / MB;
-  const bool live = j < g.P;
-  const int b0 = live ? g.cut[j] + 1 : 1, b1 = live ? g.cut[j + 1] : 0;
-  int len = b1 - b0 + 1, maxlen = len;
-  for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
-  double y = 0.0;
-  for (int t = 0; t < maxlen; ++t) {
-    const bool act = t < len;
-    double S[MB], R[MB], w[1];
-    if (act) {
-      load_row<MB>(g.data, b0 + t, i, S, R);
-      w[0] = __ldg(g.f + (long)(b0 + t) * MB + i);
-    } else {
-#pragma unroll
-      for (int c = 0; c < MB; ++c) {
-        S[c] = 0.0;
-        R[c] = i == c ? 1.0 : 0.0;
-      }
-      w[0] = 0.0;
-    }
-#pragma unroll
-    for (int l = 0; l < MB; ++l) w[0] = fma(-S[l], gshfl<MB>(y, l), w[0]);
-    lane_solve<MB, 1>(R, w, i);
-    if (act) y = w[0];
-  }
-  if (live) {
-    g.next_f[(long)(j + 1) * MB + i] = y;
-    if (j == 0) g.next_f[i] = __ldg(g.f + i);
-  }
-}
-
 __device__ __forceinline__ void cert_push(DevStatus* st, double num, double den) {
   double om = den > 0 ? num / den : num;
   if (!(om <= 1.0e308)) om = __longlong_as_double(0x7ff0000000000000ll);
@@ -183,105 +101,294 @@ __device__ __forceinline__ void cert_push(DevStatus* st, double num, double den)
   if ((threadIdx.x & 31) == 0 && om > 0) status_cert(st, om);
 }
 
-// final: x through every chunk from its left separator value (next_x[j]);
-// separator rows certified against next_x[j+1]; chunk 0 certifies the BC row.
-// With corr_f, the separator residuals r are also condensed for one
-// correction solve (A d = r, r living on the separator / BC rows only):
-// corr_f[0] = r_BC, corr_f[j+1] = R_sep^-1 r_sep.  With accumulate, the pass
-// is that correction: x += the homogeneous chain of d = next_x.
+// ---------------------------------------------------------------------------
+// factor: per block b the transfer T_b = -R_b^-1 S_b and M_b = R_b^-1, stored
+// row-interleaved like the data ([T row i | M row i], 2 MB doubles per row),
+// and per chunk Phi_j = T_last ... T_first by a shared-memory tree product.
+// One lane per block (LU in registers, no communication); a warp owns 32
+// consecutive blocks = kChainC0-block chunks, staged through shared memory with
+// a padded slot pitch (2 MB^2 + 2 doubles: conflict-free LDS.128 phases).
+// ---------------------------------------------------------------------------
+constexpr int kChainC0 = 16;  // chunk length (blocks) on every level
+
 template <int MB>
-__global__ void __launch_bounds__(128) chain_final_kernel(ChainLevelArgs g) {
-  const int lane = threadIdx.x & 31, i = lane % MB;
-  const int j = (blockIdx.x * blockDim.x + threadIdx.x) / MB;
-  const bool live = j < g.P;
-  const bool acc = g.accumulate != 0;
-  const int b0 = live ? g.cut[j] + 1 : 1, b1 = live ? g.cut[j + 1] : 0;
-  int len = b1 - b0 + 1, maxlen = len;
-  for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
-  // y: the chain (x, or d in the correction pass); yt: the value stored (x, or x_old + d)
-  double y = live ? __ldg((acc ? g.corr_x : g.next_x) + (long)j * MB + i) : 0.0;
-  double yt = (acc && live) ? __ldg(g.next_x + (long)j * MB + i) + y : y;
-  if (live && j == 0) g.x[i] = yt;
-  double num = 0.0, den = 0.0;
-  bool finite = true;
-  for (int t = 0; t < maxlen; ++t) {
-    const bool act = t < len, last = t == len - 1;
-    double S[MB], R[MB], w[2];
-    double fv = 0.0, fs = 0.0;
-    if (act) {
-      load_row<MB>(g.data, b0 + t, i, S, R);
-      if (!acc) fv = __ldg(g.f + (long)(b0 + t) * MB + i);
-      if (acc && last) fs = __ldg(g.f + (long)(b0 + t) * MB + i);
-    } else {
+struct ChainSmem {
+  static constexpr int SLOT = 2 * MB * MB + 2;
+  static constexpr int WARP = 32 * SLOT;  // doubles per warp
+};
+
+template <int MB>
+__global__ void __launch_bounds__(64) chain_tm_kernel(ChainLevelArgs g) {
+  constexpr int SLOT = ChainSmem<MB>::SLOT, RW = 2 * MB, BW = 2 * MB * MB;
+  extern __shared__ __align__(16) double csm[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  double* sm = csm + wib * ChainSmem<MB>::WARP;
+  const long w = (long)blockIdx.x * (blockDim.x >> 5) + wib;
+  const long bfirst = 32 * w + 1;  // blocks bfirst .. bfirst + 31 (chunks 2w, 2w + 1)
+  if (bfirst > g.nb - 1) return;   // warp-uniform
+  const int nblk = (int)min(32L, g.nb - bfirst);
+  // ---- stage the warp's blocks into padded slots: one TMA bulk copy per lane
+  __shared__ __align__(8) uint64_t tbar[2];
+  uint64_t* bar = tbar + wib;
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    mbar_arrive_expect_tx(bar, (uint32_t)nblk * BW * 8);
+  }
+  __syncwarp();
+  if (lane < nblk) bulk_g2s(sm + lane * SLOT, g.data + MB * MB + (bfirst - 1 + lane) * BW, BW * 8, bar);
+  mbar_wait(bar, 0);
+  // ---- per lane: LU of R (no pivoting), then T = -R^-1 S and M = R^-1 column by column
+  double* slot = sm + lane * SLOT;
+  if (lane < nblk) {
+    double R[MB * MB];
 #pragma unroll
-      for (int c = 0; c < MB; ++c) {
-        S[c] = 0.0;
-        R[c] = i == c ? 1.0 : 0.0;
+    for (int i = 0; i < MB; ++i)
+#pragma unroll
+      for (int c = 0; c < MB; ++c) R[(i) * MB + (c)] = slot[i * RW + MB + c];
+#pragma unroll
+    for (int k = 0; k < MB; ++k) {
+      const double p = fast_rcp(R[k * MB + k]);
+      R[k * MB + k] = p;  // keep the reciprocal pivot
+#pragma unroll
+      for (int i = 0; i < MB; ++i) {
+        if (i > k) {
+          const double l = R[i * MB + k] * p;
+          R[i * MB + k] = l;
+#pragma unroll
+          for (int c = 0; c < MB; ++c)
+            if (c > k) R[i * MB + c] = fma(-l, R[k * MB + c], R[i * MB + c]);
+        }
       }
     }
-    // separator row: residual of S x_prev + R x_sep = f with the reduced value
-    // (acc: with the corrected values old x + d on both sides)
-    const long os = (long)(b0 + t) * MB + i;
-    const double xs = (act && last) ? __ldg((acc ? g.corr_x : g.next_x) + (long)(j + 1) * MB + i) : 0.0;
-    const double xst = (acc && act && last) ? __ldg(g.next_x + (long)(j + 1) * MB + i) + xs : xs;
-    double sg = 0.0, ab = 0.0;
-    w[0] = fv;
+#pragma unroll 1
+    for (int c = 0; c < 2 * MB; ++c) {
+      double y[MB];
 #pragma unroll
-    for (int l = 0; l < MB; ++l) {
-      const double yl = gshfl<MB>(y, l), xl = gshfl<MB>(xst, l), ytl = gshfl<MB>(yt, l);
-      const double p1 = S[l] * ytl, p2 = R[l] * xl;
-      sg += p1 + p2;
-      ab += fabs(p1) + fabs(p2);
-      w[0] = fma(-S[l], yl, w[0]);
-    }
-    const double fr = acc ? fs : fv;
-    w[1] = (act && last) ? fr - sg : 0.0;
-    if (act && last) {
-      const double om_num = fabs(fr - sg), om_den = fabs(fr) + ab;
-      if (om_num * den > num * om_den || (den == 0.0 && om_num > 0)) {  // keep the max ratio
-        num = om_num;
-        den = om_den;
+      for (int i = 0; i < MB; ++i) y[i] = c < MB ? -slot[i * RW + c] : (i == c - MB ? 1.0 : 0.0);
+#pragma unroll
+      for (int i = 0; i < MB; ++i)
+#pragma unroll
+        for (int k = 0; k < MB; ++k)
+          if (k < i) y[i] = fma(-R[i * MB + k], y[k], y[i]);
+#pragma unroll
+      for (int ii = 0; ii < MB; ++ii) {
+        const int i = MB - 1 - ii;
+#pragma unroll
+        for (int k = 0; k < MB; ++k)
+          if (k > i) y[i] = fma(-R[i * MB + k], y[k], y[i]);
+        y[i] *= R[i * MB + i];
       }
+#pragma unroll
+      for (int i = 0; i < MB; ++i) slot[i * RW + c] = y[i];  // T (c < MB) over S, M over R
     }
-    lane_solve<MB, 2>(R, w, i);
-    if (act) {
-      y = last ? xs : w[0];
-      yt = acc ? (last ? xst : g.x[os] + y) : y;
-      finite &= isfinite(yt);
-      g.x[os] = yt;
-      if (last && g.corr_f) g.corr_f[(long)(j + 1) * MB + i] = w[1];
+  } else {  // missing blocks of a short last chunk: T = I
+#pragma unroll
+    for (int i = 0; i < MB; ++i)
+#pragma unroll
+      for (int c = 0; c < MB; ++c) slot[i * RW + c] = i == c ? 1.0 : 0.0;
+  }
+  __syncwarp();
+  // ---- store [T | M] (same layout as the data rows)
+  {
+    double2* dst = reinterpret_cast<double2*>(g.tm + (bfirst - 1) * BW);
+    const int tot2 = nblk * BW / 2;
+    for (int e0 = lane; e0 < tot2; e0 += 32) {
+      const int e = 2 * e0;
+      dst[e0] = *reinterpret_cast<const double2*>(sm + (e / BW) * SLOT + e % BW);
     }
   }
-  if (!acc) {  // BC row (chunk 0): Ba x_0 + Bb x_{nb-1} = f_0; every group runs the shuffles
+  __syncwarp();
+  // ---- Phi of the two chunks: tree of products P = later * earlier, in the T slots
+#pragma unroll 1
+  for (int h = 1; h < kChainC0; h <<= 1) {
+    const int pairs = kChainC0 / (2 * h);  // per chunk
+    if (lane < 2 * pairs) {
+      const int c = lane / pairs, k = lane % pairs;
+      double* Bs = sm + (c * kChainC0 + 2 * k * h) * SLOT;  // earlier (right factor), result slot
+      const double* As = sm + (c * kChainC0 + 2 * k * h + h) * SLOT;
+      double B[MB * MB];
+#pragma unroll
+      for (int i = 0; i < MB; ++i)
+#pragma unroll
+        for (int l = 0; l < MB; ++l) B[(i) * MB + (l)] = Bs[i * RW + l];
+#pragma unroll
+      for (int i = 0; i < MB; ++i) {
+        double a[MB], o[MB];
+#pragma unroll
+        for (int l = 0; l < MB; ++l) a[l] = As[i * RW + l];
+#pragma unroll
+        for (int cc = 0; cc < MB; ++cc) {
+          double acc = a[0] * B[(0) * MB + (cc)];
+#pragma unroll
+          for (int l = 1; l < MB; ++l) acc = fma(a[l], B[(l) * MB + (cc)], acc);
+          o[cc] = acc;
+        }
+#pragma unroll
+        for (int cc = 0; cc < MB; ++cc) Bs[i * RW + cc] = o[cc];
+      }
+    }
+    __syncwarp();
+  }
+  // ---- next level rows: [ -Phi_j | I ] for the chunks of this warp
+  for (int e = lane; e < 2 * BW; e += 32) {
+    const int c = e / BW, r = e % BW, i = r / RW, cc = r % RW;
+    const long j = 2 * w + c;
+    if (j < g.P) {
+      const double v = cc < MB ? -sm[c * kChainC0 * SLOT + i * RW + cc] : (i == cc - MB ? 1.0 : 0.0);
+      g.next_data[MB * MB + j * BW + r] = v;
+    }
+  }
+  if (w == 0)
+    for (int e = lane; e < MB * MB; e += 32) g.next_data[e] = __ldg(g.data + e);
+}
+
+// ---------------------------------------------------------------------------
+// chain passes: MB lanes per chunk (lane i = row i), 32 / MB chunks per warp.
+// Each step needs row i of [T | M] (128 B per lane, 1 KB contiguous per
+// group: coalesced) and f of the block; loads run kPre steps ahead in a
+// register ring inside a fully unrolled kChainC0-step chain.  MODE 0:
+// condense (phi, chain from zero), 1: final (x from x_sep, condensed
+// separator residuals), 2: the correction (x += homogeneous chain of d,
+// certificate of the corrected separator rows).  Chunk j = blocks
+// 16j+1 .. 16j+16 (the last one may be shorter).
+// ---------------------------------------------------------------------------
+constexpr int kPre = 3;
+
+template <int MB, int MODE>
+__global__ void __launch_bounds__(128) chain_pass_kernel(ChainLevelArgs g) {
+  constexpr int BW = 2 * MB * MB, RW = 2 * MB;
+  const int lane = threadIdx.x & 31, i = lane % MB;
+  const long j = ((long)blockIdx.x * blockDim.x + threadIdx.x) / MB;
+  const bool live = j < g.P;
+  const long b0 = live ? g.cut[j] + 1 : 1, b1 = live ? g.cut[j + 1] : 0;
+  const int len = (int)(b1 - b0 + 1);
+  double y = 0.0, yt = 0.0;
+  if (MODE == 1 && live) y = yt = __ldg(g.next_x + j * MB + i);
+  if (MODE == 2 && live) {
+    y = __ldg(g.corr_x + j * MB + i);
+    yt = __ldg(g.next_x + j * MB + i) + y;
+  }
+  if (MODE != 0 && live && j == 0) g.x[i] = yt;
+  // register ring: T row, M row, f of the block (MODE 0/1), old x (MODE 2)
+  double Tq[kPre][MB], Mq[kPre][MB], Fq[kPre][MB], Xq[kPre];
+  auto fetch = [&](int t, int slot) {
+    if (t < len) {
+      const double2* row = reinterpret_cast<const double2*>(g.tm + (b0 + t - 1) * BW + (long)i * RW);
+#pragma unroll
+      for (int c = 0; c < MB / 2; ++c) {
+        const double2 tv = __ldg(row + c);
+        Tq[slot][2 * c] = tv.x;
+        Tq[slot][2 * c + 1] = tv.y;
+      }
+      if (MODE != 2) {
+        const double2* fr = reinterpret_cast<const double2*>(g.f + (b0 + t) * MB);
+#pragma unroll
+        for (int c = 0; c < MB / 2; ++c) {
+          const double2 mv = __ldg(row + MB / 2 + c), fv = __ldg(fr + c);
+          Mq[slot][2 * c] = mv.x;
+          Mq[slot][2 * c + 1] = mv.y;
+          Fq[slot][2 * c] = fv.x;
+          Fq[slot][2 * c + 1] = fv.y;
+        }
+      } else {
+        Xq[slot] = g.x[(b0 + t) * MB + i];
+      }
+    }
+  };
+#pragma unroll
+  for (int t = 0; t < kPre; ++t) fetch(t, t);
+  double num = 0.0, den = 0.0;
+  bool finite = true;
+#pragma unroll
+  for (int t = 0; t < kChainC0; ++t) {
+    const int sl = t % kPre;
+    const bool act = t < len, last = t == len - 1;
+    double a = 0.0;
+    if (MODE != 2)
+#pragma unroll
+      for (int l = 0; l < MB; ++l) a = fma(Mq[sl][l], Fq[sl][l], a);
+#pragma unroll
+    for (int l = 0; l < MB; ++l) a = fma(Tq[sl][l], gshfl<MB>(y, l), a);
+    const double xold = MODE == 2 ? Xq[sl] : 0.0;
+    // correction: certificate of the corrected separator row r = f - S x_prev - R x_sep
+    double S[MB], R[MB];
+    const bool cert_here = MODE == 2 && act && last;
+    if (cert_here) load_row<MB>(g.data, b0 + t, i, S, R);
+    double sg = 0.0, ab = 0.0;
+    if (MODE == 2) {
+#pragma unroll
+      for (int l = 0; l < MB; ++l) {
+        const double pl = gshfl<MB>(yt, l);
+        if (cert_here) {
+          const double p1 = S[l] * pl;
+          sg += p1;
+          ab += fabs(p1);
+        }
+      }
+    }
+    if (act) {
+      const long os = (b0 + t) * MB + i;
+      if (!last) {
+        y = a;
+        yt = MODE == 2 ? xold + y : y;
+      } else if (MODE == 1) {
+        const double xs = __ldg(g.next_x + (j + 1) * MB + i);
+        if (g.corr_f) g.corr_f[(j + 1) * MB + i] = a - xs;  // R^-1 r_sep
+        y = yt = xs;
+      } else if (MODE == 2) {
+        y = __ldg(g.corr_x + (j + 1) * MB + i);
+        yt = __ldg(g.next_x + (j + 1) * MB + i) + y;
+      } else {
+        y = a;
+      }
+      if (MODE != 0) {
+        g.x[os] = yt;
+        finite &= isfinite(yt);
+      }
+    }
+    if (t + kPre < kChainC0) fetch(t + kPre, sl);
+    if (MODE == 2) {
+#pragma unroll
+      for (int l = 0; l < MB; ++l) {
+        const double xl = gshfl<MB>(yt, l);
+        if (cert_here) {
+          const double p2 = R[l] * xl;
+          sg += p2;
+          ab += fabs(p2);
+        }
+      }
+      if (cert_here) {
+        const double fv = __ldg(g.f + (b0 + t) * MB + i);
+        const double on = fabs(fv - sg), od = fabs(fv) + ab;
+        if (on * den > num * od || (den == 0.0 && on > 0)) {
+          num = on;
+          den = od;
+        }
+      }
+    }
+  }
+  if (MODE == 0 && live) {
+    g.next_f[(j + 1) * MB + i] = y;
+    if (j == 0) g.next_f[i] = __ldg(g.f + i);
+  }
+  if (MODE == 1 && g.corr_f) {  // BC row residual (chunk 0; every group runs the shuffles)
     const bool bc = live && j == 0;
     const double x0 = bc ? __ldg(g.next_x + i) : 0.0;
     const double xe = bc ? __ldg(g.next_x + (long)g.P * MB + i) : 0.0;
-    double sg = 0.0, ab = 0.0;
+    double sg = 0.0;
 #pragma unroll
     for (int l = 0; l < MB; ++l) {
       const double a0 = gshfl<MB>(x0, l), ae = gshfl<MB>(xe, l);
-      if (bc) {
-        const double p1 = __ldg(g.data + i * MB + l) * a0;
-        const double p2 = __ldg(g.corner + i * MB + l) * ae;
-        sg += p1 + p2;
-        ab += fabs(p1) + fabs(p2);
-      }
+      if (bc) sg += __ldg(g.data + i * MB + l) * a0 + __ldg(g.corner + i * MB + l) * ae;
     }
-    if (bc) {
-      const double fv = __ldg(g.f + i);
-      const double om_num = fabs(fv - sg), om_den = fabs(fv) + ab;
-      if (om_num * den > num * om_den || (den == 0.0 && om_num > 0)) {
-        num = om_num;
-        den = om_den;
-      }
-      if (g.corr_f) g.corr_f[i] = fv - sg;
-    }
+    if (bc) g.corr_f[i] = __ldg(g.f + i) - sg;
   }
-  if (!finite) num = __longlong_as_double(0x7ff0000000000000ll), den = 1.0;
-  if (g.status) cert_push(g.status, num, den);
+  if (MODE != 0) {
+    if (!finite) num = __longlong_as_double(0x7ff0000000000000ll), den = 1.0;
+    if (g.status) cert_push(g.status, num, den);
+  }
 }
 
-// componentwise backward error of the BC row Ba x_0 + Bb x_{nb-1} = f_0 (one warp)
 template <int MB>
 __global__ void chain_bc_cert_kernel(ChainLevelArgs g) {
   const int lane = threadIdx.x, i = lane % MB;

@@ -718,18 +718,17 @@ struct ChainLevel {
   double* x = nullptr;
   std::vector<int> hcut;
   DevBuf<int> cut;
-  DevBuf<double> next_data, next_f, next_x, corr_x;
+  DevBuf<double> next_data, next_f, next_x, corr_x, tm;
 };
 
 constexpr int kChainDirect = 64;  // levels with at most this many block rows are solved by one warp
-constexpr int kChainChunk = 32;   // chunk length (steps) of the reduced levels
-constexpr int kChainChunk0 = 16;  // chunk length of level 0
 
 struct ChainSolver {
   int MB = 0;
   bool possible = false;
   const double* corner = nullptr;
   std::vector<std::unique_ptr<ChainLevel>> lv;
+  DevBuf<double> falign;
   int launches = 0;
 
   void init(const psg_desc& A, const Plan& P) {
@@ -738,17 +737,24 @@ struct ChainSolver {
     if (A.kind != PSG_BABD || A.s != A.m || A.r != 0 || !P.has_corner) return;
     if (A.corner_rows != A.m || A.corner_cols != A.m) return;
     if (A.m != 2 && A.m != 4 && A.m != 8) return;
+    if (reinterpret_cast<uintptr_t>(A.data) & 15) return;  // blocks arrive by 16-byte bulk copies
     MB = A.m;
     corner = A.corner;
     auto L = std::make_unique<ChainLevel>();
     L->nb = A.n / MB;
     L->data = A.data;
-    // level-0 chunks of ~kChainChunk0 blocks (internal; independent of the
+    // chunks of kChainC0 blocks on every level (internal; independent of the
     // reference plan, whose reduced system the exact path keeps)
-    L->P = (L->nb - 1 + kChainChunk0 - 1) / kChainChunk0;
-    for (int k = 0; k <= L->P; ++k) L->hcut.push_back(int((long)k * (L->nb - 1) / L->P));
+    auto cuts = [](ChainLevel& c) {
+      c.P = (c.nb - 1 + kChainC0 - 1) / kChainC0;
+      c.hcut.clear();
+      for (int k = 0; k < c.P; ++k) c.hcut.push_back(k * kChainC0);
+      c.hcut.push_back(c.nb - 1);
+    };
+    cuts(*L);
     for (;;) {
       ChainLevel& c = *L;
+      c.tm.alloc((size_t)(c.nb - 1) * 2 * MB * MB);
       c.cut.alloc(c.hcut.size());
       CUDA_TRY(cudaMemcpy(c.cut.p, c.hcut.data(), sizeof(int) * c.hcut.size(), cudaMemcpyHostToDevice));
       const int nb2 = c.P + 1;
@@ -767,8 +773,7 @@ struct ChainSolver {
         lv.push_back(std::move(N));
         break;
       }
-      N->P = (nb2 - 1 + kChainChunk - 1) / kChainChunk;
-      for (int k = 0; k <= N->P; ++k) N->hcut.push_back(int((long)k * (nb2 - 1) / N->P));
+      cuts(*N);
       L = std::move(N);
     }
     possible = true;
@@ -791,19 +796,33 @@ struct ChainSolver {
     g.next_data = L.next_data.p;
     g.next_f = L.next_f.p;
     g.next_x = L.next_x.p;
+    g.tm = L.tm.p;
     g.status = st;
     return g;
   }
 
   template <int M>
   void factor_t(cudaStream_t s) {
+    constexpr int bytes = ChainSmem<M>::WARP * 8;
+    static bool attr = false;
+    if (!attr) {
+      CUDA_TRY(cudaFuncSetAttribute(chain_tm_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+      attr = true;
+    }
     for (auto& L : lv) {
       if (L->direct) break;
-      const int threads = L->P * M;
-      chain_factor_kernel<M><<<(threads + 127) / 128, 128, 0, s>>>(args(*L, nullptr));
+      const long warps = (L->nb - 1 + 31) / 32;
+      chain_tm_kernel<M><<<(int)warps, 32, bytes, s>>>(args(*L, nullptr));
       LAUNCH_CHECK();
       ++launches;
     }
+  }
+
+  template <int M, int MODE>
+  void pass(ChainLevelArgs a, cudaStream_t s) {
+    chain_pass_kernel<M, MODE><<<(a.P * M + 127) / 128, 128, 0, s>>>(a);
+    LAUNCH_CHECK();
+    ++launches;
   }
 
   template <int M>
@@ -812,9 +831,7 @@ struct ChainSolver {
     lv[0]->x = x;
     for (auto& L : lv) {
       if (L->direct) break;
-      chain_condense_kernel<M><<<(L->P * M + 127) / 128, 128, 0, s>>>(args(*L, nullptr));
-      LAUNCH_CHECK();
-      ++launches;
+      pass<M, 0>(args(*L, nullptr), s);
     }
     if (ev) CUDA_TRY(cudaEventRecord(ev[1], s));
     upper_t<M>(s, 1);
@@ -823,28 +840,22 @@ struct ChainSolver {
     ChainLevel& L0 = *lv[0];
     ChainLevelArgs a = args(L0, nullptr);
     a.corr_f = L0.next_f.p;
-    chain_final_kernel<M><<<(L0.P * M + 127) / 128, 128, 0, s>>>(a);
-    LAUNCH_CHECK();
-    ++launches;
+    pass<M, 1>(a, s);
     // correction: A d = r (separator rows) through the reduced levels, then x += d
     lv[1]->x = L0.corr_x.p;
     for (size_t l = 1; l < lv.size(); ++l) {
       ChainLevel& L = *lv[l];
       if (L.direct) break;
-      chain_condense_kernel<M><<<(L.P * M + 127) / 128, 128, 0, s>>>(args(L, nullptr));
-      LAUNCH_CHECK();
-      ++launches;
+      pass<M, 0>(args(L, nullptr), s);
     }
     upper_t<M>(s, 1);
     lv[1]->x = L0.next_x.p;
     ChainLevelArgs c = args(L0, st);  // certifies the corrected separator rows
-    c.accumulate = 1;
     c.corr_x = L0.corr_x.p;
-    chain_final_kernel<M><<<(L0.P * M + 127) / 128, 128, 0, s>>>(c);
-    LAUNCH_CHECK();
+    pass<M, 2>(c, s);
     chain_bc_cert_kernel<M><<<1, 32, 0, s>>>(args(L0, st));
     LAUNCH_CHECK();
-    launches += 2;
+    launches += 1;
   }
 
   // direct solve of the last level and final passes of levels >= from (top down)
@@ -853,12 +864,7 @@ struct ChainSolver {
     chain_direct_kernel<M><<<1, 32, 0, s>>>(args(*lv.back(), nullptr));
     LAUNCH_CHECK();
     ++launches;
-    for (size_t l = lv.size() - 1; l-- > from;) {
-      ChainLevel& L = *lv[l];
-      chain_final_kernel<M><<<(L.P * M + 127) / 128, 128, 0, s>>>(args(L, nullptr));
-      LAUNCH_CHECK();
-      ++launches;
-    }
+    for (size_t l = lv.size() - 1; l-- > from;) pass<M, 1>(args(*lv[l], nullptr), s);
   }
 
   void factor(cudaStream_t s) {
@@ -868,6 +874,11 @@ struct ChainSolver {
   }
   // status slot must be reset by the caller
   void solve(const double* f, double* x, DevStatus* st, cudaStream_t s, cudaEvent_t* ev) {
+    if (reinterpret_cast<uintptr_t>(f) & 15) {  // the staged passes bulk-copy f: 16-byte alignment
+      falign.alloc((size_t)lv[0]->nb * MB);
+      CUDA_TRY(cudaMemcpyAsync(falign.p, f, sizeof(double) * lv[0]->nb * MB, cudaMemcpyDeviceToDevice, s));
+      f = falign.p;
+    }
     if (MB == 8) solve_t<8>(f, x, st, s, ev);
     else if (MB == 4) solve_t<4>(f, x, st, s, ev);
     else solve_t<2>(f, x, st, s, ev);
