@@ -178,6 +178,8 @@ struct BlkArgs {
   int nseg;
   double* rec;         // certificate records (4K per body) or null
   DevStatus* status;
+  long boff[9];        // banded: A(row, row + d) = data[boff[d + K] + row] (host-computed)
+  long data_len;       // entries in data (staging over-read bound)
 };
 
 template <int K, int M>
@@ -189,9 +191,11 @@ struct BlkSmem {
   static constexpr int MAT_BD = (2 * K + 1) * PB;  // banded staging (bands -K..K)
   static constexpr int STASH = 32 * M * (2 * K * K + K);
   static constexpr int MAT = (MAT_BT > STASH ? MAT_BT : STASH);
-  static constexpr int MATB = (MAT_BD > STASH ? MAT_BD : STASH);
-  static constexpr int F = NBMAX * K + 1;
-  static constexpr int bytes(int layout) { return 8 * ((layout == kBlkBlockTri ? MAT : MATB) + F); }
+  static constexpr int RB = NBMAX * K + 4;         // banded: per-band TMA region (even: 16-byte aligned)
+  static constexpr int MATB = (2 * K + 1) * RB;    // >= STASH
+  static constexpr int MAT_ALIGNED = (MAT + 1) & ~1;
+  static constexpr int F = NBMAX * K + 4;          // rhs region (TMA, shifted)
+  static constexpr int bytes(int layout) { return 8 * ((layout == kBlkBlockTri ? MAT_ALIGNED : MATB) + F); }
 };
 
 // Certificate record of one body (4K doubles): for its left separator rows u,
@@ -202,12 +206,14 @@ struct BlkSmem {
 template <int K, int M, int LAYOUT>
 __global__ void __launch_bounds__(32) blk_segment_solve_kernel(BlkArgs g) {
   using SM = BlkSmem<K, M>;
-  constexpr int P = SM::P, PB = SM::PB;
+  constexpr int P = SM::P;
   constexpr int KK = K * K;
-  constexpr int MATD = LAYOUT == kBlkBlockTri ? SM::MAT : SM::MATB;
+  constexpr int MATD = LAYOUT == kBlkBlockTri ? SM::MAT_ALIGNED : SM::MATB;
+  constexpr int RB = SM::RB;
   constexpr unsigned FULL = 0xffffffffu;
   extern __shared__ __align__(16) double sm[];
-  double* smf = sm + MATD;  // rhs / solution by body row
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ int boffs[2 * K + 2];  // banded: smem offset of row 0 of band d (d + K); [2K+1]: f
   const int lane = threadIdx.x;
   const int seg = blockIdx.x;
   const GPart Pt = g.part[seg];
@@ -218,57 +224,54 @@ __global__ void __launch_bounds__(32) blk_segment_solve_kernel(BlkArgs g) {
   const long n = g.n;
   const int lsi = seg - 1, rsi = seg;
 
-  // ---- staging (element-major / band-major)
+  // ---- staging: rhs (and banded: every band) by TMA bulk copies, one lane per array;
+  //      block tridiagonal: element-major transposition through registers
+  constexpr int NARR = LAYOUT == kBlkBlockTri ? 1 : 2 * K + 2;
+  if (lane == 0) mbar_init(&bar, NARR);
+  __syncwarp();
+  RowArr X{};
+  double* xbase = nullptr;
+  if (lane < NARR) {
+    if (lane == NARR - 1) {  // rhs
+      X = make_rows(g.f, 0, (int)n, 0, n);
+      xbase = sm + MATD;
+    } else {
+      const int d = lane - K;
+      const bool inb = d >= -g.s && d <= g.r;
+      const long bo = inb ? g.boff[lane] : 0;
+      X = make_rows(g.data + bo, inb ? (d < 0 ? -d : 0) : 0, inb ? (int)(n - (d > 0 ? d : 0)) : 0, -bo,
+                    g.data_len - bo);
+      xbase = sm + lane * RB;
+    }
+    uint32_t tx = 0;
+    const int shift = stage_issue(X, b, b + NR, xbase, &bar, &tx);
+    mbar_arrive_expect_tx(&bar, tx);
+    boffs[lane] = (int)(xbase - sm) + 1 + shift;
+  }
   if (LAYOUT == kBlkBlockTri) {
     // block rows B0..B0+NB-1 are contiguous: [(3 B0 - 1) KK, (3 (B0+NB) - 1) KK)
     const long B0 = b / K;
     const long g0 = (3 * B0 - 1) * KK;
-    const long tot = (long)NB * 3 * KK;
+    const int tot = NB * 3 * KK;
     const long glen = (3 * (n / K) - 2) * KK;
+    const int ilo = (int)(g0 < 0 ? -g0 : 0);
+    const int ihi = (int)(glen - g0 < tot ? glen - g0 : tot);
     constexpr int U = 16;  // loads in flight per lane
-    for (long i0 = lane; i0 < tot; i0 += 32 * U) {
+    for (int i0 = lane; i0 < tot; i0 += 32 * U) {
       double v[U];
 #pragma unroll
       for (int k = 0; k < U; ++k) {
-        const long i = i0 + 32 * k, gi = g0 + i;
-        v[k] = (i < tot && gi >= 0 && gi < glen) ? __ldg(g.data + gi) : 0.0;
+        const int i = i0 + 32 * k;
+        v[k] = (i >= ilo && i < ihi) ? __ldg(g.data + g0 + i) : 0.0;
       }
 #pragma unroll
       for (int k = 0; k < U; ++k) {
-        const long i = i0 + 32 * k;
+        const int i = i0 + 32 * k;
         if (i < tot) {
-          const int q = (int)(i / (3 * KK)), e = (int)(i % (3 * KK));
+          const int q = i / (3 * KK), e = i - q * (3 * KK);
           sm[e * P + q] = v[k];
         }
       }
-    }
-  } else {
-    constexpr int U = 8;
-    for (int d = -g.s; d <= g.r; ++d) {
-      const long bs = band_start(n, g.s, d) - (d < 0 ? -d : 0);
-      for (int x0 = lane; x0 < NR; x0 += 32 * U) {
-        double v[U];
-#pragma unroll
-        for (int k = 0; k < U; ++k) {
-          const int xr = x0 + 32 * k;
-          const long row = b + xr, col = row + d;
-          v[k] = (xr < L && col >= 0 && col < n) ? __ldg(g.data + bs + row) : 0.0;
-        }
-#pragma unroll
-        for (int k = 0; k < U; ++k)
-          if (x0 + 32 * k < NR) sm[(d + K) * PB + x0 + 32 * k] = v[k];
-      }
-    }
-  }
-  {
-    constexpr int U = 8;
-    for (int x0 = lane; x0 < NR; x0 += 32 * U) {
-      double v[U];
-#pragma unroll
-      for (int k = 0; k < U; ++k) v[k] = x0 + 32 * k < L ? __ldg(g.f + b + x0 + 32 * k) : 0.0;
-#pragma unroll
-      for (int k = 0; k < U; ++k)
-        if (x0 + 32 * k < NR) smf[x0 + 32 * k] = v[k];
     }
   }
   Vec<K> xl, xrv;
@@ -277,6 +280,14 @@ __global__ void __launch_bounds__(32) blk_segment_solve_kernel(BlkArgs g) {
     xl.v[u] = Pt.ls >= 0 ? __ldg(g.xsep + (long)lsi * K + u) : 0.0;
     xrv.v[u] = Pt.rs >= 0 ? __ldg(g.xsep + (long)rsi * K + u) : 0.0;
   }
+  mbar_wait(&bar, 0);
+  if (lane < NARR) stage_fixup(X, b, b + NR, sm + boffs[lane]);
+  __syncwarp();
+  double* smf = sm + boffs[NARR - 1];  // rhs / solution by body row
+  for (int xr = L + lane; xr < NR; xr += 32) smf[xr] = 0.0;  // padding rows
+  int bo[2 * K + 1];
+#pragma unroll
+  for (int t = 0; t < 2 * K + 1; ++t) bo[t] = LAYOUT == kBlkBanded ? boffs[t] : 0;
   __syncwarp();
   // staged A(b+xrow, b+ycol) (0 outside the structure)
   auto elem = [&](int xrow, int ycol) -> double {
@@ -289,7 +300,7 @@ __global__ void __launch_bounds__(32) blk_segment_solve_kernel(BlkArgs g) {
     } else {
       const int d = ycol - xrow;
       if (d < -g.s || d > g.r) return 0.0;
-      return sm[(d + K) * PB + xrow];
+      return sm[boffs[d + K] + xrow];
     }
   };
   // fold the separator couplings of the first / last K body rows into the rhs
@@ -323,8 +334,8 @@ __global__ void __launch_bounds__(32) blk_segment_solve_kernel(BlkArgs g) {
         if (LAYOUT == kBlkBlockTri) {
           val = sm[(blk * KK + u * K + v) * P + q];
         } else {
-          const int d = ycol - xrow;
-          val = (d >= -g.s && d <= g.r) ? sm[(d + K) * PB + xrow] : 0.0;
+          const int d = (blk - 1) * K + v - u;  // compile-time after unrolling
+          val = (d >= -g.s && d <= g.r) ? sm[bo[d + K] + xrow] : 0.0;
         }
         if (xrow >= L)
           val = (blk == 1 && u == v) ? 1.0 : 0.0;  // padding: identity, decoupled
@@ -538,7 +549,7 @@ __global__ void __launch_bounds__(32) blk_segment_solve_kernel(BlkArgs g) {
       } else {
         const int d = (int)(col - row);
         if (d < -g.s || d > g.r) return 0.0;
-        return __ldg(g.data + band_start(n, g.s, d) + row - (d < 0 ? -d : 0));
+        return __ldg(g.data + g.boff[d + K] + row);
       }
     };
     if (lane < K) {
@@ -583,6 +594,7 @@ struct BlkSpecArgs {
   const int* sep;  // separator start rows
   double* W;       // out: per separator (1 + 2 HB) K*K: T^-1 | W^T_0..HB-1 | W^L_0..HB-1
   double* Tdiag;   // out: per separator the K*K block A_SS (certificate)
+  long boff[9];    // banded: A(row, row + d) = data[boff[d + K] + row]
 };
 
 // A(i, j) for the block kinds (0 outside the structure)
@@ -597,7 +609,7 @@ __device__ __forceinline__ double blk_at(const BlkSpecArgs& g, int K, long i, lo
   }
   const long d = j - i;
   if (d < -g.s || d > g.r) return 0.0;
-  return __ldg(g.data + band_start(g.n, g.s, (int)d) + (i - (d < 0 ? -d : 0)));
+  return __ldg(g.data + g.boff[d + K] + i);
 }
 
 // distributed K x K (K <= 4) algebra inside a 16-lane half (base 0 or 16),
@@ -650,7 +662,7 @@ __global__ void __launch_bounds__(128) blk_spec_factor_kernel(BlkSpecArgs g) {
   auto prep = [&](int t, long& off, bool& ok) {
     const int d = v - u + (t - 1) * K;
     ok = act && (g.layout == kBlkBlockTri || (d >= -g.s && d <= g.r));
-    off = g.layout == kBlkBlockTri ? (long)t * KK + u * K + v : (ok ? band_start(n, g.s, d) - (d < 0 ? -d : 0) + u : 0);
+    off = g.layout == kBlkBlockTri ? (long)t * KK + u * K + v : (ok ? g.boff[d + K] + u : 0);
   };
   long oD, oF, oN;
   bool kD, kF, kN;

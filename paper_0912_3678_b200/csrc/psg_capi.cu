@@ -531,6 +531,17 @@ void envelope_of(int kind, int m, int s, int r, int& es, int& er) {  // scalar_e
 // ----------------------------------------------------------------------------
 // K x K block speculative path (blk_kernels.cuh)
 // ----------------------------------------------------------------------------
+// banded band bases: A(row, row + d) = data[boff[d + K] + row] (structmat.cpp:33-38 layout)
+void fill_band_offsets(BlkArgs& a, int K, long n, int s_, int r_, size_t data_len) {
+  for (int t = 0; t < 9; ++t) a.boff[t] = 0;
+  long off = 0;
+  for (int d = -s_; d <= r_; ++d) {
+    if (d + K >= 0 && d + K < 9) a.boff[d + K] = off - (d < 0 ? -d : 0);
+    off += n - (d < 0 ? -d : d);
+  }
+  a.data_len = (long)data_len;
+}
+
 template <int K, int M, int LAYOUT>
 void launch_blk_kernel(const BlkArgs& a, cudaStream_t s) {
   constexpr int bytes = BlkSmem<K, M>::bytes(LAYOUT);
@@ -647,6 +658,7 @@ struct BlkSolver {
     base.data = A.data;
     base.part = part.p;
     base.nseg = nseg;
+    fill_band_offsets(base, K, A.n, A.s, A.r, A.data_len);
     possible = true;
   }
 
@@ -663,6 +675,7 @@ struct BlkSolver {
     g.sep = sep.p;
     g.W = W.p;
     g.Tdiag = Tdiag.p;
+    for (int t = 0; t < 9; ++t) g.boff[t] = base.boff[t];
     const int grid = (nsep + 3) / 4;
     if (K == 4)
       blk_spec_factor_kernel<4, blk_hb(4)><<<grid, 128, 0, s>>>(g);
@@ -1082,6 +1095,9 @@ struct GenSolver {
     a.nseg = L.p;
     a.rec = nullptr;
     a.status = g.status;
+    fill_band_offsets(a, L.k, L.A.n, L.A.s, L.A.r,
+                      layout == kBlkBanded ? (size_t)body_entry_count(PSG_BANDED, L.A.n, 1, L.A.s, L.A.r)
+                                           : (size_t)(3 * (L.A.n / L.k) - 2) * L.k * L.k);
     return launch_blk_segments(L.k, (maxL + L.k - 1) / L.k, layout, a, s);
   }
 
