@@ -182,20 +182,22 @@ struct BlkArgs {
   long data_len;       // entries in data (staging over-read bound)
 };
 
-template <int K, int M>
+template <int K, int M, int NW = 1>
 struct BlkSmem {
-  static constexpr int NBMAX = 32 * M;             // block rows per body
+  static constexpr int NT = 32 * NW;               // threads per body
+  static constexpr int NBMAX = NT * M;             // block rows per body
   static constexpr int P = NBMAX + 1;              // element-major pitch (odd)
   static constexpr int PB = NBMAX * K + 1;         // banded: band pitch (odd)
   static constexpr int MAT_BT = 3 * K * K * P;     // block tridiagonal staging
   static constexpr int MAT_BD = (2 * K + 1) * PB;  // banded staging (bands -K..K)
-  static constexpr int STASH = 32 * M * (2 * K * K + K);
+  static constexpr int STASH = NT * M * (2 * K * K + K);
   static constexpr int MAT = (MAT_BT > STASH ? MAT_BT : STASH);
   static constexpr int RB = NBMAX * K + 4;         // banded: per-band TMA region (even: 16-byte aligned)
   static constexpr int MATB = (2 * K + 1) * RB;    // >= STASH
   static constexpr int MAT_ALIGNED = (MAT + 1) & ~1;
   static constexpr int F = NBMAX * K + 4;          // rhs region (TMA, shifted)
-  static constexpr int bytes(int layout) { return 8 * ((layout == kBlkBlockTri ? MAT_ALIGNED : MATB) + F); }
+  static constexpr int XCH = NW > 1 ? NT * (2 * K * K + K) : 0;  // cross-warp exchange (NW > 1)
+  static constexpr int bytes(int layout) { return 8 * ((layout == kBlkBlockTri ? MAT_ALIGNED : MATB) + F + XCH); }
 };
 
 // Certificate record of one body (4K doubles): for its left separator rows u,
@@ -203,9 +205,10 @@ struct BlkSmem {
 // and for its right separator rows with the body's last rows
 //   rec[2K..3K) signed                      rec[3K..4K) abs.
 
-template <int K, int M, int LAYOUT>
-__global__ void __launch_bounds__(32) blk_segment_solve_kernel(BlkArgs g) {
-  using SM = BlkSmem<K, M>;
+template <int K, int M, int LAYOUT, int NW>
+__global__ void __launch_bounds__(32 * NW) blk_segment_solve_kernel(BlkArgs g) {
+  using SM = BlkSmem<K, M, NW>;
+  constexpr int NT = SM::NT;
   constexpr int P = SM::P;
   constexpr int KK = K * K;
   constexpr int MATD = LAYOUT == kBlkBlockTri ? SM::MAT_ALIGNED : SM::MATB;
@@ -214,8 +217,15 @@ __global__ void __launch_bounds__(32) blk_segment_solve_kernel(BlkArgs g) {
   extern __shared__ __align__(16) double sm[];
   __shared__ __align__(8) uint64_t bar;
   __shared__ int boffs[2 * K + 2];  // banded: smem offset of row 0 of band d (d + K); [2K+1]: f
-  const int lane = threadIdx.x;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
   const int seg = blockIdx.x;
+  auto SYNC = [&]() {
+    if (NW > 1)
+      __syncthreads();
+    else
+      __syncwarp();
+  };
   const GPart Pt = g.part[seg];
   const long b = Pt.b;
   const int L = Pt.L;
@@ -227,12 +237,12 @@ __global__ void __launch_bounds__(32) blk_segment_solve_kernel(BlkArgs g) {
   // ---- staging: rhs (and banded: every band) by TMA bulk copies, one lane per array;
   //      block tridiagonal: element-major transposition through registers
   constexpr int NARR = LAYOUT == kBlkBlockTri ? 1 : 2 * K + 2;
-  if (lane == 0) mbar_init(&bar, NARR);
-  __syncwarp();
+  if (tid == 0) mbar_init(&bar, NARR);
+  SYNC();
   RowArr X{};
   double* xbase = nullptr;
-  if (lane < NARR) {
-    if (lane == NARR - 1) {  // rhs
+  if (tid < NARR) {
+    if (tid == NARR - 1) {  // rhs
       X = make_rows(g.f, 0, (int)n, 0, n);
       xbase = sm + MATD;
     } else {
@@ -246,7 +256,7 @@ __global__ void __launch_bounds__(32) blk_segment_solve_kernel(BlkArgs g) {
     uint32_t tx = 0;
     const int shift = stage_issue(X, b, b + NR, xbase, &bar, &tx);
     mbar_arrive_expect_tx(&bar, tx);
-    boffs[lane] = (int)(xbase - sm) + 1 + shift;
+    boffs[tid] = (int)(xbase - sm) + 1 + shift;
   }
   if (LAYOUT == kBlkBlockTri) {
     // block rows B0..B0+NB-1 are contiguous: [(3 B0 - 1) KK, (3 (B0+NB) - 1) KK)
@@ -257,16 +267,16 @@ __global__ void __launch_bounds__(32) blk_segment_solve_kernel(BlkArgs g) {
     const int ilo = (int)(g0 < 0 ? -g0 : 0);
     const int ihi = (int)(glen - g0 < tot ? glen - g0 : tot);
     constexpr int U = 16;  // loads in flight per lane
-    for (int i0 = lane; i0 < tot; i0 += 32 * U) {
+    for (int i0 = tid; i0 < tot; i0 += NT * U) {
       double v[U];
 #pragma unroll
       for (int k = 0; k < U; ++k) {
-        const int i = i0 + 32 * k;
+        const int i = i0 + NT * k;
         v[k] = (i >= ilo && i < ihi) ? __ldg(g.data + g0 + i) : 0.0;
       }
 #pragma unroll
       for (int k = 0; k < U; ++k) {
-        const int i = i0 + 32 * k;
+        const int i = i0 + NT * k;
         if (i < tot) {
           const int q = i / (3 * KK), e = i - q * (3 * KK);
           sm[e * P + q] = v[k];
@@ -281,14 +291,14 @@ __global__ void __launch_bounds__(32) blk_segment_solve_kernel(BlkArgs g) {
     xrv.v[u] = Pt.rs >= 0 ? __ldg(g.xsep + (long)rsi * K + u) : 0.0;
   }
   mbar_wait(&bar, 0);
-  if (lane < NARR) stage_fixup(X, b, b + NR, sm + boffs[lane]);
-  __syncwarp();
+  if (tid < NARR) stage_fixup(X, b, b + NR, sm + boffs[tid]);
+  SYNC();
   double* smf = sm + boffs[NARR - 1];  // rhs / solution by body row
-  for (int xr = L + lane; xr < NR; xr += 32) smf[xr] = 0.0;  // padding rows
+  for (int xr = L + tid; xr < NR; xr += NT) smf[xr] = 0.0;  // padding rows
   int bo[2 * K + 1];
 #pragma unroll
   for (int t = 0; t < 2 * K + 1; ++t) bo[t] = LAYOUT == kBlkBanded ? boffs[t] : 0;
-  __syncwarp();
+  SYNC();
   // staged A(b+xrow, b+ycol) (0 outside the structure)
   auto elem = [&](int xrow, int ycol) -> double {
     if (LAYOUT == kBlkBlockTri) {
@@ -304,15 +314,15 @@ __global__ void __launch_bounds__(32) blk_segment_solve_kernel(BlkArgs g) {
     }
   };
   // fold the separator couplings of the first / last K body rows into the rhs
-  if (lane < K) {
+  if (tid < K) {
     if (Pt.ls >= 0) {
-      double fv = smf[lane];
+      double fv = smf[tid];
 #pragma unroll
-      for (int t = 0; t < K; ++t) fv = fma(-elem(lane, t - K), xl.v[t], fv);
-      smf[lane] = fv;
+      for (int t = 0; t < K; ++t) fv = fma(-elem(tid, t - K), xl.v[t], fv);
+      smf[tid] = fv;
     }
-  } else if (lane >= 16 && lane < 16 + K) {
-    const int xrow = L - K + (lane - 16);
+  } else if (tid >= 16 && tid < 16 + K) {
+    const int xrow = L - K + (tid - 16);
     if (Pt.rs >= 0) {
       double fv = smf[xrow];
 #pragma unroll
@@ -320,7 +330,7 @@ __global__ void __launch_bounds__(32) blk_segment_solve_kernel(BlkArgs g) {
       smf[xrow] = fv;
     }
   }
-  __syncwarp();
+  SYNC();
 
   // block (q, blk) with separator columns and padding rows masked out
   auto load_blk = [&](int q, int blk) {
@@ -350,7 +360,31 @@ __global__ void __launch_bounds__(32) blk_segment_solve_kernel(BlkArgs g) {
   Blk<K> AP[M], CP[M];
   Vec<K> DP[M];
   double rsum = 0.0;
-  const int q0 = lane * M;
+  const int q0 = tid * M;
+  double* xch = sm + (LAYOUT == kBlkBlockTri ? SM::MAT_ALIGNED : SM::MATB) + SM::F;  // NW > 1 exchange
+  // NW > 1: write a block row (a, c, d) of thread tid into the exchange area / read thread src's
+  auto xput = [&](const Blk<K>& a, const Blk<K>& c, const Vec<K>& d) {
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+#pragma unroll
+      for (int v = 0; v < K; ++v) {
+        xch[(u * K + v) * NT + tid] = a.v[u][v];
+        xch[(K * K + u * K + v) * NT + tid] = c.v[u][v];
+      }
+      xch[(2 * K * K + u) * NT + tid] = d.v[u];
+    }
+  };
+  auto xget = [&](int src, Blk<K>& a, Blk<K>& c, Vec<K>& d) {
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+#pragma unroll
+      for (int v = 0; v < K; ++v) {
+        a.v[u][v] = xch[(u * K + v) * NT + src];
+        c.v[u][v] = xch[(K * K + u * K + v) * NT + src];
+      }
+      d.v[u] = xch[(2 * K * K + u) * NT + src];
+    }
+  };
 #pragma unroll
   for (int j = 0; j < M; ++j) {
     const int q = q0 + j;
@@ -409,7 +443,7 @@ __global__ void __launch_bounds__(32) blk_segment_solve_kernel(BlkArgs g) {
   Vec<K> de = DP[0];
   blk_set_eye<K>(be);
   blk_set_zero<K>(al);
-  {
+  if (NW == 1) {
     const int lo1 = lane > 0 ? lane - 1 : 0;
     const Blk<K> pa = blk_shfl<K>(AP[M - 1], lo1);
     if (lane > 0) {
@@ -420,31 +454,44 @@ __global__ void __launch_bounds__(32) blk_segment_solve_kernel(BlkArgs g) {
     if (lane > 0) blk_mul_sub<K>(be, AP[0], pc);
     const Vec<K> pd = vec_shfl<K>(DP[M - 1], lo1);
     if (lane > 0) blk_mv_sub<K>(de, AP[0], pd);
+  } else {
+    xput(AP[M - 1], CP[M - 1], DP[M - 1]);
+    __syncthreads();
+    if (tid > 0) {
+      Blk<K> pa, pc;
+      Vec<K> pd;
+      xget(tid - 1, pa, pc, pd);
+      al = blk_mul<K>(AP[0], pa);
+      blk_neg<K>(al);
+      blk_mul_sub<K>(be, AP[0], pc);
+      blk_mv_sub<K>(de, AP[0], pd);
+    }
   }
   blk_mul_sub<K>(be, CP[0], AP[M - 1]);
   blk_mv_sub<K>(de, CP[0], DP[M - 1]);
   ga = blk_mul<K>(CP[0], CP[M - 1]);
   blk_neg<K>(ga);
-  // stash the chunk state in the consumed staging area (lane-interleaved)
-  __syncwarp();
+  // stash the chunk state in the consumed staging area (thread-interleaved)
+  SYNC();
   {
-    double* st = sm + lane;
+    double* st = sm + tid;
 #pragma unroll
     for (int j = 0; j < M; ++j)
 #pragma unroll
       for (int u = 0; u < K; ++u) {
 #pragma unroll
         for (int v = 0; v < K; ++v) {
-          st[32 * ((j * K + u) * (2 * K + 1) + 2 * v)] = AP[j].v[u][v];
-          st[32 * ((j * K + u) * (2 * K + 1) + 2 * v + 1)] = CP[j].v[u][v];
+          st[NT * ((j * K + u) * (2 * K + 1) + 2 * v)] = AP[j].v[u][v];
+          st[NT * ((j * K + u) * (2 * K + 1) + 2 * v + 1)] = CP[j].v[u][v];
         }
-        st[32 * ((j * K + u) * (2 * K + 1) + 2 * K)] = DP[j].v[u];
+        st[NT * ((j * K + u) * (2 * K + 1) + 2 * K)] = DP[j].v[u];
       }
   }
   blk_inv<K>(be, &rsum);
   al = blk_mul<K>(be, al);
   ga = blk_mul<K>(be, ga);
   de = blk_mv<K>(be, de);
+  if (NW == 1) {
 #pragma unroll 1
   for (int st = 1; st < 32; st <<= 1) {
     const bool hl = lane >= st, hh = lane + st < 32;
@@ -481,23 +528,69 @@ __global__ void __launch_bounds__(32) blk_segment_solve_kernel(BlkArgs g) {
     blk_neg<K>(ga);
     de = blk_mv<K>(nb, nd);
   }
+  } else {
+#pragma unroll 1
+    for (int st = 1; st < NT; st <<= 1) {
+      const bool hl = tid >= st, hh = tid + st < NT;
+      __syncthreads();
+      xput(al, ga, de);
+      __syncthreads();
+      Blk<K> nb, na, ng;
+      blk_set_eye<K>(nb);
+      Vec<K> nd = de;
+      blk_set_zero<K>(na);
+      blk_set_zero<K>(ng);
+      if (hl) {
+        Blk<K> la, lg;
+        Vec<K> ld;
+        xget(tid - st, la, lg, ld);
+        blk_mul_sub<K>(nb, al, lg);
+        na = blk_mul<K>(al, la);
+        blk_mv_sub<K>(nd, al, ld);
+      }
+      if (hh) {
+        Blk<K> ha, hg;
+        Vec<K> hd;
+        xget(tid + st, ha, hg, hd);
+        blk_mul_sub<K>(nb, ga, ha);
+        ng = blk_mul<K>(ga, hg);
+        blk_mv_sub<K>(nd, ga, hd);
+      }
+      blk_inv<K>(nb, &rsum);
+      al = blk_mul<K>(nb, na);
+      blk_neg<K>(al);
+      ga = blk_mul<K>(nb, ng);
+      blk_neg<K>(ga);
+      de = blk_mv<K>(nb, nd);
+    }
+  }
   // ---- back-substitution
   const Vec<K> Fv = de;
-  Vec<K> Fn = vec_shfl<K>(Fv, lane < 31 ? lane + 1 : lane);
-  if (lane == 31)
+  Vec<K> Fn;
+  if (NW == 1) {
+    Fn = vec_shfl<K>(Fv, lane < 31 ? lane + 1 : lane);
+  } else {
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < K; ++u) xch[u * NT + tid] = Fv.v[u];
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < K; ++u) Fn.v[u] = tid + 1 < NT ? xch[u * NT + tid + 1] : 0.0;
+  }
+  if (tid == NT - 1)
 #pragma unroll
     for (int u = 0; u < K; ++u) Fn.v[u] = 0.0;
 #pragma unroll
   for (int j = 0; j < M; ++j) {
-    const double* st = sm + lane;
+    const double* st = sm + tid;
 #pragma unroll
     for (int u = 0; u < K; ++u) {
 #pragma unroll
       for (int v = 0; v < K; ++v) {
-        AP[j].v[u][v] = st[32 * ((j * K + u) * (2 * K + 1) + 2 * v)];
-        CP[j].v[u][v] = st[32 * ((j * K + u) * (2 * K + 1) + 2 * v + 1)];
+        AP[j].v[u][v] = st[NT * ((j * K + u) * (2 * K + 1) + 2 * v)];
+        CP[j].v[u][v] = st[NT * ((j * K + u) * (2 * K + 1) + 2 * v + 1)];
       }
-      DP[j].v[u] = st[32 * ((j * K + u) * (2 * K + 1) + 2 * K)];
+      DP[j].v[u] = st[NT * ((j * K + u) * (2 * K + 1) + 2 * K)];
     }
   }
   Vec<K> Ev = DP[M - 1];
@@ -533,9 +626,9 @@ __global__ void __launch_bounds__(32) blk_segment_solve_kernel(BlkArgs g) {
       if (!all_ok) status_nonfinite(g.status, seg);
     }
   }
-  __syncwarp();
-  for (int r = lane; r < L; r += 32) g.x[b + r] = smf[r];
-  if (lane < K && Pt.rs >= 0) g.x[Pt.rs + lane] = xrv.v[lane];
+  SYNC();
+  for (int r = tid; r < L; r += NT) g.x[b + r] = smf[r];
+  if (tid < K && Pt.rs >= 0) g.x[Pt.rs + tid] = xrv.v[tid];
   // ---- certificate records: the separator rows' couplings to this body
   if (g.rec) {
     double* rc = g.rec + (long)seg * 4 * K;
@@ -552,20 +645,20 @@ __global__ void __launch_bounds__(32) blk_segment_solve_kernel(BlkArgs g) {
         return __ldg(g.data + g.boff[d + K] + row);
       }
     };
-    if (lane < K) {
+    if (tid < K) {
       double sg = 0.0, ab = 0.0;
       if (Pt.ls >= 0) {
-        const long row = Pt.ls + lane;
+        const long row = Pt.ls + tid;
         for (int t = 0; t < 2 * K && t < L; ++t) {
           const double pr = at(row, b + t) * smf[t];
           sg += pr;
           ab += fabs(pr);
         }
       }
-      rc[lane] = sg;
-      rc[K + lane] = ab;
-    } else if (lane >= 16 && lane < 16 + K) {
-      const int u = lane - 16;
+      rc[tid] = sg;
+      rc[K + tid] = ab;
+    } else if (tid >= 16 && tid < 16 + K) {
+      const int u = tid - 16;
       double sg = 0.0, ab = 0.0;
       if (Pt.rs >= 0) {
         const long row = Pt.rs + u;
@@ -678,29 +771,37 @@ __global__ void __launch_bounds__(128) blk_spec_factor_kernel(BlkSpecArgs g) {
     const long col = r0 + v + (t - 1) * K;
     return (col >= 0 && col < n) ? __ldg(g.data + off + r0) : 0.0;
   };
-  double Dg[HB], Fc[HB], Nc[HB];
-#pragma unroll
-  for (int i = 0; i < HB; ++i) {
-    const long r0 = h == 0 ? S - (long)(HB - i) * K : S + K + (long)(HB - 1 - i) * K;
-    Dg[i] = act ? ld(r0, 1, oD, kD) : eye;
-    Fc[i] = ld(r0, tF, oF, kF);
-    Nc[i] = ld(r0, tN, oN, kN);
-  }
   // couplings with the separator: B1 = A(S+u, S-K+v) / C0 = A(S+u, S+K+v);
   // near block -> separator: A(S-K+u, S+v) / A(S+K+u, S+v)
   const double Bc = act ? blk_at(g, K, S + u, h == 0 ? S - K + v : S + K + v) : 0.0;
   const double Cc = act ? blk_at(g, K, h == 0 ? S - K + u : S + K + u, S + v) : 0.0;
   const double Dss = act ? blk_at(g, K, S + u, S + v) : eye;
   double rsum = 0.0;
-  double Np[HB];  // Np[i] = Fc[i+1] G_i (the weights' transfer from block i+1 to block i)
+  // far -> near sweep with the next block's loads in flight; only the
+  // transfer products Np[i] = Fc[i+1] G_i stay in registers
+  auto row0 = [&](int i) -> long { return h == 0 ? S - (long)(HB - i) * K : S + K + (long)(HB - 1 - i) * K; };
+  double Dn = act ? ld(row0(0), 1, oD, kD) : eye, Fn = ld(row0(0), tF, oF, kF), Nn = ld(row0(0), tN, oN, kN);
+  double G = 0.0, Ncp = 0.0;  // previous block's inverse pivot and its coupling toward this block
+  double Np[HB];
 #pragma unroll
   for (int i = 0; i < HB; ++i) {
-    if (i > 0) Dg[i] -= dmul(Fc[i], dmul(Dg[i - 1], Nc[i - 1], base, u, v, K), base, u, v, K);
-    const double Gi = dinv(Dg[i], base, u, v, K, &rsum);
-    Dg[i] = act ? Gi : 0.0;
-    if (i > 0) Np[i - 1] = dmul(Fc[i], Dg[i - 1], base, u, v, K);
+    double D = Dn;
+    const double Fc = Fn, Nc = Nn;
+    if (i + 1 < HB) {
+      const long r1 = row0(i + 1);
+      Dn = act ? ld(r1, 1, oD, kD) : eye;
+      Fn = ld(r1, tF, oF, kF);
+      Nn = ld(r1, tN, oN, kN);
+    }
+    if (i > 0) {
+      D -= dmul(Fc, dmul(G, Ncp, base, u, v, K), base, u, v, K);
+      Np[i - 1] = dmul(Fc, G, base, u, v, K);
+    }
+    const double Gi = dinv(D, base, u, v, K, &rsum);
+    G = act ? Gi : 0.0;
+    Ncp = Nc;
   }
-  const double Xn = Dg[HB - 1];  // near diagonal block of the truncated inverse
+  const double Xn = G;  // near diagonal block of the truncated inverse
   const double part = dmul(Bc, dmul(Xn, Cc, base, u, v, K), base, u, v, K);
   const double other = __shfl_xor_sync(0xffffffffu, part, 16);
   double Ti = dinv(Dss - part - other, base, u, v, K, &rsum);

@@ -542,43 +542,51 @@ void fill_band_offsets(BlkArgs& a, int K, long n, int s_, int r_, size_t data_le
   a.data_len = (long)data_len;
 }
 
-template <int K, int M, int LAYOUT>
+template <int K, int M, int LAYOUT, int NW>
 void launch_blk_kernel(const BlkArgs& a, cudaStream_t s) {
-  constexpr int bytes = BlkSmem<K, M>::bytes(LAYOUT);
+  constexpr int bytes = BlkSmem<K, M, NW>::bytes(LAYOUT);
   static bool attr = false;
   if (!attr) {
-    CUDA_TRY(cudaFuncSetAttribute(blk_segment_solve_kernel<K, M, LAYOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  bytes));
+    CUDA_TRY(cudaFuncSetAttribute(blk_segment_solve_kernel<K, M, LAYOUT, NW>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     attr = true;
   }
-  blk_segment_solve_kernel<K, M, LAYOUT><<<a.nseg, 32, bytes, s>>>(a);
+  blk_segment_solve_kernel<K, M, LAYOUT, NW><<<a.nseg, 32 * NW, bytes, s>>>(a);
   LAUNCH_CHECK();
 }
 
-// chunk depth M per block size: 32 M block rows per body
-int blk_chunk(int K, int NB) {
-  if (K == 4) return NB <= 64 ? 2 : 0;
-  if (K == 3) return NB <= 64 ? 2 : (NB <= 96 ? 3 : 0);
-  if (K == 2) return NB <= 96 ? 3 : (NB <= 160 ? 5 : 0);
-  return 0;
+// chunk depth M and warps NW per body: 32 NW M block rows per body
+struct BlkShape {
+  int M, NW;
+};
+BlkShape blk_shape(int K, int NB) {
+  if (K == 4) return NB <= 64 ? BlkShape{2, 1} : (NB <= 128 ? BlkShape{2, 2} : BlkShape{0, 0});
+  if (K == 3)
+    return NB <= 64 ? BlkShape{2, 1} : (NB <= 96 ? BlkShape{3, 1} : (NB <= 192 ? BlkShape{3, 2} : BlkShape{0, 0}));
+  if (K == 2)
+    return NB <= 96 ? BlkShape{3, 1} : (NB <= 160 ? BlkShape{5, 1} : (NB <= 320 ? BlkShape{5, 2} : BlkShape{0, 0}));
+  return BlkShape{0, 0};
 }
-int blk_max_nb(int K) { return K == 4 ? 64 : (K == 3 ? 96 : 160); }
+int blk_max_nb(int K) { return K == 4 ? 128 : (K == 3 ? 192 : 320); }
 
 bool launch_blk_segments(int K, int NB, int layout, const BlkArgs& a, cudaStream_t s) {
-  const int M = blk_chunk(K, NB);
-#define PSG_BLK_CASE(KK_, MM_)                                                   \
-  if (K == KK_ && M == MM_) {                                                    \
+  const BlkShape sh = blk_shape(K, NB);
+#define PSG_BLK_CASE(KK_, MM_, NW_)                                              \
+  if (K == KK_ && sh.M == MM_ && sh.NW == NW_) {                                 \
     if (layout == kBlkBlockTri)                                                  \
-      launch_blk_kernel<KK_, MM_, kBlkBlockTri>(a, s);                           \
+      launch_blk_kernel<KK_, MM_, kBlkBlockTri, NW_>(a, s);                      \
     else                                                                         \
-      launch_blk_kernel<KK_, MM_, kBlkBanded>(a, s);                             \
+      launch_blk_kernel<KK_, MM_, kBlkBanded, NW_>(a, s);                        \
     return true;                                                                 \
   }
-  PSG_BLK_CASE(4, 2)
-  PSG_BLK_CASE(3, 2)
-  PSG_BLK_CASE(3, 3)
-  PSG_BLK_CASE(2, 3)
-  PSG_BLK_CASE(2, 5)
+  PSG_BLK_CASE(4, 2, 1)
+  PSG_BLK_CASE(4, 2, 2)
+  PSG_BLK_CASE(3, 2, 1)
+  PSG_BLK_CASE(3, 3, 1)
+  PSG_BLK_CASE(3, 3, 2)
+  PSG_BLK_CASE(2, 3, 1)
+  PSG_BLK_CASE(2, 5, 1)
+  PSG_BLK_CASE(2, 5, 2)
 #undef PSG_BLK_CASE
   return false;
 }
@@ -643,7 +651,7 @@ struct BlkSolver {
       hpart[g].rs = g < nsep ? hsep[g] : -1;
     }
     NB = (maxL + K - 1) / K;
-    if (minL < blk_hb(K) * K || minL < 2 * K || blk_chunk(K, NB) == 0 || nsep < 1) return;
+    if (minL < blk_hb(K) * K || minL < 2 * K || blk_shape(K, NB).M == 0 || nsep < 1) return;
     part.alloc(nseg);
     sep.alloc(nsep);
     CUDA_TRY(cudaMemcpy(part.p, hpart.data(), sizeof(GPart) * nseg, cudaMemcpyHostToDevice));
