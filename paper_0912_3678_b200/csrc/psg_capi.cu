@@ -624,8 +624,24 @@ struct BlkSolver {
     hpart.clear();
     hsep.clear();
     int maxL = 0, minL = INT_MAX;
+    // reference bodies, neighbours merged (with the separator between them)
+    // while the union still fits one body kernel: fewer separators means less
+    // factor / separator work for the same body work
+    std::vector<std::pair<int, int>> bodies;
     for (int i = 0; i < P.p; ++i) {
       const int b = P.body_begin(i), L = P.body_end(i) - b;
+      if (!bodies.empty()) {
+        auto& c = bodies.back();
+        const int merged = c.second + K + L;
+        if ((merged + K - 1) / K <= blk_max_nb(K)) {
+          c.second = merged;
+          continue;
+        }
+      }
+      bodies.emplace_back(b, L);
+    }
+    for (size_t i = 0; i < bodies.size(); ++i) {
+      const int b = bodies[i].first, L = bodies[i].second;
       const int Lu = L / unit;
       auto nb_of = [&](int t) { return (((Lu - (t - 1) * ku) + t - 1) / t * unit + K - 1) / K; };
       int t = 1;
@@ -638,7 +654,7 @@ struct BlkSolver {
         maxL = std::max(maxL, len);
         minL = std::min(minL, len);
         cur += len;
-        if (u + 1 < t || i + 1 < P.p) {
+        if (u + 1 < t || i + 1 < bodies.size()) {
           hsep.push_back(cur);
           cur += K;
         }
