@@ -503,12 +503,6 @@ struct TriSolver {
     }
   }
 
-  long long reduced_ops(bool spec) const {
-    if (spec) return (long long)(S0.nseg - 1) * (2 * kHalo + 1);  // one 65-term dot product per separator
-    long long ops = 0;
-    for (size_t l = 1; l < lv.size(); ++l) ops += 12LL * lv[l]->q;
-    return ops;
-  }
 };
 
 // ----------------------------------------------------------------------------
@@ -1131,15 +1125,6 @@ struct GenSolver {
       lv[1]->x = lv[0]->x_next.p;
     }
   }
-
-  long long reduced_ops() const {
-    long long ops = 0;
-    for (size_t l = 1; l < lv.size(); ++l) {
-      const long n = lv[l]->A.n;
-      ops += (long long)n * (lv[l]->es + 1 + lv[l]->er) * (lv[l]->es + 2);
-    }
-    return ops;
-  }
 };
 
 }  // namespace
@@ -1533,6 +1518,20 @@ Outcome read_status(const DevStatus& st) {
   return o;
 }
 
+// SolveStats::reduced_ops: multiply-adds of phase 2 as a function of the
+// reference plan's reduced system only (q blocks of size k; SPEC's
+// "sequential fraction" law), whatever internal segmentation the GPU uses:
+// speculative -- one (2H+1)-block weight product per separator;
+// exact -- block-tridiagonal elimination, ~6 k^3 per block.
+long long reduced_ops_of(const psg_handle* h, bool spec) {
+  const long long q = h->plan.sep_count(), k = h->plan.sep_size;
+  if (spec) {
+    const long long H = h->generic ? (long long)blk_hb((int)k) : kHalo;
+    return q * (2 * H + 1) * k * k;
+  }
+  return 6 * q * k * k * k;
+}
+
 void ensure_exact_generic(psg_handle* h, cudaStream_t s) {
   if (h->exact_factored) return;
   h->gen.launches = 0;
@@ -1593,6 +1592,7 @@ void generic_blocking(psg_handle* h, const double* df, double* dx, cudaStream_t 
       h->solve_launches = launches;
       if (stats) {
         add_phase_stats(h, stats, h->ev);
+        stats->reduced_ops += reduced_ops_of(h, true);
         stats->certificate = std::max(stats->certificate, o.cert);
         stats->speculative = 1;
       }
@@ -1606,7 +1606,7 @@ void generic_blocking(psg_handle* h, const double* df, double* dx, cudaStream_t 
   h->solve_launches = generic_solve(h, df, dx, s, stats != nullptr, &cert);
   if (stats) {
     add_phase_stats(h, stats, h->ev);
-    stats->reduced_ops += h->gen.reduced_ops();
+    stats->reduced_ops += reduced_ops_of(h, false);
     stats->certificate = std::max(stats->certificate, cert);
     stats->speculative = 0;
     stats->fallbacks += fallbacks;
@@ -1678,7 +1678,7 @@ void tri_solve_blocking(psg_handle* h, const double* df, double* dx, cudaStream_
     stats->phase1_seconds += t01 * 1e-3;  // accumulate like SolveStats (src/parfact.cpp:233-237)
     stats->phase2_seconds += t12 * 1e-3;
     stats->phase3_seconds += t23 * 1e-3;
-    stats->reduced_ops += h->tri.reduced_ops(spec_used);
+    stats->reduced_ops += reduced_ops_of(h, spec_used);
     stats->certificate = std::max(stats->certificate, cert);
     stats->speculative = spec_used ? 1 : 0;
     stats->fallbacks += fallbacks;
@@ -1735,7 +1735,7 @@ void drain(psg_handle* h, psg_stats* stats) {
       cudaEventElapsedTime(&t23, h->ring_t[pd.slot][2], h->ring_t[pd.slot][3]);
       stats->phase1_seconds += t01 * 1e-3;
       stats->phase3_seconds += t23 * 1e-3;
-      if (!h->generic) stats->reduced_ops += h->tri.reduced_ops(pd.spec);
+      stats->reduced_ops += reduced_ops_of(h, pd.spec);
       stats->certificate = std::max(stats->certificate, o.cert);
       stats->speculative = pd.spec ? 1 : 0;
     }
@@ -1954,7 +1954,7 @@ int psg_solve_reduced(const psg_handle* hc, const double* rhs, double* x, int on
       if (!on_device) CUDA_TRY(cudaMemcpyAsync(x, xo, sizeof(double) * dim, cudaMemcpyDeviceToHost, s));
       CUDA_TRY(cudaStreamSynchronize(s));
       CUDA_TRY(cudaEventRecord(h->ev_done, s));
-      if (stats) stats->reduced_ops += h->gen.reduced_ops();
+      if (stats) stats->reduced_ops += reduced_ops_of(h, false);
       return 0;
     }
     if (h->refined) throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "reduced system was refined internally (bodies > 1056 rows)"};
@@ -1979,7 +1979,7 @@ int psg_solve_reduced(const psg_handle* hc, const double* rhs, double* x, int on
     if (!on_device) CUDA_TRY(cudaMemcpyAsync(x, xo, sizeof(double) * q, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     CUDA_TRY(cudaEventRecord(h->ev_done, s));
-    if (stats) stats->reduced_ops += h->tri.reduced_ops(false);
+    if (stats) stats->reduced_ops += reduced_ops_of(h, false);
     return 0;
   } catch (const Fail& f_) {
     return set_err(err, errlen, f_.code, f_.msg);
