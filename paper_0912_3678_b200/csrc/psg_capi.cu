@@ -1729,12 +1729,14 @@ void drain(psg_handle* h, psg_stats* stats) {
   for (const auto& pd : todo) {
     CUDA_TRY(cudaEventSynchronize(h->ring_done[pd.slot]));
     const Outcome o = read_status(h->h_ring[pd.slot]);
-    if (stats && pd.timing) {
-      float t01 = 0, t23 = 0;
-      cudaEventElapsedTime(&t01, h->ring_t[pd.slot][0], h->ring_t[pd.slot][1]);
-      cudaEventElapsedTime(&t23, h->ring_t[pd.slot][2], h->ring_t[pd.slot][3]);
-      stats->phase1_seconds += t01 * 1e-3;
-      stats->phase3_seconds += t23 * 1e-3;
+    if (stats) {
+      if (pd.timing) {  // phase times only for solves enqueued with timing
+        float t01 = 0, t23 = 0;
+        cudaEventElapsedTime(&t01, h->ring_t[pd.slot][0], h->ring_t[pd.slot][1]);
+        cudaEventElapsedTime(&t23, h->ring_t[pd.slot][2], h->ring_t[pd.slot][3]);
+        stats->phase1_seconds += t01 * 1e-3;
+        stats->phase3_seconds += t23 * 1e-3;
+      }
       stats->reduced_ops += reduced_ops_of(h, pd.spec);
       stats->certificate = std::max(stats->certificate, o.cert);
       stats->speculative = pd.spec ? 1 : 0;

@@ -5,6 +5,7 @@
 set -u
 cd "$(dirname "$0")/.."
 O=gpurun_out
+TAG=${TAG:-r01}
 mkdir -p $O
 Q=${1:-}
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > $O/gpu.txt 2>&1
@@ -37,3 +38,14 @@ python tools/cfg_step.py 3 3 > /dev/null 2>&1 && \
 python tools/cfg_step.py 4 3 > /dev/null 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:"chain_" \
   -c 12 -o $O/full_cfg4 python tools/cfg_step.py 4 3 > $O/ncu_full4.log 2>&1; echo "ncu-full4 rc=$?"
+# summarise on the box (the .ncu-rep files are too large to travel back)
+python tools/summarize_ncu.py $O/prof ${TAG:-r01} > $O/summary.log 2>&1; echo "summary rc=$?"
+for k in "tri_segment_solve" "tri_spec_factor" "tri_spec_sep"; do
+  python tools/ncu_lines.py $O/full.ncu-rep "$k" --top 25 > $O/prof/lines_$k.txt 2>&1
+done
+python tools/ncu_lines.py $O/full_cfg2.ncu-rep blk_segment --top 25 > $O/prof/lines_cfg2_blk_segment.txt 2>&1
+python tools/ncu_lines.py $O/full_cfg2.ncu-rep blk_spec_factor --top 25 > $O/prof/lines_cfg2_blk_spec_factor.txt 2>&1
+python tools/ncu_lines.py $O/full_cfg3.ncu-rep blk_segment --top 25 > $O/prof/lines_cfg3_blk_segment.txt 2>&1
+python tools/ncu_lines.py $O/full_cfg4.ncu-rep chain_final --top 25 > $O/prof/lines_cfg4_chain_final.txt 2>&1
+mkdir -p /tmp/ncu_reps && mv $O/*.ncu-rep /tmp/ncu_reps/ 2>/dev/null
+du -sh $O
