@@ -5,22 +5,30 @@
 //   block row b >= 1  [ ... S_b  R_b ... ]                        x_b = R_b^-1 (f_b - S_b x_{b-1})
 //
 // i.e. a block lower-bidiagonal chain closed by the boundary condition.
-// With separators sigma_0 = 0 < sigma_1 < ... < sigma_P = nb - 1 (the
-// reference plan's separator blocks, src/partition.cpp:52-105), chunk j runs
-// the chain over blocks sigma_j + 1 .. sigma_{j+1}:
+// Chunk boundaries sigma_j = 16 j (internal, independent of the reference
+// plan) cut the chain into chunks; chunk j maps x_{sigma_j} to
 //     x_{sigma_{j+1}} = Phi_j x_{sigma_j} + phi_j,
-//     Phi_j = prod T_b, T_b = -R_b^-1 S_b      (factor: the body's F T G
-//                                               blocks, src/localfact.cpp)
-//     phi_j = the chain from 0 with f        (condense)
-// The reduced system in x_sigma is again a BVP-layout BABD (R = I, S = -Phi,
-// same Ba / Bb), solved by the same kernels recursively and finally by one
-// warp (chain_direct_kernel, partial pivoting on the small BC system).  The
-// final pass propagates x through every chunk and certifies the separator
-// rows (componentwise backward error of the row S x_prev + R x_sep = f).
+//     Phi_j = prod T_b, T_b = -R_b^-1 S_b    (the body's F T G coupling block,
+//                                             src/localfact.cpp:182-225)
+//     phi_j = the chain from 0 with f         (condense, src/localfact.cpp:765-781)
 //
-// MB lanes per chunk (lane i = row i of every block), 32 / MB chunks per
-// warp; all shuffles are executed by the whole warp (chunk lengths differ by
-// at most one step; shorter chunks idle through the last step).
+//   factor  chain_tm_kernel: per block T_b and M_b = R_b^-1 (one block per
+//           lane, LU in registers), stored beside the data; Phi_j by a
+//           shared-memory tree product; the next level's rows [-Phi_j | I].
+//   solve   chain_pass_kernel<0>: phi_j (condense) -> the reduced system in
+//           x_sigma is again a BVP-layout BABD (S = -Phi, R = I, same Ba / Bb),
+//           solved by the same kernels level by level, the last level by one
+//           warp (chain_direct_kernel, partial pivoting on the BC system);
+//           chain_pass_kernel<1>: x through every chunk from x_sigma, plus
+//           the separator rows' residuals condensed to R^-1 r (the chain's
+//           end value differs from the affine map by rounding, ~8 eps |x| per
+//           step); one correction A d = r through the reduced levels and
+//           chain_pass_kernel<2>: x += the homogeneous chain of d, certifying
+//           the corrected separator rows (componentwise backward error),
+//           chain_bc_cert_kernel the BC row.
+//
+// Passes: MB lanes per chunk (lane i = row i of every block), 32 / MB chunks
+// per warp; shuffles are executed by the whole warp (shorter chunks idle).
 #pragma once
 
 #include "psg_common.cuh"
