@@ -675,6 +675,338 @@ __global__ void __launch_bounds__(32 * NW) blk_segment_solve_kernel(BlkArgs g) {
 }
 
 // ---------------------------------------------------------------------------
+// body solver, narrow variant (block tridiagonal): LPB lanes per body, MC
+// block rows per lane, 32 / LPB bodies per warp.  Rows come straight from
+// global memory (each lane reads its own contiguous block rows); the chunk
+// state (AP, CP, DP per row) is parked in a lane-interleaved shared stash
+// instead of registers; the interface system has LPB rows (log2 LPB block-PCR
+// steps).  MC = 4: a quarter of the block-PCR work per block row of the
+// 2-rows-per-lane kernel, 37 KB of stash per warp (config 2: 3.6x fewer
+// instructions; ncu profiles/r01_*cfg2*).
+// ---------------------------------------------------------------------------
+template <int K, int MC, int LPB>
+struct BlkNarrow {
+  static constexpr int SR = 2 * K * K + K;           // stash doubles per row
+  static constexpr int BYTES = 8 * 32 * MC * SR;     // per warp
+};
+
+template <int K, int MC, int LPB>
+__global__ void __launch_bounds__(32) blk_body_narrow_kernel(BlkArgs g) {
+  static_assert(MC >= 3, "the chunk elimination's row-0 step needs at least 3 rows per lane");
+  static_assert(LPB >= 2 && LPB <= 32 && (LPB & (LPB - 1)) == 0, "lanes per body: power of two");
+  constexpr int KK = K * K, SR = BlkNarrow<K, MC, LPB>::SR, G = 32 / LPB;
+  constexpr unsigned FULL = 0xffffffffu;
+  extern __shared__ __align__(16) double stash[];
+  const int lane = threadIdx.x, grp = lane / LPB, r = lane % LPB;
+  const int seg = blockIdx.x * G + grp;
+  const bool live = seg < g.nseg;
+  const GPart Pt = g.part[live ? seg : g.nseg - 1];
+  const long b = Pt.b;
+  const int L = Pt.L, NB = L / K;
+  const long B0 = b / K, NBall = g.n / K;
+  const bool hasl = live && Pt.ls >= 0, hasr = live && Pt.rs >= 0;
+  Vec<K> xl, xrv;
+#pragma unroll
+  for (int u = 0; u < K; ++u) {
+    xl.v[u] = hasl ? __ldg(g.xsep + (long)(seg - 1) * K + u) : 0.0;
+    xrv.v[u] = hasr ? __ldg(g.xsep + (long)seg * K + u) : 0.0;
+  }
+  auto st = [&](int j, int e) -> double& { return stash[(j * SR + e) * 32 + lane]; };
+  auto put = [&](int j, const Blk<K>& A, const Blk<K>& C, const Vec<K>& D) {
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+#pragma unroll
+      for (int v = 0; v < K; ++v) {
+        st(j, u * K + v) = A.v[u][v];
+        st(j, KK + u * K + v) = C.v[u][v];
+      }
+      st(j, 2 * KK + u) = D.v[u];
+    }
+  };
+  auto get = [&](int j, Blk<K>& A, Blk<K>& C, Vec<K>& D) {
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+#pragma unroll
+      for (int v = 0; v < K; ++v) {
+        A.v[u][v] = st(j, u * K + v);
+        C.v[u][v] = st(j, KK + u * K + v);
+      }
+      D.v[u] = st(j, 2 * KK + u);
+    }
+  };
+  // block row q of the body: sub / diag / super block pointers (padding = identity,
+  // separator couplings folded into the rhs)
+  auto rowp = [&](int q) -> const double* {
+    const long B = B0 + q;
+    return g.data + (B == 0 ? -KK : (3 * B - 1) * KK);  // sub | diag | super
+  };
+  auto load_blk = [&](int q, int t, Blk<K>& X) {  // t = 0 sub, 1 diag, 2 super
+    const long B = B0 + q;
+    const bool pad = !live || q >= NB;
+    const bool zero = t == 0 ? (q == 0 || B == 0) : (t == 2 ? (q == NB - 1 || B + 1 >= NBall) : false);
+    const double* p = rowp(q) + t * KK;
+#pragma unroll
+    for (int u = 0; u < K; ++u)
+#pragma unroll
+      for (int v = 0; v < K; ++v)
+        X.v[u][v] = pad ? (t == 1 && u == v ? 1.0 : 0.0) : (zero ? 0.0 : __ldg(p + u * K + v));
+  };
+  auto load_f = [&](int q, Vec<K>& F) {
+    const bool pad = !live || q >= NB;
+#pragma unroll
+    for (int u = 0; u < K; ++u) F.v[u] = pad ? 0.0 : __ldg(g.f + b + (long)q * K + u);
+    if (pad) return;
+    if (q == 0 && hasl) {  // F -= A(first row, left separator) x_l
+      const double* p = rowp(q);
+#pragma unroll
+      for (int u = 0; u < K; ++u)
+#pragma unroll
+        for (int v = 0; v < K; ++v) F.v[u] = fma(-__ldg(p + u * K + v), xl.v[v], F.v[u]);
+    }
+    if (q == NB - 1 && hasr) {  // F -= C(last row, right separator) x_r
+      const double* p = rowp(q) + 2 * KK;
+#pragma unroll
+      for (int u = 0; u < K; ++u)
+#pragma unroll
+        for (int v = 0; v < K; ++v) F.v[u] = fma(-__ldg(p + u * K + v), xrv.v[v], F.v[u]);
+    }
+  };
+  // ---- chunk elimination (Laszlo): AP_j y_first + y_j + CP_j y_last = DP_j, rows to the stash
+  const int q0 = r * MC;
+  double rsum = 0.0;
+  Blk<K> APp, CPp;
+  Vec<K> DPp;
+#pragma unroll 1
+  for (int j = 0; j < MC; ++j) {
+    const int q = q0 + j;
+    Blk<K> Ab, Db;
+    load_blk(q, 0, Ab);
+    load_blk(q, 1, Db);
+    Vec<K> Fv;
+    load_f(q, Fv);
+    Blk<K> APj, CPj;
+    Vec<K> DPj;
+    if (j >= 2) blk_mul_sub<K>(Db, Ab, CPp);
+    blk_inv<K>(Db, &rsum);
+    if (j >= 2) blk_mv_sub<K>(Fv, Ab, DPp);
+    DPj = blk_mv<K>(Db, Fv);
+    if (j >= 2) {
+      const Blk<K> aap = blk_mul<K>(Ab, APp);
+      APj = blk_mul<K>(Db, aap);
+      blk_neg<K>(APj);
+    } else {
+      APj = blk_mul<K>(Db, Ab);
+    }
+    {
+      Blk<K> Cb;
+      load_blk(q, 2, Cb);
+      CPj = blk_mul<K>(Db, Cb);
+    }
+    put(j, APj, CPj, DPj);
+    APp = APj;
+    CPp = CPj;
+    DPp = DPj;
+  }
+  // backward: rows MC-3 .. 1 in terms of (y_first, y_last)
+  {
+    Blk<K> An = APp, Cn = CPp;  // row j+1 (starts at MC-2 below)
+    Vec<K> Dn = DPp;
+    get(MC - 2, An, Cn, Dn);
+#pragma unroll 1
+    for (int j = MC - 3; j >= 1; --j) {
+      Blk<K> Aj, Cj;
+      Vec<K> Dj;
+      get(j, Aj, Cj, Dj);
+      blk_mv_sub<K>(Dj, Cj, Dn);
+      blk_mul_sub<K>(Aj, Cj, An);
+      Cj = blk_mul<K>(Cj, Cn);
+      blk_neg<K>(Cj);
+      put(j, Aj, Cj, Dj);
+      An = Aj;
+      Cn = Cj;
+      Dn = Dj;
+    }
+  }
+  // row 0 in terms of (y_prev_last, y_0, y_last)
+  Blk<K> A0, C0;
+  Vec<K> D0;
+  get(0, A0, C0, D0);
+  {
+    Blk<K> A1, C1;
+    Vec<K> D1;
+    get(1, A1, C1, D1);
+    Blk<K> R;
+    blk_set_eye<K>(R);
+    blk_mul_sub<K>(R, C0, A1);
+    blk_inv<K>(R, &rsum);
+    blk_mv_sub<K>(D0, C0, D1);
+    D0 = blk_mv<K>(R, D0);
+    A0 = blk_mul<K>(R, A0);
+    const Blk<K> cc = blk_mul<K>(C0, C1);
+    C0 = blk_mul<K>(R, cc);
+    blk_neg<K>(C0);
+    put(0, A0, C0, D0);
+  }
+  // ---- interface rows (LPB per body), block PCR inside the lane group;
+  // row MC-1 (APp, CPp, DPp) is unchanged by the backward pass and stays in the stash
+  Blk<K> al, ga, be;
+  Vec<K> de = D0;
+  blk_set_eye<K>(be);
+  blk_set_zero<K>(al);
+  {
+    const int lo1 = r > 0 ? lane - 1 : lane;
+    const Blk<K> pa = blk_shfl<K>(APp, lo1);
+    const Blk<K> pc = blk_shfl<K>(CPp, lo1);
+    const Vec<K> pd = vec_shfl<K>(DPp, lo1);
+    if (r > 0) {
+      al = blk_mul<K>(A0, pa);
+      blk_neg<K>(al);
+      blk_mul_sub<K>(be, A0, pc);
+      blk_mv_sub<K>(de, A0, pd);
+    }
+  }
+  blk_mul_sub<K>(be, C0, APp);
+  blk_mv_sub<K>(de, C0, DPp);
+  ga = blk_mul<K>(C0, CPp);
+  blk_neg<K>(ga);
+  blk_inv<K>(be, &rsum);
+  al = blk_mul<K>(be, al);
+  ga = blk_mul<K>(be, ga);
+  de = blk_mv<K>(be, de);
+#pragma unroll 1
+  for (int sd = 1; sd < LPB; sd <<= 1) {
+    const bool hl = r >= sd, hh = r + sd < LPB;
+    const int sl = hl ? lane - sd : lane, sh = hh ? lane + sd : lane;
+    Blk<K> nb, na, ng;
+    blk_set_eye<K>(nb);
+    Vec<K> nd = de;
+    {
+      const Blk<K> lg = blk_shfl<K>(ga, sl);
+      if (hl) blk_mul_sub<K>(nb, al, lg);
+      const Blk<K> la = blk_shfl<K>(al, sl);
+      if (hl)
+        na = blk_mul<K>(al, la);
+      else
+        blk_set_zero<K>(na);
+      const Vec<K> ld = vec_shfl<K>(de, sl);
+      if (hl) blk_mv_sub<K>(nd, al, ld);
+    }
+    {
+      const Blk<K> ha = blk_shfl<K>(al, sh);
+      if (hh) blk_mul_sub<K>(nb, ga, ha);
+      const Blk<K> hg = blk_shfl<K>(ga, sh);
+      if (hh)
+        ng = blk_mul<K>(ga, hg);
+      else
+        blk_set_zero<K>(ng);
+      const Vec<K> hd = vec_shfl<K>(de, sh);
+      if (hh) blk_mv_sub<K>(nd, ga, hd);
+    }
+    blk_inv<K>(nb, &rsum);
+    al = blk_mul<K>(nb, na);
+    blk_neg<K>(al);
+    ga = blk_mul<K>(nb, ng);
+    blk_neg<K>(ga);
+    de = blk_mv<K>(nb, nd);
+  }
+  // ---- back-substitution, x straight to global
+  const Vec<K> Fv = de;
+  Vec<K> Fn = vec_shfl<K>(Fv, r + 1 < LPB ? lane + 1 : lane);
+  if (r + 1 == LPB)
+#pragma unroll
+    for (int u = 0; u < K; ++u) Fn.v[u] = 0.0;
+  Vec<K> Ev;
+  {
+    Blk<K> aE, cE;
+    get(MC - 1, aE, cE, Ev);
+    blk_mv_sub<K>(Ev, aE, Fv);
+    blk_mv_sub<K>(Ev, cE, Fn);
+  }
+  bool finite = true;
+  Vec<K> yfirst = Fv, ylast;
+#pragma unroll
+  for (int u = 0; u < K; ++u) ylast.v[u] = 0.0;
+  const int qlast = NB - 1;
+#pragma unroll 1
+  for (int j = 0; j < MC; ++j) {
+    Vec<K> y;
+    if (j == 0) {
+      y = Fv;
+    } else if (j == MC - 1) {
+      y = Ev;
+    } else {
+      Blk<K> Aj, Cj;
+      Vec<K> Dj;
+      get(j, Aj, Cj, Dj);
+      y = Dj;
+      blk_mv_sub<K>(y, Aj, Fv);
+      blk_mv_sub<K>(y, Cj, Ev);
+    }
+    const int q = q0 + j;
+    if (live && q < NB) {
+#pragma unroll
+      for (int u = 0; u < K; ++u) {
+        finite &= isfinite(y.v[u]);
+        g.x[b + (long)q * K + u] = y.v[u];
+      }
+      if (q == qlast) ylast = y;
+    }
+  }
+  if (live && r == 0 && hasr)
+#pragma unroll
+    for (int u = 0; u < K; ++u) g.x[Pt.rs + u] = xrv.v[u];
+  if (g.status) {
+    const unsigned gm = (LPB == 32 ? FULL : ((1u << LPB) - 1u)) << (grp * LPB);
+    const unsigned badp = __ballot_sync(FULL, !isfinite(rsum)) & gm;
+    const unsigned badf = __ballot_sync(FULL, !finite) & gm;
+    if (live && r == 0) {
+      if (badp) status_pivot(g.status, seg);
+      if (badf) status_nonfinite(g.status, seg);
+    }
+  }
+  // ---- certificate records: separator rows' couplings to the first / last body block
+  if (g.rec && live) {
+    double* rc = g.rec + (long)seg * 4 * K;
+    if (r == 0) {  // left: the separator block row's super block times y(first block)
+#pragma unroll
+      for (int u = 0; u < K; ++u) {
+        double sg = 0.0, ab = 0.0;
+        if (hasl) {
+          const long BS = B0 - 1;
+          const double* cp = g.data + (BS == 0 ? KK : (3 * BS - 1) * KK + 2 * KK);
+#pragma unroll
+          for (int v = 0; v < K; ++v) {
+            const double pr = __ldg(cp + u * K + v) * yfirst.v[v];
+            sg += pr;
+            ab += fabs(pr);
+          }
+        }
+        rc[u] = sg;
+        rc[K + u] = ab;
+      }
+    }
+    if (q0 <= qlast && qlast < q0 + MC) {  // right: its sub block times y(last block)
+#pragma unroll
+      for (int u = 0; u < K; ++u) {
+        double sg = 0.0, ab = 0.0;
+        if (hasr) {
+          const long BR = B0 + NB;
+          const double* ap = g.data + (3 * BR - 1) * KK;
+#pragma unroll
+          for (int v = 0; v < K; ++v) {
+            const double pr = __ldg(ap + u * K + v) * ylast.v[v];
+            sg += pr;
+            ab += fabs(pr);
+          }
+        }
+        rc[2 * K + u] = sg;
+        rc[3 * K + u] = ab;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // speculative factor: warp per separator, half-warp per side, one block
 // element per lane (lane e = 4u + v of its half), HB block rows per side.
 // ---------------------------------------------------------------------------

@@ -563,7 +563,26 @@ BlkShape blk_shape(int K, int NB) {
 }
 int blk_max_nb(int K) { return K == 4 ? 128 : (K == 3 ? 192 : 320); }
 
+template <int K, int MC, int LPB>
+void launch_blk_narrow(const BlkArgs& a, cudaStream_t s) {
+  constexpr int bytes = BlkNarrow<K, MC, LPB>::BYTES;
+  static bool attr = false;
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(blk_body_narrow_kernel<K, MC, LPB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  bytes));
+    attr = true;
+  }
+  constexpr int G = 32 / LPB;
+  blk_body_narrow_kernel<K, MC, LPB><<<(a.nseg + G - 1) / G, 32, bytes, s>>>(a);
+  LAUNCH_CHECK();
+}
+
+
 bool launch_blk_segments(int K, int NB, int layout, const BlkArgs& a, cudaStream_t s) {
+  if (layout == kBlkBlockTri && K == 4) {  // narrow body kernel: 4 block rows per lane, 16 or 32 lanes per body
+    if (NB <= 64) return launch_blk_narrow<4, 4, 16>(a, s), true;
+    if (NB <= 128) return launch_blk_narrow<4, 4, 32>(a, s), true;
+  }
   const BlkShape sh = blk_shape(K, NB);
 #define PSG_BLK_CASE(KK_, MM_, NW_)                                              \
   if (K == KK_ && sh.M == MM_ && sh.NW == NW_) {                                 \
