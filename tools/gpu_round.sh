@@ -30,10 +30,10 @@ for c in 2 3 4; do
     python tools/cfg_step.py $c 3 > /dev/null 2>&1; echo "cfg$c list rc=$?"
 done
 python tools/cfg_step.py 2 3 > /dev/null 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"blk_spec_factor|blk_spec_sep|blk_segment|blk_cert" \
+  ncu --set full --clock-control none --import-source on -k regex:"blk_spec_factor|blk_spec_sep|blk_segment|blk_body_narrow|blk_band_narrow|blk_cert" \
   -c 4 -o $O/full_cfg2 python tools/cfg_step.py 2 3 > $O/ncu_full2.log 2>&1; echo "ncu-full2 rc=$?"
 python tools/cfg_step.py 3 3 > /dev/null 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"blk_spec_factor|blk_spec_sep|blk_segment|blk_cert" \
+  ncu --set full --clock-control none --import-source on -k regex:"blk_spec_factor|blk_spec_sep|blk_segment|blk_body_narrow|blk_band_narrow|blk_cert" \
   -c 4 -o $O/full_cfg3 python tools/cfg_step.py 3 3 > $O/ncu_full3.log 2>&1; echo "ncu-full3 rc=$?"
 python tools/cfg_step.py 4 3 > /dev/null 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:"chain_" \
@@ -43,9 +43,9 @@ python tools/summarize_ncu.py $O/prof ${TAG:-r01} > $O/summary.log 2>&1; echo "s
 for k in "tri_segment_solve" "tri_spec_factor" "tri_spec_sep"; do
   python tools/ncu_lines.py $O/full.ncu-rep "$k" --top 25 > $O/prof/lines_$k.txt 2>&1
 done
-python tools/ncu_lines.py $O/full_cfg2.ncu-rep blk_segment --top 25 > $O/prof/lines_cfg2_blk_segment.txt 2>&1
+python tools/ncu_lines.py $O/full_cfg2.ncu-rep "blk_segment|blk_body_narrow" --top 25 > $O/prof/lines_cfg2_blk_body.txt 2>&1
 python tools/ncu_lines.py $O/full_cfg2.ncu-rep blk_spec_factor --top 25 > $O/prof/lines_cfg2_blk_spec_factor.txt 2>&1
-python tools/ncu_lines.py $O/full_cfg3.ncu-rep blk_segment --top 25 > $O/prof/lines_cfg3_blk_segment.txt 2>&1
+python tools/ncu_lines.py $O/full_cfg3.ncu-rep "blk_segment|blk_band_narrow" --top 25 > $O/prof/lines_cfg3_blk_body.txt 2>&1
 python tools/ncu_lines.py $O/full_cfg4.ncu-rep chain_final --top 25 > $O/prof/lines_cfg4_chain_final.txt 2>&1
 mkdir -p /tmp/ncu_reps && mv $O/*.ncu-rep /tmp/ncu_reps/ 2>/dev/null
 du -sh $O

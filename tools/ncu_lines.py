@@ -13,7 +13,7 @@ top = int(sys.argv[sys.argv.index("--top") + 1]) if "--top" in sys.argv else 30
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass",
                       "--kernel-name", "regex:" + kre], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
-fname, hdr, lines = None, None, []
+fname, hdr, lines, func = None, None, [], None
 for r in rows:
     if not r:
         continue
@@ -32,6 +32,8 @@ for r in rows:
         num = lambda v: float(v) if v not in ("", "-") else 0.0
         lines.append((fname, int(r[0]), r[1], num(r[hdr["Warp Stall Sampling (All Samples)"]]),
                       num(r[hdr["Instructions Executed"]])))
+if func is None:
+    sys.exit(f"no kernel matching {kre!r} in {rep}")
 tot = sum(x[3] for x in lines) or 1.0
 print(func, "samples", tot)
 for f, ln, src, v, ins in sorted(lines, key=lambda x: -x[3])[:top]:
