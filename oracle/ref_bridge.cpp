@@ -15,12 +15,14 @@
 // factor/solve path.
 #include <omp.h>
 
+#include <algorithm>
 #include <cstring>
 #include <exception>
 #include <string>
 #include <vector>
 
 #include "parsol/errors.hpp"
+#include "parsol/io.hpp"
 #include "parsol/parfact.hpp"
 #include "parsol/seqref.hpp"
 #include "parsol/structmat.hpp"
@@ -159,6 +161,48 @@ int ref_generate_random(int kind, int n, int m, int s, int r, unsigned long long
   } catch (const std::exception& e) {
     return report(e, err, errlen);
   }
+}
+
+// STRUCTMAT / VEC text through the reference writer / parser (src/io.cpp):
+// returns the byte length (writing at most cap bytes), or -1 - error code.
+long ref_write_matrix(void* hm, const char* comment, char* out, size_t cap) {
+  std::vector<std::string> c;
+  if (comment) c.emplace_back(comment);
+  const std::string s = write_matrix(static_cast<RefMat*>(hm)->A, c);
+  std::memcpy(out, s.data(), std::min(cap, s.size()));
+  return (long)s.size();
+}
+
+long ref_write_vector(const double* v, size_t n, const char* comment, char* out, size_t cap) {
+  std::vector<std::string> c;
+  if (comment) c.emplace_back(comment);
+  const std::string s = write_vector(Vector(v, v + n), c);
+  std::memcpy(out, s.data(), std::min(cap, s.size()));
+  return (long)s.size();
+}
+
+// parse a STRUCTMAT text with the reference parser: 0 and a new matrix handle, or 1 + Errc
+int ref_parse_matrix(const char* text, size_t len, void** out, char* err, size_t errlen) {
+  try {
+    auto* h = new RefMat;
+    h->A = parse_matrix(std::string(text, len));
+    *out = h;
+    return 0;
+  } catch (const std::exception& e) {
+    return report(e, err, errlen);
+  }
+}
+
+int ref_mat_dims(void* hm, int* kind, int* n, int* m, int* s, int* r, size_t* len, double* data) {
+  const auto& A = static_cast<RefMat*>(hm)->A;
+  *kind = int(A.kind);
+  *n = A.n;
+  *m = A.m;
+  *s = A.s;
+  *r = A.r;
+  *len = A.data.size();
+  if (data) std::memcpy(data, A.data.data(), sizeof(double) * A.data.size());
+  return 0;
 }
 
 int ref_plan(void* hm, int p, int* body_begin, int* body_end, int* sep_start, int* sep_count,

@@ -3,6 +3,8 @@
     libpsg.so          CUDA kernels + the C ABI (include/psg.h)
     libparsol_b200.so  C++ host API mirroring the reference headers
                        (include/parsol/*.hpp) on top of libpsg.so
+    psg                command-line tool (generate / solve / verify / plan /
+                       bench with STRUCTMAT / VEC files), cli/psg.cpp
 
 Run ``python -m paper_0912_3678_b200.build`` or ``__graft_entry__.build()``.
 """
@@ -26,6 +28,8 @@ NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-
 
 LIBPSG = os.path.join(PKG, "libpsg.so")
 LIBHOST = os.path.join(PKG, "libparsol_b200.so")
+CLI = os.path.join(PKG, "psg")
+CUDA_HOME = os.path.dirname(os.path.dirname(NVCC))
 
 
 def _run(cmd, verbose):
@@ -56,8 +60,13 @@ def build(verbose: bool = True, force: bool = False, ptxas_verbose: bool = False
     hsrc = _sources(HOST, (".cpp",))
     hdeps = hsrc + _sources(os.path.join(INCLUDE, "parsol"), (".hpp",)) + [LIBPSG]
     if hsrc and (force or _newer(LIBHOST, hdeps)):
-        _run(["g++", "-O2", "-std=c++20", "-fPIC", "-shared", "-I" + INCLUDE, "-o", LIBHOST, *hsrc,
+        _run(["g++", "-O2", "-std=c++20", "-fPIC", "-fopenmp", "-shared", "-I" + INCLUDE, "-o", LIBHOST, *hsrc,
               "-L" + PKG, "-lpsg", "-Wl,-rpath,$ORIGIN"], verbose)
+    csrc = _sources(os.path.join(PKG, "cli"), (".cpp",))
+    if csrc and (force or _newer(CLI, csrc + [LIBHOST])):
+        _run(["g++", "-O2", "-std=c++20", "-I" + INCLUDE, "-I" + os.path.join(CUDA_HOME, "include"), "-o", CLI,
+              *csrc, "-L" + PKG, "-lparsol_b200", "-lpsg", "-L" + os.path.join(CUDA_HOME, "lib64"), "-lcudart",
+              "-fopenmp", "-Wl,-rpath,$ORIGIN", "-Wl,-rpath," + os.path.join(CUDA_HOME, "lib64")], verbose)
 
 
 if __name__ == "__main__":

@@ -3,6 +3,7 @@
 // parfact examples that test_parfact.cpp leaves as placeholders).
 //   test_host_api --cpu   host-only checks (no device work)
 //   test_host_api --gpu   factor / solve / residual on the B200
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -11,6 +12,7 @@
 #include <vector>
 
 #include "parsol/errors.hpp"
+#include "parsol/io.hpp"
 #include "parsol/parfact.hpp"
 #include "parsol/partition.hpp"
 #include "parsol/rng.hpp"
@@ -132,6 +134,45 @@ static void cpu_tests() {
   CHECK(std::string(strategy_name(Strategy::Lud)) == "lud" && strategy_from_name("cr") == Strategy::CyclicReduction);
   CHECK(!strategy_supports(Strategy::CyclicReduction, Kind::Banded, 2, 1));
   CHECK(strategy_supports(Strategy::Arce, Kind::Babd, 1, 1));
+  // STRUCTMAT / VEC round trips, bit-exact (reference io.hpp; tests/test_structmat.cpp round trip)
+  for (auto c : std::vector<std::array<int, 5>>{{0, 57, 1, 2, 3}, {1, 48, 4, 1, 1}, {2, 60, 4, 2, 2}, {3, 64, 4, 2, 2},
+                                                 {0, 33, 1, 1, 1}}) {
+    StructuredMatrix A = generate_random(Kind(c[0]), c[1], c[2], c[3], c[4], 7 + c[1], 2.0);
+    const std::string txt = write_matrix(A, {"round trip"});
+    CHECK(txt.rfind("STRUCTMAT 1 ", 0) == 0);
+    CHECK(parse_matrix(txt) == A);
+    CHECK(write_matrix(parse_matrix(txt), {"round trip"}) == txt);
+  }
+  {
+    Vector v = random_vector(41, 3);
+    v.push_back(-0.0);
+    v.push_back(1e-310);  // subnormal
+    const Vector w = parse_vector(write_vector(v, {"c"}));
+    CHECK(w.size() == v.size());
+    bool same = true;
+    for (size_t i = 0; i < v.size(); ++i) same &= std::memcmp(&v[i], &w[i], sizeof(double)) == 0;
+    CHECK(same);
+    CHECK(format_hex(1.5) == "0x1.8p+0");
+  }
+  auto errc_of = [](const std::function<void()>& fn) {
+    try {
+      fn();
+    } catch (const Error& e) {
+      return int(e.code());
+    }
+    return -1;
+  };
+  CHECK(errc_of([] { parse_matrix(""); }) == int(Errc::ParseError));
+  CHECK(errc_of([] { parse_matrix("STRUCTMAT 2 banded 3 1 1 1\n"); }) == int(Errc::UnsupportedVersion));
+  CHECK(errc_of([] { parse_matrix("STRUCTMAT 1 banded 3 1 1 1\n0x1p+0\n"); }) == int(Errc::ParseError));
+  CHECK(errc_of([] { parse_matrix("STRUCTMAT 1 babd 4 2 1 1\n"); }) == int(Errc::ParseError));  // corner shape
+  CHECK(errc_of([] { parse_matrix("STRUCTMAT 1 wat 3 1 1 1\n"); }) == int(Errc::ParseError));
+  CHECK(errc_of([] { parse_vector("VEC 1 2\n0x1p+0\nabc\n"); }) == int(Errc::ParseError));
+  CHECK(errc_of([] { parse_vector("VEC 1 1\n# c\n0x1p+0\n"); }) == -1);
+  CHECK(errc_of([] {
+          parse_matrix("STRUCTMAT 1 banded 3 1 1 1\n1\n2\n3\n4\n5\n6\n7\n8\n");
+        }) == int(Errc::ParseError));  // trailing data
+  CHECK(errc_of([] { read_file("/nonexistent/x.mat"); }) == int(Errc::IoError));
 }
 
 // ---------------------------------------------------------------- on the GPU
