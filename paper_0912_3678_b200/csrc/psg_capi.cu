@@ -15,6 +15,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -60,30 +61,95 @@ int set_err(char* err, size_t errlen, int code, const std::string& msg) {
 
 #define LAUNCH_CHECK() CUDA_TRY(cudaGetLastError())
 
+// A handle's buffers live on the device it was factored on: every entry
+// point that takes a handle runs there and restores the caller's device.
+struct DeviceGuard {
+  int prev = -1, want = -1;
+  explicit DeviceGuard(int d) : want(d) {
+    if (cudaGetDevice(&prev) == cudaSuccess && prev != d) cudaSetDevice(d);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0 && prev != want) cudaSetDevice(prev);
+  }
+};
+
+// The dynamic shared memory opt-in is a per-device attribute: set it once per
+// (kernel, device), also for processes that drive several GPUs.
+void ensure_smem(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(mu);
+  if (done.count({kernel, dev})) return;
+  CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.insert({kernel, dev});
+}
+
 // Process-wide cache of device blocks keyed by byte size: repeated
 // parallel_factor calls on same-shaped systems reuse memory instead of
 // paying cudaMalloc (and its implicit device synchronisation) each time.
 // Blocks are returned only after the owning handle's work has completed.
+// Device buffers are recycled by exact size (a handle re-created per step,
+// as the drop-in path does, costs no cudaMalloc/cudaFree), keyed by device.
+// At most kCacheCap bytes stay cached; an allocation that fails with
+// out-of-memory flushes the cache and retries.
 struct BlockCache {
+  static constexpr size_t kCacheCap = size_t(8) << 30;
   std::mutex mu;
-  std::multimap<size_t, void*> free_;
+  std::multimap<std::pair<int, size_t>, void*> free_;
+  size_t cached = 0;
+  static int device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+  }
+  void flush() {
+    std::lock_guard<std::mutex> g(mu);
+    int cur = device();
+    for (auto& kv : free_) {
+      cudaSetDevice(kv.first.first);
+      cudaFree(kv.second);
+    }
+    cudaSetDevice(cur);
+    free_.clear();
+    cached = 0;
+  }
   void* get(size_t bytes) {
+    const int dev = device();
     {
       std::lock_guard<std::mutex> g(mu);
-      auto it = free_.find(bytes);
+      auto it = free_.find({dev, bytes});
       if (it != free_.end()) {
         void* p = it->second;
         free_.erase(it);
+        cached -= bytes;
         return p;
       }
     }
     void* p = nullptr;
-    CUDA_TRY(cudaMalloc(&p, bytes));
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaErrorMemoryAllocation) {
+      cudaGetLastError();  // clear the sticky-free error state of the failed call
+      flush();
+      e = cudaMalloc(&p, bytes);
+    }
+    CUDA_TRY(e);
     return p;
   }
-  void put(void* p, size_t bytes) {
-    std::lock_guard<std::mutex> g(mu);
-    free_.emplace(bytes, p);
+  void put(void* p, size_t bytes, int dev) {
+    {
+      std::lock_guard<std::mutex> g(mu);
+      if (cached + bytes <= kCacheCap) {
+        free_.emplace(std::make_pair(dev, bytes), p);
+        cached += bytes;
+        return;
+      }
+    }
+    int cur = device();
+    cudaSetDevice(dev);
+    cudaFree(p);
+    cudaSetDevice(cur);
   }
 };
 
@@ -96,12 +162,13 @@ template <typename T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0, bytes = 0;
+  int dev = 0;  // device the buffer lives on
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() { reset(); }
   void reset() {
-    if (p) block_cache().put(p, bytes);
+    if (p) block_cache().put(p, bytes, dev);
     p = nullptr;
     n = bytes = 0;
   }
@@ -109,6 +176,7 @@ struct DevBuf {
     if (count <= n && p) return;
     reset();
     bytes = ((sizeof(T) * std::max<size_t>(count, 1)) + 511) & ~size_t(511);
+    dev = BlockCache::device();
     p = static_cast<T*>(block_cache().get(bytes));
     n = count;
   }
@@ -539,12 +607,7 @@ void fill_band_offsets(BlkArgs& a, int K, long n, int s_, int r_, size_t data_le
 template <int K, int M, int LAYOUT, int NW>
 void launch_blk_kernel(const BlkArgs& a, cudaStream_t s) {
   constexpr int bytes = BlkSmem<K, M, NW>::bytes(LAYOUT);
-  static bool attr = false;
-  if (!attr) {
-    CUDA_TRY(cudaFuncSetAttribute(blk_segment_solve_kernel<K, M, LAYOUT, NW>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    attr = true;
-  }
+  ensure_smem(reinterpret_cast<const void*>(blk_segment_solve_kernel<K, M, LAYOUT, NW>), bytes);
   blk_segment_solve_kernel<K, M, LAYOUT, NW><<<a.nseg, 32 * NW, bytes, s>>>(a);
   LAUNCH_CHECK();
 }
@@ -566,12 +629,7 @@ int blk_max_nb(int K) { return K == 4 ? 128 : (K == 3 ? 192 : 320); }
 template <int K, int MC, int LPB>
 void launch_blk_narrow(const BlkArgs& a, cudaStream_t s) {
   constexpr int bytes = BlkNarrow<K, MC, LPB>::BYTES;
-  static bool attr = false;
-  if (!attr) {
-    CUDA_TRY(cudaFuncSetAttribute(blk_body_narrow_kernel<K, MC, LPB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  bytes));
-    attr = true;
-  }
+  ensure_smem(reinterpret_cast<const void*>(blk_body_narrow_kernel<K, MC, LPB>), bytes);
   constexpr int G = 32 / LPB;
   blk_body_narrow_kernel<K, MC, LPB><<<(a.nseg + G - 1) / G, 32, bytes, s>>>(a);
   LAUNCH_CHECK();
@@ -854,11 +912,7 @@ struct ChainSolver {
   template <int M>
   void factor_t(cudaStream_t s) {
     constexpr int bytes = ChainSmem<M>::WARP * 8;
-    static bool attr = false;
-    if (!attr) {
-      CUDA_TRY(cudaFuncSetAttribute(chain_tm_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-      attr = true;
-    }
+    ensure_smem(reinterpret_cast<const void*>(chain_tm_kernel<M>), bytes);
     for (auto& L : lv) {
       if (L->direct) break;
       const long warps = (L->nb - 1 + 31) / 32;
@@ -1152,7 +1206,8 @@ struct GenSolver {
 // the handle
 // ----------------------------------------------------------------------------
 struct psg_handle {
-  psg_desc A{};  // device view
+  int device = 0;  // where the factorization lives (DeviceGuard in every entry point)
+  psg_desc A{};    // device view
   Plan plan;
   int strategy = 0;
   DevBuf<double> own_data, own_corner;
@@ -1397,6 +1452,7 @@ int psg_factor(const psg_desc* Ain, int p, int strategy, double tol, void* strea
   *out = nullptr;
   try {
     std::unique_ptr<psg_handle> h(new psg_handle);
+    CUDA_TRY(cudaGetDevice(&h->device));
     validate(*Ain);
     check_strategy(*Ain, strategy);
     h->plan = make_plan(*Ain, p);
@@ -1441,9 +1497,14 @@ int psg_factor(const psg_desc* Ain, int p, int strategy, double tol, void* strea
   }
 }
 
-void psg_release(psg_handle* h) { delete h; }
+void psg_release(psg_handle* h) {
+  if (!h) return;
+  DeviceGuard dg(h->device);
+  delete h;
+}
 
 int psg_set_option(psg_handle* h, int option, double value) {
+  DeviceGuard dg(h->device);
   std::lock_guard<std::mutex> g(h->mu);
   try {
     switch (option) {
@@ -1709,6 +1770,7 @@ void tri_solve_blocking(psg_handle* h, const double* df, double* dx, cudaStream_
 int psg_solve(const psg_handle* hc, const double* f, double* x, int on_device, void* stream, psg_stats* stats,
               char* err, size_t errlen) {
   psg_handle* h = const_cast<psg_handle*>(hc);
+  DeviceGuard dg(h->device);
   std::lock_guard<std::mutex> g(h->mu);
   try {
     cudaStream_t s = (cudaStream_t)stream;
@@ -1775,6 +1837,7 @@ void drain(psg_handle* h, psg_stats* stats) {
 int psg_solve_async(const psg_handle* hc, const double* f, double* x, int timing, void* stream, char* err,
                     size_t errlen) {
   psg_handle* h = const_cast<psg_handle*>(hc);
+  DeviceGuard dg(h->device);
   std::lock_guard<std::mutex> g(h->mu);
   try {
     cudaStream_t s = (cudaStream_t)stream;
@@ -1810,6 +1873,7 @@ int psg_solve_async(const psg_handle* hc, const double* f, double* x, int timing
 
 int psg_sync(const psg_handle* hc, psg_stats* stats, char* err, size_t errlen) {
   psg_handle* h = const_cast<psg_handle*>(hc);
+  DeviceGuard dg(h->device);
   std::lock_guard<std::mutex> g(h->mu);
   try {
     if (stats) {
@@ -1828,6 +1892,7 @@ int psg_sync(const psg_handle* hc, psg_stats* stats, char* err, size_t errlen) {
 // New matrix values with the same structure (kind, n, m, s, r, corner shape):
 // recompute the factor data on the handle's buffers (no re-planning).
 int psg_refactor(psg_handle* h, const psg_desc* A, void* stream, char* err, size_t errlen) {
+  DeviceGuard dg(h->device);
   std::lock_guard<std::mutex> g(h->mu);
   try {
     validate(*A);
@@ -1889,6 +1954,7 @@ int psg_reduced_info(const psg_handle* h, int* q, int* dim, int* k, int* has_cor
 
 int psg_reduced_blocks(const psg_handle* hc, double* diag, double* sub, double* super, char* err, size_t errlen) {
   psg_handle* h = const_cast<psg_handle*>(hc);
+  DeviceGuard dg(h->device);
   std::lock_guard<std::mutex> g(h->mu);
   try {
     CUDA_TRY(cudaEventSynchronize(h->ev_done));
@@ -1953,6 +2019,7 @@ int psg_reduced_blocks(const psg_handle* hc, double* diag, double* sub, double* 
 int psg_solve_reduced(const psg_handle* hc, const double* rhs, double* x, int on_device, void* stream,
                       psg_stats* stats, char* err, size_t errlen) {
   psg_handle* h = const_cast<psg_handle*>(hc);
+  DeviceGuard dg(h->device);
   std::lock_guard<std::mutex> g(h->mu);
   try {
     cudaStream_t s = (cudaStream_t)stream;
@@ -2011,6 +2078,7 @@ int psg_solve_reduced(const psg_handle* hc, const double* rhs, double* x, int on
 // weight rows (nsep x 68), 1: speculative Tdiag (nsep).  Returns the count.
 long psg_debug_buffer(const psg_handle* hc, int what, double* out, long cap) {
   psg_handle* h = const_cast<psg_handle*>(hc);
+  DeviceGuard dg(h->device);
   std::lock_guard<std::mutex> g(h->mu);
   if (cudaEventSynchronize(h->ev_done) != cudaSuccess) return -1;
   const DevBuf<double>& b = what == 0 ? h->tri.wts : h->tri.Tdiag;
