@@ -73,6 +73,23 @@ struct DeviceGuard {
   }
 };
 
+// Launch with programmatic stream serialization (PDL): the kernel may start
+// while its predecessor drains and calls pdl_wait() before consuming its output.
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel, args...));
+}
+
 // The dynamic shared memory opt-in is a per-device attribute: set it once per
 // (kernel, device), also for processes that drive several GPUs.
 void ensure_smem(const void* kernel, int bytes) {
@@ -387,20 +404,26 @@ SegMap segment_uniform(int q, int& maxlen) {
 }
 
 template <int M>
-void launch_segment_solve(const TriSolveArgs& a, int nseg, cudaStream_t s) {
+void launch_segment_solve(const TriSolveArgs& a, int nseg, cudaStream_t s, bool pdl) {
   constexpr int bytes = TriWarpSmem<M>::BYTES;
-  tri_segment_solve_kernel<M><<<nseg, 32, bytes, s>>>(a);
+  if (pdl)
+    launch_pdl(tri_segment_solve_kernel<M>, dim3(nseg), dim3(32), bytes, s, a);
+  else
+    tri_segment_solve_kernel<M><<<nseg, 32, bytes, s>>>(a);
 }
 
-void segment_solve(const TriSolveArgs& a, int nseg, int maxlen, cudaStream_t s) {
+// pdl: K3 stages A and F before waiting for its predecessor -- only valid
+// when neither is produced by the preceding kernel (the speculative solve:
+// user f, predecessor = the separator kernel)
+void segment_solve(const TriSolveArgs& a, int nseg, int maxlen, cudaStream_t s, bool pdl = false) {
   if (maxlen <= 32 * 5)
-    launch_segment_solve<5>(a, nseg, s);
+    launch_segment_solve<5>(a, nseg, s, pdl);
   else if (maxlen <= 32 * 9)
-    launch_segment_solve<9>(a, nseg, s);
+    launch_segment_solve<9>(a, nseg, s, pdl);
   else if (maxlen <= 32 * 17)
-    launch_segment_solve<17>(a, nseg, s);
+    launch_segment_solve<17>(a, nseg, s, pdl);
   else if (maxlen <= 32 * 33)
-    launch_segment_solve<33>(a, nseg, s);
+    launch_segment_solve<33>(a, nseg, s, pdl);
   else
     throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "segment longer than the per-warp capacity"};
   LAUNCH_CHECK();
@@ -455,7 +478,7 @@ struct TriSolver {
   }
 
   // level-0 back-substitution and separator certificate
-  void k3_and_cert(const RowArr& F, double* x, const double* xs, DevStatus* st, cudaStream_t s) {
+  void k3_and_cert(const RowArr& F, double* x, const double* xs, DevStatus* st, cudaStream_t s, bool pdl = false) {
     TriSolveArgs a{};
     a.A = A0;
     a.F = F;
@@ -464,9 +487,9 @@ struct TriSolver {
     a.x = x;
     a.crec = crec.p;
     a.status = st;
-    segment_solve(a, S0.nseg, maxlen0, s);
-    tri_cert_kernel<<<blocks_for(S0.nseg - 1, 256), 256, 0, s>>>(S0.nseg - 1, crec.p, st);
-    LAUNCH_CHECK();
+    segment_solve(a, S0.nseg, maxlen0, s, pdl);
+    launch_pdl(tri_cert_kernel, dim3(blocks_for(S0.nseg - 1, 256)), dim3(256), 0, s, S0.nseg - 1,
+               (const double4*)crec.p, st);
     launches += 2;
   }
 
@@ -480,7 +503,7 @@ struct TriSolver {
       CUDA_TRY(cudaEventRecord(ev[1], s));
       CUDA_TRY(cudaEventRecord(ev[2], s));
     }
-    k3_and_cert(F, x, xsep.p, st, s);
+    k3_and_cert(F, x, xsep.p, st, s, /*pdl=*/true);  // K3 stages its rows while the separators finish
   }
 
   // ---- exact multi-level path ----------------------------------------------

@@ -157,6 +157,14 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 
 // Reciprocal: MUFU approximation + two Newton steps (<= 1 ulp; no slow-path
 // branch).  0 -> inf and inf/NaN -> NaN propagate to the non-finite check.
+// Programmatic dependent launch (sm_90+): a kernel launched with the
+// programmatic-serialization attribute may start before its predecessor in
+// the stream has finished; pdl_wait() blocks until the predecessor's writes
+// are visible, pdl_trigger() lets the successor's CTAs launch early.  Both are
+// no-ops for ordinary launches.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 __device__ __forceinline__ double fast_rcp(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));

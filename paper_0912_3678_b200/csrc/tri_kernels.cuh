@@ -318,6 +318,7 @@ __global__ void __launch_bounds__(32) tri_spec_factor_kernel(TriRows A, SegMap S
 constexpr int kSepPerWarp = 4;
 __global__ void __launch_bounds__(256) tri_spec_sep_kernel(RowArr F, SegMap S, const double* __restrict__ wts,
                                                             double* __restrict__ xsep, DevStatus* reset) {
+  pdl_trigger();  // K3 may launch and stage its rows while the separators finish
   const int lane = threadIdx.x & 31;
   if (reset && blockIdx.x == 0 && threadIdx.x < kCertSlots + 2) {  // first kernel of the solve: fresh status
     if (threadIdx.x < kCertSlots)
@@ -427,6 +428,7 @@ __global__ void __launch_bounds__(32) tri_segment_solve_kernel(TriSolveArgs args
   double* sB = smem + 1 * ROW + 2 + __shfl_sync(FULL, shift, 1);
   double* sC = smem + 2 * ROW + 2 + __shfl_sync(FULL, shift, 2);
   double* sF = smem + 3 * ROW + 2 + __shfl_sync(FULL, shift, 3);
+  pdl_wait();  // the separator values come from the previous kernel (staging above overlaps it)
   const double xl = has_l ? args.xsep[seg - 1] : 0.0;
   const double xr = has_r ? args.xsep[seg] : 0.0;
   mbar_wait(&bar, 0);
@@ -571,6 +573,7 @@ __global__ void __launch_bounds__(32) tri_segment_solve_kernel(TriSolveArgs args
 // the separators, so this bounds the error the speculative interface let in.
 // ----------------------------------------------------------------------------
 __global__ void tri_cert_kernel(int nsep, const double4* __restrict__ crec, DevStatus* st) {
+  pdl_wait();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   double w = 0.0;
   if (j < nsep) {
