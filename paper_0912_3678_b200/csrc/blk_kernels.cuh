@@ -285,6 +285,7 @@ __global__ void __launch_bounds__(32 * NW) blk_segment_solve_kernel(BlkArgs g) {
     }
   }
   Vec<K> xl, xrv;
+  pdl_wait();  // separator values from the previous kernel (the staging above overlaps it)
 #pragma unroll
   for (int u = 0; u < K; ++u) {
     xl.v[u] = Pt.ls >= 0 ? __ldg(g.xsep + (long)lsi * K + u) : 0.0;
@@ -706,6 +707,7 @@ __global__ void __launch_bounds__(32) blk_body_narrow_kernel(BlkArgs g) {
   const long B0 = b / K, NBall = g.n / K;
   const bool hasl = live && Pt.ls >= 0, hasr = live && Pt.rs >= 0;
   Vec<K> xl, xrv;
+  pdl_wait();  // separator values from the previous kernel
 #pragma unroll
   for (int u = 0; u < K; ++u) {
     xl.v[u] = hasl ? __ldg(g.xsep + (long)(seg - 1) * K + u) : 0.0;
@@ -1160,6 +1162,7 @@ __global__ void __launch_bounds__(128) blk_spec_sep_kernel(const double* __restr
                                                            int nsep, const double* __restrict__ f,
                                                            double* __restrict__ xsep, DevStatus* reset) {
   constexpr int KK = K * K, NBK = 1 + 2 * HB, BPI = 32 / KK;
+  pdl_trigger();  // the body kernel may launch and stage its rows early
   const int lane = threadIdx.x & 31;
   const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (reset && blockIdx.x == 0 && threadIdx.x < kCertSlots + 2) {
@@ -1199,6 +1202,7 @@ template <int K>
 __global__ void blk_cert_kernel(const double* __restrict__ Tdiag, const int* __restrict__ sep, int nsep,
                                 const double* __restrict__ f, const double* __restrict__ xsep,
                                 const double* __restrict__ rec, DevStatus* st) {
+  pdl_wait();
   double worst = 0.0;
   for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < (long)nsep * K; t += (long)gridDim.x * blockDim.x) {
     const long j = t / K;

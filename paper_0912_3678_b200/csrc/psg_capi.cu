@@ -628,10 +628,13 @@ void fill_band_offsets(BlkArgs& a, int K, long n, int s_, int r_, size_t data_le
 }
 
 template <int K, int M, int LAYOUT, int NW>
-void launch_blk_kernel(const BlkArgs& a, cudaStream_t s) {
+void launch_blk_kernel(const BlkArgs& a, cudaStream_t s, bool pdl) {
   constexpr int bytes = BlkSmem<K, M, NW>::bytes(LAYOUT);
   ensure_smem(reinterpret_cast<const void*>(blk_segment_solve_kernel<K, M, LAYOUT, NW>), bytes);
-  blk_segment_solve_kernel<K, M, LAYOUT, NW><<<a.nseg, 32 * NW, bytes, s>>>(a);
+  if (pdl)
+    launch_pdl(blk_segment_solve_kernel<K, M, LAYOUT, NW>, dim3(a.nseg), dim3(32 * NW), bytes, s, a);
+  else
+    blk_segment_solve_kernel<K, M, LAYOUT, NW><<<a.nseg, 32 * NW, bytes, s>>>(a);
   LAUNCH_CHECK();
 }
 
@@ -650,27 +653,32 @@ BlkShape blk_shape(int K, int NB) {
 int blk_max_nb(int K) { return K == 4 ? 128 : (K == 3 ? 192 : 320); }
 
 template <int K, int MC, int LPB>
-void launch_blk_narrow(const BlkArgs& a, cudaStream_t s) {
+void launch_blk_narrow(const BlkArgs& a, cudaStream_t s, bool pdl) {
   constexpr int bytes = BlkNarrow<K, MC, LPB>::BYTES;
   ensure_smem(reinterpret_cast<const void*>(blk_body_narrow_kernel<K, MC, LPB>), bytes);
   constexpr int G = 32 / LPB;
-  blk_body_narrow_kernel<K, MC, LPB><<<(a.nseg + G - 1) / G, 32, bytes, s>>>(a);
+  if (pdl)
+    launch_pdl(blk_body_narrow_kernel<K, MC, LPB>, dim3((a.nseg + G - 1) / G), dim3(32), bytes, s, a);
+  else
+    blk_body_narrow_kernel<K, MC, LPB><<<(a.nseg + G - 1) / G, 32, bytes, s>>>(a);
   LAUNCH_CHECK();
 }
 
 
-bool launch_blk_segments(int K, int NB, int layout, const BlkArgs& a, cudaStream_t s) {
+// pdl: the body kernel stages A and f before waiting for its predecessor --
+// only for the speculative solve (user f, predecessor = the separator kernel)
+bool launch_blk_segments(int K, int NB, int layout, const BlkArgs& a, cudaStream_t s, bool pdl = false) {
   if (layout == kBlkBlockTri && K == 4) {  // narrow body kernel: 4 block rows per lane, 16 or 32 lanes per body
-    if (NB <= 64) return launch_blk_narrow<4, 4, 16>(a, s), true;
-    if (NB <= 128) return launch_blk_narrow<4, 4, 32>(a, s), true;
+    if (NB <= 64) return launch_blk_narrow<4, 4, 16>(a, s, pdl), true;
+    if (NB <= 128) return launch_blk_narrow<4, 4, 32>(a, s, pdl), true;
   }
   const BlkShape sh = blk_shape(K, NB);
 #define PSG_BLK_CASE(KK_, MM_, NW_)                                              \
   if (K == KK_ && sh.M == MM_ && sh.NW == NW_) {                                 \
     if (layout == kBlkBlockTri)                                                  \
-      launch_blk_kernel<KK_, MM_, kBlkBlockTri, NW_>(a, s);                      \
+      launch_blk_kernel<KK_, MM_, kBlkBlockTri, NW_>(a, s, pdl);                 \
     else                                                                         \
-      launch_blk_kernel<KK_, MM_, kBlkBanded, NW_>(a, s);                        \
+      launch_blk_kernel<KK_, MM_, kBlkBanded, NW_>(a, s, pdl);                   \
     return true;                                                                 \
   }
   PSG_BLK_CASE(4, 2, 1)
@@ -825,14 +833,19 @@ struct BlkSolver {
     a.xsep = xsep.p;
     a.rec = rec.p;
     a.status = st;
-    if (!launch_blk_segments(K, NB, layout, a, s)) throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "block body too long"};
+    if (!launch_blk_segments(K, NB, layout, a, s, /*pdl=*/true))
+      throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "block body too long"};
     const int cg = std::min(148 * 8, (nsep * K + 255) / 256);
+    const double* Td = Tdiag.p;
+    const int* sp = sep.p;
+    const double* xs = xsep.p;
+    const double* rc = rec.p;
     if (K == 4)
-      blk_cert_kernel<4><<<cg, 256, 0, s>>>(Tdiag.p, sep.p, nsep, f, xsep.p, rec.p, st);
+      launch_pdl(blk_cert_kernel<4>, dim3(cg), dim3(256), 0, s, Td, sp, nsep, f, xs, rc, st);
     else if (K == 3)
-      blk_cert_kernel<3><<<cg, 256, 0, s>>>(Tdiag.p, sep.p, nsep, f, xsep.p, rec.p, st);
+      launch_pdl(blk_cert_kernel<3>, dim3(cg), dim3(256), 0, s, Td, sp, nsep, f, xs, rc, st);
     else
-      blk_cert_kernel<2><<<cg, 256, 0, s>>>(Tdiag.p, sep.p, nsep, f, xsep.p, rec.p, st);
+      launch_pdl(blk_cert_kernel<2>, dim3(cg), dim3(256), 0, s, Td, sp, nsep, f, xs, rc, st);
     LAUNCH_CHECK();
     launches += 3;
   }
