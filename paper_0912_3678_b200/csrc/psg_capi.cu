@@ -441,6 +441,7 @@ struct TriSolver {
   // speculative path buffers
   DevBuf<double> wts, Tdiag, xsep;
   DevBuf<double4> crec;  // per-segment certificate records
+  DevBuf<unsigned> cctr;  // certificate kernel: finished-block counter (last block publishes the status)
   // exact multi-level path (built on demand)
   std::vector<std::unique_ptr<TriLevel>> lv;
   int launches = 0;
@@ -462,6 +463,8 @@ struct TriSolver {
       S0.len = len0.p;
     }
     crec.alloc(S0.nseg);
+    cctr.alloc(1);
+    CUDA_TRY(cudaMemsetAsync(cctr.p, 0, sizeof(unsigned), s));
     if (S0.nseg > 1) xsep.alloc(S0.nseg - 1);
   }
 
@@ -478,7 +481,9 @@ struct TriSolver {
   }
 
   // level-0 back-substitution and separator certificate
-  void k3_and_cert(const RowArr& F, double* x, const double* xs, DevStatus* st, cudaStream_t s, bool pdl = false) {
+  // host_out: a pinned host slot the certificate kernel publishes the final status to
+  void k3_and_cert(const RowArr& F, double* x, const double* xs, DevStatus* st, cudaStream_t s, bool pdl = false,
+                   DevStatus* host_out = nullptr) {
     TriSolveArgs a{};
     a.A = A0;
     a.F = F;
@@ -489,11 +494,12 @@ struct TriSolver {
     a.status = st;
     segment_solve(a, S0.nseg, maxlen0, s, pdl);
     launch_pdl(tri_cert_kernel, dim3(blocks_for(S0.nseg - 1, 256)), dim3(256), 0, s, S0.nseg - 1,
-               (const double4*)crec.p, st);
+               (const double4*)crec.p, st, host_out, cctr.p);
     launches += 2;
   }
 
-  void spec_solve(const RowArr& F, double* x, DevStatus* st, cudaStream_t s, cudaEvent_t* ev) {
+  void spec_solve(const RowArr& F, double* x, DevStatus* st, cudaStream_t s, cudaEvent_t* ev,
+                  DevStatus* host_out = nullptr) {
     const int nsep = S0.nseg - 1;
     tri_spec_sep_kernel<<<blocks_for((long)blocks_for(nsep, kSepPerWarp) * 32, 256), 256, 0, s>>>(F, S0, wts.p,
                                                                                                    xsep.p, st);
@@ -503,7 +509,7 @@ struct TriSolver {
       CUDA_TRY(cudaEventRecord(ev[1], s));
       CUDA_TRY(cudaEventRecord(ev[2], s));
     }
-    k3_and_cert(F, x, xsep.p, st, s, /*pdl=*/true);  // K3 stages its rows while the separators finish
+    k3_and_cert(F, x, xsep.p, st, s, /*pdl=*/true, host_out);  // K3 stages its rows while the separators finish
   }
 
   // ---- exact multi-level path ----------------------------------------------
@@ -1737,7 +1743,8 @@ int tri_enqueue(psg_handle* h, const double* df, double* dx, cudaStream_t s, Dev
   h->tri.launches = 0;
   if (ev) CUDA_TRY(cudaEventRecord(ev[0], s));
   if (spec) {
-    h->tri.spec_solve(make_rows(df, 0, n), dx, st, s, ev);  // the first kernel resets the status slot
+    // the first kernel resets the status slot, the last one publishes it to hst
+    h->tri.spec_solve(make_rows(df, 0, n), dx, st, s, ev, hst);
   } else {
     DevStatus init{};
     for (int i = 0; i < kCertSlots; ++i) init.cert_bits[i] = 0ull;
@@ -1748,7 +1755,7 @@ int tri_enqueue(psg_handle* h, const double* df, double* dx, cudaStream_t s, Dev
     h->tri.exact_solve(make_rows(df, 0, n), dx, st, s, ev);
   }
   if (ev) CUDA_TRY(cudaEventRecord(ev[3], s));
-  CUDA_TRY(cudaMemcpyAsync(hst, st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
+  if (!spec) CUDA_TRY(cudaMemcpyAsync(hst, st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaEventRecord(done, s));
   return h->tri.launches;
 }

@@ -572,19 +572,41 @@ __global__ void __launch_bounds__(32) tri_segment_solve_kernel(TriSolveArgs args
 // with the body values y from K3.  The body rows are solved exactly given
 // the separators, so this bounds the error the speculative interface let in.
 // ----------------------------------------------------------------------------
-__global__ void tri_cert_kernel(int nsep, const double4* __restrict__ crec, DevStatus* st) {
+// omega of separator j from the records of its two segments (R = j, N = j + 1)
+__device__ __forceinline__ double tri_omega(const double4& R, const double4& N) {
+  const double r = ((R.z - R.x) - R.y) - N.w;  // f_t - a_t y_{t-1} - b_t x_t - c_t y_{t+1}
+  const double den = fabs(R.z) + fabs(R.x) + fabs(R.y) + fabs(N.w);
+  double w = den > 0.0 ? fabs(r) / den : (r != 0.0 ? __longlong_as_double(0x7ff0000000000000ll) : 0.0);
+  if (!(w <= 1.0e300)) w = __longlong_as_double(0x7ff0000000000000ll);
+  return w;
+}
+
+__global__ void tri_cert_kernel(int nsep, const double4* __restrict__ crec, DevStatus* st, DevStatus* host_out,
+                                unsigned* done_ctr) {
   pdl_wait();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   double w = 0.0;
-  if (j < nsep) {
-    const double4 R = crec[j], N = crec[j + 1];
-    const double r = ((R.z - R.x) - R.y) - N.w;  // f_t - a_t y_{t-1} - b_t x_t - c_t y_{t+1}
-    const double den = fabs(R.z) + fabs(R.x) + fabs(R.y) + fabs(N.w);
-    w = den > 0.0 ? fabs(r) / den : (r != 0.0 ? __longlong_as_double(0x7ff0000000000000ll) : 0.0);
-    if (!(w <= 1.0e300)) w = __longlong_as_double(0x7ff0000000000000ll);
-  }
+  if (j < nsep) w = tri_omega(crec[j], crec[j + 1]);
   for (int o = 16; o > 0; o >>= 1) w = fmax(w, __shfl_xor_sync(0xffffffffu, w, o));
   if ((threadIdx.x & 31) == 0 && w > 0.0) status_cert(st, w);
+  if (!host_out) return;
+  // the last block to finish publishes the solve's status straight into the
+  // caller's pinned host slot (no device-to-host copy in the stream)
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(done_ctr, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(st);
+  volatile unsigned long long* dst = reinterpret_cast<volatile unsigned long long*>(host_out);
+  for (int i = threadIdx.x; i < (int)(sizeof(DevStatus) / 8); i += blockDim.x) dst[i] = atomicAdd(
+      const_cast<unsigned long long*>(src + i), 0ull);  // coherent read of the atomically-updated words
+  if (threadIdx.x == 0) *done_ctr = 0u;
+  __threadfence_system();
 }
 
 }  // namespace psg
