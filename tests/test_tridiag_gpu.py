@@ -240,3 +240,28 @@ def test_async_repairs_failed_speculation(cuda):
     assert st.fallbacks == 1
     want, _ = O.parallel_solve(A, p, f)
     assert O.rel_err(x.cpu().numpy(), want) <= 1e-10
+
+
+def test_large_n_64bit_offsets(cuda):
+    """Maximum sizes: n = 2^28 + 12345 (byte offsets beyond 2^31 in every
+    array; ragged bodies), speculative path, certified, residual <= 1e-13."""
+    torch = cuda
+    n = (1 << 28) + 12345
+    A, f = psg.generate_config(1, n, 11)
+    F = psg.parallel_factor(A, 1 << 18)
+    st = psg.SolveStats()
+    x = psg.solve(F, f, st)
+    assert st.speculative == 1 and st.certificate <= 1e-14
+    assert psg.residual(A, x, f) <= 1e-13
+    # spot rows near the end against the row equations directly (host, exact arithmetic on fp64 values)
+    d = A.data
+    for r in (n - 1, n - 2, (1 << 28) - 7, 1 << 27):
+        a = d[r - 1].item() if r > 0 else 0.0
+        b = d[n - 1 + r].item()
+        c = d[2 * n - 1 + r].item() if r < n - 1 else 0.0
+        xm = x[r - 1].item() if r > 0 else 0.0
+        xp = x[r + 1].item() if r < n - 1 else 0.0
+        lhs = a * xm + b * x[r].item() + c * xp
+        assert abs(lhs - f[r].item()) <= 1e-12 * (abs(a * xm) + abs(b * x[r].item()) + abs(c * xp) + abs(f[r].item()))
+    del A, f, x, F
+    torch.cuda.empty_cache()
