@@ -23,6 +23,7 @@
 
 #include "parsol/errors.hpp"
 #include "parsol/io.hpp"
+#include "parsol/odeparallel.hpp"
 #include "parsol/parfact.hpp"
 #include "parsol/seqref.hpp"
 #include "parsol/structmat.hpp"
@@ -203,6 +204,35 @@ int ref_mat_dims(void* hm, int* kind, int* n, int* m, int* s, int* r, size_t* le
   *len = A.data.size();
   if (data) std::memcpy(data, A.data.data(), sizeof(double) * A.data.size());
   return 0;
+}
+
+// The reference's time-parallel IVP solver (src/odeparallel.cpp:184-252) with
+// the forcing given as a C callback g(t, out[m], ctx); parallel = 0 runs
+// solve_ivp_sequential.  out: (p N + 1) m trajectory values.
+int ref_ode_solve(int m, const double* L, const double* y0, double t0, double T, int p, int N, int method,
+                  void (*g)(double, double*, void*), void* ctx, int parallel, double* out, char* err,
+                  size_t errlen) {
+  try {
+    IVProblem prob;
+    prob.L = DenseMatrix(m, m);
+    std::memcpy(prob.L.a.data(), L, sizeof(double) * m * m);
+    prob.y0.assign(y0, y0 + m);
+    prob.t0 = t0;
+    prob.T = T;
+    if (g)
+      prob.g = [g, ctx, m](double t) {
+        Vector v(m, 0.0);
+        g(t, v.data(), ctx);
+        return v;
+      };
+    TimeGrid grid = coarse_mesh(t0, T, p, N);
+    OdeMethod meth = method == 0 ? OdeMethod::ImplicitEuler : OdeMethod::Trapezoidal;
+    Trajectory tr = parallel ? solve_ivp_parallel(prob, grid, meth) : solve_ivp_sequential(prob, grid, meth);
+    std::memcpy(out, tr.flat.data(), sizeof(double) * tr.flat.size());
+    return 0;
+  } catch (const std::exception& e) {
+    return report(e, err, errlen);
+  }
 }
 
 int ref_plan(void* hm, int p, int* body_begin, int* body_end, int* sep_start, int* sep_count,

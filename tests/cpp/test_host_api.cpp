@@ -13,6 +13,7 @@
 
 #include "parsol/errors.hpp"
 #include "parsol/io.hpp"
+#include "parsol/odeparallel.hpp"
 #include "parsol/parfact.hpp"
 #include "parsol/partition.hpp"
 #include "parsol/rng.hpp"
@@ -175,6 +176,124 @@ static void cpu_tests() {
   CHECK(errc_of([] { read_file("/nonexistent/x.mat"); }) == int(Errc::IoError));
 }
 
+// ODE windows on the host (reference SPEC.md odeparallel examples)
+static IVProblem scalar_ivp(double lambda, double y0, double T) {
+  IVProblem P;
+  P.L = DenseMatrix(1, 1);
+  P.L.at(0, 0) = lambda;
+  P.y0 = {y0};
+  P.T = T;
+  return P;
+}
+
+static IVProblem random_ivp(int m, std::uint64_t seed, double T) {
+  IVProblem P;
+  P.L = DenseMatrix(m, m);
+  Vector r = random_vector(m * m + m, seed);
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < m; ++j) P.L.at(i, j) = r[i * m + j] - (i == j ? 2.0 : 0.0);
+  P.y0 = Vector(r.end() - m, r.end());
+  P.g = [m](double t) {
+    Vector g(m);
+    for (int q = 0; q < m; ++q) g[q] = std::sin((q + 1) * t) + 0.5;
+    return g;
+  };
+  P.T = T;
+  return P;
+}
+
+static Trajectory host_pipeline(const IVProblem& P, const TimeGrid& G, OdeMethod meth) {
+  std::vector<WindowSolution> sols;
+  for (int i = 1; i <= G.windows(); ++i) sols.push_back(solve_window_homogeneous(discretize_window(P, G, i, meth)));
+  return parallel_update(G, sols, reduced_recursion(sols, P.y0));
+}
+
+static Trajectory host_sequential(const IVProblem& P, const TimeGrid& G, OdeMethod meth) {
+  Trajectory tr{P.dim(), G.windows(), G.N, P.y0};
+  Vector y = P.y0;
+  for (int i = 1; i <= G.windows(); ++i) {
+    Vector seg = window_forward(discretize_window(P, G, i, meth), y);
+    tr.flat.insert(tr.flat.end(), seg.begin(), seg.end());
+    y = Vector(seg.end() - P.dim(), seg.end());
+  }
+  return tr;
+}
+
+static void cpu_ode_tests() {
+  auto errc_of = [](const std::function<void()>& fn) {
+    try {
+      fn();
+    } catch (const Error& e) {
+      return int(e.code());
+    }
+    return -1;
+  };
+  TimeGrid G = coarse_mesh(0, 1, 4, 10);
+  CHECK(G.windows() == 4 && G.tau[2] == 0.5 && std::fabs(G.h[1] - 0.025) < 1e-17);
+  TimeGrid G2 = coarse_mesh({0, 0.1, 1}, 5);
+  CHECK(std::fabs(G2.h[0] - 0.02) < 1e-17 && std::fabs(G2.h[1] - 0.18) < 1e-16);
+  CHECK(coarse_mesh(0, 1, 1, 1).windows() == 1);
+  CHECK(errc_of([] { coarse_mesh(1, 1, 2, 2); }) == int(Errc::InvalidInterval));
+  CHECK(errc_of([] { coarse_mesh(0, 1, 0, 2); }) == int(Errc::InvalidInterval));
+  CHECK(errc_of([] { coarse_mesh({0, 0.5, 0.5}, 2); }) == int(Errc::InvalidInterval));
+  CHECK(std::string(method_name(OdeMethod::Trapezoidal)) == "trap" &&  // src/odeparallel.cpp:10-17
+        method_from_name("euler") == OdeMethod::ImplicitEuler && method_from_name("trapezoidal") == OdeMethod::Trapezoidal);
+  CHECK(errc_of([] { method_from_name("rk4"); }) == int(Errc::InvalidParameter));
+  // scalar lambda = -1, h = 0.1, implicit Euler: diagonal 1.1; w_N = 1.1^-10
+  {
+    IVProblem P = scalar_ivp(-1.0, 1.0, 1.0);
+    WindowSystem W = discretize_window(P, coarse_mesh(0, 1, 1, 10), 1, OdeMethod::ImplicitEuler);
+    CHECK(std::fabs(W.diag.at(0, 0) - 1.1) < 1e-15);
+    WindowSolution S = solve_window_homogeneous(W);
+    CHECK(std::fabs(S.w_tail().at(0, 0) - std::pow(1.1, -10)) < 1e-14);
+    CHECK(inf_norm(S.z) == 0.0);  // g = 0 -> z = 0
+    // trapezoidal one step h = 0.2: amplification 0.9/1.1
+    WindowSystem Wt = discretize_window(scalar_ivp(-1.0, 1.0, 0.2), coarse_mesh(0, 0.2, 1, 1), 1,
+                                        OdeMethod::Trapezoidal);
+    CHECK(std::fabs(window_forward(Wt, {1.0})[0] - 0.9 / 1.1) < 1e-15);
+  }
+  // L = 0, g = 1, y0 = 0, implicit Euler: y_n = n h
+  {
+    IVProblem P = scalar_ivp(0.0, 0.0, 1.0);
+    P.g = [](double) { return Vector{1.0}; };
+    Trajectory tr = host_sequential(P, coarse_mesh(0, 1, 2, 5), OdeMethod::ImplicitEuler);
+    bool ok = true;
+    for (int n = 0; n <= 10; ++n) ok &= std::fabs(tr.flat[n] - n * 0.1) < 1e-15;
+    CHECK(ok);
+  }
+  // reduced recursion on a scalar geometric chain: w_N = 0.5, z_N = 1, y0 = 0
+  {
+    std::vector<WindowSolution> sols(4);
+    for (auto& s : sols) {
+      s.m = 1, s.N = 1, s.z = {1.0}, s.w = DenseMatrix(1, 1);
+      s.w.at(0, 0) = 0.5;
+    }
+    auto in = reduced_recursion(sols, {0.0});
+    CHECK(in[0][0] == 0 && in[1][0] == 1 && in[2][0] == 1.5 && in[3][0] == 1.75);
+  }
+  // window matrices: M w = v and M z = g (dense residual oracle)
+  {
+    IVProblem P = random_ivp(3, 77, 1.0);
+    for (OdeMethod meth : {OdeMethod::ImplicitEuler, OdeMethod::Trapezoidal}) {
+      WindowSystem W = discretize_window(P, coarse_mesh(0, 1, 2, 6), 2, meth);
+      WindowSolution S = solve_window_homogeneous(W);
+      const DenseMatrix M = W.m_dense();
+      CHECK(inf_norm(sub(matmul(M, S.w), W.v_dense())) <= 1e-12);
+      Vector r = matvec(M, S.z);
+      for (size_t q = 0; q < r.size(); ++q) r[q] -= W.gvec[q];
+      CHECK(inf_norm(r) <= 1e-12);
+    }
+  }
+  // parallel / sequential equivalence of the reference's window pipeline
+  for (OdeMethod meth : {OdeMethod::ImplicitEuler, OdeMethod::Trapezoidal})
+    for (int p : {2, 4, 8})
+      for (int m : {1, 3, 6}) {
+        IVProblem P = random_ivp(m, 100 + p * 7 + m, 2.0);
+        TimeGrid Gp = coarse_mesh(0, 2, p, 25);
+        CHECK(rel_err(host_pipeline(P, Gp, meth).flat, host_sequential(P, Gp, meth).flat) <= 1e-12);
+      }
+}
+
 // ---------------------------------------------------------------- on the GPU
 static void gpu_tests() {
   // identity -> x = f, T_p = I
@@ -261,13 +380,53 @@ static void gpu_tests() {
   }
 }
 
+static void gpu_ode_tests() {
+  // scalar lambda = -1, g = 0, y0 = 1, implicit Euler, p = 4, N = 25: y(1) = 1.01^-100
+  {
+    IVProblem P = scalar_ivp(-1.0, 1.0, 1.0);
+    Trajectory tr = solve_ivp_parallel(P, coarse_mesh(0, 1, 4, 25), OdeMethod::ImplicitEuler);
+    CHECK(tr.flat.size() == 101 && std::fabs(tr.endpoint()[0] - std::pow(1.01, -100)) <= 1e-14);
+  }
+  // L = 0, g = 0, y0 = c: constant trajectory
+  {
+    IVProblem P;
+    P.L = DenseMatrix(2, 2);
+    P.y0 = {3.0, -2.0};
+    Trajectory tr = solve_ivp_parallel(P, coarse_mesh(0, 1, 3, 7), OdeMethod::Trapezoidal);
+    bool ok = true;
+    for (int k = 0; k <= 21; ++k) ok &= tr.entry(k) == P.y0;
+    CHECK(ok);
+  }
+  // GPU trajectory vs the host window pipeline and the sequential iteration
+  for (OdeMethod meth : {OdeMethod::ImplicitEuler, OdeMethod::Trapezoidal})
+    for (int p : {1, 2, 4, 8})
+      for (int m : {1, 3, 4, 6, 8}) {
+        IVProblem P = random_ivp(m, 300 + p * 11 + m, 2.0);
+        TimeGrid Gp = coarse_mesh(0, 2, p, 100);
+        const Trajectory got = solve_ivp_parallel(P, Gp, meth);
+        CHECK(rel_err(got.flat, host_sequential(P, Gp, meth).flat) <= 1e-12);
+        CHECK(rel_err(got.flat, host_pipeline(P, Gp, meth).flat) <= 1e-12);
+        if (p == 1) CHECK(solve_ivp_sequential(P, Gp, meth).flat == got.flat);
+      }
+  // non-uniform mesh
+  {
+    IVProblem P = random_ivp(4, 9, 1.0);
+    TimeGrid Gp = coarse_mesh({0, 0.05, 0.3, 0.31, 1.0}, 40);
+    CHECK(rel_err(solve_ivp_parallel(P, Gp, OdeMethod::Trapezoidal).flat,
+                  host_sequential(P, Gp, OdeMethod::Trapezoidal).flat) <= 1e-12);
+  }
+}
+
 int main(int argc, char** argv) {
   const bool cpu = argc < 2 || std::strcmp(argv[1], "--gpu") != 0;
   try {
-    if (cpu)
+    if (cpu) {
       cpu_tests();
-    else
+      cpu_ode_tests();
+    } else {
       gpu_tests();
+      gpu_ode_tests();
+    }
   } catch (const std::exception& e) {
     std::fprintf(stderr, "uncaught exception: %s\n", e.what());
     return 2;
