@@ -23,6 +23,8 @@
  *   psg_plan            <- plan_partition()       include/parsol/partition.hpp:82
  *   psg_reduced_*       <- ParallelFactorization::reduced (ReducedSystem,
  *                          include/parsol/parfact.hpp:14-22)
+ *   psg_ode_trajectory  <- solve_ivp_parallel()   include/parsol/odeparallel.hpp (reference
+ *                          proj/include/parsol/odeparallel.hpp; impl src/odeparallel.cpp:183-233)
  *   psg_generate_config -- (new) device generator of the BASELINE configs,
  *                          bit-identical to SplitMix64 (include/parsol/rng.hpp)
  */
@@ -144,6 +146,15 @@ int psg_residual(const psg_desc* A, const double* x, const double* f, int on_dev
                  void* stream, double* out, char* err, size_t errlen);
 int psg_matvec(const psg_desc* A, const double* x, double* y, int on_device, void* stream,
                char* err, size_t errlen); /* host vectors (on_device = 0) are staged through the device */
+
+/* Time-parallel linear IVP trajectory (solve_ivp_parallel): the one-step
+ * recursion diag_w y_k = sub_w y_{k-1} + g_k over p windows of N steps,
+ * closed by y_0 = y0, solved as one BVP-layout BABD on the device (the chain
+ * path).  win: p x (diag_w, sub_w), each m x m row-major (host); g: host,
+ * (p N + 1) m = y0 followed by the method right-hand sides g_1 .. g_pN;
+ * out: host, (p N + 1) m trajectory.  1 <= m <= 8.  Blocks until done. */
+int psg_ode_trajectory(int m, int p, int N, const double* win, const double* g, double* out, void* stream,
+                       psg_stats* stats, char* err, size_t errlen);
 
 /* BASELINE config generator on the device (same stream mapping and values as
  * oracle/parsol_oracle.c or_generate_config).  Shapes via psg_config_shape. */

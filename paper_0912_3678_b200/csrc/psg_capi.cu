@@ -26,6 +26,7 @@
 #include "tri_kernels.cuh"
 #include "blk_kernels.cuh"
 #include "chain_kernels.cuh"
+#include "ode_kernels.cuh"
 
 using namespace psg;
 
@@ -1837,6 +1838,59 @@ int psg_solve(const psg_handle* hc, const double* f, double* x, int on_device, v
       CUDA_TRY(cudaStreamSynchronize(s));
     }
     CUDA_TRY(cudaEventRecord(h->ev_done, s));
+    return 0;
+  } catch (const Fail& f_) {
+    return set_err(err, errlen, f_.code, f_.msg);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// time-parallel IVP trajectory (src/odeparallel.cpp:183-233)
+// ---------------------------------------------------------------------------
+int psg_ode_trajectory(int m, int p, int N, const double* win, const double* g, double* out, void* stream,
+                       psg_stats* stats, char* err, size_t errlen) {
+  try {
+    if (m < 1 || m > 8) throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "the GPU trajectory solve supports dimension 1..8"};
+    if (p < 1 || N < 1) throw Fail{PSG_E_INVALID_INTERVAL, "p and N must be >= 1"};
+    cudaStream_t s = (cudaStream_t)stream;
+    const int MB = m <= 2 ? 2 : (m <= 4 ? 4 : 8);
+    const long long steps = (long long)p * N, nsteps = std::max<long long>(steps, 64), nb = nsteps + 1;
+    if ((long long)MB * nb > INT_MAX) throw Fail{PSG_E_TOO_LARGE_FOR_DENSE, "trajectory too long for one solve"};
+    const size_t len = size_t(MB) * MB + size_t(nsteps) * 2 * MB * MB;
+    DevBuf<double> dwin, dg, ddata, dcorner, df, dx, dout;
+    dwin.alloc(size_t(p) * 2 * m * m);
+    dg.alloc(size_t(steps + 1) * m);
+    ddata.alloc(len);
+    dcorner.alloc(size_t(MB) * MB);
+    df.alloc(size_t(MB) * nb);
+    dx.alloc(size_t(MB) * nb);
+    dout.alloc(size_t(steps + 1) * m);
+    CUDA_TRY(cudaMemcpyAsync(dwin.p, win, sizeof(double) * p * 2 * m * m, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(dg.p, g, sizeof(double) * (steps + 1) * m, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemsetAsync(dcorner.p, 0, sizeof(double) * MB * MB, s));
+    const int grid = 148 * 8, tpb = 256;
+    switch (MB) {
+      case 2: ode_assemble_kernel<2><<<grid, tpb, 0, s>>>(m, steps, nsteps, N, dwin.p, dg.p, ddata.p, df.p); break;
+      case 4: ode_assemble_kernel<4><<<grid, tpb, 0, s>>>(m, steps, nsteps, N, dwin.p, dg.p, ddata.p, df.p); break;
+      default: ode_assemble_kernel<8><<<grid, tpb, 0, s>>>(m, steps, nsteps, N, dwin.p, dg.p, ddata.p, df.p); break;
+    }
+    LAUNCH_CHECK();
+    psg_desc A{PSG_BABD, int(MB * nb), MB, MB, 0, ddata.p, len, dcorner.p, MB, MB, 1};
+    const int pp = (int)std::max<long long>(2, std::min<long long>(4096, nb / 16));
+    psg_handle* h = nullptr;
+    int rc = psg_factor(&A, pp, PSG_LU, 0.0, stream, &h, err, errlen);
+    if (rc) return rc;
+    rc = psg_solve(h, df.p, dx.p, 1, stream, stats, err, errlen);
+    psg_release(h);
+    if (rc) return rc;
+    switch (MB) {
+      case 2: ode_unpad_kernel<2><<<grid, tpb, 0, s>>>(m, steps, dx.p, dout.p); break;
+      case 4: ode_unpad_kernel<4><<<grid, tpb, 0, s>>>(m, steps, dx.p, dout.p); break;
+      default: ode_unpad_kernel<8><<<grid, tpb, 0, s>>>(m, steps, dx.p, dout.p); break;
+    }
+    LAUNCH_CHECK();
+    CUDA_TRY(cudaMemcpyAsync(out, dout.p, sizeof(double) * (steps + 1) * m, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
     return 0;
   } catch (const Fail& f_) {
     return set_err(err, errlen, f_.code, f_.msg);

@@ -9,11 +9,14 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <functional>
+#include <string>
 
 #include "parsol/errors.hpp"
 #include "parsol/odeparallel.hpp"
 #include "parsol/parfact.hpp"
 #include "parsol/structmat.hpp"
+#include "psg.h"
 
 namespace parsol {
 
@@ -176,54 +179,122 @@ Trajectory parallel_update(const TimeGrid& grid, const std::vector<WindowSolutio
 // ---------------------------------------------------------------------------
 // the GPU trajectory solve
 // ---------------------------------------------------------------------------
-Trajectory solve_ivp_parallel(const IVProblem& prob, const TimeGrid& grid, OdeMethod method, SolveStats* stats) {
-  const int m = prob.dim(), p = grid.windows(), N = grid.N;
-  if (m < 1) fail(Errc::DimensionMismatch, "empty system");
-  if ((int)prob.y0.size() != m) fail(Errc::DimensionMismatch, "y0 length");
-  if (m > 8) fail(Errc::UnsupportedStructure, "the GPU trajectory solve supports systems of dimension <= 8");
-  const int MB = m <= 2 ? 2 : (m <= 4 ? 4 : 8);  // padded block size: inert components
-  const long steps = (long)p * N;
-  const long nsteps = std::max<long>(steps, 64);  // short trajectories: identity steps appended
-  const long nb = nsteps + 1;
-  if ((long)MB * nb > 0x7fffffffL) fail(Errc::TooLargeForDense, "trajectory too long for one solve");
-  const long BW = 2L * MB * MB;
-  std::vector<double> data(std::size_t(MB) * MB + std::size_t(nsteps) * BW, 0.0);
-  std::vector<double> f(std::size_t(MB) * nb, 0.0);
-  for (int i = 0; i < MB; ++i) data[std::size_t(i) * MB + i] = 1.0;  // y_0 = y0
-  std::copy(prob.y0.begin(), prob.y0.end(), f.begin());
-  long k = 0;  // step index (block row k + 1)
-  for (int w = 1; w <= p; ++w) {
-    const WindowSystem W = discretize_window(prob, grid, w, method);
-    // one block row per step: [ -sub | diag ], padding rows [ -I | I ]
-    std::vector<double> row(BW, 0.0);
-    for (int i = 0; i < MB; ++i)
-      for (int j = 0; j < MB; ++j) {
-        const bool real = i < m && j < m;
-        row[std::size_t(i) * 2 * MB + j] = real ? -W.sub.at(i, j) : (i == j ? -1.0 : 0.0);
-        row[std::size_t(i) * 2 * MB + MB + j] = real ? W.diag.at(i, j) : (i == j ? 1.0 : 0.0);
+namespace {
+
+// g(t) written straight into out[m] (no per-sample allocation).
+using Sampler = std::function<void(double, double*)>;
+
+// Window i's blocks and method right-hand sides, sampled at exactly the
+// reference's points (src/odeparallel.cpp:96-109: t_n = tstart + n h, and
+// t_n - h for the trapezoidal left end).  A trapezoidal left sample is
+// taken from the previous step when t_n - h equals the previous t_n
+// bitwise, so the values match the reference's two-calls-per-step loop.
+void window_blocks(const DenseMatrix& L, const TimeGrid& grid, int i, OdeMethod method, const Sampler& g, double* win,
+                   double* rhs) {
+  const int m = L.rows, N = grid.N;
+  const double h = grid.h[i - 1], tstart = grid.tau[i - 1];
+  const std::size_t mm = std::size_t(m) * m;
+  DenseMatrix D(m, m);
+  for (int r = 0; r < m; ++r)
+    for (int c = 0; c < m; ++c) {
+      const double id = r == c ? 1.0 : 0.0;
+      const double l = L.at(r, c);
+      if (method == OdeMethod::ImplicitEuler) {
+        D.at(r, c) = id - l * h;
+        win[mm + r * m + c] = id;
+      } else {
+        D.at(r, c) = id - l * (h / 2);
+        win[mm + r * m + c] = id + l * (h / 2);
       }
-    for (int s = 0; s < N; ++s, ++k) {
-      std::copy(row.begin(), row.end(), data.begin() + MB * MB + k * BW);
-      for (int q = 0; q < m; ++q) f[std::size_t(k + 1) * MB + q] = W.gvec[std::size_t(s) * m + q];
+    }
+  try {
+    DenseLu lu(D);
+  } catch (const Error&) {
+    fail(Errc::StepTooLarge, "window matrix singular for h = " + std::to_string(h));
+  }
+  std::copy(D.a.begin(), D.a.end(), win);
+  std::vector<double> g0(m), gn(m);
+  double prev_t = 0;
+  for (int n = 1; n <= N; ++n) {
+    const double tn = tstart + n * h;
+    double* out = rhs + std::size_t(n - 1) * m;
+    if (method == OdeMethod::ImplicitEuler) {
+      g(tn, out);
+      for (int q = 0; q < m; ++q) out[q] *= h;
+      continue;
+    }
+    const double tl = tn - h;
+    if (n > 1 && tl == prev_t)
+      g0.swap(gn);
+    else
+      g(tl, g0.data());
+    g(tn, gn.data());
+    prev_t = tn;
+    for (int q = 0; q < m; ++q) out[q] = h / 2 * (g0[q] + gn[q]);
+  }
+}
+
+// The trajectory ((p N + 1) m, into out) of y' = L y + g on grid.
+void trajectory_on_gpu(const DenseMatrix& L, const double* y0, const TimeGrid& grid, OdeMethod method,
+                       const Sampler& g, double* out, psg_stats* st) {
+  const int m = L.rows, p = grid.windows(), N = grid.N;
+  if (m < 1) fail(Errc::DimensionMismatch, "empty system");
+  if (L.cols != m) fail(Errc::DimensionMismatch, "L must be square");
+  if (m > 8) fail(Errc::UnsupportedStructure, "the GPU trajectory solve supports systems of dimension <= 8");
+  const std::size_t mm = std::size_t(m) * m, steps = std::size_t(p) * N;
+  std::vector<double> win(std::size_t(p) * 2 * mm), rhs((steps + 1) * m);
+  std::copy(y0, y0 + m, rhs.begin());
+  // windows concurrently, as in the reference (src/odeparallel.cpp:199-209:
+  // g is called from worker threads)
+  std::vector<std::string> errs(p);
+  std::vector<int> codes(p, -1);
+#pragma omp parallel for schedule(static)
+  for (int w = 1; w <= p; ++w) {
+    try {
+      window_blocks(L, grid, w, method, g, win.data() + std::size_t(w - 1) * 2 * mm,
+                    rhs.data() + m + std::size_t(w - 1) * N * m);
+    } catch (const Error& e) {
+      codes[w - 1] = int(e.code());
+      errs[w - 1] = e.detail();
     }
   }
-  for (; k < nsteps; ++k)  // appended identity steps: y_{k+1} = y_k
-    for (int i = 0; i < MB; ++i) {
-      data[MB * MB + k * BW + std::size_t(i) * 2 * MB + i] = -1.0;
-      data[MB * MB + k * BW + std::size_t(i) * 2 * MB + MB + i] = 1.0;
+  for (int w = 0; w < p; ++w)
+    if (codes[w] >= 0) fail(Errc(codes[w]), errs[w]);
+  char err[256] = {0};
+  const int rc = psg_ode_trajectory(m, p, N, win.data(), rhs.data(), out, nullptr, st, err, sizeof err);
+  if (rc) fail(Errc(rc - 1), err);
+}
+
+}  // namespace
+
+Trajectory solve_ivp_parallel(const IVProblem& prob, const TimeGrid& grid, OdeMethod method, SolveStats* stats) {
+  const int m = prob.dim();
+  if ((int)prob.y0.size() != m) fail(Errc::DimensionMismatch, "y0 length");
+  Sampler g = [&prob, m](double t, double* out) {
+    if (!prob.g) {
+      std::fill(out, out + m, 0.0);
+      return;
     }
-  StructuredMatrix A = make(Kind::Babd, (int)(MB * nb), MB, MB, 0, std::move(data),
-                            std::vector<double>(std::size_t(MB) * MB, 0.0), MB, MB);
-  const int pp = (int)std::max<long>(2, std::min<long>(4096, nb / 16));
-  ParallelFactorization F = parallel_factor(A, pp, Strategy::Lu);
-  const Vector x = solve(F, f, stats);
+    const Vector v = prob.g(t);
+    if ((int)v.size() != m) fail(Errc::DimensionMismatch, "g(t) length");
+    std::copy(v.begin(), v.end(), out);
+  };
   Trajectory tr;
   tr.m = m;
-  tr.p = p;
-  tr.N = N;
-  tr.flat.resize(std::size_t(steps + 1) * m);
-  for (long b = 0; b <= steps; ++b)
-    for (int q = 0; q < m; ++q) tr.flat[std::size_t(b) * m + q] = x[std::size_t(b) * MB + q];
+  tr.p = grid.windows();
+  tr.N = grid.N;
+  tr.flat.resize((std::size_t(tr.p) * tr.N + 1) * m);
+  psg_stats st{};
+  trajectory_on_gpu(prob.L, prob.y0.data(), grid, method, g, tr.flat.data(), &st);
+  if (stats) {
+    stats->factor_seconds = st.factor_seconds;
+    stats->phase1_seconds = st.phase1_seconds;
+    stats->phase2_seconds = st.phase2_seconds;
+    stats->phase3_seconds = st.phase3_seconds;
+    stats->reduced_ops = st.reduced_ops;
+    stats->certificate = st.certificate;
+    stats->fallbacks = st.fallbacks;
+  }
   return tr;
 }
 
@@ -243,23 +314,19 @@ extern "C" int psg_ode_solve(int m, const double* L, const double* y0, double t0
                              char* err, size_t errlen) {
   using namespace parsol;
   try {
-    IVProblem prob;
-    prob.L = DenseMatrix(m, m);
-    std::copy(L, L + std::size_t(m) * m, prob.L.a.begin());
-    prob.y0.assign(y0, y0 + m);
-    prob.t0 = t0;
-    prob.T = T;
-    if (g)
-      prob.g = [g, ctx, m](double t) {
-        Vector v(m, 0.0);
-        g(t, v.data(), ctx);
-        return v;
-      };
+    if (m < 1) fail(Errc::DimensionMismatch, "empty system");
+    DenseMatrix Lm(m, m);
+    std::copy(L, L + std::size_t(m) * m, Lm.a.begin());
     const TimeGrid grid = coarse_mesh(t0, T, p, N);
-    SolveStats st;
-    const Trajectory tr = solve_ivp_parallel(prob, grid, method == 0 ? OdeMethod::ImplicitEuler : OdeMethod::Trapezoidal,
-                                             &st);
-    std::copy(tr.flat.begin(), tr.flat.end(), out);
+    Sampler sampler = [g, ctx, m](double t, double* o) {
+      if (g)
+        g(t, o, ctx);
+      else
+        std::fill(o, o + m, 0.0);
+    };
+    psg_stats st{};
+    trajectory_on_gpu(Lm, y0, grid, method == 0 ? OdeMethod::ImplicitEuler : OdeMethod::Trapezoidal, sampler, out,
+                      &st);
     if (certificate) *certificate = st.certificate;
     return 0;
   } catch (const Error& e) {
