@@ -122,6 +122,13 @@ int psg_refactor(psg_handle* h, const psg_desc* A, void* stream, char* err, size
 /* Reduced system metadata (ReducedSystem, parfact.hpp:14-22): q kept blocks,
  * scalar dimension, block size k, corner flag. */
 int psg_reduced_info(const psg_handle* h, int* q, int* dim, int* k, int* has_corner);
+/* Reduced-system layout in position order (ReducedSystem::positions /
+ * block_sizes, src/parfact.cpp:72-88): q entries, each a separator (size k)
+ * or, for LuPivot / Qr, an adaptive extra (size 1). */
+int psg_reduced_layout(const psg_handle* h, int* positions, int* sizes);
+/* Dense dim x dim image of the reduced matrix T (ReducedSystem::T), row-major,
+ * for every strategy; callers bound dim (the C++ layer: 4096). */
+int psg_reduced_dense(const psg_handle* h, double* T, char* err, size_t errlen);
 /* Host copies of the reduced matrix T in block form (k x k row-major
  * blocks): diag[q], sub[q] (coupling of block i to i-1; sub[0] = corner
  * coupling when has_corner), super[q] (coupling of block i to i+1).  Any

@@ -108,6 +108,9 @@ def ref():
         R.ref_factor.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p), _dp,
                                  C.c_char_p, C.c_size_t]
         R.ref_fact_destroy.argtypes = [C.c_void_p]
+        R.ref_factor_tol.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, C.POINTER(C.c_void_p), C.c_char_p,
+                                     C.c_size_t]
+        R.ref_fact_layout.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         R.ref_fact_dims.argtypes = [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]
         R.ref_fact_T.argtypes = [C.c_void_p, _dp]
         R.ref_fact_local.argtypes = [C.c_void_p, C.c_int, _dp, _dp, _dp, _dp]
@@ -303,6 +306,14 @@ class RefMatrix:
             raise OracleError(rc, err.value.decode())
         return RefFact(h, self.n, secs.value)
 
+    def factor_tol(self, p: int, strategy: int, tol: float):
+        h = C.c_void_p()
+        err = C.create_string_buffer(512)
+        rc = ref().ref_factor_tol(self.h, p, strategy, tol, C.byref(h), err, 512)
+        if rc:
+            raise OracleError(rc, err.value.decode())
+        return RefFact(h, self.n, 0.0)
+
     def solve_sequential(self, f):
         f = np.ascontiguousarray(f, np.float64)
         x = np.empty(self.n, np.float64)
@@ -342,6 +353,13 @@ class RefFact:
         q, dim = C.c_int(), C.c_int()
         ref().ref_fact_dims(self.h, C.byref(q), C.byref(dim))
         return q.value, dim.value
+
+    def layout(self):
+        q, _ = self.dims()
+        pos = np.empty(q, np.int32)
+        size = np.empty(q, np.int32)
+        ref().ref_fact_layout(self.h, pos.ctypes.data, size.ctypes.data)
+        return pos, size
 
     def T(self):
         _, dim = self.dims()

@@ -88,6 +88,27 @@ int ref_factor(void* hm, int p, int strategy, void** out, double* seconds, char*
   }
 }
 
+int ref_factor_tol(void* hm, int p, int strategy, double tol, void** out, char* err, size_t errlen) {
+  try {
+    auto* f = new RefFact;
+    f->F = parallel_factor(static_cast<RefMat*>(hm)->A, p, Strategy(strategy), tol);
+    *out = f;
+    return 0;
+  } catch (const std::exception& e) {
+    return report(e, err, errlen);
+  }
+}
+
+// ReducedSystem positions / block sizes in position order (src/parfact.cpp:72-88)
+int ref_fact_layout(void* hf, int* positions, int* sizes) {
+  auto& R = static_cast<RefFact*>(hf)->F.reduced;
+  for (int j = 0; j < R.q; ++j) {
+    positions[j] = R.positions[j];
+    sizes[j] = R.block_sizes[j];
+  }
+  return 0;
+}
+
 void ref_fact_destroy(void* h) { delete static_cast<RefFact*>(h); }
 
 int ref_fact_dims(void* hf, int* q, int* dim) {

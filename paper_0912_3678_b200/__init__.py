@@ -125,6 +125,8 @@ def lib():
         L.psg_release.restype = None
         L.psg_reduced_info.argtypes = [vp] + [C.POINTER(C.c_int)] * 4
         L.psg_reduced_blocks.argtypes = [vp, vp, vp, vp, cp, sz]
+        L.psg_reduced_layout.argtypes = [vp, vp, vp]
+        L.psg_reduced_dense.argtypes = [vp, vp, cp, sz]
         L.psg_solve_reduced.argtypes = [vp, vp, vp, ip, vp, C.POINTER(SolveStats), cp, sz]
         L.psg_plan.argtypes = [C.POINTER(_Desc), ip] + [C.POINTER(C.c_int)] * 5 + [cp, sz]
         L.psg_residual.argtypes = [C.POINTER(_Desc), vp, vp, ip, vp, C.POINTER(C.c_double), cp, sz]
@@ -245,6 +247,20 @@ class ParallelFactorization:
         err = C.create_string_buffer(512)
         _check(lib().psg_reduced_blocks(self.handle, d.ctypes.data, sb.ctypes.data, sp.ctypes.data, err, 512), err)
         return sb, d, sp
+
+    def reduced_layout(self):
+        """ReducedSystem positions and block sizes, position order (psg_reduced_layout)."""
+        pos = np.empty(self.q, np.int32)
+        size = np.empty(self.q, np.int32)
+        lib().psg_reduced_layout(self.handle, pos.ctypes.data, size.ctypes.data)
+        return pos, size
+
+    def reduced_dense(self):
+        """Dense image of the reduced matrix T (psg_reduced_dense)."""
+        T = np.empty((self.dim, self.dim))
+        err = C.create_string_buffer(512)
+        _check(lib().psg_reduced_dense(self.handle, T.ctypes.data, err, 512), err)
+        return T
 
     def solve(self, f, x=None, stats: SolveStats | None = None, stream=None):
         return solve(self, f, stats=stats, x=x, stream=stream)

@@ -59,6 +59,13 @@ __device__ __forceinline__ double sm_at(const SMView& A, long i, long j) {
     if (d < -A.s || d > A.r) return 0.0;
     return __ldg(A.data + sm_band_off(A.n, A.s, (int)d) + (i - (d < 0 ? -d : 0)));
   }
+  if (A.kind == 4) {  // CirculantLike: band d = (j - i) mod n, wrapped (src/structmat.cpp:103-107, 137-142)
+    long dd = j - i;
+    if (dd < 0) dd += A.n;
+    if (!(dd <= A.r || A.n - dd <= A.s)) return 0.0;
+    const long d = dd <= A.r ? dd : dd - A.n;
+    return __ldg(A.data + (d + A.s) * (long)A.n + i);
+  }
   if (A.kind == 1) {
     const long bi = i / m, bj = j / m;
     if (bi - bj > 1 || bj - bi > 1) return 0.0;

@@ -172,6 +172,13 @@ __device__ double row_dot(const MatView& A, long i, const double* __restrict__ x
       const long blk = bi > 0 ? bj - bi + 1 : bj - bi;
       acc = __dadd_rn(acc, __dmul_rn(A.data[off + blk * m * m + (i - bi * m) * m + (j - bj * m)], x[j]));
     }
+  } else if (A.kind == 4) {  // circulant-like: columns (i + d) mod n, ascending (src/structmat.cpp:234-245)
+    for (int d = -A.s; d <= A.r; ++d)  // wrapped past the end: smallest columns
+      if (i + d >= n) acc = __dadd_rn(acc, __dmul_rn(A.data[(long)(d + A.s) * n + i], x[i + d - n]));
+    for (int d = -A.s; d <= A.r; ++d)
+      if (i + d >= 0 && i + d < n) acc = __dadd_rn(acc, __dmul_rn(A.data[(long)(d + A.s) * n + i], x[i + d]));
+    for (int d = -A.s; d <= A.r; ++d)  // wrapped before the start: largest columns
+      if (i + d < 0) acc = __dadd_rn(acc, __dmul_rn(A.data[(long)(d + A.s) * n + i], x[i + d + n]));
   } else {  // abd / babd: closed-form block-row offsets
     const long b = i / m;
     const long c0 = b * m - A.s > 0 ? b * m - A.s : 0;

@@ -27,6 +27,7 @@
 #include "blk_kernels.cuh"
 #include "chain_kernels.cuh"
 #include "ode_kernels.cuh"
+#include "piv_kernels.cuh"
 
 using namespace psg;
 
@@ -318,18 +319,19 @@ struct Plan {
 
 Plan make_plan(const psg_desc& A, int p) {
   if (p < 2) throw Fail{PSG_E_TOO_MANY_PARTITIONS, "p must be >= 2"};
-  if (A.kind == PSG_CIRCULANT)
-    throw Fail{PSG_E_UNSUPPORTED_KIND, "circulant-like matrices are not supported on the GPU path"};
+  if (A.kind == PSG_CIRCULANT && A.r != 0)  // src/partition.cpp:53-55
+    throw Fail{PSG_E_UNSUPPORTED_KIND, "circulant-like corner content is not canonical; permute_corner first"};
   Plan P;
   P.kind = A.kind;
   P.n = A.n;
   P.m = A.m;
   P.p = p;
-  P.sep_size = A.kind == PSG_BANDED ? std::max(A.s, A.r) : A.m;
-  P.has_corner = A.kind == PSG_BABD;
+  const bool scalar = A.kind == PSG_BANDED || A.kind == PSG_CIRCULANT;
+  P.sep_size = scalar ? std::max(A.s, A.r) : A.m;
+  P.has_corner = A.kind == PSG_BABD || A.kind == PSG_CIRCULANT;
   const int k = P.sep_size;
   const long seps = P.has_corner ? p + 1L : p - 1L;
-  P.unit = A.kind == PSG_BANDED ? 1 : A.m;
+  P.unit = scalar ? 1 : A.m;
   if (k % P.unit != 0) throw Fail{PSG_E_UNSUPPORTED_KIND, "separator does not tile blocks"};
   const long n_units = A.n / P.unit;
   P.k_units = k / P.unit;
@@ -1248,6 +1250,268 @@ struct GenSolver {
 // ----------------------------------------------------------------------------
 // the handle
 // ----------------------------------------------------------------------------
+// ----------------------------------------------------------------------------
+// Pivoting strategies (LuPivot / Qr) and the circulant-like kind
+// (piv_kernels.cuh): one warp per body, adaptive extras, the reduced band
+// factored by the same engine in dense-LU mode.
+// ----------------------------------------------------------------------------
+struct PivRecBuf {
+  DevBuf<int4> meta;
+  DevBuf<unsigned char> tslot, aslot;
+  DevBuf<double> mu, av, tau, urow, uspk;
+  PivRec view{};
+  void alloc(size_t steps, int NT, int NA, int URW, int NS) {
+    meta.alloc(steps);
+    tslot.alloc(steps * NT);
+    mu.alloc(steps * NT);
+    aslot.alloc(steps * NA);
+    av.alloc(steps * NA);
+    tau.alloc(steps);
+    urow.alloc(steps * URW);
+    uspk.alloc(steps * NS);
+    view = PivRec{meta.p, tslot.p, mu.p, aslot.p, av.p, tau.p, urow.p, uspk.p, NT, NA, URW, NS};
+  }
+};
+
+struct PivSolver {
+  SMView A{};  // canonical matrix (circulant-like: rows rotated)
+  Plan P;
+  int p = 0, k = 0, es = 0, er = 0, strategy = kPvPartial, cap = 0, KD = 0;
+  double tol = 1e-8;
+  bool corner = false;
+  std::vector<GPart> hpart;
+  DevBuf<GPart> part;
+  PivRecBuf rb, rr_rec;
+  DevBuf<double> kept;
+  DevBuf<int> ndef, xpos, status, koff;
+  std::vector<int> hndef, hxpos, hkoff;
+  // the reduced system
+  int dim = 0, w = 0, kb = 0, q = 0;
+  std::vector<int> rpos, rsize;  // position order: global start, size (k or 1)
+  DevBuf<double> rband, rborder;
+  // solve scratch
+  DevBuf<double> ghat, kr, rrhs, xk, rghat;
+  int launches = 0;
+
+  static size_t smem_bytes() { return sizeof(PivSmem); }
+
+  PivArgs args() const {
+    PivArgs a{};
+    a.A = A;
+    a.part = part.p;
+    a.p = p;
+    a.k = k;
+    a.es = es;
+    a.er = er;
+    a.strategy = strategy;
+    a.tol = tol;
+    a.cap = cap;
+    a.KD = KD;
+    a.kept = kept.p;
+    a.ndef = ndef.p;
+    a.xpos = xpos.p;
+    a.rband = rband.p;
+    a.rborder = rborder.p;
+    a.dim = dim;
+    a.w = w;
+    a.kb = kb;
+    a.rec = rb.view;
+    a.status = status.p;
+    a.ghat = ghat.p;
+    a.kr = kr.p;
+    a.xk = xk.p;
+    a.koff = koff.p;
+    return a;
+  }
+
+  void init(const SMView& Av, const Plan& plan, int strat, double tol_) {
+    A = Av;
+    P = plan;
+    p = plan.p;
+    k = plan.sep_size;
+    corner = plan.has_corner;
+    strategy = strat;
+    tol = tol_;
+    envelope_of(A.kind == PSG_CIRCULANT ? PSG_BANDED : A.kind, A.m, A.s, A.r, es, er);
+    if (es + er + 1 > kPvRing || es > 31)
+      throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "band envelope too wide for the pivoting GPU path"};
+    if (k > kGenMaxK) throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "separator block too large for the pivoting GPU path"};
+    cap = std::min({16, kPvSpk - 2 * k, kPvSlots - 1 - es - 2 * k});
+    if (strategy == kPvNoPivot) cap = std::max(cap, 1);
+    if (cap < 1) throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "no room for deferred pivots in the pivoting GPU path"};
+    KD = 2 * k + cap;
+    hpart.resize(p);
+    for (int i = 0; i < p; ++i) {
+      const int lsi = corner ? i : i - 1, rsi = corner ? i + 1 : i;
+      hpart[i] = GPart{plan.body_begin(i), plan.body_end(i) - plan.body_begin(i), lsi >= 0 ? plan.sep_start(lsi) : -1,
+                       rsi < plan.sep_count() ? plan.sep_start(rsi) : -1};
+    }
+    part.alloc(p);
+    CUDA_TRY(cudaMemcpy(part.p, hpart.data(), sizeof(GPart) * p, cudaMemcpyHostToDevice));
+    rb.alloc((size_t)A.n, es + 2 * k + cap, es + 1, es + er + 1, 2 * k + cap);
+    kept.alloc((size_t)p * KD * KD);
+    ndef.alloc(p);
+    xpos.alloc((size_t)p * cap);
+    status.alloc(4);
+    koff.alloc(p);
+    ghat.alloc(A.n);
+    kr.alloc((size_t)p * KD);
+    static bool attr_done[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr_done[dev & 63]) {
+      CUDA_TRY(cudaFuncSetAttribute(piv_factor_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes()));
+      CUDA_TRY(cudaFuncSetAttribute(piv_factor_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes()));
+      attr_done[dev & 63] = true;
+    }
+  }
+
+  void check_status(cudaStream_t s) {
+    int st[4];
+    CUDA_TRY(cudaMemcpyAsync(st, status.p, sizeof st, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (st[2] != INT_MAX)
+      throw Fail{PSG_E_ZERO_PIVOT, "partition " + std::to_string(st[2] + 1) + ": zero pivot in the no-pivot elimination"};
+    if (st[1] != INT_MAX)
+      throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "partition " + std::to_string(st[1] + 1) + ": more than " +
+                                                 std::to_string(cap) + " deferred pivots in one body"};
+    if (st[0] != INT_MAX)
+      throw Fail{PSG_E_EXHAUSTED_BODY, "partition " + std::to_string(st[0] + 1) +
+                                          ": every pivot deferred; body is structurally degenerate"};
+    if (st[3] != INT_MAX) throw Fail{PSG_E_SINGULAR_REDUCED_SYSTEM, "reduced system is singular"};
+  }
+
+  void reset_status(cudaStream_t s) {
+    const int init[4] = {INT_MAX, INT_MAX, INT_MAX, INT_MAX};
+    CUDA_TRY(cudaMemcpyAsync(status.p, init, sizeof init, cudaMemcpyHostToDevice, s));
+  }
+
+  void factor(cudaStream_t s) {
+    launches = 0;
+    reset_status(s);
+    PivArgs a = args();
+    piv_factor_kernel<0><<<p, 32, smem_bytes(), s>>>(a);
+    LAUNCH_CHECK();
+    ++launches;
+    hndef.resize(p);
+    hxpos.resize((size_t)p * cap);
+    CUDA_TRY(cudaMemcpyAsync(hndef.data(), ndef.p, sizeof(int) * p, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(hxpos.data(), xpos.p, sizeof(int) * hxpos.size(), cudaMemcpyDeviceToHost, s));
+    check_status(s);
+    // reduced layout in position order (src/parfact.cpp:72-88): separators and extras
+    rpos.clear();
+    rsize.clear();
+    hkoff.assign(p, 0);
+    int maxkd = 1;
+    auto add_sep = [&](int j) {
+      rpos.push_back(P.sep_start(j));
+      rsize.push_back(k);
+    };
+    int off = 0;
+    std::vector<int> sepoff(P.sep_count());
+    if (corner) {
+      sepoff[0] = 0;
+      add_sep(0);
+      off = k;
+    }
+    for (int i = 0; i < p; ++i) {
+      const int k0 = hpart[i].ls >= 0 ? k : 0, k1 = hpart[i].rs >= 0 ? k : 0;
+      hkoff[i] = off - k0;
+      for (int e = 0; e < hndef[i]; ++e) {
+        rpos.push_back(hpart[i].b + hxpos[(size_t)i * cap + e]);
+        rsize.push_back(1);
+      }
+      off += hndef[i];
+      if (k1) {
+        const int j = corner ? i + 1 : i;
+        sepoff[j] = off;
+        add_sep(j);
+        off += k;
+      }
+      maxkd = std::max(maxkd, k0 + hndef[i] + k1);
+    }
+    dim = off;
+    q = (int)rpos.size();
+    w = maxkd - 1;
+    kb = corner ? k : 0;
+    CUDA_TRY(cudaMemcpyAsync(koff.p, hkoff.data(), sizeof(int) * p, cudaMemcpyHostToDevice, s));
+    rband.alloc((size_t)dim * (2 * w + 1));
+    rborder.alloc((size_t)dim * std::max(kb, 1));
+    CUDA_TRY(cudaMemsetAsync(rband.p, 0, sizeof(double) * (size_t)dim * (2 * w + 1), s));
+    CUDA_TRY(cudaMemsetAsync(rborder.p, 0, sizeof(double) * (size_t)dim * std::max(kb, 1), s));
+    a = args();
+    piv_assemble_kernel<0><<<p, 32, 0, s>>>(a);
+    LAUNCH_CHECK();
+    piv_assemble_kernel<1><<<p, 32, 0, s>>>(a);
+    LAUNCH_CHECK();
+    launches += 2;
+    // the reduced LU with partial pivoting (src/parfact.cpp:134-166)
+    rr_rec.alloc((size_t)dim, w + 1, 1, 2 * w + 1, std::max(kb, 1));
+    rrhs.alloc(dim);
+    xk.alloc(dim);
+    rghat.alloc(dim);
+    a = args();
+    a.rec = rr_rec.view;
+    piv_factor_kernel<1><<<1, 32, smem_bytes(), s>>>(a);
+    LAUNCH_CHECK();
+    ++launches;
+    check_status(s);
+  }
+
+  PivArgs reduced_args(const double* r, double* x) const {
+    PivArgs a = args();
+    a.rec = rr_rec.view;
+    a.rr = r;
+    a.xk = x;
+    a.ghat = rghat.p;
+    return a;
+  }
+
+  void solve(const double* df, double* dx, cudaStream_t s, cudaEvent_t* ev) {
+    PivArgs a = args();
+    a.f = df;
+    a.x = dx;
+    if (ev) CUDA_TRY(cudaEventRecord(ev[0], s));
+    piv_condense_kernel<<<p, 32, 0, s>>>(a);
+    LAUNCH_CHECK();
+    piv_rrhs_kernel<<<p, 32, 0, s>>>(a, rrhs.p);
+    LAUNCH_CHECK();
+    if (ev) CUDA_TRY(cudaEventRecord(ev[1], s));
+    piv_reduced_solve_kernel<<<1, 32, 0, s>>>(reduced_args(rrhs.p, xk.p));
+    LAUNCH_CHECK();
+    if (ev) CUDA_TRY(cudaEventRecord(ev[2], s));
+    piv_backsolve_kernel<<<p, 32, 0, s>>>(a);
+    LAUNCH_CHECK();
+    if (ev) CUDA_TRY(cudaEventRecord(ev[3], s));
+    launches = 4;
+  }
+
+  void solve_reduced(const double* r, double* x, cudaStream_t s) {
+    piv_reduced_solve_kernel<<<1, 32, 0, s>>>(reduced_args(r, x));
+    LAUNCH_CHECK();
+  }
+
+  // exact operation count of the reference's dense reduced LU (src/parfact.cpp:134-184)
+  long long reduced_ops() const {
+    const long long n = dim;
+    return 3 * (n * (n - 1) / 2) + (n - 1) * n * (2 * n - 1) / 6 + n;
+  }
+
+  void dense_T(double* T) const {
+    std::vector<double> band((size_t)dim * (2 * w + 1)), border((size_t)dim * std::max(kb, 1));
+    CUDA_TRY(cudaMemcpy(band.data(), rband.p, sizeof(double) * band.size(), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(border.data(), rborder.p, sizeof(double) * border.size(), cudaMemcpyDeviceToHost));
+    std::fill(T, T + (size_t)dim * dim, 0.0);
+    for (int r = 0; r < dim; ++r) {
+      for (int d = 0; d <= 2 * w; ++d) {
+        const int c = r - w + d;
+        if (c >= 0 && c < dim - kb) T[(size_t)r * dim + c] = band[(size_t)r * (2 * w + 1) + d];
+      }
+      for (int u = 0; u < kb; ++u) T[(size_t)r * dim + (dim - kb + u)] = border[(size_t)r * kb + u];
+    }
+  }
+};
+
 struct psg_handle {
   int device = 0;  // where the factorization lives (DeviceGuard in every entry point)
   psg_desc A{};    // device view
@@ -1258,6 +1522,9 @@ struct psg_handle {
   GenSolver gen;
   BlkSolver blk;                        // speculative path of the K x K block kinds
   ChainSolver chain;                    // BVP-layout BABD chain path
+  std::unique_ptr<PivSolver> piv;       // LuPivot / Qr, and every strategy of the circulant-like kind
+  int rot = 0;                          // circulant-like: rows rotated down by rot (permute_corner)
+  DevBuf<double> d_fperm;               // rotated rhs
   bool generic = false;                 // non-tridiagonal kinds: generic exact path
   double refine_tol = 1e-14;            // generic path: refine once when ||Ax-f||/||f|| exceeds this
   double last_residual = 0.0;
@@ -1367,7 +1634,7 @@ void check_strategy(const psg_desc& A, int strategy) {
         throw Fail{PSG_E_UNSUPPORTED_KIND, "strategy arce does not support this kind"};
       throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "strategy arce has no GPU path"};
     case PSG_LUPIVOT:
-    case PSG_QR: throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "pivoting strategies have no GPU path"};
+    case PSG_QR: return;  // every kind (src/localfact.cpp:31-42)
     default: throw Fail{PSG_E_INVALID_PARAMETER, "unknown strategy"};
   }
 }
@@ -1378,6 +1645,13 @@ bool is_tridiag(const psg_desc& A) { return A.kind == PSG_BANDED && A.s == 1 && 
 void run_factor(psg_handle* h, cudaStream_t s) {
   h->tri.launches = 0;
   CUDA_TRY(cudaEventRecord(h->ev_f0, s));
+  if (h->piv) {
+    h->piv->factor(s);
+    h->spec_factored = h->exact_factored = true;
+    h->factor_launches = h->piv->launches;
+    CUDA_TRY(cudaEventRecord(h->ev_f1, s));
+    return;
+  }
   if (h->generic) {
     h->gen.launches = 0;
     h->blk.launches = 0;
@@ -1489,15 +1763,71 @@ int psg_plan(const psg_desc* A, int p, int* body_begin, int* body_end, int* sep_
   }
 }
 
+// Device copy of A for a pivoting handle; circulant-like rows rotated down by
+// r so all wrap content sits in the upper-right corner (permute_corner,
+// src/partition.cpp:175-202): the canonical matrix has bandwidths (s + r, 0).
+void piv_set_matrix(psg_handle* h, const psg_desc& Ain, cudaStream_t s) {
+  h->A = Ain;
+  const double* src = Ain.data;
+  DevBuf<double> staged;
+  if (!Ain.on_device) {
+    (Ain.kind == PSG_CIRCULANT && Ain.r > 0 ? staged : h->own_data).alloc(Ain.data_len);
+    double* dst = Ain.kind == PSG_CIRCULANT && Ain.r > 0 ? staged.p : h->own_data.p;
+    CUDA_TRY(cudaMemcpyAsync(dst, Ain.data, sizeof(double) * Ain.data_len, cudaMemcpyHostToDevice, s));
+    src = dst;
+    h->A.data = dst;
+    if (Ain.corner) {
+      const size_t cn = (size_t)Ain.corner_rows * Ain.corner_cols;
+      h->own_corner.alloc(cn);
+      CUDA_TRY(cudaMemcpyAsync(h->own_corner.p, Ain.corner, sizeof(double) * cn, cudaMemcpyHostToDevice, s));
+      h->A.corner = h->own_corner.p;
+    }
+    h->A.on_device = 1;
+  }
+  h->rot = 0;
+  if (Ain.kind == PSG_CIRCULANT && Ain.r > 0) {
+    h->own_data.alloc(Ain.data_len);
+    piv_rotate_kernel<<<148 * 8, 256, 0, s>>>(Ain.n, Ain.s + Ain.r + 1, Ain.r, src, h->own_data.p);
+    LAUNCH_CHECK();
+    h->A.data = h->own_data.p;
+    h->A.s = Ain.s + Ain.r;
+    h->A.r = 0;
+    h->rot = Ain.r;
+    CUDA_TRY(cudaStreamSynchronize(s));  // staged source goes back to the cache
+  }
+}
+
+int piv_strategy_of(int strategy) {
+  return strategy == PSG_LUPIVOT ? kPvPartial : strategy == PSG_QR ? kPvQr : kPvNoPivot;
+}
+
 int psg_factor(const psg_desc* Ain, int p, int strategy, double tol, void* stream, psg_handle** out, char* err,
                size_t errlen) {
-  (void)tol;
   *out = nullptr;
   try {
     std::unique_ptr<psg_handle> h(new psg_handle);
     CUDA_TRY(cudaGetDevice(&h->device));
     validate(*Ain);
     check_strategy(*Ain, strategy);
+    if (strategy == PSG_LUPIVOT || strategy == PSG_QR || Ain->kind == PSG_CIRCULANT) {
+      cudaStream_t s = (cudaStream_t)stream;
+      for (cudaEvent_t* e : {&h->ev_f0, &h->ev_f1, &h->ev_done, &h->ev[0], &h->ev[1], &h->ev[2], &h->ev[3]})
+        *e = event_pool().get();
+      h->strategy = strategy;
+      piv_set_matrix(h.get(), *Ain, s);
+      h->plan = make_plan(h->A, p);
+      h->generic = true;
+      CUDA_TRY(cudaStreamSynchronize(s));
+      h->piv = std::make_unique<PivSolver>();
+      SMView V{h->A.kind, h->A.n, h->A.m, h->A.s, h->A.r, h->A.data, h->A.corner, h->A.corner_rows, h->A.corner_cols};
+      h->piv->init(V, h->plan, piv_strategy_of(strategy), tol);
+      h->d_status.alloc(1);
+      h->h_status = static_cast<DevStatus*>(pinned_slots().get());
+      run_factor(h.get(), s);
+      CUDA_TRY(cudaEventRecord(h->ev_done, s));
+      *out = h.release();
+      return 0;
+    }
     h->plan = make_plan(*Ain, p);
     h->generic = !is_tridiag(*Ain);
     cudaStream_t s = (cudaStream_t)stream;
@@ -1704,6 +2034,52 @@ void add_phase_stats(psg_handle* h, psg_stats* stats, cudaEvent_t* ev) {
 
 // Generic kinds, blocking: the block speculative path when possible, else (or
 // when its certificate fails) the exact generic path with residual refinement.
+// Pivoting handles: solve, certify by the normwise residual, refine once.
+void piv_blocking(psg_handle* h, const double* df, double* dx, cudaStream_t s, psg_stats* stats) {
+  const int n = h->A.n;
+  const double* f = df;
+  if (h->rot) {  // the rhs of the row-rotated matrix (ParallelFactorization::row_perm)
+    h->d_fperm.alloc(n);
+    piv_rotate_kernel<<<148 * 8, 256, 0, s>>>(n, 1, h->rot, df, h->d_fperm.p);
+    LAUNCH_CHECK();
+    f = h->d_fperm.p;
+  }
+  PivSolver& P = *h->piv;
+  P.solve(f, dx, s, stats ? h->ev : nullptr);
+  int launches = P.launches + (h->rot ? 1 : 0);
+  MatView v{h->A.kind, h->A.n, h->A.m, h->A.s, h->A.r, h->A.data, h->A.corner, h->A.corner_rows, h->A.corner_cols};
+  h->d_r.alloc(n);
+  h->d_norm.alloc(2);
+  auto resid = [&]() {
+    unsigned long long hb[2];
+    CUDA_TRY(cudaMemsetAsync(h->d_norm.p, 0, 2 * sizeof(unsigned long long), s));
+    residual_vec_kernel<<<148 * 8, 256, 0, s>>>(v, dx, f, h->d_r.p, h->d_norm.p);
+    LAUNCH_CHECK();
+    CUDA_TRY(cudaMemcpyAsync(hb, h->d_norm.p, sizeof hb, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    const double num = bits_to_double(hb[0]), den = bits_to_double(hb[1]);
+    return den > 0 ? num / den : num;
+  };
+  double rel = resid();
+  ++launches;
+  if (rel > h->refine_tol && rel == rel) {
+    h->d_d.alloc(n);
+    P.solve(h->d_r.p, h->d_d.p, s, nullptr);
+    axpy_kernel<<<148 * 8, 256, 0, s>>>(n, h->d_d.p, dx);
+    LAUNCH_CHECK();
+    launches += P.launches + 2;
+    rel = resid();
+  }
+  if (!(rel == rel)) throw Fail{PSG_E_SINGULAR_REDUCED_SYSTEM, "non-finite solution"};
+  h->solve_launches = launches;
+  if (stats) {
+    add_phase_stats(h, stats, h->ev);
+    stats->reduced_ops += P.reduced_ops();
+    stats->certificate = std::max(stats->certificate, rel);
+    stats->speculative = 0;
+  }
+}
+
 void generic_blocking(psg_handle* h, const double* df, double* dx, cudaStream_t s, psg_stats* stats) {
   int fallbacks = 0;
   if (h->use_blk() || h->use_chain()) {
@@ -1828,7 +2204,9 @@ int psg_solve(const psg_handle* hc, const double* f, double* x, int on_device, v
       df = h->d_f.p;
       dx = h->d_x.p;
     }
-    if (h->generic) {
+    if (h->piv) {
+      piv_blocking(h, df, dx, s, stats);
+    } else if (h->generic) {
       generic_blocking(h, df, dx, s, stats);
     } else {
       tri_solve_blocking(h, df, dx, s, stats);
@@ -1938,6 +2316,11 @@ int psg_solve_async(const psg_handle* hc, const double* f, double* x, int timing
   std::lock_guard<std::mutex> g(h->mu);
   try {
     cudaStream_t s = (cudaStream_t)stream;
+    if (h->piv) {  // pivoting handles certify by a residual pass: blocking
+      piv_blocking(h, f, x, s, nullptr);
+      CUDA_TRY(cudaEventRecord(h->ev_done, s));
+      return 0;
+    }
     if (h->generic && !h->spec_mode()) {  // the exact generic path certifies by a residual pass: blocking
       generic_blocking(h, f, x, s, nullptr);
       CUDA_TRY(cudaEventRecord(h->ev_done, s));
@@ -1993,10 +2376,21 @@ int psg_refactor(psg_handle* h, const psg_desc* A, void* stream, char* err, size
   std::lock_guard<std::mutex> g(h->mu);
   try {
     validate(*A);
-    if (A->kind != h->A.kind || A->n != h->A.n || A->m != h->A.m || A->s != h->A.s || A->r != h->A.r ||
+    const int hs = h->A.s - h->rot, hr = h->rot ? h->rot : h->A.r;  // bandwidths as given (before permute_corner)
+    if (A->kind != h->A.kind || A->n != h->A.n || A->m != h->A.m || A->s != hs || A->r != hr ||
         A->corner_rows != h->A.corner_rows || A->corner_cols != h->A.corner_cols)
       throw Fail{PSG_E_DIMENSION_MISMATCH, "psg_refactor needs the factored structure"};
     cudaStream_t s = (cudaStream_t)stream;
+    if (h->piv) {  // new values may defer other pivots: the reduced layout is rebuilt
+      CUDA_TRY(cudaEventSynchronize(h->ev_done));
+      piv_set_matrix(h, *A, s);
+      CUDA_TRY(cudaStreamSynchronize(s));
+      h->piv->A.data = h->A.data;
+      h->piv->A.corner = h->A.corner;
+      run_factor(h, s);
+      CUDA_TRY(cudaEventRecord(h->ev_done, s));
+      return 0;
+    }
     // Pending asynchronous solves are NOT drained here: the factor kernels run
     // after them in stream order.  Their certificates are checked at psg_sync
     // against the matrix values current then, so callers must psg_sync before
@@ -2041,6 +2435,13 @@ int psg_refactor(psg_handle* h, const psg_desc* A, void* stream, char* err, size
 }
 
 int psg_reduced_info(const psg_handle* h, int* q, int* dim, int* k, int* has_corner) {
+  if (h->piv) {
+    if (q) *q = h->piv->q;
+    if (dim) *dim = h->piv->dim;
+    if (k) *k = h->plan.sep_size;
+    if (has_corner) *has_corner = h->plan.has_corner ? 1 : 0;
+    return 0;
+  }
   const int qq = h->plan.sep_count();
   if (q) *q = qq;
   if (dim) *dim = qq * h->plan.sep_size;
@@ -2049,12 +2450,61 @@ int psg_reduced_info(const psg_handle* h, int* q, int* dim, int* k, int* has_cor
   return 0;
 }
 
+int psg_reduced_layout(const psg_handle* h, int* positions, int* sizes) {
+  if (h->piv) {
+    for (int j = 0; j < h->piv->q; ++j) {
+      if (positions) positions[j] = h->piv->rpos[j];
+      if (sizes) sizes[j] = h->piv->rsize[j];
+    }
+    return 0;
+  }
+  for (int j = 0; j < h->plan.sep_count(); ++j) {
+    if (positions) positions[j] = h->plan.sep_start(j);
+    if (sizes) sizes[j] = h->plan.sep_size;
+  }
+  return 0;
+}
+
+int psg_reduced_dense(const psg_handle* hc, double* T, char* err, size_t errlen) {
+  psg_handle* h = const_cast<psg_handle*>(hc);
+  DeviceGuard dg(h->device);
+  try {
+    {
+      std::lock_guard<std::mutex> g(h->mu);
+      CUDA_TRY(cudaEventSynchronize(h->ev_done));
+      if (h->piv) {
+        h->piv->dense_T(T);
+        return 0;
+      }
+    }
+    const int q = h->plan.sep_count(), k = h->plan.sep_size, kk = k * k, dim = q * k;
+    std::vector<double> dg_(static_cast<size_t>(q) * kk), sb(static_cast<size_t>(q) * kk), sp(static_cast<size_t>(q) * kk);
+    const int rc = psg_reduced_blocks(hc, dg_.data(), sb.data(), sp.data(), err, errlen);
+    if (rc) return rc;
+    std::fill(T, T + (size_t)dim * dim, 0.0);
+    for (int j = 0; j < q; ++j)
+      for (int t = 0; t < k; ++t)
+        for (int u = 0; u < k; ++u) {
+          T[(size_t)(j * k + t) * dim + j * k + u] = dg_[(size_t)j * kk + t * k + u];
+          if (j > 0) T[(size_t)(j * k + t) * dim + (j - 1) * k + u] = sb[(size_t)j * kk + t * k + u];
+          if (j + 1 < q) T[(size_t)(j * k + t) * dim + (j + 1) * k + u] = sp[(size_t)j * kk + t * k + u];
+        }
+    if (h->plan.has_corner)
+      for (int t = 0; t < k; ++t)
+        for (int u = 0; u < k; ++u) T[(size_t)t * dim + (q - 1) * k + u] += sb[t * k + u];
+    return 0;
+  } catch (const Fail& f_) {
+    return set_err(err, errlen, f_.code, f_.msg);
+  }
+}
+
 int psg_reduced_blocks(const psg_handle* hc, double* diag, double* sub, double* super, char* err, size_t errlen) {
   psg_handle* h = const_cast<psg_handle*>(hc);
   DeviceGuard dg(h->device);
   std::lock_guard<std::mutex> g(h->mu);
   try {
     CUDA_TRY(cudaEventSynchronize(h->ev_done));
+    if (h->piv) throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "reduced system has adaptive extras: use psg_reduced_dense"};
     if (h->generic) {
       if (!h->exact_factored) {  // parallel_factor's ReducedSystem comes from the exact path
         ensure_exact_generic(h, nullptr);
@@ -2120,6 +2570,25 @@ int psg_solve_reduced(const psg_handle* hc, const double* rhs, double* x, int on
   std::lock_guard<std::mutex> g(h->mu);
   try {
     cudaStream_t s = (cudaStream_t)stream;
+    if (h->piv) {
+      const int dim = h->piv->dim;
+      DevBuf<double> dr, dxv;
+      const double* r = rhs;
+      double* xo = x;
+      if (!on_device) {
+        dr.alloc(dim);
+        dxv.alloc(dim);
+        CUDA_TRY(cudaMemcpyAsync(dr.p, rhs, sizeof(double) * dim, cudaMemcpyHostToDevice, s));
+        r = dr.p;
+        xo = dxv.p;
+      }
+      h->piv->solve_reduced(r, xo, s);
+      if (!on_device) CUDA_TRY(cudaMemcpyAsync(x, xo, sizeof(double) * dim, cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaStreamSynchronize(s));
+      CUDA_TRY(cudaEventRecord(h->ev_done, s));
+      if (stats) stats->reduced_ops += h->piv->reduced_ops();
+      return 0;
+    }
     if (h->generic) {
       if (h->gen.lv.size() < 2) throw Fail{PSG_E_INVALID_PARAMETER, "no reduced system"};
       ensure_exact_generic(h, s);

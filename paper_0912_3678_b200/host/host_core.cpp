@@ -272,7 +272,6 @@ bool StructuredMatrix::corner_canonical() const {
 
 StructuredMatrix make(Kind kind, int n, int m, int s, int r, std::vector<double> data, std::vector<double> corner,
                       int corner_rows, int corner_cols) {
-  if (kind == Kind::CirculantLike) fail(Errc::UnsupportedKind, "circulant-like matrices have no GPU path");
   const psg_desc d = host_desc(kind, n, m, s, r, data, corner, corner_rows, corner_cols);
   char err[512];
   if (int rc = psg_validate(&d, err, sizeof err)) fail(Errc(rc - 1), err);
@@ -374,12 +373,31 @@ PartitionPlan plan_partition(const StructuredMatrix& A, int p) {
   plan.m = A.m;
   plan.p = p;
   plan.sep_size = k;
-  plan.has_corner = A.kind == Kind::Babd;
-  plan.corner_rows = A.corner_rows;
-  plan.corner_cols = A.corner_cols;
+  plan.has_corner = A.kind == Kind::Babd || A.kind == Kind::CirculantLike;
+  plan.corner_rows = A.kind == Kind::CirculantLike ? A.s : A.corner_rows;  // wrap extent (src/partition.cpp:68-71)
+  plan.corner_cols = A.kind == Kind::CirculantLike ? A.s : A.corner_cols;
   for (int i = 0; i < p; ++i) plan.body_ranges.emplace_back(bb[i], be[i]);
   plan.separator_starts.assign(ss.begin(), ss.begin() + cnt);
   return plan;
+}
+
+// Rotate a circulant-like matrix's rows down by r so every wrapped entry sits
+// in the upper-right corner (reference src/partition.cpp:175-202): a pure
+// relabelling of the stored bands; the GPU factorization does the same
+// rotation on the device (psg_factor).
+std::pair<StructuredMatrix, Permutation> permute_corner(const StructuredMatrix& A) {
+  if (A.kind != Kind::CirculantLike && A.kind != Kind::Babd)
+    fail(Errc::UnsupportedKind, "permute_corner applies to circulant-like and BABD matrices");
+  Permutation perm;
+  perm.source.resize(A.n);
+  for (int i = 0; i < A.n; ++i) perm.source[i] = i;
+  if (A.corner_canonical()) return {A, perm};
+  const int n = A.n, s = A.s, r = A.r;
+  for (int i = 0; i < n; ++i) perm.source[i] = ((i - r) % n + n) % n;
+  std::vector<double> data(std::size_t(s + r + 1) * n);
+  for (int q = 0; q <= s + r; ++q)
+    for (int i = 0; i < n; ++i) data[std::size_t(q) * n + i] = A.data[std::size_t(q) * n + perm.source[i]];
+  return {make(Kind::CirculantLike, n, 1, s + r, 0, std::move(data)), perm};
 }
 
 DenseMatrix PartitionBlock::local_dense() const {

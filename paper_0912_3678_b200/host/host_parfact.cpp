@@ -38,7 +38,14 @@ ParallelFactorization parallel_factor(const StructuredMatrix& A, int p, Strategy
   char err[512];
   ParallelFactorization F;
   F.strategy = strategy;
-  F.plan = plan_partition(A, p);
+  if (A.kind == Kind::CirculantLike && !A.corner_canonical()) {  // src/parfact.cpp:29-35
+    auto [B, perm] = permute_corner(A);
+    F.plan = plan_partition(B, p);
+    F.permuted = true;
+    F.row_perm = std::move(perm);  // applied on the device by psg_solve
+  } else {
+    F.plan = plan_partition(A, p);
+  }
   psg_handle* h = nullptr;
   const psg_desc d = host_desc(A);
   check(psg_factor(&d, p, int(strategy), tol, nullptr, &h, err, sizeof err), err);
@@ -50,37 +57,34 @@ ParallelFactorization parallel_factor(const StructuredMatrix& A, int p, Strategy
   R.q = q;
   R.dim = dim;
   R.has_corner = corner != 0;
-  for (int j = 0; j < q; ++j) {
-    R.block_sizes.push_back(k);
-    R.positions.push_back(F.plan.separator_starts[j]);
-    R.offsets.push_back(j * k);
+  // layout in position order: separators and (LuPivot / Qr) adaptive extras (src/parfact.cpp:72-88)
+  R.positions.resize(q);
+  R.block_sizes.resize(q);
+  psg_reduced_layout(h, R.positions.data(), R.block_sizes.data());
+  for (int b = 0, off = 0; b < q; ++b) {
+    R.offsets.push_back(off);
+    off += R.block_sizes[b];
   }
-  // kept_maps (src/parfact.cpp:106-127): reduced indices of each partition's separators
+  // kept_maps (src/parfact.cpp:106-127): [left separator | extras by position | right separator]
   F.kept_maps.assign(p, {});
+  const auto find_block = [&](int position) {
+    return int(std::lower_bound(R.positions.begin(), R.positions.end(), position) - R.positions.begin());
+  };
   for (int i = 0; i < p; ++i) {
     const int left = corner ? i : i - 1, right = corner ? i + 1 : i;
+    const int nsep = int(F.plan.separator_starts.size());
+    std::vector<int>& map = F.kept_maps[i];
     if (left >= 0)
-      for (int t = 0; t < k; ++t) F.kept_maps[i].push_back(left * k + t);
-    if (right < q)
-      for (int t = 0; t < k; ++t) F.kept_maps[i].push_back(right * k + t);
+      for (int t = 0; t < k; ++t) map.push_back(R.offsets[find_block(F.plan.separator_starts[left])] + t);
+    auto [b, e] = F.plan.body_ranges[i];
+    for (int blk = find_block(b); blk < q && R.positions[blk] < e; ++blk) map.push_back(R.offsets[blk]);
+    if (right < nsep)
+      for (int t = 0; t < k; ++t) map.push_back(R.offsets[find_block(F.plan.separator_starts[right])] + t);
   }
   if (dim <= kDenseReducedLimit) {  // dense image of T for callers and oracles
-    const int kk = k * k;
-    std::vector<double> dg(std::size_t(q) * kk), sb(std::size_t(q) * kk), sp(std::size_t(q) * kk);
-    check(psg_reduced_blocks(h, dg.data(), sb.data(), sp.data(), err, sizeof err), err);
     R.T = DenseMatrix(dim, dim);
-    for (int j = 0; j < q; ++j)
-      for (int t = 0; t < k; ++t)
-        for (int u = 0; u < k; ++u) {
-          R.T.at(j * k + t, j * k + u) = dg[std::size_t(j) * kk + t * k + u];
-          if (j > 0) R.T.at(j * k + t, (j - 1) * k + u) = sb[std::size_t(j) * kk + t * k + u];
-          if (j + 1 < q) R.T.at(j * k + t, (j + 1) * k + u) = sp[std::size_t(j) * kk + t * k + u];
-        }
-    if (corner)
-      for (int t = 0; t < k; ++t)
-        for (int u = 0; u < k; ++u) R.T.at(t, (q - 1) * k + u) += sb[t * k + u];
+    check(psg_reduced_dense(h, R.T.a.data(), err, sizeof err), err);
   }
-  psg_stats s{};
   F.factor_seconds = 0;
   return F;
 }

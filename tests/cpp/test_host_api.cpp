@@ -358,6 +358,28 @@ static void gpu_tests() {
     // solve_sequential runs on the GPU too
     CHECK(rel_err(solve_sequential(A, f), x) <= 1e-12);
   }
+  // circulant-like (reference permute_corner + LuPivot): rows rotated, wrap in the corner
+  {
+    const int n = 64;
+    std::vector<double> d(3 * n);
+    Vector r = random_vector(3 * n, 17);
+    for (int i = 0; i < 3 * n; ++i) d[i] = r[i];
+    StructuredMatrix C = make(Kind::CirculantLike, n, 1, 1, 1, d);
+    auto [B, perm] = permute_corner(C);
+    CHECK(B.s == 2 && B.r == 0 && B.corner_canonical() && perm.source[0] == n - 1);
+    CHECK(B.at(5, 3) == C.at(4, 3) && B.at(0, n - 1) == C.at(n - 1, n - 1));
+    Vector f = random_vector(n, 3);
+    Vector want = lu_solve(to_dense(C), f);
+    for (Strategy st : {Strategy::LuPivot, Strategy::Qr}) {
+      ParallelFactorization F = parallel_factor(C, 4, st);
+      CHECK(F.permuted && F.plan.has_corner && F.plan.sep_size == 2);
+      CHECK(rel_err(solve(F, f), want) <= 1e-10);
+      // the reduced system: q blocks in position order, T dense, solve_reduced consistent
+      CHECK(int(F.reduced.positions.size()) == F.reduced.q && F.reduced.T.rows == F.reduced.dim);
+      Vector rhs = random_vector(F.reduced.dim, 5);
+      CHECK(rel_err(solve_reduced(F, rhs), lu_solve(F.reduced.T, rhs)) <= 1e-10);
+    }
+  }
   // errors: zero pivot tagged with the partition (test_localfact.cpp:369-385, parfact.cpp:61-68)
   {
     const int n = 3000;
@@ -374,7 +396,12 @@ static void gpu_tests() {
       ok = e.code() == Errc::ZeroPivot && e.detail().find("partition 2") != std::string::npos;
     }
     CHECK(ok);
-    CHECK_THROWS_CODE(parallel_factor(A, 3, Strategy::LuPivot), Errc::UnsupportedStructure);
+    // ZeroPivot "signals: use LUPivot or QR" (SPEC localfact): both solve the same matrix
+    for (Strategy st : {Strategy::LuPivot, Strategy::Qr}) {
+      ParallelFactorization Fp = parallel_factor(A, 3, st);
+      CHECK(residual(A, solve(Fp, Vector(n, 1.0)), Vector(n, 1.0)) <= 1e-13);
+      CHECK(Fp.reduced.q >= 2 && Fp.kept_maps.size() == 3);
+    }
     CHECK_THROWS_CODE(parallel_factor(generate_random(Kind::Banded, 30, 1, 2, 1, 5, 2.0), 3, Strategy::CyclicReduction),
                       Errc::UnsupportedKind);
   }

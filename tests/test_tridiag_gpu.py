@@ -143,12 +143,11 @@ def test_strategies_and_errors(cuda):
     A, f = O.generate_config(0, 4096, 4)
     GA = psg.StructuredMatrix(A.kind, A.n, A.m, A.s, A.r, _dev(cuda, A.data))
     want, _ = O.parallel_solve(A, 8, f)
-    for s in (psg.Strategy.Lu, psg.Strategy.Lud, psg.Strategy.CyclicReduction):
+    for s in (psg.Strategy.Lu, psg.Strategy.Lud, psg.Strategy.CyclicReduction, psg.Strategy.LuPivot, psg.Strategy.Qr):
         F = psg.parallel_factor(GA, 8, s)
         got = psg.solve(F, _dev(cuda, f)).cpu().numpy()
         assert O.rel_err(got, want) <= 1e-12
-    for s, code in ((psg.Strategy.LuPivot, psg.Errc.UnsupportedStructure), (psg.Strategy.Qr, psg.Errc.UnsupportedStructure),
-                    (psg.Strategy.Arce, psg.Errc.UnsupportedKind)):
+    for s, code in ((psg.Strategy.Arce, psg.Errc.UnsupportedKind),):
         with pytest.raises(psg.Error) as ei:
             psg.parallel_factor(GA, 8, s)
         assert ei.value.code == code
