@@ -85,7 +85,8 @@ typedef struct psg_handle psg_handle;
 /* Factor A on p partitions (parallel_factor).  tol is accepted for API
  * parity (the reference uses it only for LuPivot/Qr).  Lu, Lud and (where the
  * reference allows it) CyclicReduction share the same GPU kernels;
- * Arce/LuPivot/Qr return UnsupportedStructure (no CPU fallback). */
+ * LuPivot/Qr (and every strategy on the circulant-like kind) run the pivoting
+ * engine; Arce returns UnsupportedStructure (no CPU fallback). */
 int psg_factor(const psg_desc* A, int p, int strategy, double tol, void* stream,
                psg_handle** out, char* err, size_t errlen);
 
