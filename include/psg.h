@@ -25,6 +25,9 @@
  *                          include/parsol/parfact.hpp:14-22)
  *   psg_ode_trajectory  <- solve_ivp_parallel()   include/parsol/odeparallel.hpp (reference
  *                          proj/include/parsol/odeparallel.hpp; impl src/odeparallel.cpp:183-233)
+ *   psg_pr_*            <- propagate / parareal_init / parareal_iterate / parareal_solve
+ *                          include/parsol/parareal.hpp (reference proj/include/parsol/parareal.hpp;
+ *                          impl src/parareal.cpp:56-117)
  *   psg_generate_config -- (new) device generator of the BASELINE configs,
  *                          bit-identical to SplitMix64 (include/parsol/rng.hpp)
  */
@@ -163,6 +166,27 @@ int psg_matvec(const psg_desc* A, const double* x, double* y, int on_device, voi
  * out: host, (p N + 1) m trajectory.  1 <= m <= 8.  Blocks until done. */
 int psg_ode_trajectory(int m, int p, int N, const double* win, const double* g, double* out, void* stream,
                        psg_stats* stats, char* err, size_t errlen);
+
+/* Parareal for linear IVPs (src/parareal.cpp:56-117; the C++ layer
+ * include/parsol/parareal.hpp builds the steppers).  Each propagator is a
+ * per-window stepper y <- T y + Minv rhs_n, n = 1..S: T and Minv are nmat
+ * distinct m x m matrices (row-major), mat[i] picks window i+1's; rhs is
+ * p x S x m (host).  1 <= m <= 64.  inits are p x m (window initial values,
+ * inits[0] = y0). */
+typedef struct psg_pr psg_pr;
+int psg_pr_create(int m, int p, const double* y0, int Sf, int nmat_f, const double* Tf, const double* Mf,
+                  const int* matf, const double* rhsf, int Sc, int nmat_c, const double* Tc, const double* Mc,
+                  const int* matc, const double* rhsc, psg_pr** out, char* err, size_t errlen);
+int psg_pr_set_inits(psg_pr* h, const double* inits);
+int psg_pr_get_inits(psg_pr* h, double* inits, double* fine); /* fine: (p-1) x m, F_i inits[i-1]; may be NULL */
+int psg_pr_coarse_sweep(psg_pr* h, char* err, size_t errlen); /* parareal_init */
+int psg_pr_iterate(psg_pr* h, double* update, double* scale, char* err, size_t errlen); /* parareal_iterate */
+/* parareal_solve: coarse sweep, then iterations until update <= tol * max(scale, 1e-300); history[k-1] = update. */
+int psg_pr_solve(psg_pr* h, double tol, int max_iter, int* iterations, double* history, int* converged,
+                 char* err, size_t errlen);
+/* propagate(): which = 0 fine, 1 coarse; window i in 1..p; y, out host m-vectors. */
+int psg_pr_apply(psg_pr* h, int which, int i, const double* y, double* out, char* err, size_t errlen);
+void psg_pr_release(psg_pr* h);
 
 /* BASELINE config generator on the device (same stream mapping and values as
  * oracle/parsol_oracle.c or_generate_config).  Shapes via psg_config_shape. */

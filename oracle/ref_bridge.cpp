@@ -24,6 +24,7 @@
 #include "parsol/errors.hpp"
 #include "parsol/io.hpp"
 #include "parsol/odeparallel.hpp"
+#include "parsol/parareal.hpp"
 #include "parsol/parfact.hpp"
 #include "parsol/seqref.hpp"
 #include "parsol/structmat.hpp"
@@ -267,6 +268,57 @@ int ref_plan(void* hm, int p, int* body_begin, int* body_end, int* sep_start, in
     for (int j = 0; j < plan.sep_count(); ++j) sep_start[j] = plan.separator_starts[j];
     *sep_count = plan.sep_count();
     *sep_size = plan.sep_size;
+    return 0;
+  } catch (const std::exception& e) {
+    return report(e, err, errlen);
+  }
+}
+
+// Parareal through the reference (src/parareal.cpp:94-120): same arguments as
+// psg_parareal_solve in libparsol_b200.
+int ref_parareal_solve(int m, const double* L, const double* y0, double t0, double T, int p, int N,
+                       void (*g)(double, double*, void*), void* ctx, int fkind, int fmethod, int fsteps, int ckind,
+                       int cmethod, int csteps, double tol, int max_iter, double* inits, double* history,
+                       int history_cap, int* iterations, int* converged, char* err, size_t errlen) {
+  try {
+    IVProblem prob;
+    prob.L = DenseMatrix(m, m);
+    std::copy(L, L + size_t(m) * m, prob.L.a.begin());
+    prob.y0.assign(y0, y0 + m);
+    prob.t0 = t0;
+    prob.T = T;
+    if (g)
+      prob.g = [g, ctx, m](double t) {
+        Vector v(m, 0.0);
+        g(t, v.data(), ctx);
+        return v;
+      };
+    auto prop = [](int kind, int method, int steps) {
+      Propagator P;
+      P.kind = PropagatorKind(kind);
+      P.method = method == 0 ? OdeMethod::ImplicitEuler : OdeMethod::Trapezoidal;
+      P.steps = steps;
+      return P;
+    };
+    const TimeGrid grid = coarse_mesh(t0, T, p, N);
+    const PararealResult r = parareal_solve(prob, grid, prop(fkind, fmethod, fsteps), prop(ckind, cmethod, csteps),
+                                            tol, max_iter);
+    for (int i = 0; i < p; ++i) std::copy(r.inits[i].begin(), r.inits[i].end(), inits + size_t(i) * m);
+    for (int k = 0; k < int(r.history.size()) && k < history_cap; ++k) history[k] = r.history[k];
+    *iterations = r.iterations;
+    *converged = r.converged ? 1 : 0;
+    return 0;
+  } catch (const std::exception& e) {
+    return report(e, err, errlen);
+  }
+}
+
+int ref_expm(int m, const double* L, double t, double* out, char* err, size_t errlen) {
+  try {
+    DenseMatrix A(m, m);
+    std::copy(L, L + size_t(m) * m, A.a.begin());
+    const DenseMatrix E = matrix_exponential(A, t);
+    std::copy(E.a.begin(), E.a.end(), out);
     return 0;
   } catch (const std::exception& e) {
     return report(e, err, errlen);

@@ -28,6 +28,7 @@
 #include "chain_kernels.cuh"
 #include "ode_kernels.cuh"
 #include "piv_kernels.cuh"
+#include "pr_kernels.cuh"
 
 using namespace psg;
 
@@ -2273,6 +2274,198 @@ int psg_ode_trajectory(int m, int p, int N, const double* win, const double* g, 
   } catch (const Fail& f_) {
     return set_err(err, errlen, f_.code, f_.msg);
   }
+}
+
+// ---------------------------------------------------------------------------
+// Parareal (pr_kernels.cuh; src/parareal.cpp:56-117)
+// ---------------------------------------------------------------------------
+struct psg_pr {
+  int device = 0, m = 0, p = 0;
+  struct Side {
+    int S = 0;
+    DevBuf<double> T, Minv, rhs, c;
+    DevBuf<int> mat;
+    PrStepper view() const { return PrStepper{S, T.p, Minv.p, rhs.p, c.p, mat.p}; }
+  } F, G;
+  DevBuf<double> y0, in0, in1, fine, gold, norms, tmp;
+  int cur = 0;  // which of in0 / in1 holds the current inits
+  double* inits() { return cur ? in1.p : in0.p; }
+  double* other() { return cur ? in0.p : in1.p; }
+};
+
+namespace {
+
+void pr_side(psg_pr::Side& sd, int m, int p, int S, int nmat, const double* T, const double* M, const int* mat,
+             const double* rhs) {
+  if (S < 1 || nmat < 1) throw Fail{PSG_E_INVALID_PARAMETER, "propagator needs >= 1 step and >= 1 matrix"};
+  sd.S = S;
+  sd.T.alloc((size_t)nmat * m * m);
+  sd.Minv.alloc((size_t)nmat * m * m);
+  sd.mat.alloc(p);
+  sd.rhs.alloc((size_t)p * S * m);
+  sd.c.alloc((size_t)p * S * m);
+  CUDA_TRY(cudaMemcpy(sd.T.p, T, sizeof(double) * nmat * m * m, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(sd.Minv.p, M, sizeof(double) * nmat * m * m, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(sd.mat.p, mat, sizeof(int) * p, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(sd.rhs.p, rhs, sizeof(double) * (size_t)p * S * m, cudaMemcpyHostToDevice));
+  const long tasks = (long)p * S;
+  pr_prep_kernel<<<(unsigned)((tasks + 7) / 8), 256>>>(m, p, S, sd.Minv.p, sd.mat.p, sd.rhs.p, sd.c.p);
+  LAUNCH_CHECK();
+}
+
+PrArgs pr_args(psg_pr* h, int with_fine) {
+  PrArgs a{};
+  a.m = h->m;
+  a.p = h->p;
+  a.F = h->F.view();
+  a.G = h->G.view();
+  a.y0 = h->y0.p;
+  a.old_inits = h->inits();
+  a.new_inits = h->other();
+  a.fine = h->fine.p;
+  a.gold = h->gold.p;
+  a.norms = h->norms.p;
+  a.with_fine = with_fine;
+  return a;
+}
+
+void pr_smem_attr() {
+  static bool done[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (done[dev & 63]) return;
+  for (const void* k : {(const void*)pr_fine_kernel, (const void*)pr_sweep_kernel, (const void*)pr_apply_kernel})
+    CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PrSmem)));
+  done[dev & 63] = true;
+}
+
+// one Parareal iteration (with_fine) or the initial coarse sweep; returns {update, scale}
+std::pair<double, double> pr_step(psg_pr* h, int with_fine) {
+  PrArgs a = pr_args(h, with_fine);
+  if (with_fine && h->p > 1) {
+    pr_fine_kernel<<<h->p - 1, 32, sizeof(PrSmem)>>>(a);
+    LAUNCH_CHECK();
+  }
+  pr_sweep_kernel<<<1, 32, sizeof(PrSmem)>>>(a);
+  LAUNCH_CHECK();
+  double nb[2];
+  CUDA_TRY(cudaMemcpy(nb, h->norms.p, sizeof nb, cudaMemcpyDeviceToHost));
+  h->cur ^= 1;
+  return {nb[0], nb[1]};
+}
+
+}  // namespace
+
+int psg_pr_create(int m, int p, const double* y0, int Sf, int nmat_f, const double* Tf, const double* Mf,
+                  const int* matf, const double* rhsf, int Sc, int nmat_c, const double* Tc, const double* Mc,
+                  const int* matc, const double* rhsc, psg_pr** out, char* err, size_t errlen) {
+  *out = nullptr;
+  try {
+    if (m < 1 || m > kPrMaxM) throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "Parareal on the GPU supports dimension 1..64"};
+    if (p < 1) throw Fail{PSG_E_INVALID_INTERVAL, "need at least one window"};
+    pr_smem_attr();
+    std::unique_ptr<psg_pr> h(new psg_pr);
+    CUDA_TRY(cudaGetDevice(&h->device));
+    h->m = m;
+    h->p = p;
+    pr_side(h->F, m, p, Sf, nmat_f, Tf, Mf, matf, rhsf);
+    pr_side(h->G, m, p, Sc, nmat_c, Tc, Mc, matc, rhsc);
+    h->y0.alloc(m);
+    CUDA_TRY(cudaMemcpy(h->y0.p, y0, sizeof(double) * m, cudaMemcpyHostToDevice));
+    for (DevBuf<double>* b : {&h->in0, &h->in1, &h->fine, &h->gold}) {
+      b->alloc((size_t)p * m);
+      CUDA_TRY(cudaMemset(b->p, 0, sizeof(double) * (size_t)p * m));
+    }
+    h->norms.alloc(2);
+    h->tmp.alloc(2 * (size_t)m);
+    CUDA_TRY(cudaDeviceSynchronize());
+    *out = h.release();
+    return 0;
+  } catch (const Fail& f_) {
+    return set_err(err, errlen, f_.code, f_.msg);
+  }
+}
+
+int psg_pr_set_inits(psg_pr* h, const double* inits) {
+  DeviceGuard dg(h->device);
+  return cudaMemcpy(h->inits(), inits, sizeof(double) * (size_t)h->p * h->m, cudaMemcpyHostToDevice) == cudaSuccess
+             ? 0 : 1 + PSG_E_CUDA;
+}
+
+int psg_pr_get_inits(psg_pr* h, double* inits, double* fine) {
+  DeviceGuard dg(h->device);
+  const size_t bytes = sizeof(double) * (size_t)h->p * h->m;
+  if (inits && cudaMemcpy(inits, h->inits(), bytes, cudaMemcpyDeviceToHost) != cudaSuccess) return 1 + PSG_E_CUDA;
+  if (fine && h->p > 1 &&
+      cudaMemcpy(fine, h->fine.p, sizeof(double) * (size_t)(h->p - 1) * h->m, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return 1 + PSG_E_CUDA;
+  return 0;
+}
+
+int psg_pr_coarse_sweep(psg_pr* h, char* err, size_t errlen) {
+  DeviceGuard dg(h->device);
+  try {
+    pr_step(h, 0);
+    return 0;
+  } catch (const Fail& f_) {
+    return set_err(err, errlen, f_.code, f_.msg);
+  }
+}
+
+int psg_pr_iterate(psg_pr* h, double* update, double* scale, char* err, size_t errlen) {
+  DeviceGuard dg(h->device);
+  try {
+    const auto [u, sc] = pr_step(h, 1);
+    if (update) *update = u;
+    if (scale) *scale = sc;
+    return 0;
+  } catch (const Fail& f_) {
+    return set_err(err, errlen, f_.code, f_.msg);
+  }
+}
+
+int psg_pr_solve(psg_pr* h, double tol, int max_iter, int* iterations, double* history, int* converged, char* err,
+                 size_t errlen) {
+  DeviceGuard dg(h->device);
+  try {
+    if (!(tol > 0)) throw Fail{PSG_E_INVALID_PARAMETER, "tol must be positive"};
+    if (max_iter < 0) max_iter = 2 * h->p;
+    pr_step(h, 0);  // initial iterate: the sequential coarse sweep
+    *iterations = 0;
+    *converged = 1;
+    if (h->p == 1) return 0;
+    for (int k = 1; k <= max_iter; ++k) {
+      const auto [u, sc] = pr_step(h, 1);
+      if (history) history[k - 1] = u;
+      *iterations = k;
+      if (u <= tol * std::max(sc, 1e-300)) return 0;  // src/parareal.cpp:104-110
+    }
+    *converged = 0;
+    return 0;
+  } catch (const Fail& f_) {
+    return set_err(err, errlen, f_.code, f_.msg);
+  }
+}
+
+int psg_pr_apply(psg_pr* h, int which, int i, const double* y, double* out, char* err, size_t errlen) {
+  DeviceGuard dg(h->device);
+  try {
+    if (i < 1 || i > h->p) throw Fail{PSG_E_INDEX_OUT_OF_RANGE, "window index"};
+    CUDA_TRY(cudaMemcpy(h->tmp.p, y, sizeof(double) * h->m, cudaMemcpyHostToDevice));
+    pr_apply_kernel<<<1, 32, sizeof(PrSmem)>>>((which ? h->G : h->F).view(), h->m, i, h->tmp.p, h->tmp.p + h->m);
+    LAUNCH_CHECK();
+    CUDA_TRY(cudaMemcpy(out, h->tmp.p + h->m, sizeof(double) * h->m, cudaMemcpyDeviceToHost));
+    return 0;
+  } catch (const Fail& f_) {
+    return set_err(err, errlen, f_.code, f_.msg);
+  }
+}
+
+void psg_pr_release(psg_pr* h) {
+  if (!h) return;
+  DeviceGuard dg(h->device);
+  cudaDeviceSynchronize();
+  delete h;
 }
 
 namespace {
