@@ -70,21 +70,36 @@ __device__ __forceinline__ void pr_stage(double* Tt, const double* T, int m) {
   __syncwarp();
 }
 
-// S steps of y <- T y + c_n on the warp's state ys (shared, m doubles).
+// S steps of y <- T y + c_n on the warp's state ys (shared, m doubles); c may
+// be null (no forcing).  Four partial sums per row keep the FMA chains short.
 __device__ __forceinline__ void pr_steps(double* ys, const double* Tt, const double* c, int m, int S) {
   const int lane = threadIdx.x & 31;
+  const bool r0 = lane < m, r1 = lane + 32 < m;
   for (int n = 0; n < S; ++n) {
-    const double* cn = c + (long)n * m;
-    double a0 = lane < m ? cn[lane] : 0.0, a1 = lane + 32 < m ? cn[lane + 32] : 0.0;
-    double t0 = 0.0, t1 = 0.0;
-    for (int j = 0; j < m; ++j) {
+    double a0 = 0.0, a1 = 0.0;
+    if (c) {
+      const double* cn = c + (long)n * m;
+      a0 = r0 ? cn[lane] : 0.0;
+      a1 = r1 ? cn[lane + 32] : 0.0;
+    }
+    double s0[4] = {0.0, 0.0, 0.0, 0.0}, s1[4] = {0.0, 0.0, 0.0, 0.0};
+    int j = 0;
+    for (; j + 4 <= m; j += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double yj = ys[j + u];
+        if (r0) s0[u] = __fma_rn(Tt[(j + u) * m + lane], yj, s0[u]);
+        if (r1) s1[u] = __fma_rn(Tt[(j + u) * m + lane + 32], yj, s1[u]);
+      }
+    }
+    for (; j < m; ++j) {
       const double yj = ys[j];
-      if (lane < m) t0 = __fma_rn(Tt[j * m + lane], yj, t0);
-      if (lane + 32 < m) t1 = __fma_rn(Tt[j * m + lane + 32], yj, t1);
+      if (r0) s0[0] = __fma_rn(Tt[j * m + lane], yj, s0[0]);
+      if (r1) s1[0] = __fma_rn(Tt[j * m + lane + 32], yj, s1[0]);
     }
     __syncwarp();
-    if (lane < m) ys[lane] = __dadd_rn(t0, a0);
-    if (lane + 32 < m) ys[lane + 32] = __dadd_rn(t1, a1);
+    if (r0) ys[lane] = __dadd_rn(__dadd_rn(s0[0], s0[1]) + __dadd_rn(s0[2], s0[3]), a0);
+    if (r1) ys[lane + 32] = __dadd_rn(__dadd_rn(s1[0], s1[1]) + __dadd_rn(s1[2], s1[3]), a1);
     __syncwarp();
   }
 }
@@ -106,7 +121,7 @@ __global__ void __launch_bounds__(32) pr_fine_kernel(PrArgs a) {
     pr_stage(S.Tt, P.T + (long)P.mat[i - 1] * m * m, m);
     for (int r = lane; r < m; r += 32) S.y[r] = a.old_inits[(long)(i - 1) * m + r];
     __syncwarp();
-    pr_steps(S.y, S.Tt, P.c + (long)(i - 1) * P.S * m, m, P.S);
+    pr_steps(S.y, S.Tt, P.c ? P.c + (long)(i - 1) * P.S * m : nullptr, m, P.S);
     for (int r = lane; r < m; r += 32) out[(long)(i - 1) * m + r] = S.y[r];
     __syncwarp();
   }
@@ -132,7 +147,7 @@ __global__ void __launch_bounds__(32) pr_sweep_kernel(PrArgs a) {
       pr_stage(S.Tt, a.G.T + (long)mi * m * m, m);
       staged = mi;
     }
-    pr_steps(S.y, S.Tt, a.G.c + (long)(i - 1) * a.G.S * m, m, a.G.S);  // gnew = G_i y_new[i-1]
+    pr_steps(S.y, S.Tt, a.G.c ? a.G.c + (long)(i - 1) * a.G.S * m : nullptr, m, a.G.S);  // gnew = G_i y_new[i-1]
     for (int r = lane; r < m; r += 32) {
       double v = S.y[r];
       if (a.with_fine)  // F + (gnew - gold) (src/parareal.cpp:81-86)
@@ -163,7 +178,7 @@ __global__ void __launch_bounds__(32) pr_apply_kernel(PrStepper P, int m, int i,
   pr_stage(S.Tt, P.T + (long)P.mat[i - 1] * m * m, m);
   for (int r = lane; r < m; r += 32) S.y[r] = y[r];
   __syncwarp();
-  pr_steps(S.y, S.Tt, P.c + (long)(i - 1) * P.S * m, m, P.S);
+  pr_steps(S.y, S.Tt, P.c ? P.c + (long)(i - 1) * P.S * m : nullptr, m, P.S);
   for (int r = lane; r < m; r += 32) out[r] = S.y[r];
 }
 

@@ -2285,7 +2285,7 @@ struct psg_pr {
     int S = 0;
     DevBuf<double> T, Minv, rhs, c;
     DevBuf<int> mat;
-    PrStepper view() const { return PrStepper{S, T.p, Minv.p, rhs.p, c.p, mat.p}; }
+    PrStepper view() const { return PrStepper{S, T.p, Minv.p, rhs.n ? rhs.p : nullptr, rhs.n ? c.p : nullptr, mat.p}; }
   } F, G;
   DevBuf<double> y0, in0, in1, fine, gold, norms, tmp;
   int cur = 0;  // which of in0 / in1 holds the current inits
@@ -2302,11 +2302,12 @@ void pr_side(psg_pr::Side& sd, int m, int p, int S, int nmat, const double* T, c
   sd.T.alloc((size_t)nmat * m * m);
   sd.Minv.alloc((size_t)nmat * m * m);
   sd.mat.alloc(p);
-  sd.rhs.alloc((size_t)p * S * m);
-  sd.c.alloc((size_t)p * S * m);
   CUDA_TRY(cudaMemcpy(sd.T.p, T, sizeof(double) * nmat * m * m, cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(sd.Minv.p, M, sizeof(double) * nmat * m * m, cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(sd.mat.p, mat, sizeof(int) * p, cudaMemcpyHostToDevice));
+  if (!rhs) return;  // no forcing: c = 0 (PrStepper::c null)
+  sd.rhs.alloc((size_t)p * S * m);
+  sd.c.alloc((size_t)p * S * m);
   CUDA_TRY(cudaMemcpy(sd.rhs.p, rhs, sizeof(double) * (size_t)p * S * m, cudaMemcpyHostToDevice));
   const long tasks = (long)p * S;
   pr_prep_kernel<<<(unsigned)((tasks + 7) / 8), 256>>>(m, p, S, sd.Minv.p, sd.mat.p, sd.rhs.p, sd.c.p);

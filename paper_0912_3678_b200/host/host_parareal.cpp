@@ -25,7 +25,7 @@ struct StepperHost {
   int S = 1;
   std::vector<double> T, M;  // distinct m x m matrices
   std::vector<int> mat;      // per window
-  std::vector<double> rhs;   // p x S x m
+  std::vector<double> rhs;   // p x S x m (empty: no forcing)
   int nmat() const { return int(mat.empty() ? 0 : *std::max_element(mat.begin(), mat.end()) + 1); }
 };
 
@@ -45,7 +45,7 @@ StepperHost discrete_stepper(const IVProblem& prob, const TimeGrid& grid, OdeMet
   StepperHost st;
   st.S = steps;
   st.mat.resize(p);
-  st.rhs.assign(std::size_t(p) * steps * m, 0.0);
+  if (prob.g) st.rhs.assign(std::size_t(p) * steps * m, 0.0);
   std::map<std::uint64_t, int> by_h;
   std::vector<int> first;  // a window of each distinct step size
   for (int i = 1; i <= p; ++i) {
@@ -60,7 +60,7 @@ StepperHost discrete_stepper(const IVProblem& prob, const TimeGrid& grid, OdeMet
   std::vector<std::string> errs(p);
   std::vector<int> codes(p, -1);
 #pragma omp parallel for schedule(static)
-  for (int i = 1; i <= p; ++i) {
+  for (int i = 1; i <= (prob.g ? p : 0); ++i) {
     try {
       const TimeGrid local = coarse_mesh({grid.tau[i - 1], grid.tau[i]}, steps);
       const WindowSystem W = discretize_window(prob, local, 1, method);
@@ -93,8 +93,8 @@ std::unique_ptr<PrHandle> make_pr(const IVProblem& prob, const StepperHost& F, c
   auto H = std::make_unique<PrHandle>();
   char err[256] = {0};
   const int rc = psg_pr_create(prob.dim(), p, prob.y0.data(), F.S, F.nmat(), F.T.data(), F.M.data(), F.mat.data(),
-                               F.rhs.data(), G.S, G.nmat(), G.T.data(), G.M.data(), G.mat.data(), G.rhs.data(),
-                               &H->h, err, sizeof err);
+                               F.rhs.empty() ? nullptr : F.rhs.data(), G.S, G.nmat(), G.T.data(), G.M.data(),
+                               G.mat.data(), G.rhs.empty() ? nullptr : G.rhs.data(), &H->h, err, sizeof err);
   if (rc) fail(Errc(rc - 1), err);
   return H;
 }
@@ -123,8 +123,8 @@ StepperHost stepper_of(const Propagator& P, const IVProblem& prob, const TimeGri
     }
     st.mat[i - 1] = it->second;
   }
-  st.rhs.assign(std::size_t(p) * m, 0.0);
   if (prob.g) {
+    st.rhs.assign(std::size_t(p) * m, 0.0);
     const StepperHost D = discrete_stepper(prob, grid, P.method, P.steps);
     auto H = make_pr(prob, D, D, p);
     char err[256] = {0};
