@@ -9,6 +9,9 @@
 //   psg verify   -m A.mat -f F.vec|ones --p P [--strategy lu] [--tol T]
 //   psg plan     -m A.mat --p P
 //   psg bench    --config C --size Z --p P [--reps R] [--seed X]
+//   psg ode      --problem heat|decay --m M [--lambda L] --p P --N N [--method ie|trap] [--T T] [-o Y.traj]
+//   psg parareal --problem heat|decay --m M --p P --N N [--method ie|trap] [--coarse ie|trap|expm]
+//                [--coarse-steps C] [--tol T] [--max-iter K] [-o H.csv]
 //
 // Exit codes: 0 ok, 1 usage / parse / I/O error, 2 numeric failure; errors
 // are reported on stderr as `ERROR <code> <detail>`.  Benchmark output is CSV
@@ -28,6 +31,8 @@
 
 #include "parsol/errors.hpp"
 #include "parsol/io.hpp"
+#include "parsol/odeparallel.hpp"
+#include "parsol/parareal.hpp"
 #include "parsol/parfact.hpp"
 #include "parsol/partition.hpp"
 #include "parsol/seqref.hpp"
@@ -54,7 +59,7 @@ struct Args {
 };
 
 Args parse_args(int argc, char** argv) {
-  if (argc < 2) fail(Errc::InvalidParameter, "usage: psg <generate|solve|verify|plan|bench> [options]");
+  if (argc < 2) fail(Errc::InvalidParameter, "usage: psg <generate|solve|verify|plan|bench|ode|parareal> [options]");
   Args a;
   a.cmd = argv[1];
   for (int i = 2; i < argc; ++i) {
@@ -238,6 +243,57 @@ int cmd_bench(const Args& a) {
   return 0;
 }
 
+// the bundled problems (reference parareal.hpp: heat_problem, decay_problem)
+IVProblem problem_of(const Args& a) {
+  const std::string pr = a.str("problem", "heat");
+  const double t0 = a.real("t0", 0.0);
+  if (pr == "heat") return heat_problem((int)a.num("m", 32), t0, a.real("T", 0.1));
+  if (pr == "decay") return decay_problem(a.real("lambda", -1.0), t0, a.real("T", 1.0));
+  fail(Errc::InvalidParameter, "unknown problem '" + pr + "' (heat, decay)");
+}
+
+int cmd_ode(const Args& a) {
+  const IVProblem prob = problem_of(a);
+  const int p = (int)std::stol(a.need("p")), N = (int)std::stol(a.need("N"));
+  const OdeMethod meth = method_from_name(a.str("method", "ie"));
+  const TimeGrid grid = coarse_mesh(prob.t0, prob.T, p, N);
+  SolveStats st;
+  const auto t0 = std::chrono::steady_clock::now();
+  const Trajectory tr = solve_ivp_parallel(prob, grid, meth, &st);
+  const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (a.has("out")) write_file(a.str("out"), write_trajectory(tr.flat, tr.m, tr.p, tr.N));
+  const Vector e = tr.endpoint();
+  std::printf("m %d p %d N %d method %s seconds %.6f certificate %.3e\n", tr.m, p, N, method_name(meth), secs,
+              st.certificate);
+  std::printf("endpoint[0] %s (%.15e)\n", format_hex(e[0]).c_str(), e[0]);
+  return 0;
+}
+
+int cmd_parareal(const Args& a) {
+  const IVProblem prob = problem_of(a);
+  const int p = (int)std::stol(a.need("p")), N = (int)std::stol(a.need("N"));
+  Propagator fine;
+  fine.kind = PropagatorKind::FineDiscrete;
+  fine.method = method_from_name(a.str("method", "ie"));
+  fine.steps = N;
+  Propagator coarse;
+  const std::string cs = a.str("coarse", "ie");
+  coarse.kind = cs == "expm" ? PropagatorKind::MatrixExponential : PropagatorKind::CoarseDiscrete;
+  coarse.method = cs == "expm" ? OdeMethod::ImplicitEuler : method_from_name(cs);
+  coarse.steps = (int)a.num("coarse-steps", 1);
+  const TimeGrid grid = coarse_mesh(prob.t0, prob.T, p, N);
+  const auto t0 = std::chrono::steady_clock::now();
+  const PararealResult r = parareal_solve(prob, grid, fine, coarse, a.real("tol", 1e-8), (int)a.num("max-iter", -1));
+  const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  std::string csv = "iter,update_norm\n";
+  for (std::size_t k = 0; k < r.history.size(); ++k) csv += std::to_string(k + 1) + "," + format_hex(r.history[k]) + "\n";
+  if (a.has("out")) write_file(a.str("out"), csv);
+  else std::fputs(csv.c_str(), stdout);
+  std::printf("iterations %d converged %d seconds %.6f\n", r.iterations, r.converged ? 1 : 0, secs);
+  if (!r.converged) fail(Errc::NotConverged, "no convergence in " + std::to_string(r.iterations) + " iterations");
+  return 0;
+}
+
 bool numeric(Errc c) {
   switch (c) {
     case Errc::ZeroPivot:
@@ -261,6 +317,8 @@ int main(int argc, char** argv) {
     if (a.cmd == "verify") return cmd_solve(a, true);
     if (a.cmd == "plan") return cmd_plan(a);
     if (a.cmd == "bench") return cmd_bench(a);
+    if (a.cmd == "ode") return cmd_ode(a);
+    if (a.cmd == "parareal") return cmd_parareal(a);
     fail(Errc::InvalidParameter, "unknown command '" + a.cmd + "'");
   } catch (const Error& e) {
     std::fprintf(stderr, "ERROR %s %s\n", errc_name(e.code()), e.detail().c_str());

@@ -156,3 +156,55 @@ def test_numeric_failure_exit_code(psg_bin, tmp_path, cuda):
     res = run("solve", "-m", tmp_path / "z.mat", "-f", "ones", "--p", 2)
     assert res.returncode == 2, res.stdout + res.stderr
     assert res.stderr.startswith("ERROR ")
+
+
+def _traj(path):
+    lines = [t for t in path.read_text().split("\n") if t and not t.startswith("#")]
+    head = lines[0].split()
+    assert head[:2] == ["TRAJ", "1"]
+    m, p, N = (int(v) for v in head[2:5])
+    vals = np.array([float.fromhex(t) for t in lines[1:]])
+    return vals.reshape(p * N + 1, m)
+
+
+@pytest.mark.gpu
+def test_ode_and_parareal_commands(psg_bin, tmp_path, cuda):
+    """`ode` writes a TRAJ file equal to the reference's trajectory; `parareal`
+    prints the `iter,update_norm` CSV of the reference's iteration, exit 2 on
+    non-convergence (SPEC cli)."""
+    import ctypes as C
+    m, p, N = 8, 4, 25
+    res = run("ode", "--problem", "heat", "--m", m, "--p", p, "--N", N, "--method", "trap", "-o", tmp_path / "y.traj")
+    assert res.returncode == 0, res.stderr
+    Y = _traj(tmp_path / "y.traj")
+    inv = float(m + 1) ** 2
+    L = np.ascontiguousarray(np.diag(-2 * inv * np.ones(m)) + np.diag(inv * np.ones(m - 1), 1) +
+                             np.diag(inv * np.ones(m - 1), -1))
+    y0 = np.sin(np.pi * np.arange(1, m + 1) / (m + 1))
+    want = np.zeros((p * N + 1) * m)
+    err = C.create_string_buffer(256)
+    G = C.CFUNCTYPE(None, C.c_double, C.POINTER(C.c_double), C.c_void_p)
+    rc = O.ref().ref_ode_solve(C.c_int(m), L.ctypes.data_as(C.c_void_p), y0.ctypes.data_as(C.c_void_p),
+                               C.c_double(0.0), C.c_double(0.1), C.c_int(p), C.c_int(N), C.c_int(1),
+                               C.cast(None, G), C.c_void_p(None), C.c_int(0), want.ctypes.data_as(C.c_void_p), err,
+                               C.c_size_t(256))
+    assert rc == 0, err.value
+    assert O.rel_err(Y.ravel(), want) <= 1e-12
+    res = run("parareal", "--problem", "heat", "--m", 16, "--p", 8, "--N", 50, "-o", tmp_path / "h.csv")
+    assert res.returncode == 0, res.stderr
+    rows = (tmp_path / "h.csv").read_text().strip().split("\n")
+    assert rows[0] == "iter,update_norm" and len(rows) > 2
+    it = int(res.stdout.split()[1])
+    assert it == len(rows) - 1
+    res = run("parareal", "--problem", "heat", "--m", 16, "--p", 8, "--N", 50, "--tol", "1e-15", "--max-iter", 1)
+    assert res.returncode == 2 and res.stderr.startswith("ERROR NotConverged")
+
+
+@pytest.mark.gpu
+def test_pivoting_strategy_command(psg_bin, tmp_path, cuda):
+    res = run("generate", "--kind", "circulant", "--n", 200, "--s", 1, "--r", 1, "--seed", 5, "--dominance", 1,
+              "-o", tmp_path / "c.mat")
+    assert res.returncode == 0, res.stderr
+    for st in ("lupivot", "qr"):
+        res = run("verify", "-m", tmp_path / "c.mat", "-f", "ones", "--p", 4, "--strategy", st)
+        assert res.returncode == 0, res.stdout + res.stderr
