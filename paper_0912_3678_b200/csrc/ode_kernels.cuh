@@ -16,36 +16,34 @@
 // with w = k / N for k < p N (identity step otherwise); f = [y0 | g_1 .. g_pN]
 // padded per block.  win = p x (diag, sub), each m x m row-major.
 template <int MB>
-__global__ void ode_assemble_kernel(int m, long long steps, long long nsteps, int N, const double* __restrict__ win,
-                                    const double* __restrict__ g, double* __restrict__ data, double* __restrict__ f) {
-  constexpr int BW = 2 * MB * MB;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long total = (long long)MB * MB + nsteps * BW;
-  for (long long t = t0; t < total; t += stride) {
-    double v;
-    if (t < MB * MB) {
-      v = (t / MB == t % MB) ? 1.0 : 0.0;
-    } else {
-      const long long u = t - MB * MB;
-      const long long k = u / BW;
-      const int e = int(u - k * BW);
-      const int i = e / (2 * MB), jj = e - i * 2 * MB;
-      const bool left = jj < MB;
-      const int j = left ? jj : jj - MB;
-      if (k < steps && i < m && j < m) {
-        const double* W = win + (k / N) * 2LL * m * m;
-        v = left ? -W[m * m + i * m + j] : W[i * m + j];
-      } else {
-        v = (i == j) ? (left ? -1.0 : 1.0) : 0.0;
-      }
+__global__ void __launch_bounds__(256) ode_assemble_kernel(int m, long long steps, long long nsteps, int N,
+                                                            const double* __restrict__ win,
+                                                            const double* __restrict__ g, double* __restrict__ data,
+                                                            double* __restrict__ f) {
+  constexpr int BW = 2 * MB * MB;     // doubles per block row (a power of two)
+  constexpr int RPB = 256 / BW > 0 ? 256 / BW : 1;  // block rows per 256 threads
+  const int e = threadIdx.x % BW, rl = threadIdx.x / BW;
+  const int i = e / (2 * MB), jj = e % (2 * MB);
+  const bool left = jj < MB;
+  const int j = left ? jj : jj - MB;
+  const bool real = i < m && j < m;
+  const double pad = (i == j) ? (left ? -1.0 : 1.0) : 0.0;
+  if (blockIdx.x == 0 && threadIdx.x < MB * MB) data[threadIdx.x] = (threadIdx.x / MB == threadIdx.x % MB) ? 1.0 : 0.0;
+  // block row k + 1 of the BABD (k = step index): one 32-bit window lookup per element
+  for (long long k = (long long)blockIdx.x * RPB + rl; k < nsteps; k += (long long)gridDim.x * RPB) {
+    double v = pad;
+    if (k < steps && real) {
+      const int w = (int)((unsigned)k / (unsigned)N);
+      const double* W = win + (long long)w * 2 * m * m;
+      v = left ? -W[m * m + i * m + j] : W[i * m + j];
     }
-    data[t] = v;
+    data[MB * MB + k * BW + e] = v;
   }
   const long long nf = (nsteps + 1) * MB;
-  for (long long t = t0; t < nf; t += stride) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < nf; t += stride) {
     const long long b = t / MB;
-    const int q = int(t - b * MB);
+    const int q = (int)(t % MB);
     f[t] = (b <= steps && q < m) ? g[b * m + q] : 0.0;
   }
 }

@@ -152,6 +152,40 @@ __device__ __forceinline__ void pv_entering(const PvGeo& G, int t, Fn&& fn) {
     for (int u = 0; u < G.k1; ++u) fn(2, u);
 }
 
+// Values of an entering row for the window [t, t + 64): ring slots lane and
+// lane + 32 (v0, v1) and spike column lane (v2).  kind 0 / 1 / 2: top
+// separator / body (or reduced) row / bottom separator.
+template <int MODE>
+__device__ __forceinline__ void pv_row_vals(const PivArgs& g, const GPart& P, const PvGeo& G, int kind, int idx,
+                                            int t, double& v0, double& v1, double& v2) {
+  const int lane = threadIdx.x;
+  for (int h = 0; h < 2; ++h) {
+    const int q = lane + 32 * h;
+    const int c = t + ((q - t) & 63);  // column held by ring slot q in the window [t, t + 64)
+    double v = 0.0;
+    if (c < G.ring_end) {
+      if (MODE == 1) {
+        if (c >= idx - g.w && c <= idx + g.w) v = g.rband[(long)idx * (2 * g.w + 1) + (c - idx + g.w)];
+      } else if (kind == 1) {
+        if (c >= idx - G.es && c <= idx + G.er) v = sm_at(g.A, (long)P.b + idx, (long)P.b + c);
+      } else {
+        v = sm_at(g.A, kind == 0 ? (long)P.ls + idx : (long)P.rs + idx, (long)P.b + c);
+      }
+    }
+    (h == 0 ? v0 : v1) = v;
+  }
+  double v = 0.0;
+  if (MODE == 1) {
+    if (lane < g.kb) v = g.rborder[(long)idx * g.kb + lane];
+  } else if (kind == 1) {
+    if (lane < G.k0) v = sm_at(g.A, (long)P.b + idx, (long)P.ls + lane);
+    else if (lane < G.k0 + G.k1) v = sm_at(g.A, (long)P.b + idx, (long)P.rs + lane - G.k0);
+  } else if (kind == 2) {  // right separator diagonal a_right; top x right-separator is zero in the frame
+    if (lane >= G.k0 && lane < G.k0 + G.k1) v = sm_at(g.A, (long)P.rs + idx, (long)P.rs + lane - G.k0);
+  }
+  v2 = v;
+}
+
 // ---------------------------------------------------------------------------
 // the factor engine
 // ---------------------------------------------------------------------------
@@ -208,35 +242,25 @@ __global__ void __launch_bounds__(32) piv_factor_kernel(PivArgs g) {
   int nact = 0, ndef = 0;
   bool failed = false;
 
+  // entering body / reduced rows of steps t + 1 and t + 2, prefetched into registers
+  double pa0 = 0.0, pa1 = 0.0, pa2 = 0.0, pb0 = 0.0, pb1 = 0.0, pb2 = 0.0;
+  if (1 + G.es < G.L) pv_row_vals<MODE>(g, P, G, 1, 1 + G.es, 1, pa0, pa1, pa2);
+  if (2 + G.es < G.L) pv_row_vals<MODE>(g, P, G, 1, 2 + G.es, 2, pb0, pb1, pb2);
   for (int t = 0; t < G.L && !failed; ++t) {
-    // ---- rows entering at this step
+    // ---- rows entering at this step (the order pv_entering replays)
     pv_entering(G, t, [&](int kind, int idx) {
       const int sl = pv_alloc(S.fst, top);
-      for (int h = 0; h < 2; ++h) {
-        const int q = lane + 32 * h;
-        const int c = t + ((q - t) & 63);  // column held by ring slot q in the window [t, t + 64)
-        double v = 0.0;
-        if (c < G.ring_end) {
-          if (MODE == 1) {
-            if (c >= idx - g.w && c <= idx + g.w) v = g.rband[(long)idx * (2 * g.w + 1) + (c - idx + g.w)];
-          } else if (kind == 1) {
-            if (c >= idx - G.es && c <= idx + G.er) v = sm_at(g.A, (long)P.b + idx, (long)P.b + c);
-          } else {
-            v = sm_at(g.A, kind == 0 ? (long)P.ls + idx : (long)P.rs + idx, (long)P.b + c);
-          }
-        }
-        S.W[sl][q] = v;
+      double v0, v1, v2;
+      if (kind == 1 && t >= 1) {
+        v0 = pa0;
+        v1 = pa1;
+        v2 = pa2;
+      } else {
+        pv_row_vals<MODE>(g, P, G, kind, idx, t, v0, v1, v2);
       }
-      double v = 0.0;
-      if (MODE == 1) {
-        if (lane < g.kb) v = g.rborder[(long)idx * g.kb + lane];
-      } else if (kind == 1) {
-        if (lane < G.k0) v = sm_at(g.A, (long)P.b + idx, (long)P.ls + lane);
-        else if (lane < G.k0 + G.k1) v = sm_at(g.A, (long)P.b + idx, (long)P.rs + lane - G.k0);
-      } else if (kind == 2) {  // right separator diagonal a_right; top x right-separator is zero in the frame
-        if (lane >= G.k0 && lane < G.k0 + G.k1) v = sm_at(g.A, (long)P.rs + idx, (long)P.rs + lane - G.k0);
-      }
-      S.W[sl][kPvRing + lane] = v;
+      S.W[sl][lane] = v0;
+      S.W[sl][lane + 32] = v1;
+      S.W[sl][kPvRing + lane] = v2;
       if (lane == 0) {
         if (kind == 1) {
           S.st[sl] = 0;
@@ -250,6 +274,12 @@ __global__ void __launch_bounds__(32) piv_factor_kernel(PivArgs g) {
       if (kind == 1) ++nact;
       __syncwarp();
     });
+    if (t >= 1) {  // pa held step t's row: shift, fetch step t + 2's
+      pa0 = pb0;
+      pa1 = pb1;
+      pa2 = pb2;
+      if (t + 2 + G.es < G.L) pv_row_vals<MODE>(g, P, G, 1, t + 2 + G.es, t + 2, pb0, pb1, pb2);
+    }
 
     const int c = t;
     const int pc = c < G.ring_end ? (c & 63) : kPvRing + (c - G.ring_end);
@@ -492,6 +522,50 @@ __global__ void __launch_bounds__(32) piv_factor_kernel(PivArgs g) {
   }
 }
 
+// One step's records, loaded a step ahead (they do not depend on the data).
+struct PvStepRec {
+  int4 mt;
+  int s0, s1;        // target slots of entries lane, lane + 32
+  double m0, m1;     // their multipliers
+  int a0;            // Qr: reflector slot / entry of lane
+  double av0, tau;
+};
+
+__device__ __forceinline__ PvStepRec pv_load_rec(const PivRec& R, long ri) {
+  const int lane = threadIdx.x;
+  PvStepRec r;
+  r.mt = R.meta[ri];
+  r.s0 = lane < R.NT ? R.tslot[ri * R.NT + lane] : 0;
+  r.m0 = lane < R.NT ? R.mu[ri * R.NT + lane] : 0.0;
+  r.s1 = lane + 32 < R.NT ? R.tslot[ri * R.NT + lane + 32] : 0;
+  r.m1 = lane + 32 < R.NT ? R.mu[ri * R.NT + lane + 32] : 0.0;
+  r.a0 = lane < R.NA ? R.aslot[ri * R.NA + lane] : 0;
+  r.av0 = lane < R.NA ? R.av[ri * R.NA + lane] : 0.0;
+  r.tau = R.tau[ri];
+  return r;
+}
+
+// Apply one recorded elimination step to the slot values (condense replay).
+__device__ __forceinline__ void pv_apply_rec(double* val, const PvStepRec& r, double* ghat_out, double* av) {
+  const int lane = threadIdx.x;
+  if (r.mt.z > 0) {  // Qr reflector: s = tau * sum_u v_u val[rows_u]
+    if (lane < r.mt.z) av[lane] = r.av0;
+    __syncwarp();
+    double part = lane < r.mt.z ? __dmul_rn(r.av0, val[r.a0]) : 0.0;
+    double sum = 0.0;
+    for (int u = 0; u < r.mt.z; ++u) sum = __dadd_rn(sum, __shfl_sync(0xffffffffu, part, u));
+    sum = __dmul_rn(sum, r.tau);
+    __syncwarp();
+    if (lane < r.mt.z) val[r.a0] = pv_sub(val[r.a0], sum, r.av0);
+    __syncwarp();
+  }
+  const double pv = val[r.mt.x];
+  if (lane == 0 && ghat_out) *ghat_out = pv;
+  if (lane < r.mt.y) val[r.s0] = pv_sub(val[r.s0], r.m0, pv);
+  if (lane + 32 < r.mt.y) val[r.s1] = pv_sub(val[r.s1], r.m1, pv);
+  __syncwarp();
+}
+
 // ---------------------------------------------------------------------------
 // condense replay (phase 1) for the bodies: ghat per step, kept rhs per body
 // ---------------------------------------------------------------------------
@@ -510,50 +584,54 @@ __global__ void __launch_bounds__(32) piv_condense_kernel(PivArgs g) {
   int top;
   pv_init_stack(S.fst, top);
   int nd = 0;
+  PvStepRec cur = pv_load_rec(g.rec, P.b), nxt = cur;
+  if (G.L > 1) nxt = pv_load_rec(g.rec, (long)P.b + 1);
+  double fin = (1 + G.es < G.L) ? g.f[(long)P.b + 1 + G.es] : 0.0;  // entering rhs of step t + 1
   for (int t = 0; t < G.L; ++t) {
     pv_entering(G, t, [&](int kind, int idx) {
       const int sl = pv_alloc(S.fst, top);
       if (lane == 0) {
-        S.val[sl] = kind == 1 ? g.f[(long)P.b + idx] : 0.0;
+        S.val[sl] = kind == 1 ? (t >= 1 ? fin : g.f[(long)P.b + idx]) : 0.0;
         if (kind != 1) S.sep[kind == 0 ? idx : G.k0 + idx] = sl;
       }
       __syncwarp();
     });
-    const long ri = (long)P.b + t;
-    const int4 mt = g.rec.meta[ri];
-    if (mt.x < 0) {
-      if (lane == 0) S.def[nd] = mt.w;
+    fin = (t + 1 + G.es < G.L) ? g.f[(long)P.b + t + 1 + G.es] : 0.0;  // step t + 1's entering rhs
+    const PvStepRec r = cur;
+    cur = nxt;
+    if (t + 2 < G.L) nxt = pv_load_rec(g.rec, (long)P.b + t + 2);
+    if (r.mt.x < 0) {
+      if (lane == 0) S.def[nd] = r.mt.w;
       ++nd;
       __syncwarp();
       continue;
     }
-    if (mt.z > 0) {  // Qr reflector
-      const double tau = g.rec.tau[ri];
-      if (lane < mt.z) S.av[lane] = g.rec.av[ri * g.rec.NA + lane];
-      __syncwarp();
-      double s = 0.0;
-      for (int u = 0; u < mt.z; ++u) s = __dadd_rn(s, __dmul_rn(S.av[u], S.val[g.rec.aslot[ri * g.rec.NA + u]]));
-      s = __dmul_rn(s, tau);
-      __syncwarp();
-      if (lane < mt.z) {
-        const int sl = g.rec.aslot[ri * g.rec.NA + lane];
-        S.val[sl] = pv_sub(S.val[sl], s, S.av[lane]);
-      }
-      __syncwarp();
-    }
-    const double pv = S.val[mt.x];
-    if (lane == 0) g.ghat[ri] = pv;
-    for (int i = lane; i < mt.y; i += 32) {
-      const int sl = g.rec.tslot[ri * g.rec.NT + i];
-      S.val[sl] = pv_sub(S.val[sl], g.rec.mu[ri * g.rec.NT + i], pv);
-    }
-    pv_free(S.fst, top, mt.x);
+    pv_apply_rec(S.val, r, g.ghat + (long)P.b + t, S.av);
+    pv_free(S.fst, top, r.mt.x);
   }
   const int kd = G.k0 + nd + G.k1;
   for (int a = lane; a < kd; a += 32) {
     const int sl = a < G.k0 ? S.sep[a] : (a < G.k0 + nd ? S.def[a - G.k0] : S.sep[G.k0 + (a - G.k0 - nd)]);
     g.kr[(long)body * g.KD + a] = S.val[sl];
   }
+}
+
+// Back-substitution records of one step, loaded a step ahead.
+struct PvBackRec {
+  int4 mt;
+  double u0, u1, us, diag, gh;
+};
+
+__device__ __forceinline__ PvBackRec pv_load_back(const PivRec& R, const double* ghat, long ri) {
+  const int lane = threadIdx.x;
+  PvBackRec b;
+  b.mt = R.meta[ri];
+  b.u0 = lane + 1 < R.URW ? R.urow[ri * R.URW + lane + 1] : 0.0;
+  b.u1 = lane + 33 < R.URW ? R.urow[ri * R.URW + lane + 33] : 0.0;
+  b.us = lane < R.NS ? R.uspk[ri * R.NS + lane] : 0.0;
+  b.diag = R.urow[ri * R.URW];
+  b.gh = ghat[ri];
+  return b;
 }
 
 // ---------------------------------------------------------------------------
@@ -575,21 +653,24 @@ __global__ void __launch_bounds__(32) piv_backsolve_kernel(PivArgs g) {
   S.xr[lane] = 0.0;
   S.xr[lane + 32] = 0.0;
   __syncwarp();
-  const int URW = g.rec.URW, NS = g.rec.NS;
   int d = nd - 1;
+  PvBackRec cur = pv_load_back(g.rec, g.ghat, (long)P.b + L - 1), nxt = cur;
+  if (L > 1) nxt = pv_load_back(g.rec, g.ghat, (long)P.b + L - 2);
   for (int t = L - 1; t >= 0; --t) {
-    const long ri = (long)P.b + t;
-    const int4 mt = g.rec.meta[ri];
+    const PvBackRec r = cur;
+    cur = nxt;
+    if (t >= 2) nxt = pv_load_back(g.rec, g.ghat, (long)P.b + t - 2);
     double xv;
-    if (mt.x < 0) {
+    if (r.mt.x < 0) {
       xv = g.xk[ko + k0 + d];
       --d;
     } else {
       double acc = 0.0;
-      for (int j = lane + 1; j < URW && t + j < L; j += 32) acc = __fma_rn(g.rec.urow[ri * URW + j], S.xr[(t + j) & 63], acc);
-      if (lane < NS) acc = __fma_rn(g.rec.uspk[ri * NS + lane], S.xs[lane], acc);
+      if (t + lane + 1 < L) acc = __fma_rn(r.u0, S.xr[(t + lane + 1) & 63], acc);
+      if (t + lane + 33 < L) acc = __fma_rn(r.u1, S.xr[(t + lane + 33) & 63], acc);
+      acc = __fma_rn(r.us, S.xs[lane], acc);
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      xv = (g.ghat[ri] - acc) / g.rec.urow[ri * URW];
+      xv = (r.gh - acc) / r.diag;
     }
     __syncwarp();
     if (lane == 0) {
@@ -661,37 +742,44 @@ __global__ void __launch_bounds__(32) piv_reduced_solve_kernel(PivArgs g) {
   G.tb = -1;
   int top;
   pv_init_stack(S.fst, top);
+  PvStepRec cur = pv_load_rec(g.rec, 0), nxt = cur;
+  if (G.L > 1) nxt = pv_load_rec(g.rec, 1);
+  double fin = (1 + G.es < G.L) ? g.rr[1 + G.es] : 0.0;
   for (int t = 0; t < G.L; ++t) {
     pv_entering(G, t, [&](int, int idx) {
       const int sl = pv_alloc(S.fst, top);
-      if (lane == 0) S.val[sl] = g.rr[idx];
+      if (lane == 0) S.val[sl] = t >= 1 ? fin : g.rr[idx];
       __syncwarp();
     });
-    const int4 mt = g.rec.meta[t];
-    const double pv = S.val[mt.x];
-    if (lane == 0) g.ghat[t] = pv;
-    for (int i = lane; i < mt.y; i += 32) {
-      const int sl = g.rec.tslot[(long)t * g.rec.NT + i];
-      S.val[sl] = pv_sub(S.val[sl], g.rec.mu[(long)t * g.rec.NT + i], pv);
-    }
-    pv_free(S.fst, top, mt.x);
+    fin = (t + 1 + G.es < G.L) ? g.rr[t + 1 + G.es] : 0.0;  // step t + 1's entering rhs
+    const PvStepRec r = cur;
+    cur = nxt;
+    if (t + 2 < G.L) nxt = pv_load_rec(g.rec, t + 2);
+    pv_apply_rec(S.val, r, g.ghat + t, S.av);
+    pv_free(S.fst, top, r.mt.x);
   }
   S.xr[lane] = 0.0;
   S.xr[lane + 32] = 0.0;
   S.xs[lane] = 0.0;
   __syncwarp();
-  const int URW = g.rec.URW, NS = g.rec.NS;
+  __threadfence_block();
+  PvBackRec bc = pv_load_back(g.rec, g.ghat, G.L - 1), bn = bc;
+  if (G.L > 1) bn = pv_load_back(g.rec, g.ghat, G.L - 2);
   for (int t = G.L - 1; t >= 0; --t) {
-    double acc = 0.0;
+    const PvBackRec r = bc;
+    bc = bn;
+    if (t >= 2) bn = pv_load_back(g.rec, g.ghat, t - 2);
     const bool spike = t >= G.ring_end;
-    if (!spike)
-      for (int j = lane + 1; j < URW && t + j < G.ring_end; j += 32)
-        acc = __fma_rn(g.rec.urow[(long)t * URW + j], S.xr[(t + j) & 63], acc);
     const int sown = spike ? t - G.ring_end : -1;
-    if (lane < NS && lane < g.kb && lane != sown) acc = __fma_rn(g.rec.uspk[(long)t * NS + lane], S.xs[lane], acc);
+    double acc = 0.0;
+    if (!spike) {
+      if (t + lane + 1 < G.ring_end) acc = __fma_rn(r.u0, S.xr[(t + lane + 1) & 63], acc);
+      if (t + lane + 33 < G.ring_end) acc = __fma_rn(r.u1, S.xr[(t + lane + 33) & 63], acc);
+    }
+    if (lane < g.kb && lane != sown) acc = __fma_rn(r.us, S.xs[lane], acc);
+    const double dgs = __shfl_sync(0xffffffffu, r.us, sown < 0 ? 0 : sown);
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    const double dg = spike ? g.rec.uspk[(long)t * NS + sown] : g.rec.urow[(long)t * URW];
-    const double xv = (g.ghat[t] - acc) / dg;
+    const double xv = (r.gh - acc) / (spike ? dgs : r.diag);
     __syncwarp();
     if (lane == 0) {
       if (spike) S.xs[sown] = xv;

@@ -109,21 +109,72 @@ struct PrSmem {
   double y[kPrMaxM];
 };
 
-// One warp per window i = 1 .. p-1: fine[i-1] = F_i old[i-1], gold[i-1] = G_i old[i-1].
-__global__ void __launch_bounds__(32) pr_fine_kernel(PrArgs a) {
-  extern __shared__ __align__(16) unsigned char pr_smem_raw[];
-  PrSmem& S = *reinterpret_cast<PrSmem*>(pr_smem_raw);
-  const int i = blockIdx.x + 1, lane = threadIdx.x, m = a.m;
+// Fine / old-coarse propagations, one CTA of NW warps per window i = 1..p-1:
+// fine[i-1] = F_i old[i-1], gold[i-1] = G_i old[i-1].  Warp w owns columns
+// [16w, 16w + 16) of T in registers (rows lane, lane + 32); partial row sums
+// meet in shared memory, so one step is a 16-deep FMA chain plus a reduction.
+struct PrFineSmem {
+  double part[4][kPrMaxM];
+  double y[kPrMaxM];
+};
+
+template <int NW>
+__global__ void __launch_bounds__(32 * NW) pr_fine_kernel(PrArgs a) {
+  __shared__ PrFineSmem S;
+  const int i = blockIdx.x + 1, m = a.m;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (i >= a.p) return;
+  const bool r0 = lane < m, r1 = lane + 32 < m;
   for (int h = 0; h < 2; ++h) {
     const PrStepper& P = h == 0 ? a.F : a.G;
     double* out = h == 0 ? a.fine : a.gold;
-    pr_stage(S.Tt, P.T + (long)P.mat[i - 1] * m * m, m);
-    for (int r = lane; r < m; r += 32) S.y[r] = a.old_inits[(long)(i - 1) * m + r];
-    __syncwarp();
-    pr_steps(S.y, S.Tt, P.c ? P.c + (long)(i - 1) * P.S * m : nullptr, m, P.S);
-    for (int r = lane; r < m; r += 32) out[(long)(i - 1) * m + r] = S.y[r];
-    __syncwarp();
+    const double* T = P.T + (long)P.mat[i - 1] * m * m;
+    double t0[16], t1[16];
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) {
+      const int j = 16 * w + jj;
+      t0[jj] = (r0 && j < m) ? T[lane * m + j] : 0.0;
+      t1[jj] = (r1 && j < m) ? T[(lane + 32) * m + j] : 0.0;
+    }
+    for (int r = threadIdx.x; r < m; r += 32 * NW) S.y[r] = a.old_inits[(long)(i - 1) * m + r];
+    __syncthreads();
+    const double* c = P.c ? P.c + (long)(i - 1) * P.S * m : nullptr;
+    for (int n = 0; n < P.S; ++n) {
+      double s0a = 0.0, s0b = 0.0, s1a = 0.0, s1b = 0.0;
+#pragma unroll
+      for (int jj = 0; jj < 16; jj += 2) {
+        const double ya = S.y[16 * w + jj], yb = S.y[16 * w + jj + 1];
+        s0a = __fma_rn(t0[jj], ya, s0a);
+        s0b = __fma_rn(t0[jj + 1], yb, s0b);
+        s1a = __fma_rn(t1[jj], ya, s1a);
+        s1b = __fma_rn(t1[jj + 1], yb, s1b);
+      }
+      const double cn0 = (c && w == 0 && r0) ? c[(long)n * m + lane] : 0.0;
+      const double cn1 = (c && w == 0 && r1) ? c[(long)n * m + lane + 32] : 0.0;
+      if (NW == 1) {
+        __syncwarp();
+        if (r0) S.y[lane] = __dadd_rn(__dadd_rn(s0a, s0b), cn0);
+        if (r1) S.y[lane + 32] = __dadd_rn(__dadd_rn(s1a, s1b), cn1);
+        __syncwarp();
+      } else {
+        S.part[w][lane] = __dadd_rn(s0a, s0b);
+        S.part[w][lane + 32] = __dadd_rn(s1a, s1b);
+        __syncthreads();
+        if (w == 0) {
+          double v0 = S.part[0][lane], v1 = S.part[0][lane + 32];
+#pragma unroll
+          for (int q = 1; q < NW; ++q) {
+            v0 = __dadd_rn(v0, S.part[q][lane]);
+            v1 = __dadd_rn(v1, S.part[q][lane + 32]);
+          }
+          if (r0) S.y[lane] = __dadd_rn(v0, cn0);
+          if (r1) S.y[lane + 32] = __dadd_rn(v1, cn1);
+        }
+        __syncthreads();
+      }
+    }
+    for (int r = threadIdx.x; r < m; r += 32 * NW) out[(long)(i - 1) * m + r] = S.y[r];
+    __syncthreads();
   }
 }
 
@@ -141,23 +192,40 @@ __global__ void __launch_bounds__(32) pr_sweep_kernel(PrArgs a) {
   }
   __syncwarp();
   int staged = -1;
+  // window i's fine / gold / old rows (lanes hold rows lane, lane + 32), loaded one window ahead
+  auto load3 = [&](int i, double* v) {
+    for (int h = 0; h < 2; ++h) {
+      const int r = lane + 32 * h;
+      const bool ok = i < a.p && r < m;
+      v[3 * h + 0] = ok && a.with_fine ? a.fine[(long)(i - 1) * m + r] : 0.0;
+      v[3 * h + 1] = ok && a.with_fine ? a.gold[(long)(i - 1) * m + r] : 0.0;
+      v[3 * h + 2] = ok ? a.old_inits[(long)i * m + r] : 0.0;
+    }
+  };
+  double cur[6], nxt[6];
+  load3(1, cur);
   for (int i = 1; i < a.p; ++i) {
+    load3(i + 1, nxt);
     const int mi = a.G.mat[i - 1];
     if (mi != staged) {
       pr_stage(S.Tt, a.G.T + (long)mi * m * m, m);
       staged = mi;
     }
     pr_steps(S.y, S.Tt, a.G.c ? a.G.c + (long)(i - 1) * a.G.S * m : nullptr, m, a.G.S);  // gnew = G_i y_new[i-1]
-    for (int r = lane; r < m; r += 32) {
+    for (int h = 0; h < 2; ++h) {
+      const int r = lane + 32 * h;
+      if (r >= m) continue;
       double v = S.y[r];
       if (a.with_fine)  // F + (gnew - gold) (src/parareal.cpp:81-86)
-        v = __dadd_rn(a.fine[(long)(i - 1) * m + r], __dsub_rn(v, a.gold[(long)(i - 1) * m + r]));
+        v = __dadd_rn(cur[3 * h], __dsub_rn(v, cur[3 * h + 1]));
       a.new_inits[(long)i * m + r] = v;
       S.y[r] = v;
-      upd = fmax(upd, fabs(__dsub_rn(v, a.old_inits[(long)i * m + r])));
+      upd = fmax(upd, fabs(__dsub_rn(v, cur[3 * h + 2])));
       scale = fmax(scale, fabs(v));
     }
     __syncwarp();
+#pragma unroll
+    for (int q = 0; q < 6; ++q) cur[q] = nxt[q];
   }
   for (int o = 16; o > 0; o >>= 1) {
     upd = fmax(upd, __shfl_xor_sync(0xffffffffu, upd, o));

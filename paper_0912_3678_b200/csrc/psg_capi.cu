@@ -2335,7 +2335,7 @@ void pr_smem_attr() {
   int dev = 0;
   cudaGetDevice(&dev);
   if (done[dev & 63]) return;
-  for (const void* k : {(const void*)pr_fine_kernel, (const void*)pr_sweep_kernel, (const void*)pr_apply_kernel})
+  for (const void* k : {(const void*)pr_sweep_kernel, (const void*)pr_apply_kernel})
     CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PrSmem)));
   done[dev & 63] = true;
 }
@@ -2344,7 +2344,11 @@ void pr_smem_attr() {
 std::pair<double, double> pr_step(psg_pr* h, int with_fine) {
   PrArgs a = pr_args(h, with_fine);
   if (with_fine && h->p > 1) {
-    pr_fine_kernel<<<h->p - 1, 32, sizeof(PrSmem)>>>(a);
+    const int nw = (h->m + 15) / 16;
+    if (nw <= 1) pr_fine_kernel<1><<<h->p - 1, 32>>>(a);
+    else if (nw == 2) pr_fine_kernel<2><<<h->p - 1, 64>>>(a);
+    else if (nw == 3) pr_fine_kernel<3><<<h->p - 1, 96>>>(a);
+    else pr_fine_kernel<4><<<h->p - 1, 128>>>(a);
     LAUNCH_CHECK();
   }
   pr_sweep_kernel<<<1, 32, sizeof(PrSmem)>>>(a);
