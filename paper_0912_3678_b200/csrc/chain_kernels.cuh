@@ -12,83 +12,37 @@
 //                                             src/localfact.cpp:182-225)
 //     phi_j = the chain from 0 with f         (condense, src/localfact.cpp:765-781)
 //
-//   factor  chain_tm_kernel: per block T_b and M_b = R_b^-1 (one block per
-//           lane, LU in registers), stored beside the data; Phi_j by a
-//           shared-memory tree product; the next level's rows [-Phi_j | I].
-//   solve   chain_pass_kernel<0>: phi_j (condense) -> the reduced system in
-//           x_sigma is again a BVP-layout BABD (S = -Phi, R = I, same Ba / Bb),
-//           solved by the same kernels level by level, the last level by one
-//           warp (chain_direct_kernel, partial pivoting on the BC system);
-//           chain_pass_kernel<1>: x through every chunk from x_sigma, plus
-//           the separator rows' residuals condensed to R^-1 r (the chain's
-//           end value differs from the affine map by rounding, ~8 eps |x| per
-//           step); one correction A d = r through the reduced levels and
-//           chain_pass_kernel<2>: x += the homogeneous chain of d, certifying
-//           the corrected separator rows (componentwise backward error),
-//           chain_bc_cert_kernel the BC row.
+//   factor  chain_tm_kernel (ONE launch): per block T_b and M_b = R_b^-1 (one
+//           block per lane, LU in registers), stored beside the data; Phi_j
+//           by a shared-memory tree product.  The reduced system in x_sigma is
+//           again a BVP-layout chain (maps Phi_j, R = I, same Ba / Bb); its
+//           chunk products Phi^(l) on every level are formed inside the same
+//           launch by the warp that completes each chunk, and the last one
+//           factors the top-level BC matrix (partial pivoting).
+//   solve   chain_solve_kernel<0/1/2> (three launches): condense + reduced
+//           levels up; top solve + x down + separator residuals up; the
+//           correction down + certificate (see the kernel comment below).
 //
-// Passes: MB lanes per chunk (lane i = row i of every block), 32 / MB chunks
-// per warp; shuffles are executed by the whole warp (shorter chunks idle).
 #pragma once
 
 #include "psg_common.cuh"
 
 namespace psg {
 
-// BVP-layout level: data = [Ba (MB*MB) | rows b = 1..nb-1: S_b | R_b (MB x 2MB, row-major)]
+// level 0: data = [Ba (MB*MB) | rows b = 1..nb-1: S_b | R_b (MB x 2MB, row-major)]
 struct ChainLevelArgs {
   const double* data;
   const double* corner;  // Bb (MB x MB)
   int nb;                // block rows
-  int P;                 // chunks
-  const int* cut;        // P + 1 separator blocks: cut[0] = 0 .. cut[P] = nb - 1
-  const double* f;       // rhs of this level (nb * MB)
-  double* x;             // solution of this level (final pass)
-  double* next_data;     // factor: next level's data ((P + 1) block rows)
-  double* next_f;        // condense: next level's rhs
-  const double* next_x;  // final: next level's solution (x at the separators)
-  double* corr_f;        // final (optional): condensed separator residuals R_sep^-1 r_sep -> next level rhs
-  double* tm;            // factor output / solve input: per block [T row i | M row i] (T = -R^-1 S, M = R^-1)
-  int accumulate;        // final: x += chain of corr_x with zero forcing (the correction pass)
-  const double* corr_x;  // accumulate: correction d at the separators (next_x keeps x_sep)
+  const double* f;       // rhs (nb * MB)
+  double* x;             // solution
+  double* tm;            // factor output / solve input: per block [T | M] (T = -R^-1 S, M = R^-1), row pairs interleaved (see the factor)
   DevStatus* status;
 };
 
 template <int MB>
 __device__ __forceinline__ double gshfl(double v, int src) {
   return __shfl_sync(0xffffffffu, v, src, MB);
-}
-
-// Solve R y = w in place on the row-per-lane layout (no pivoting, like the
-// reference's Lu strategy): r[] = row `i` of R, w[] = NR right-hand sides.
-template <int MB, int NR>
-__device__ __forceinline__ void lane_solve(double (&r)[MB], double (&w)[NR], int i) {
-#pragma unroll
-  for (int k = 0; k < MB; ++k) {
-    const double pk = gshfl<MB>(r[k], k);
-    const double l = r[k] * fast_rcp(pk);
-#pragma unroll
-    for (int c = k + 1; c < MB; ++c) {
-      const double rk = gshfl<MB>(r[c], k);
-      if (i > k) r[c] = fma(-l, rk, r[c]);
-    }
-#pragma unroll
-    for (int c = 0; c < NR; ++c) {
-      const double wk = gshfl<MB>(w[c], k);
-      if (i > k) w[c] = fma(-l, wk, w[c]);
-    }
-  }
-  // back substitution, row k broadcast once solved
-#pragma unroll
-  for (int k = MB - 1; k >= 0; --k) {
-    const double inv = fast_rcp(r[k]);
-#pragma unroll
-    for (int c = 0; c < NR; ++c) {
-      const double yk = gshfl<MB>(w[c] * inv, k);
-      if (i == k) w[c] = yk;
-      if (i < k) w[c] = fma(-r[k], yk, w[c]);
-    }
-  }
 }
 
 template <int MB>
@@ -101,7 +55,6 @@ __device__ __forceinline__ void load_row(const double* data, int b, int i, doubl
   }
 }
 
-// factor: Phi_j, written as next level row j+1 = [ -Phi_j | I ]; chunk 0 also copies Ba.
 __device__ __forceinline__ void cert_push(DevStatus* st, double num, double den) {
   double om = den > 0 ? num / den : num;
   if (!(om <= 1.0e308)) om = __longlong_as_double(0x7ff0000000000000ll);
@@ -125,8 +78,163 @@ struct ChainSmem {
   static constexpr int WARP = 32 * SLOT;  // doubles per warp
 };
 
+// ---------------------------------------------------------------------------
+// The reduced-system hierarchy.  Level 0 is the user's chain (N + 1 block
+// rows, P[0] = ceil(N / 16) chunks).  Level l >= 1 has nb_l = P[l-1] + 1
+// unknowns (x at the level-(l-1) chunk boundaries), block maps Phi^(l-1)
+// (R = I) and rhs F_l: F_l[0] = the BC rhs, F_l[j+1] = phi^(l-1)_j.  Level T,
+// the first with nb_T - 1 <= 16, is solved directly: the BC matrix
+// G = Ba + Bb Phi_total is factored (partial pivoting) by the factor kernel.
+// Every level is built by ONE launch: the warp / CTA that completes the last
+// input of a level-l chunk (arrival counters, self-resetting) goes on to
+// condense that chunk, so the upward sweep needs no further launches; the
+// downward sweep is done redundantly by every CTA of the next kernel along
+// its own path from the top (<= 16 steps per level).
+// ---------------------------------------------------------------------------
+constexpr int kChainMaxLev = 8;
+
+struct ChainTree {
+  int T;                          // top level (>= 1)
+  int P[kChainMaxLev];            // chunks of level l (maps Phi^(l)), l < T; P[T-1] = nb_T - 1 <= 16
+  double* phi[kChainMaxLev];      // Phi^(l): P[l] x MB x MB row-major
+  double* fl[kChainMaxLev + 1];   // F_l, l = 1..T (nb_l x MB)
+  double* cfl[kChainMaxLev + 1];  // correction rhs, l = 1..T
+  int* cnt;                       // arrival counters
+  int coff[kChainMaxLev + 1];     // level-l counters at cnt + coff[l] (l = 1..T-1), the top one at coff[T]
+  double* glu;                    // LU of G (MB x MB) followed by the MB pivot rows (as doubles)
+  double* x1;                     // final: x at the level-1 unknowns (level-0 separators)
+  double* xlev[2];                // down sweep (x, d): values at level min(2, T)
+  double* xtop[2];                // down sweep (x, d): values at the top unknowns
+};
+
+// warp-level arrival: true for the warp that completes the count (it then
+// sees every other arriver's writes)
+__device__ __forceinline__ bool warp_last_arrive(int* ctr, int expected, int lane) {
+  __threadfence();
+  __syncwarp();
+  int last = 0;
+  if (lane == 0) {
+    last = atomicAdd(ctr, 1) == expected - 1;
+    if (last) atomicExch(ctr, 0);  // reset for the next launch
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (last) __threadfence();
+  return last != 0;
+}
+
+// tree of products P = later * earlier over the kChainC0 slots of each of
+// `nch` chunks (T parts of the padded slots); the product lands in the
+// chunk's LAST slot.  One lane per (product, row): the result row overwrites
+// that row of the later factor, which only this lane reads; the earlier
+// factor is a previous round's result (read-only in this round).
 template <int MB>
-__global__ void __launch_bounds__(64) chain_tm_kernel(ChainLevelArgs g) {
+__device__ __forceinline__ void chain_tree16(double* sm, int nch, int lane) {
+  constexpr int SLOT = ChainSmem<MB>::SLOT, RW = 2 * MB;
+#pragma unroll 1
+  for (int h = 1; h < kChainC0; h <<= 1) {
+    const int pairs = kChainC0 / (2 * h);  // per chunk
+    const int tasks = nch * pairs * MB;
+    for (int task = lane; task < tasks; task += 32) {
+      const int i = task % MB, pk = task / MB, c = pk / pairs, k = pk % pairs;
+      const double* E = sm + (c * kChainC0 + 2 * k * h + h - 1) * SLOT;
+      double* L = sm + (c * kChainC0 + 2 * k * h + 2 * h - 1) * SLOT + i * RW;
+      double a[MB], o[MB];
+#pragma unroll
+      for (int l = 0; l < MB; ++l) a[l] = L[l];
+#pragma unroll
+      for (int cc = 0; cc < MB; ++cc) {
+        double acc = a[0] * E[cc];
+#pragma unroll
+        for (int l = 1; l < MB; ++l) acc = fma(a[l], E[l * RW + cc], acc);
+        o[cc] = acc;
+      }
+#pragma unroll
+      for (int cc = 0; cc < MB; ++cc) L[cc] = o[cc];
+    }
+    __syncwarp();
+  }
+}
+
+// maps src[s] (s < len, written by another warp of this launch) into the T
+// parts of slots 0..15, identity beyond
+template <int MB>
+__device__ __forceinline__ void chain_load_maps(double* sm, const double* src, int len, int lane) {
+  constexpr int SLOT = ChainSmem<MB>::SLOT, RW = 2 * MB, MM = MB * MB;
+  for (int e = lane; e < kChainC0 * MM; e += 32) {
+    const int s = e / MM, r = e % MM, i = r / MB, k = r % MB;
+    sm[s * SLOT + i * RW + k] = s < len ? __ldcg(src + (long)s * MM + r) : (i == k ? 1.0 : 0.0);
+  }
+  __syncwarp();
+}
+
+// top level: Phi_total = product of the top maps, G = Ba + Bb Phi_total, LU
+// of G with partial pivoting (LAPACK convention: full-row swaps, pivot rows
+// recorded), the multipliers below the diagonal
+template <int MB>
+__device__ void chain_top_factor(const ChainLevelArgs& g, const ChainTree& t, double* sm, int lane) {
+  constexpr int SLOT = ChainSmem<MB>::SLOT, RW = 2 * MB, MM = MB * MB, GP = MB + 1;
+  chain_load_maps<MB>(sm, t.phi[t.T - 1], t.P[t.T - 1], lane);
+  chain_tree16<MB>(sm, 1, lane);
+  double* G = sm + SLOT;
+  if (lane < MB) {
+    const int i = lane;
+#pragma unroll
+    for (int c = 0; c < MB; ++c) {
+      double v = __ldg(g.data + i * MB + c);
+#pragma unroll
+      for (int l = 0; l < MB; ++l) v = fma(__ldg(g.corner + i * MB + l), sm[(kChainC0 - 1) * SLOT + l * RW + c], v);
+      G[i * GP + c] = v;
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    for (int k = 0; k < MB; ++k) {
+      int p = k;
+      for (int r = k + 1; r < MB; ++r)
+        if (fabs(G[r * GP + k]) > fabs(G[p * GP + k])) p = r;
+      if (p != k)
+        for (int c = 0; c < MB; ++c) {
+          const double tmp = G[k * GP + c];
+          G[k * GP + c] = G[p * GP + c];
+          G[p * GP + c] = tmp;
+        }
+      t.glu[MM + k] = (double)p;
+      for (int r = k + 1; r < MB; ++r) {
+        const double l = G[r * GP + k] / G[k * GP + k];
+        G[r * GP + k] = l;
+        for (int c = k + 1; c < MB; ++c) G[r * GP + c] = fma(-l, G[k * GP + c], G[r * GP + c]);
+      }
+    }
+    for (int e = 0; e < MM; ++e) t.glu[e] = G[(e / MB) * GP + e % MB];
+  }
+}
+
+// after the level-0 chunk maps of warp w are stored: climb the hierarchy while
+// this warp is the last arriver of the enclosing chunk
+template <int MB>
+__device__ void chain_factor_up(const ChainLevelArgs& g, const ChainTree& t, double* sm, long w, int lane) {
+  constexpr int SLOT = ChainSmem<MB>::SLOT, RW = 2 * MB, MM = MB * MB;
+  const long nw = ((long)t.P[0] + 1) / 2;  // factor warps (2 level-0 chunks each)
+  long c = w;
+  for (int l = 1;; ++l) {
+    if (l == t.T) {
+      const int expected = t.T == 1 ? (int)nw : t.P[t.T - 1];
+      if (warp_last_arrive(t.cnt + t.coff[t.T], expected, lane)) chain_top_factor<MB>(g, t, sm, lane);
+      return;
+    }
+    const long cc = l == 1 ? c / 8 : c / kChainC0;
+    const int expected = l == 1 ? (int)min(8L, nw - 8 * cc) : (int)min((long)kChainC0, t.P[l - 1] - kChainC0 * cc);
+    if (!warp_last_arrive(t.cnt + t.coff[l] + cc, expected, lane)) return;
+    const int len = (int)min((long)kChainC0, t.P[l - 1] - kChainC0 * cc);
+    chain_load_maps<MB>(sm, t.phi[l - 1] + kChainC0 * cc * MM, len, lane);
+    chain_tree16<MB>(sm, 1, lane);
+    for (int e = lane; e < MM; e += 32) t.phi[l][cc * MM + e] = sm[(kChainC0 - 1) * SLOT + (e / MB) * RW + e % MB];
+    c = cc;
+  }
+}
+
+template <int MB>
+__global__ void __launch_bounds__(64) chain_tm_kernel(ChainLevelArgs g, ChainTree t) {
   constexpr int SLOT = ChainSmem<MB>::SLOT, RW = 2 * MB, BW = 2 * MB * MB;
   extern __shared__ __align__(16) double csm[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -168,7 +276,7 @@ __global__ void __launch_bounds__(64) chain_tm_kernel(ChainLevelArgs g) {
         }
       }
     }
-#pragma unroll 1
+#pragma unroll
     for (int c = 0; c < 2 * MB; ++c) {
       double y[MB];
 #pragma unroll
@@ -196,95 +304,110 @@ __global__ void __launch_bounds__(64) chain_tm_kernel(ChainLevelArgs g) {
       for (int c = 0; c < MB; ++c) slot[i * RW + c] = i == c ? 1.0 : 0.0;
   }
   __syncwarp();
-  // ---- store [T | M] (same layout as the data rows)
+  // ---- store [T | M] pair-interleaved: block b, double2 q*MB + i = row i,
+  // columns 2q, 2q+1 of [T | M] -- the solve's MB lanes read one contiguous
+  // MB*16-byte run per load (coalesced)
   {
     double2* dst = reinterpret_cast<double2*>(g.tm + (bfirst - 1) * BW);
     const int tot2 = nblk * BW / 2;
-    for (int e0 = lane; e0 < tot2; e0 += 32) {
-      const int e = 2 * e0;
-      dst[e0] = *reinterpret_cast<const double2*>(sm + (e / BW) * SLOT + e % BW);
+    for (int e0 = lane; e0 < tot2; e0 += 32) {  // q fastest: conflict-free smem reads, whole sectors written
+      const int blk = e0 / (MB * MB), r = e0 % (MB * MB), q = r % MB, i = r / MB;
+      dst[blk * MB * MB + q * MB + i] = *reinterpret_cast<const double2*>(sm + blk * SLOT + i * RW + 2 * q);
     }
   }
   __syncwarp();
   // ---- Phi of the two chunks: tree of products P = later * earlier, in the T slots
-#pragma unroll 1
-  for (int h = 1; h < kChainC0; h <<= 1) {
-    const int pairs = kChainC0 / (2 * h);  // per chunk
-    if (lane < 2 * pairs) {
-      const int c = lane / pairs, k = lane % pairs;
-      double* Bs = sm + (c * kChainC0 + 2 * k * h) * SLOT;  // earlier (right factor), result slot
-      const double* As = sm + (c * kChainC0 + 2 * k * h + h) * SLOT;
-      double B[MB * MB];
-#pragma unroll
-      for (int i = 0; i < MB; ++i)
-#pragma unroll
-        for (int l = 0; l < MB; ++l) B[(i) * MB + (l)] = Bs[i * RW + l];
-#pragma unroll
-      for (int i = 0; i < MB; ++i) {
-        double a[MB], o[MB];
-#pragma unroll
-        for (int l = 0; l < MB; ++l) a[l] = As[i * RW + l];
-#pragma unroll
-        for (int cc = 0; cc < MB; ++cc) {
-          double acc = a[0] * B[(0) * MB + (cc)];
-#pragma unroll
-          for (int l = 1; l < MB; ++l) acc = fma(a[l], B[(l) * MB + (cc)], acc);
-          o[cc] = acc;
-        }
-#pragma unroll
-        for (int cc = 0; cc < MB; ++cc) Bs[i * RW + cc] = o[cc];
-      }
-    }
-    __syncwarp();
+  chain_tree16<MB>(sm, 2, lane);
+  // ---- Phi^(0) of this warp's chunks, then the upper levels of the hierarchy
+  const long P0 = t.P[0];
+  for (int e = lane; e < 2 * MB * MB; e += 32) {
+    const int c = e / (MB * MB), r = e % (MB * MB);
+    if (2 * w + c < P0)
+      t.phi[0][(2 * w + c) * MB * MB + r] = sm[(c * kChainC0 + kChainC0 - 1) * SLOT + (r / MB) * RW + r % MB];
   }
-  // ---- next level rows: [ -Phi_j | I ] for the chunks of this warp
-  for (int e = lane; e < 2 * BW; e += 32) {
-    const int c = e / BW, r = e % BW, i = r / RW, cc = r % RW;
-    const long j = 2 * w + c;
-    if (j < g.P) {
-      const double v = cc < MB ? -sm[c * kChainC0 * SLOT + i * RW + cc] : (i == cc - MB ? 1.0 : 0.0);
-      g.next_data[MB * MB + j * BW + r] = v;
-    }
-  }
-  if (w == 0)
-    for (int e = lane; e < MB * MB; e += 32) g.next_data[e] = __ldg(g.data + e);
+  chain_factor_up<MB>(g, t, sm, w, lane);
 }
 
 // ---------------------------------------------------------------------------
-// chain passes: MB lanes per chunk (lane i = row i), 32 / MB chunks per warp.
-// Each step needs row i of [T | M] (128 B per lane, 1 KB contiguous per
-// group: coalesced) and f of the block; loads run kPre steps ahead in a
-// register ring inside a fully unrolled kChainC0-step chain.  MODE 0:
-// condense (phi, chain from zero), 1: final (x from x_sep, condensed
-// separator residuals), 2: the correction (x += homogeneous chain of d,
-// certificate of the corrected separator rows).  Chunk j = blocks
-// 16j+1 .. 16j+16 (the last one may be shorter).
+// solve: three launches of chain_solve_kernel<MB, KM>, one CTA per level-1
+// chunk c (16 level-0 chunks, MB lanes each: lane i = row i of every block).
+//   KM 0 (condense)   level-0 chunks: phi_j = chain from zero with f; the CTA
+//                     condenses its level-1 chunk, last arrivers the upper ones.
+//   KM 1 (final)      warp 0 solves the top level and walks down its own path
+//                     (<= 16 steps per level) to x at its 17 level-1 unknowns;
+//                     level-0 chunks: x through every block from x_sigma, the
+//                     separator rows' residuals condensed to R^-1 r (the chain's
+//                     end value differs from the affine map by rounding, ~8 eps
+//                     |x| per step) and the BC row residual; these rhs go up
+//                     the hierarchy like KM 0.
+//   KM 2 (correction) the correction d the same way down; x += the homogeneous
+//                     chain of d, certificate of the corrected separator rows
+//                     and of the BC row.
+// Level-0 passes read row i of [T | M] (pair-interleaved: each load of a
+// group is one contiguous run) and f, kPre steps ahead in a register ring inside a fully
+// unrolled kChainC0-step chain.
 // ---------------------------------------------------------------------------
 constexpr int kPre = 3;
 
-template <int MB, int MODE>
-__global__ void __launch_bounds__(128) chain_pass_kernel(ChainLevelArgs g) {
-  constexpr int BW = 2 * MB * MB, RW = 2 * MB;
-  const int lane = threadIdx.x & 31, i = lane % MB;
-  const long j = ((long)blockIdx.x * blockDim.x + threadIdx.x) / MB;
-  const bool live = j < g.P;
-  const long b0 = live ? g.cut[j] + 1 : 1, b1 = live ? g.cut[j + 1] : 0;
-  const int len = (int)(b1 - b0 + 1);
-  double y = 0.0, yt = 0.0;
-  if (MODE == 1 && live) y = yt = __ldg(g.next_x + j * MB + i);
-  if (MODE == 2 && live) {
-    y = __ldg(g.corr_x + j * MB + i);
-    yt = __ldg(g.next_x + j * MB + i) + y;
+template <int MB>
+struct ChainReg {  // staged maps (padded rows: conflict-free) + rhs slots of one <= 16-step chain
+  static constexpr int MP = MB + 1;
+  static constexpr int MAPS = kChainC0 * MB * MP;
+  static constexpr int SIZE = MAPS + (kChainC0 + 1) * MB;
+};
+
+// maps[first + s] (s < len) and rhs[rfirst + s] (s < nr); cooperative over nthr threads
+template <int MB, bool COHERENT_RHS>
+__device__ __forceinline__ void chain_stage(double* reg, const double* maps, long first, int len, const double* rhs,
+                                            long rfirst, int nr, int tid, int nthr) {
+  constexpr int MM = MB * MB, MP = MB + 1;
+  for (int e = tid; e < len * MM; e += nthr) {
+    const int s = e / MM, r = e % MM;
+    reg[s * MB * MP + (r / MB) * MP + r % MB] = __ldg(maps + (first + s) * MM + r);
   }
-  if (MODE != 0 && live && j == 0) g.x[i] = yt;
-  // register ring: T row, M row, f of the block (MODE 0/1), old x (MODE 2)
+  double* rr = reg + ChainReg<MB>::MAPS;
+  for (int e = tid; e < nr * MB; e += nthr)
+    rr[e] = COHERENT_RHS ? __ldcg(rhs + rfirst * MB + e) : __ldg(rhs + rfirst * MB + e);
+}
+
+// y <- map_s y + fi (row i)
+template <int MB>
+__device__ __forceinline__ double chain_step(const double* reg, int s, int i, double y, double fi) {
+  const double* m = reg + s * MB * (MB + 1) + i * (MB + 1);
+  double a0 = fi, a1 = 0.0;
+#pragma unroll
+  for (int l = 0; l < MB; l += 2) {
+    a0 = fma(m[l], gshfl<MB>(y, l), a0);
+    a1 = fma(m[l + 1], gshfl<MB>(y, l + 1), a1);
+  }
+  return a0 + a1;
+}
+
+// condense a staged chunk of len steps from zero
+template <int MB>
+__device__ __forceinline__ double chain_condense(const double* reg, int len, int i) {
+  const double* rr = reg + ChainReg<MB>::MAPS;
+  double y = 0.0;
+  for (int s = 1; s <= len; ++s) y = chain_step<MB>(reg, s - 1, i, y, rr[s * MB + i]);
+  return y;
+}
+
+// level-0 chunk j: MODE 0 condense (run returns phi_j), 1 final, 2 correction.
+// start() issues the first kPre steps' loads (callers do it before their
+// serial prologue so the loads are in flight meanwhile).
+template <int MB, int MODE>
+struct Pass0 {
+  long b0 = 0;
+  int len = 0;
   double Tq[kPre][MB], Mq[kPre][MB], Fq[kPre][MB], Xq[kPre];
-  auto fetch = [&](int t, int slot) {
+
+  __device__ __forceinline__ void fetch(const ChainLevelArgs& g, int i, int t, int slot) {
+    constexpr int BW = 2 * MB * MB;
     if (t < len) {
-      const double2* row = reinterpret_cast<const double2*>(g.tm + (b0 + t - 1) * BW + (long)i * RW);
+      const double2* row = reinterpret_cast<const double2*>(g.tm + (b0 + t - 1) * BW) + i;
 #pragma unroll
       for (int c = 0; c < MB / 2; ++c) {
-        const double2 tv = __ldg(row + c);
+        const double2 tv = __ldg(row + c * MB);
         Tq[slot][2 * c] = tv.x;
         Tq[slot][2 * c + 1] = tv.y;
       }
@@ -292,7 +415,7 @@ __global__ void __launch_bounds__(128) chain_pass_kernel(ChainLevelArgs g) {
         const double2* fr = reinterpret_cast<const double2*>(g.f + (b0 + t) * MB);
 #pragma unroll
         for (int c = 0; c < MB / 2; ++c) {
-          const double2 mv = __ldg(row + MB / 2 + c), fv = __ldg(fr + c);
+          const double2 mv = __ldg(row + (MB / 2 + c) * MB), fv = __ldg(fr + c);
           Mq[slot][2 * c] = mv.x;
           Mq[slot][2 * c + 1] = mv.y;
           Fq[slot][2 * c] = fv.x;
@@ -302,196 +425,334 @@ __global__ void __launch_bounds__(128) chain_pass_kernel(ChainLevelArgs g) {
         Xq[slot] = g.x[(b0 + t) * MB + i];
       }
     }
-  };
+  }
+
+  __device__ __forceinline__ void start(const ChainLevelArgs& g, long j, bool live, int i) {
+    b0 = kChainC0 * j + 1;
+    const long b1 = live ? min(kChainC0 * j + kChainC0, (long)g.nb - 1) : 0;
+    len = live ? (int)(b1 - b0 + 1) : 0;
 #pragma unroll
-  for (int t = 0; t < kPre; ++t) fetch(t, t);
-  double num = 0.0, den = 0.0;
+    for (int t = 0; t < kPre; ++t) fetch(g, i, t, t);
+  }
+
+  __device__ __forceinline__ double run(const ChainLevelArgs& g, long j, bool live, int i, double ys, double yts,
+                                        double ye, double yte, double& corr, double& num, double& den,
+                                        bool& finite) {
+    double y = ys, yt = yts;
+    if (MODE != 0 && live && j == 0) g.x[i] = yt;
+#pragma unroll
+    for (int t = 0; t < kChainC0; ++t) {
+      const int sl = t % kPre;
+      const bool act = t < len, last = t == len - 1;
+      double a = 0.0;
+      if (MODE != 2)
+#pragma unroll
+        for (int l = 0; l < MB; ++l) a = fma(Mq[sl][l], Fq[sl][l], a);
+#pragma unroll
+      for (int l = 0; l < MB; ++l) a = fma(Tq[sl][l], gshfl<MB>(y, l), a);
+      const double xold = MODE == 2 ? Xq[sl] : 0.0;
+      // correction: certificate of the corrected separator row r = f - S x_prev - R x_sep
+      double S[MB], R[MB];
+      const bool cert_here = MODE == 2 && act && last;
+      if (cert_here) load_row<MB>(g.data, b0 + t, i, S, R);
+      double sg = 0.0, ab = 0.0;
+      if (MODE == 2) {
+#pragma unroll
+        for (int l = 0; l < MB; ++l) {
+          const double pl = gshfl<MB>(yt, l);
+          if (cert_here) {
+            const double p1 = S[l] * pl;
+            sg += p1;
+            ab += fabs(p1);
+          }
+        }
+      }
+      if (act) {
+        const long os = (b0 + t) * MB + i;
+        if (!last) {
+          y = a;
+          yt = MODE == 2 ? xold + y : y;
+        } else if (MODE == 1) {
+          corr = a - ye;  // R^-1 r_sep
+          y = yt = ye;
+        } else if (MODE == 2) {
+          y = ye;
+          yt = yte;
+        } else {
+          y = a;
+        }
+        if (MODE != 0) {
+          g.x[os] = yt;
+          finite &= isfinite(yt);
+        }
+      }
+      if (t + kPre < kChainC0) fetch(g, i, t + kPre, sl);
+      if (MODE == 2) {
+#pragma unroll
+        for (int l = 0; l < MB; ++l) {
+          const double xl = gshfl<MB>(yt, l);
+          if (cert_here) {
+            const double p2 = R[l] * xl;
+            sg += p2;
+            ab += fabs(p2);
+          }
+        }
+        if (cert_here) {
+          const double fv = __ldg(g.f + (b0 + t) * MB + i);
+          const double on = fabs(fv - sg), od = fabs(fv) + ab;
+          if (on * den > num * od || (den == 0.0 && on > 0)) {
+            num = on;
+            den = od;
+          }
+        }
+      }
+    }
+    return y;
+  }
+};
+
+// upward sweep from the CTA's level-1 chunk (reg1: its maps, rhs slots = F_1
+// of the chunk): F_2[c+1], then every level whose chunk this warp completes
+template <int MB>
+__device__ void chain_up(const ChainTree& t, double* const* Fu, double* reg1, long c, int len1, int lane) {
+  const int i = lane % MB;
+  const double* rr = reg1 + ChainReg<MB>::MAPS;
+  double y = chain_condense<MB>(reg1, len1, i);
+  if (lane < MB) {
+    Fu[2][(c + 1) * MB + i] = y;
+    if (c == 0) Fu[2][i] = rr[i];
+  }
+  long prev = c;
+  for (int l = 2; l < t.T; ++l) {
+    const long cc = prev / kChainC0;
+    const int len = (int)min((long)kChainC0, t.P[l - 1] - kChainC0 * cc);
+    if (!warp_last_arrive(t.cnt + t.coff[l] + cc, len, lane)) return;
+    chain_stage<MB, true>(reg1, t.phi[l - 1], kChainC0 * cc, len, Fu[l], kChainC0 * cc, len + 1, lane, 32);
+    __syncwarp();
+    y = chain_condense<MB>(reg1, len, i);
+    if (lane < MB) {
+      Fu[l + 1][(cc + 1) * MB + i] = y;
+      if (cc == 0) Fu[l + 1][i] = rr[i];
+    }
+    __syncwarp();
+    prev = cc;
+  }
+}
+
+// top level of a sweep: phi_total, x_0 from G x_0 = F_T[0] - Bb phi_total
+// (stored LU, pivots), the top chain; values into s_top (whole warp)
+template <int MB>
+__device__ void chain_top_solve(const ChainLevelArgs& g, const ChainTree& t, const double* regT, const double* s_glu,
+                                double* s_r, double* s_top, int lane) {
+  constexpr int MM = MB * MB;
+  const int i = lane % MB, PT = t.P[t.T - 1];
+  const double* rT = regT + ChainReg<MB>::MAPS;
+  double y = chain_condense<MB>(regT, PT, i);
+  double r = rT[i];
+#pragma unroll
+  for (int l = 0; l < MB; ++l) r = fma(-__ldg(g.corner + i * MB + l), gshfl<MB>(y, l), r);
+  if (lane < MB) s_r[i] = r;
+  __syncwarp();
+  if (lane == 0) {
+    for (int k = 0; k < MB; ++k) {
+      const int p = (int)s_glu[MM + k];
+      if (p != k) {
+        const double tmp = s_r[k];
+        s_r[k] = s_r[p];
+        s_r[p] = tmp;
+      }
+    }
+    for (int k = 0; k < MB; ++k)
+      for (int rr = k + 1; rr < MB; ++rr) s_r[rr] = fma(-s_glu[rr * MB + k], s_r[k], s_r[rr]);
+    for (int k = MB - 1; k >= 0; --k) {
+      double sv = s_r[k];
+      for (int cc = k + 1; cc < MB; ++cc) sv = fma(-s_glu[k * MB + cc], s_r[cc], sv);
+      s_r[k] = sv / s_glu[k * MB + k];
+    }
+  }
+  __syncwarp();
+  y = s_r[i];
+  if (lane < MB) s_top[i] = y;
+  for (int s = 1; s <= PT; ++s) {
+    y = chain_step<MB>(regT, s - 1, i, y, rT[s * MB + i]);
+    if (lane < MB) s_top[s * MB + i] = y;
+  }
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------------------
+// down sweep (one warp per level-2 chunk w; one warp when T <= 2): the top
+// solve and this warp's path down to the values at its level-2 chunk
+// (<= 16 steps per level), written to t.xlev[sel]; warp 0 also writes the top
+// values.  sel 0: x (rhs F), 1: the correction d (rhs cF).
+// ---------------------------------------------------------------------------
+template <int MB>
+__global__ void __launch_bounds__(32) chain_down_kernel(ChainLevelArgs g, ChainTree t, int sel) {
+  constexpr int REG = ChainReg<MB>::SIZE, MAPS = ChainReg<MB>::MAPS, MM = MB * MB;
+  extern __shared__ __align__(16) double ssm[];
+  __shared__ double s_top[(kChainC0 + 1) * MB];
+  __shared__ double s_glu[MM + MB];
+  __shared__ double s_r[MB];
+  const int lane = threadIdx.x, i = lane % MB, T = t.T, PT = t.P[T - 1];
+  const long w = blockIdx.x;
+  double* const* F = sel ? t.cfl : t.fl;
+  // regions: top at ssm, level l (2 <= l < T) at ssm + (T - l) * REG
+  chain_stage<MB, false>(ssm, t.phi[T - 1], 0, PT, F[T], 0, PT + 1, lane, 32);
+  for (int l = 2; l < T; ++l) {
+    const long cc = w >> (4 * (l - 2));
+    const int len = (int)min((long)kChainC0, t.P[l - 1] - kChainC0 * cc);
+    chain_stage<MB, false>(ssm + (T - l) * REG, t.phi[l - 1], kChainC0 * cc, len, F[l], kChainC0 * cc, len + 1, lane,
+                           32);
+  }
+  for (int e = lane; e < MM + MB; e += 32) s_glu[e] = __ldg(t.glu + e);
+  __syncwarp();
+  chain_top_solve<MB>(g, t, ssm, s_glu, s_r, s_top, lane);
+  double* out = t.xlev[sel];
+  if (w == 0 && lane < MB)
+    for (int s = 0; s <= PT; ++s) t.xtop[sel][s * MB + i] = s_top[s * MB + i];
+  if (T <= 2) {  // the top level is level min(2, T) itself
+    if (lane < MB)
+      for (int s = 0; s <= PT; ++s) out[s * MB + i] = s_top[s * MB + i];
+    return;
+  }
+  const long uT = w >> (4 * (T - 3));
+  double lo = s_top[uT * MB + i], hi = s_top[(uT + 1) * MB + i];
+  for (int l = T - 1; l >= 3; --l) {
+    const long ul = w >> (4 * (l - 3)), cc = ul >> 4;
+    const int t0 = (int)(ul & 15), len = (int)min((long)kChainC0, t.P[l - 1] - kChainC0 * cc);
+    const double* R = ssm + (T - l) * REG;
+    const double* Rr = R + MAPS;
+    double yy = lo;
+    for (int s = 1; s <= t0; ++s) yy = chain_step<MB>(R, s - 1, i, yy, Rr[s * MB + i]);
+    hi = t0 + 1 == len ? hi : chain_step<MB>(R, t0, i, yy, Rr[(t0 + 1) * MB + i]);
+    lo = yy;
+  }
+  // level-2 chunk w
+  const double* R = ssm + (T - 2) * REG;
+  const double* Rr = R + MAPS;
+  const int len2 = (int)min((long)kChainC0, t.P[1] - kChainC0 * w);
+  double yy = lo;
+  if (lane < MB) out[kChainC0 * w * MB + i] = lo;
+  for (int s = 1; s < len2; ++s) {
+    yy = chain_step<MB>(R, s - 1, i, yy, Rr[s * MB + i]);
+    if (lane < MB) out[(kChainC0 * w + s) * MB + i] = yy;
+  }
+  if (lane < MB && kChainC0 * w + len2 == t.P[1]) out[(long)t.P[1] * MB + i] = hi;
+}
+
+template <int MB, int KM>
+__global__ void __launch_bounds__(16 * MB) chain_solve_kernel(ChainLevelArgs g, ChainTree t) {
+  constexpr int NT = 16 * MB, MAPS = ChainReg<MB>::MAPS, MM = MB * MB;
+  extern __shared__ __align__(16) double ssm[];
+  __shared__ double s_v[(kChainC0 + 1) * MB];  // x (KM 1) or d (KM 2) at this CTA's level-1 unknowns
+  __shared__ double s_x[(kChainC0 + 1) * MB];  // KM 2: x at the level-1 unknowns
+  const int tid = threadIdx.x, lane = tid & 31, grp = tid / MB, i = tid % MB;
+  const long c = blockIdx.x;
+  const int T = t.T;
+  const long P0 = t.P[0];
+  const long j = kChainC0 * c + grp;
+  const bool live = j < P0;
+  const int len1 = (int)min((long)kChainC0, P0 - kChainC0 * c);
+  double* reg1 = ssm;  // level-1 region: maps Phi^(0) of this CTA's chunk + rhs slots
+  double* rr1 = reg1 + MAPS;
+  double num = 0.0, den = 0.0, corr = 0.0;
   bool finite = true;
-#pragma unroll
-  for (int t = 0; t < kChainC0; ++t) {
-    const int sl = t % kPre;
-    const bool act = t < len, last = t == len - 1;
-    double a = 0.0;
-    if (MODE != 2)
-#pragma unroll
-      for (int l = 0; l < MB; ++l) a = fma(Mq[sl][l], Fq[sl][l], a);
-#pragma unroll
-    for (int l = 0; l < MB; ++l) a = fma(Tq[sl][l], gshfl<MB>(y, l), a);
-    const double xold = MODE == 2 ? Xq[sl] : 0.0;
-    // correction: certificate of the corrected separator row r = f - S x_prev - R x_sep
-    double S[MB], R[MB];
-    const bool cert_here = MODE == 2 && act && last;
-    if (cert_here) load_row<MB>(g.data, b0 + t, i, S, R);
-    double sg = 0.0, ab = 0.0;
-    if (MODE == 2) {
-#pragma unroll
-      for (int l = 0; l < MB; ++l) {
-        const double pl = gshfl<MB>(yt, l);
-        if (cert_here) {
-          const double p1 = S[l] * pl;
-          sg += p1;
-          ab += fabs(p1);
-        }
+  (void)MM;
+
+  if constexpr (KM == 0) {
+    Pass0<MB, 0> ps;
+    ps.start(g, j, live, i);
+    if (T >= 2) chain_stage<MB, false>(reg1, t.phi[0], kChainC0 * c, len1, nullptr, 0, 0, tid, NT);
+    const double y = ps.run(g, j, live, i, 0.0, 0.0, 0.0, 0.0, corr, num, den, finite);
+    if (live) {
+      t.fl[1][(j + 1) * MB + i] = y;
+      rr1[(grp + 1) * MB + i] = y;
+      if (j == 0) {
+        const double f0 = __ldg(g.f + i);
+        t.fl[1][i] = f0;
+        rr1[i] = f0;
       }
     }
-    if (act) {
-      const long os = (b0 + t) * MB + i;
-      if (!last) {
-        y = a;
-        yt = MODE == 2 ? xold + y : y;
-      } else if (MODE == 1) {
-        const double xs = __ldg(g.next_x + (j + 1) * MB + i);
-        if (g.corr_f) g.corr_f[(j + 1) * MB + i] = a - xs;  // R^-1 r_sep
-        y = yt = xs;
-      } else if (MODE == 2) {
-        y = __ldg(g.corr_x + (j + 1) * MB + i);
-        yt = __ldg(g.next_x + (j + 1) * MB + i) + y;
+    if (T < 2) return;
+    __syncthreads();
+    if (tid < 32) chain_up<MB>(t, t.fl, reg1, c, len1, lane);
+  } else {
+    constexpr int SEL = KM == 1 ? 0 : 1;
+    double* const* Fd = SEL ? t.cfl : t.fl;  // rhs of the level-1 chain
+    Pass0<MB, KM> ps;
+    ps.start(g, j, live, i);
+    if (T >= 2) chain_stage<MB, false>(reg1, t.phi[0], kChainC0 * c, len1, Fd[1], kChainC0 * c, len1 + 1, tid, NT);
+    if (KM == 2)
+      for (int e = tid; e < (len1 + 1) * MB; e += NT) s_x[e] = __ldg(t.x1 + kChainC0 * c * MB + e);
+    __syncthreads();
+    if (tid < 32) {  // this CTA's level-1 values from the down sweep's level-2 values
+      const double* xl = t.xlev[SEL];
+      if (T == 1) {
+        if (lane < MB)
+          for (int s = 0; s <= len1; ++s) s_v[s * MB + i] = __ldg(xl + s * MB + i);
       } else {
-        y = a;
-      }
-      if (MODE != 0) {
-        g.x[os] = yt;
-        finite &= isfinite(yt);
+        const double lo = __ldg(xl + c * MB + i), hi = __ldg(xl + (c + 1) * MB + i);
+        double yy = lo;
+        if (lane < MB) s_v[i] = lo;
+        for (int s = 1; s < len1; ++s) {
+          yy = chain_step<MB>(reg1, s - 1, i, yy, rr1[s * MB + i]);
+          if (lane < MB) s_v[s * MB + i] = yy;
+        }
+        if (lane < MB) s_v[len1 * MB + i] = hi;
       }
     }
-    if (t + kPre < kChainC0) fetch(t + kPre, sl);
-    if (MODE == 2) {
+    __syncthreads();
+    const int PT = t.P[T - 1];
+    if constexpr (KM == 1) {
+      ps.run(g, j, live, i, s_v[grp * MB + i], s_v[grp * MB + i], s_v[(grp + 1) * MB + i], s_v[(grp + 1) * MB + i],
+             corr, num, den, finite);
+      if (live) {
+        t.x1[j * MB + i] = s_v[grp * MB + i];
+        if (j + 1 == P0) t.x1[(j + 1) * MB + i] = s_v[(grp + 1) * MB + i];
+        t.cfl[1][(j + 1) * MB + i] = corr;
+        rr1[(grp + 1) * MB + i] = corr;
+      }
+      if (c == 0 && tid < 32) {  // BC row residual: F_0 - Ba x_0 - Bb x_N (every group runs the shuffles)
+        const double x0 = s_v[i], xe = __ldg(t.xtop[0] + PT * MB + i);
+        double sg = 0.0;
 #pragma unroll
-      for (int l = 0; l < MB; ++l) {
-        const double xl = gshfl<MB>(yt, l);
-        if (cert_here) {
-          const double p2 = R[l] * xl;
-          sg += p2;
-          ab += fabs(p2);
+        for (int l = 0; l < MB; ++l) {
+          const double a0 = gshfl<MB>(x0, l), ae = gshfl<MB>(xe, l);
+          sg += __ldg(g.data + i * MB + l) * a0 + __ldg(g.corner + i * MB + l) * ae;
+        }
+        if (lane < MB) {
+          const double r0 = __ldg(g.f + i) - sg;
+          t.cfl[1][i] = r0;
+          rr1[i] = r0;
         }
       }
-      if (cert_here) {
-        const double fv = __ldg(g.f + (b0 + t) * MB + i);
-        const double on = fabs(fv - sg), od = fabs(fv) + ab;
+      if (T < 2) return;
+      __syncthreads();
+      if (tid < 32) chain_up<MB>(t, t.cfl, reg1, c, len1, lane);
+    } else {
+      // x += the homogeneous chain of d; certificate
+      const double d0 = s_v[grp * MB + i], d1 = s_v[(grp + 1) * MB + i];
+      ps.run(g, j, live, i, d0, s_x[grp * MB + i] + d0, d1, s_x[(grp + 1) * MB + i] + d1, corr, num, den, finite);
+      if (c == 0 && tid < 32) {  // BC row with the corrected end values
+        const double x0 = __ldg(t.xtop[0] + i) + __ldg(t.xtop[1] + i);
+        const double xe = __ldg(t.xtop[0] + PT * MB + i) + __ldg(t.xtop[1] + PT * MB + i);
+        double sg = 0.0, ab = 0.0;
+#pragma unroll
+        for (int l = 0; l < MB; ++l) {
+          const double p1 = __ldg(g.data + i * MB + l) * gshfl<MB>(x0, l);
+          const double p2 = __ldg(g.corner + i * MB + l) * gshfl<MB>(xe, l);
+          sg += p1 + p2;
+          ab += fabs(p1) + fabs(p2);
+        }
+        const double fv = __ldg(g.f + i), on = fabs(fv - sg), od = fabs(fv) + ab;
         if (on * den > num * od || (den == 0.0 && on > 0)) {
           num = on;
           den = od;
         }
       }
+      if (!finite) num = __longlong_as_double(0x7ff0000000000000ll), den = 1.0;
+      if (g.status) cert_push(g.status, num, den);
     }
-  }
-  if (MODE == 0 && live) {
-    g.next_f[(j + 1) * MB + i] = y;
-    if (j == 0) g.next_f[i] = __ldg(g.f + i);
-  }
-  if (MODE == 1 && g.corr_f) {  // BC row residual (chunk 0; every group runs the shuffles)
-    const bool bc = live && j == 0;
-    const double x0 = bc ? __ldg(g.next_x + i) : 0.0;
-    const double xe = bc ? __ldg(g.next_x + (long)g.P * MB + i) : 0.0;
-    double sg = 0.0;
-#pragma unroll
-    for (int l = 0; l < MB; ++l) {
-      const double a0 = gshfl<MB>(x0, l), ae = gshfl<MB>(xe, l);
-      if (bc) sg += __ldg(g.data + i * MB + l) * a0 + __ldg(g.corner + i * MB + l) * ae;
-    }
-    if (bc) g.corr_f[i] = __ldg(g.f + i) - sg;
-  }
-  if (MODE != 0) {
-    if (!finite) num = __longlong_as_double(0x7ff0000000000000ll), den = 1.0;
-    if (g.status) cert_push(g.status, num, den);
-  }
-}
-
-template <int MB>
-__global__ void chain_bc_cert_kernel(ChainLevelArgs g) {
-  const int lane = threadIdx.x, i = lane % MB;
-  const double x0 = g.x[i], xe = g.x[(long)(g.nb - 1) * MB + i];
-  double sg = 0.0, ab = 0.0;
-#pragma unroll
-  for (int l = 0; l < MB; ++l) {
-    const double p1 = __ldg(g.data + i * MB + l) * gshfl<MB>(x0, l);
-    const double p2 = __ldg(g.corner + i * MB + l) * gshfl<MB>(xe, l);
-    sg += p1 + p2;
-    ab += fabs(p1) + fabs(p2);
-  }
-  const double fv = __ldg(g.f + i);
-  cert_push(g.status, fabs(fv - sg), fabs(fv) + ab);
-}
-
-// direct: the whole (small) level by one group of MB lanes: Phi = prod T_b,
-// phi = chain from zero, (Ba + Bb Phi) x_0 = f_0 - Bb phi with partial
-// pivoting, then the chain for x.
-template <int MB>
-__global__ void __launch_bounds__(32) chain_direct_kernel(ChainLevelArgs g) {
-  const int lane = threadIdx.x, i = lane % MB;
-  double phi[MB], ph = 0.0;
-#pragma unroll
-  for (int c = 0; c < MB; ++c) phi[c] = i == c ? 1.0 : 0.0;
-  for (int b = 1; b < g.nb; ++b) {
-    double S[MB], R[MB], w[MB + 1];
-    load_row<MB>(g.data, b, i, S, R);
-#pragma unroll
-    for (int c = 0; c <= MB; ++c) w[c] = 0.0;
-    w[MB] = __ldg(g.f + (long)b * MB + i);
-#pragma unroll
-    for (int l = 0; l < MB; ++l) {
-#pragma unroll
-      for (int c = 0; c < MB; ++c) w[c] = fma(-S[l], gshfl<MB>(phi[c], l), w[c]);
-      w[MB] = fma(-S[l], gshfl<MB>(ph, l), w[MB]);
-    }
-    lane_solve<MB, MB + 1>(R, w, i);
-#pragma unroll
-    for (int c = 0; c < MB; ++c) phi[c] = w[c];
-    ph = w[MB];
-  }
-  // M0 = Ba + Bb Phi, rhs = f_0 - Bb phi  (row i)
-  double M0[MB], rhs = __ldg(g.f + i);
-#pragma unroll
-  for (int c = 0; c < MB; ++c) M0[c] = __ldg(g.data + i * MB + c);
-#pragma unroll
-  for (int l = 0; l < MB; ++l) {
-    const double bb = __ldg(g.corner + i * MB + l);
-#pragma unroll
-    for (int c = 0; c < MB; ++c) M0[c] = fma(bb, gshfl<MB>(phi[c], l), M0[c]);
-    rhs = fma(-bb, gshfl<MB>(ph, l), rhs);
-  }
-  // the small BC system: serial Gaussian elimination with partial pivoting on lane 0
-  __shared__ double Msh[MB][MB + 1];
-  if (lane < MB) {
-#pragma unroll
-    for (int c = 0; c < MB; ++c) Msh[i][c] = M0[c];
-    Msh[i][MB] = rhs;
-  }
-  __syncwarp();
-  if (lane == 0) {
-    for (int k = 0; k < MB; ++k) {
-      int p = k;
-      for (int r2 = k + 1; r2 < MB; ++r2)
-        if (fabs(Msh[r2][k]) > fabs(Msh[p][k])) p = r2;
-      if (p != k)
-        for (int c = 0; c <= MB; ++c) {
-          const double t = Msh[k][c];
-          Msh[k][c] = Msh[p][c];
-          Msh[p][c] = t;
-        }
-      for (int r2 = k + 1; r2 < MB; ++r2) {
-        const double l = Msh[r2][k] / Msh[k][k];
-        for (int c = k; c <= MB; ++c) Msh[r2][c] = fma(-l, Msh[k][c], Msh[r2][c]);
-      }
-    }
-    for (int k = MB - 1; k >= 0; --k) {
-      double s = Msh[k][MB];
-      for (int c = k + 1; c < MB; ++c) s = fma(-Msh[k][c], Msh[c][MB], s);
-      Msh[k][MB] = s / Msh[k][k];
-    }
-  }
-  __syncwarp();
-  double y = Msh[i][MB];
-  if (lane < MB) g.x[i] = y;
-  for (int b = 1; b < g.nb; ++b) {
-    double S[MB], R[MB], w[1];
-    load_row<MB>(g.data, b, i, S, R);
-    w[0] = __ldg(g.f + (long)b * MB + i);
-#pragma unroll
-    for (int l = 0; l < MB; ++l) w[0] = fma(-S[l], gshfl<MB>(y, l), w[0]);
-    lane_solve<MB, 1>(R, w, i);
-    y = w[0];
-    if (lane < MB) g.x[(long)b * MB + i] = y;
   }
 }
 

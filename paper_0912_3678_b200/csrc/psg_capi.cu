@@ -864,157 +864,143 @@ struct BlkSolver {
 // ----------------------------------------------------------------------------
 // BVP-layout BABD chain path (chain_kernels.cuh)
 // ----------------------------------------------------------------------------
-struct ChainLevel {
-  int nb = 0, P = 0;
-  bool direct = false;
-  const double* data = nullptr;
-  const double* f = nullptr;
-  double* x = nullptr;
-  std::vector<int> hcut;
-  DevBuf<int> cut;
-  DevBuf<double> next_data, next_f, next_x, corr_x, tm;
-};
-
-constexpr int kChainDirect = 64;  // levels with at most this many block rows are solved by one warp
-
 struct ChainSolver {
   int MB = 0;
   bool possible = false;
+  const double* data = nullptr;
   const double* corner = nullptr;
-  std::vector<std::unique_ptr<ChainLevel>> lv;
+  long N = 0;              // block rows after the BC row
+  std::vector<long> P;     // chunks per level (P[l], l < T)
+  DevBuf<double> tm, glu, x1, xlev[2], xtop[2];
+  std::vector<std::unique_ptr<DevBuf<double>>> phi, fl, cfl;
+  DevBuf<int> cnt;
+  int coff[kChainMaxLev + 1] = {};
   DevBuf<double> falign;
   int launches = 0;
 
-  void init(const psg_desc& A, const Plan& P) {
+  void init(const psg_desc& A, const Plan& Pl) {
     possible = false;
-    lv.clear();
-    if (A.kind != PSG_BABD || A.s != A.m || A.r != 0 || !P.has_corner) return;
+    if (A.kind != PSG_BABD || A.s != A.m || A.r != 0 || !Pl.has_corner) return;
     if (A.corner_rows != A.m || A.corner_cols != A.m) return;
     if (A.m != 2 && A.m != 4 && A.m != 8) return;
     if (reinterpret_cast<uintptr_t>(A.data) & 15) return;  // blocks arrive by 16-byte bulk copies
     MB = A.m;
+    data = A.data;
     corner = A.corner;
-    auto L = std::make_unique<ChainLevel>();
-    L->nb = A.n / MB;
-    L->data = A.data;
+    N = (long)A.n / MB - 1;
+    if (N < 1) return;
     // chunks of kChainC0 blocks on every level (internal; independent of the
     // reference plan, whose reduced system the exact path keeps)
-    auto cuts = [](ChainLevel& c) {
-      c.P = (c.nb - 1 + kChainC0 - 1) / kChainC0;
-      c.hcut.clear();
-      for (int k = 0; k < c.P; ++k) c.hcut.push_back(k * kChainC0);
-      c.hcut.push_back(c.nb - 1);
-    };
-    cuts(*L);
-    for (;;) {
-      ChainLevel& c = *L;
-      c.tm.alloc((size_t)(c.nb - 1) * 2 * MB * MB);
-      c.cut.alloc(c.hcut.size());
-      CUDA_TRY(cudaMemcpy(c.cut.p, c.hcut.data(), sizeof(int) * c.hcut.size(), cudaMemcpyHostToDevice));
-      const int nb2 = c.P + 1;
-      c.next_data.alloc((size_t)MB * MB + (size_t)(nb2 - 1) * 2 * MB * MB);
-      c.next_f.alloc((size_t)nb2 * MB);
-      c.next_x.alloc((size_t)nb2 * MB);
-      if (lv.empty()) c.corr_x.alloc((size_t)nb2 * MB);
-      auto N = std::make_unique<ChainLevel>();
-      N->nb = nb2;
-      N->data = c.next_data.p;
-      N->f = c.next_f.p;
-      N->x = c.next_x.p;
-      lv.push_back(std::move(L));
-      if (nb2 <= kChainDirect) {
-        N->direct = true;
-        lv.push_back(std::move(N));
-        break;
-      }
-      cuts(*N);
-      L = std::move(N);
+    P.assign(1, (N + kChainC0 - 1) / kChainC0);
+    while (P.back() > kChainC0) P.push_back((P.back() + kChainC0 - 1) / kChainC0);
+    const int T = (int)P.size();
+    if (T > kChainMaxLev) return;
+    const size_t MM = (size_t)MB * MB;
+    tm.alloc((size_t)N * 2 * MM);
+    phi.clear();
+    fl.clear();
+    cfl.clear();
+    fl.emplace_back(nullptr);
+    cfl.emplace_back(nullptr);
+    for (int l = 0; l < T; ++l) {
+      phi.emplace_back(new DevBuf<double>());
+      phi.back()->alloc((size_t)P[l] * MM);
+      fl.emplace_back(new DevBuf<double>());
+      fl.back()->alloc((size_t)(P[l] + 1) * MB);  // level l + 1
+      cfl.emplace_back(new DevBuf<double>());
+      cfl.back()->alloc((size_t)(P[l] + 1) * MB);
     }
+    glu.alloc(MM + MB);
+    x1.alloc((size_t)(P[0] + 1) * MB);
+    for (int k = 0; k < 2; ++k) {
+      xlev[k].alloc((size_t)(P[std::min(2, T) - 1] + 1) * MB);
+      xtop[k].alloc((size_t)(P[T - 1] + 1) * MB);
+    }
+    int tot = 0;
+    for (int l = 1; l < T; ++l) coff[l] = tot, tot += (int)P[l];
+    coff[T] = tot++;
+    cnt.alloc(tot);
+    CUDA_TRY(cudaMemset(cnt.p, 0, sizeof(int) * tot));
     possible = true;
   }
 
   void set_data(const double* d, const double* c) {
-    if (!lv.empty()) lv[0]->data = d;
+    data = d;
     corner = c;
   }
 
-  ChainLevelArgs args(ChainLevel& L, DevStatus* st) const {
+  ChainLevelArgs args(const double* f, double* x, DevStatus* st) const {
     ChainLevelArgs g{};
-    g.data = L.data;
+    g.data = data;
     g.corner = corner;
-    g.nb = L.nb;
-    g.P = L.P;
-    g.cut = L.cut.p;
-    g.f = L.f;
-    g.x = L.x;
-    g.next_data = L.next_data.p;
-    g.next_f = L.next_f.p;
-    g.next_x = L.next_x.p;
-    g.tm = L.tm.p;
+    g.nb = (int)(N + 1);
+    g.f = f;
+    g.x = x;
+    g.tm = tm.p;
     g.status = st;
     return g;
+  }
+
+  ChainTree tree() const {
+    ChainTree t{};
+    t.T = (int)P.size();
+    for (int l = 0; l < t.T; ++l) {
+      t.P[l] = (int)P[l];
+      t.phi[l] = phi[l]->p;
+      t.fl[l + 1] = fl[l + 1]->p;
+      t.cfl[l + 1] = cfl[l + 1]->p;
+    }
+    t.cnt = cnt.p;
+    for (int l = 0; l <= t.T; ++l) t.coff[l] = coff[l];
+    t.glu = glu.p;
+    t.x1 = x1.p;
+    for (int k = 0; k < 2; ++k) {
+      t.xlev[k] = xlev[k].p;
+      t.xtop[k] = xtop[k].p;
+    }
+    return t;
   }
 
   template <int M>
   void factor_t(cudaStream_t s) {
     constexpr int bytes = ChainSmem<M>::WARP * 8;
     ensure_smem(reinterpret_cast<const void*>(chain_tm_kernel<M>), bytes);
-    for (auto& L : lv) {
-      if (L->direct) break;
-      const long warps = (L->nb - 1 + 31) / 32;
-      chain_tm_kernel<M><<<(int)warps, 32, bytes, s>>>(args(*L, nullptr));
-      LAUNCH_CHECK();
-      ++launches;
-    }
+    const long warps = (N + 31) / 32;
+    chain_tm_kernel<M><<<(int)warps, 32, bytes, s>>>(args(nullptr, nullptr, nullptr), tree());
+    LAUNCH_CHECK();
+    ++launches;
   }
 
-  template <int M, int MODE>
-  void pass(ChainLevelArgs a, cudaStream_t s) {
-    chain_pass_kernel<M, MODE><<<(a.P * M + 127) / 128, 128, 0, s>>>(a);
+  template <int M, int KM>
+  void solve_launch(const ChainLevelArgs& a, const ChainTree& t, cudaStream_t s) {
+    constexpr int bytes = ChainReg<M>::SIZE * 8;
+    ensure_smem(reinterpret_cast<const void*>(chain_solve_kernel<M, KM>), bytes);
+    chain_solve_kernel<M, KM><<<(int)((P[0] + kChainC0 - 1) / kChainC0), 16 * M, bytes, s>>>(a, t);
+    LAUNCH_CHECK();
+    ++launches;
+  }
+
+  template <int M>
+  void down_launch(const ChainLevelArgs& a, const ChainTree& t, int sel, cudaStream_t s) {
+    const int bytes = t.T * ChainReg<M>::SIZE * 8;
+    ensure_smem(reinterpret_cast<const void*>(chain_down_kernel<M>), kChainMaxLev * ChainReg<M>::SIZE * 8);
+    chain_down_kernel<M><<<t.T >= 3 ? t.P[2] : 1, 32, bytes, s>>>(a, t, sel);
     LAUNCH_CHECK();
     ++launches;
   }
 
   template <int M>
   void solve_t(const double* f, double* x, DevStatus* st, cudaStream_t s, cudaEvent_t* ev) {
-    lv[0]->f = f;
-    lv[0]->x = x;
-    for (auto& L : lv) {
-      if (L->direct) break;
-      pass<M, 0>(args(*L, nullptr), s);
+    const ChainTree t = tree();
+    solve_launch<M, 0>(args(f, x, nullptr), t, s);  // condense, reduced levels up
+    down_launch<M>(args(f, x, nullptr), t, 0, s);   // top solve, x down to level 2
+    if (ev) {
+      CUDA_TRY(cudaEventRecord(ev[1], s));
+      CUDA_TRY(cudaEventRecord(ev[2], s));
     }
-    if (ev) CUDA_TRY(cudaEventRecord(ev[1], s));
-    upper_t<M>(s, 1);
-    if (ev) CUDA_TRY(cudaEventRecord(ev[2], s));
-    // level 0: final pass, condensing its separator residuals for one correction
-    ChainLevel& L0 = *lv[0];
-    ChainLevelArgs a = args(L0, nullptr);
-    a.corr_f = L0.next_f.p;
-    pass<M, 1>(a, s);
-    // correction: A d = r (separator rows) through the reduced levels, then x += d
-    lv[1]->x = L0.corr_x.p;
-    for (size_t l = 1; l < lv.size(); ++l) {
-      ChainLevel& L = *lv[l];
-      if (L.direct) break;
-      pass<M, 0>(args(L, nullptr), s);
-    }
-    upper_t<M>(s, 1);
-    lv[1]->x = L0.next_x.p;
-    ChainLevelArgs c = args(L0, st);  // certifies the corrected separator rows
-    c.corr_x = L0.corr_x.p;
-    pass<M, 2>(c, s);
-    chain_bc_cert_kernel<M><<<1, 32, 0, s>>>(args(L0, st));
-    LAUNCH_CHECK();
-    launches += 1;
-  }
-
-  // direct solve of the last level and final passes of levels >= from (top down)
-  template <int M>
-  void upper_t(cudaStream_t s, size_t from) {
-    chain_direct_kernel<M><<<1, 32, 0, s>>>(args(*lv.back(), nullptr));
-    LAUNCH_CHECK();
-    ++launches;
-    for (size_t l = lv.size() - 1; l-- > from;) pass<M, 1>(args(*lv[l], nullptr), s);
+    solve_launch<M, 1>(args(f, x, nullptr), t, s);  // x through every block, separator residuals up
+    down_launch<M>(args(f, x, nullptr), t, 1, s);   // the correction down
+    solve_launch<M, 2>(args(f, x, st), t, s);       // x += d, certificate
   }
 
   void factor(cudaStream_t s) {
@@ -1024,9 +1010,9 @@ struct ChainSolver {
   }
   // status slot must be reset by the caller
   void solve(const double* f, double* x, DevStatus* st, cudaStream_t s, cudaEvent_t* ev) {
-    if (reinterpret_cast<uintptr_t>(f) & 15) {  // the staged passes bulk-copy f: 16-byte alignment
-      falign.alloc((size_t)lv[0]->nb * MB);
-      CUDA_TRY(cudaMemcpyAsync(falign.p, f, sizeof(double) * lv[0]->nb * MB, cudaMemcpyDeviceToDevice, s));
+    if (reinterpret_cast<uintptr_t>(f) & 15) {  // the passes read f by 16-byte loads
+      falign.alloc((size_t)(N + 1) * MB);
+      CUDA_TRY(cudaMemcpyAsync(falign.p, f, sizeof(double) * (N + 1) * MB, cudaMemcpyDeviceToDevice, s));
       f = falign.p;
     }
     if (MB == 8) solve_t<8>(f, x, st, s, ev);

@@ -57,14 +57,17 @@ def test_chain_config4_matches_oracle(cuda, size, p):
     assert O.residual(A, x, f) <= 1e-13
 
 
-@pytest.mark.parametrize("m,nb,p", [(2, 3000, 16), (4, 2000, 40), (8, 1500, 30), (8, 5000, 4)])
+@pytest.mark.parametrize("m,nb,p", [(2, 3000, 16), (4, 2000, 40), (8, 1500, 30), (8, 5000, 4), (4, 10, 2),
+                                   (8, 200, 4), (2, 258, 3), (8, 300, 4), (8, 4114, 8)])
 def test_chain_random_bvp_matches_oracle(cuda, m, nb, p):
     A, f = random_bvp(m, nb, 11 + m)
     want, _ = O.parallel_solve(A, p, f)
     x, st, F, _ = _gpu(cuda, A, p, f)
     assert st.speculative == 1
     assert O.rel_err(x, want) <= 1e-10
-    assert O.residual(A, x, f) <= 1e-13
+    # some random instances are ill-conditioned enough that the reference
+    # itself lands above 1e-13 ((8, 200) 1.4e-13, (8, 4114) 1.2e-13): bound by it
+    assert O.residual(A, x, f) <= max(1e-13, 2.0 * O.residual(A, want, f))
 
 
 def test_chain_exact_option_matches(cuda):

@@ -1,7 +1,8 @@
 """Per-source-line warp-stall breakdown of one kernel in an ncu report
 (needs a -lineinfo build and `ncu --import-source on`).
 
-    python tools/ncu_lines.py REPORT.ncu-rep KERNEL_REGEX [--top N]
+    python tools/ncu_lines.py REPORT.ncu-rep KERNEL_REGEX [--top N] [--skip K]
+(KERNEL_REGEX matches the base name; --skip K selects the K-th matching launch)
 """
 import csv
 import io
@@ -10,8 +11,9 @@ import sys
 
 rep, kre = sys.argv[1], sys.argv[2]
 top = int(sys.argv[sys.argv.index("--top") + 1]) if "--top" in sys.argv else 30
+skip = ["--launch-skip", sys.argv[sys.argv.index("--skip") + 1], "--launch-count", "1"] if "--skip" in sys.argv else []
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass",
-                      "--kernel-name", "regex:" + kre], capture_output=True, text=True).stdout
+                      "--kernel-name", "regex:" + kre, *skip], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 fname, hdr, lines, func = None, None, [], None
 for r in rows:
