@@ -78,6 +78,14 @@ struct ChainSmem {
   static constexpr int WARP = 32 * SLOT;  // doubles per warp
 };
 
+// [T | M] of a block in the pair-interleaved order of the global tm array
+// (and of a slot once its block is factored): element (i, c) at
+// (c / 2) * 2 MB + 2 i + c % 2 -- double2 (i, c/2) transposed
+template <int MB>
+__host__ __device__ constexpr int tix(int i, int c) {
+  return (c >> 1) * 2 * MB + 2 * i + (c & 1);
+}
+
 // ---------------------------------------------------------------------------
 // The reduced-system hierarchy.  Level 0 is the user's chain (N + 1 block
 // rows, P[0] = ceil(N / 16) chunks).  Level l >= 1 has nb_l = P[l-1] + 1
@@ -129,7 +137,7 @@ __device__ __forceinline__ bool warp_last_arrive(int* ctr, int expected, int lan
 // factor is a previous round's result (read-only in this round).
 template <int MB>
 __device__ __forceinline__ void chain_tree16(double* sm, int nch, int lane) {
-  constexpr int SLOT = ChainSmem<MB>::SLOT, RW = 2 * MB;
+  constexpr int SLOT = ChainSmem<MB>::SLOT;
 #pragma unroll 1
   for (int h = 1; h < kChainC0; h <<= 1) {
     const int pairs = kChainC0 / (2 * h);  // per chunk
@@ -137,19 +145,19 @@ __device__ __forceinline__ void chain_tree16(double* sm, int nch, int lane) {
     for (int task = lane; task < tasks; task += 32) {
       const int i = task % MB, pk = task / MB, c = pk / pairs, k = pk % pairs;
       const double* E = sm + (c * kChainC0 + 2 * k * h + h - 1) * SLOT;
-      double* L = sm + (c * kChainC0 + 2 * k * h + 2 * h - 1) * SLOT + i * RW;
+      double* L = sm + (c * kChainC0 + 2 * k * h + 2 * h - 1) * SLOT;
       double a[MB], o[MB];
 #pragma unroll
-      for (int l = 0; l < MB; ++l) a[l] = L[l];
+      for (int l = 0; l < MB; ++l) a[l] = L[tix<MB>(i, l)];
 #pragma unroll
       for (int cc = 0; cc < MB; ++cc) {
-        double acc = a[0] * E[cc];
+        double acc = a[0] * E[tix<MB>(0, cc)];
 #pragma unroll
-        for (int l = 1; l < MB; ++l) acc = fma(a[l], E[l * RW + cc], acc);
+        for (int l = 1; l < MB; ++l) acc = fma(a[l], E[tix<MB>(l, cc)], acc);
         o[cc] = acc;
       }
 #pragma unroll
-      for (int cc = 0; cc < MB; ++cc) L[cc] = o[cc];
+      for (int cc = 0; cc < MB; ++cc) L[tix<MB>(i, cc)] = o[cc];
     }
     __syncwarp();
   }
@@ -159,10 +167,10 @@ __device__ __forceinline__ void chain_tree16(double* sm, int nch, int lane) {
 // parts of slots 0..15, identity beyond
 template <int MB>
 __device__ __forceinline__ void chain_load_maps(double* sm, const double* src, int len, int lane) {
-  constexpr int SLOT = ChainSmem<MB>::SLOT, RW = 2 * MB, MM = MB * MB;
+  constexpr int SLOT = ChainSmem<MB>::SLOT, MM = MB * MB;
   for (int e = lane; e < kChainC0 * MM; e += 32) {
     const int s = e / MM, r = e % MM, i = r / MB, k = r % MB;
-    sm[s * SLOT + i * RW + k] = s < len ? __ldcg(src + (long)s * MM + r) : (i == k ? 1.0 : 0.0);
+    sm[s * SLOT + tix<MB>(i, k)] = s < len ? __ldcg(src + (long)s * MM + r) : (i == k ? 1.0 : 0.0);
   }
   __syncwarp();
 }
@@ -182,7 +190,7 @@ __device__ void chain_top_factor(const ChainLevelArgs& g, const ChainTree& t, do
     for (int c = 0; c < MB; ++c) {
       double v = __ldg(g.data + i * MB + c);
 #pragma unroll
-      for (int l = 0; l < MB; ++l) v = fma(__ldg(g.corner + i * MB + l), sm[(kChainC0 - 1) * SLOT + l * RW + c], v);
+      for (int l = 0; l < MB; ++l) v = fma(__ldg(g.corner + i * MB + l), sm[(kChainC0 - 1) * SLOT + tix<MB>(l, c)], v);
       G[i * GP + c] = v;
     }
   }
@@ -228,7 +236,7 @@ __device__ void chain_factor_up(const ChainLevelArgs& g, const ChainTree& t, dou
     const int len = (int)min((long)kChainC0, t.P[l - 1] - kChainC0 * cc);
     chain_load_maps<MB>(sm, t.phi[l - 1] + kChainC0 * cc * MM, len, lane);
     chain_tree16<MB>(sm, 1, lane);
-    for (int e = lane; e < MM; e += 32) t.phi[l][cc * MM + e] = sm[(kChainC0 - 1) * SLOT + (e / MB) * RW + e % MB];
+    for (int e = lane; e < MM; e += 32) t.phi[l][cc * MM + e] = sm[(kChainC0 - 1) * SLOT + tix<MB>(e / MB, e % MB)];
     c = cc;
   }
 }
@@ -297,23 +305,27 @@ __global__ void __launch_bounds__(64) chain_tm_kernel(ChainLevelArgs g, ChainTre
 #pragma unroll
       for (int i = 0; i < MB; ++i) slot[i * RW + c] = y[i];  // T (c < MB) over S, M over R
     }
+    // ---- pair-interleave the slot in place (double2 (i, q) <-> (q, i)), then
+    // one TMA bulk store of the block: block b, double2 q*MB + i = row i,
+    // columns 2q, 2q+1 of [T | M] -- the solve's MB lanes read one contiguous
+    // MB*16-byte run per load (coalesced)
+    double2* s2 = reinterpret_cast<double2*>(slot);
+#pragma unroll
+    for (int i = 0; i < MB; ++i)
+#pragma unroll
+      for (int q = i + 1; q < MB; ++q) {
+        const double2 x = s2[i * MB + q], y = s2[q * MB + i];
+        s2[i * MB + q] = y;
+        s2[q * MB + i] = x;
+      }
+    fence_proxy_async_smem();
+    bulk_s2g(g.tm + (bfirst - 1 + lane) * BW, slot, BW * 8);
+    bulk_commit_and_wait_read();
   } else {  // missing blocks of a short last chunk: T = I
 #pragma unroll
     for (int i = 0; i < MB; ++i)
 #pragma unroll
-      for (int c = 0; c < MB; ++c) slot[i * RW + c] = i == c ? 1.0 : 0.0;
-  }
-  __syncwarp();
-  // ---- store [T | M] pair-interleaved: block b, double2 q*MB + i = row i,
-  // columns 2q, 2q+1 of [T | M] -- the solve's MB lanes read one contiguous
-  // MB*16-byte run per load (coalesced)
-  {
-    double2* dst = reinterpret_cast<double2*>(g.tm + (bfirst - 1) * BW);
-    const int tot2 = nblk * BW / 2;
-    for (int e0 = lane; e0 < tot2; e0 += 32) {  // q fastest: conflict-free smem reads, whole sectors written
-      const int blk = e0 / (MB * MB), r = e0 % (MB * MB), q = r % MB, i = r / MB;
-      dst[blk * MB * MB + q * MB + i] = *reinterpret_cast<const double2*>(sm + blk * SLOT + i * RW + 2 * q);
-    }
+      for (int c = 0; c < MB; ++c) slot[tix<MB>(i, c)] = i == c ? 1.0 : 0.0;
   }
   __syncwarp();
   // ---- Phi of the two chunks: tree of products P = later * earlier, in the T slots
@@ -323,7 +335,7 @@ __global__ void __launch_bounds__(64) chain_tm_kernel(ChainLevelArgs g, ChainTre
   for (int e = lane; e < 2 * MB * MB; e += 32) {
     const int c = e / (MB * MB), r = e % (MB * MB);
     if (2 * w + c < P0)
-      t.phi[0][(2 * w + c) * MB * MB + r] = sm[(c * kChainC0 + kChainC0 - 1) * SLOT + (r / MB) * RW + r % MB];
+      t.phi[0][(2 * w + c) * MB * MB + r] = sm[(c * kChainC0 + kChainC0 - 1) * SLOT + tix<MB>(r / MB, r % MB)];
   }
   chain_factor_up<MB>(g, t, sm, w, lane);
 }
