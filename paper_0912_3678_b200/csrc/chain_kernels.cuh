@@ -411,7 +411,7 @@ template <int MB, int MODE>
 struct Pass0 {
   long b0 = 0;
   int len = 0;
-  double Tq[kPre][MB], Mq[kPre][MB], Fq[kPre][MB], Xq[kPre];
+  double Tq[kPre][MB], Mq[kPre][MB], Fq[kPre], Xq[kPre];  // Fq: f_i of the block (row i; shuffled for M f)
 
   __device__ __forceinline__ void fetch(const ChainLevelArgs& g, int i, int t, int slot) {
     constexpr int BW = 2 * MB * MB;
@@ -424,15 +424,13 @@ struct Pass0 {
         Tq[slot][2 * c + 1] = tv.y;
       }
       if (MODE != 2) {
-        const double2* fr = reinterpret_cast<const double2*>(g.f + (b0 + t) * MB);
 #pragma unroll
         for (int c = 0; c < MB / 2; ++c) {
-          const double2 mv = __ldg(row + (MB / 2 + c) * MB), fv = __ldg(fr + c);
+          const double2 mv = __ldg(row + (MB / 2 + c) * MB);
           Mq[slot][2 * c] = mv.x;
           Mq[slot][2 * c + 1] = mv.y;
-          Fq[slot][2 * c] = fv.x;
-          Fq[slot][2 * c + 1] = fv.y;
         }
+        Fq[slot] = __ldg(g.f + (b0 + t) * MB + i);
       } else {
         Xq[slot] = g.x[(b0 + t) * MB + i];
       }
@@ -459,7 +457,7 @@ struct Pass0 {
       double a = 0.0;
       if (MODE != 2)
 #pragma unroll
-        for (int l = 0; l < MB; ++l) a = fma(Mq[sl][l], Fq[sl][l], a);
+        for (int l = 0; l < MB; ++l) a = fma(Mq[sl][l], gshfl<MB>(Fq[sl], l), a);
 #pragma unroll
       for (int l = 0; l < MB; ++l) a = fma(Tq[sl][l], gshfl<MB>(y, l), a);
       const double xold = MODE == 2 ? Xq[sl] : 0.0;
