@@ -24,7 +24,7 @@ python $B > $O/plain.log 2>&1 && \
 python tools/profile_step.py > $O/pplain.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:"tri_spec_factor|tri_spec_sep|tri_segment_solve|tri_cert" \
   -s 4 -c 4 -o $O/full python tools/profile_step.py > $O/ncu_full.log 2>&1; echo "ncu-full rc=$?"
-for c in 2 3 4; do
+for c in 0 2 3 4; do
   python tools/cfg_step.py $c 3 > $O/cfg$c.log 2>&1 && \
     ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_cfg$c.csv \
     python tools/cfg_step.py $c 3 > /dev/null 2>&1; echo "cfg$c list rc=$?"
@@ -46,6 +46,7 @@ done
 python tools/ncu_lines.py $O/full_cfg2.ncu-rep "blk_segment|blk_body_narrow" --top 25 > $O/prof/lines_cfg2_blk_body.txt 2>&1
 python tools/ncu_lines.py $O/full_cfg2.ncu-rep blk_spec_factor --top 25 > $O/prof/lines_cfg2_blk_spec_factor.txt 2>&1
 python tools/ncu_lines.py $O/full_cfg3.ncu-rep "blk_segment|blk_band_narrow" --top 25 > $O/prof/lines_cfg3_blk_body.txt 2>&1
-python tools/ncu_lines.py $O/full_cfg4.ncu-rep chain_final --top 25 > $O/prof/lines_cfg4_chain_final.txt 2>&1
+python tools/ncu_lines.py $O/full_cfg4.ncu-rep chain_tm --top 25 > $O/prof/lines_cfg4_chain_tm.txt 2>&1
+python tools/ncu_lines.py $O/full_cfg4.ncu-rep chain_solve --skip 1 --top 25 > $O/prof/lines_cfg4_chain_final.txt 2>&1
 mkdir -p /tmp/ncu_reps && mv $O/*.ncu-rep /tmp/ncu_reps/ 2>/dev/null
 du -sh $O

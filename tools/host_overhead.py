@@ -30,3 +30,28 @@ for _ in range(200):
     F.close()
 torch.cuda.synchronize()
 print(f"factor only: {(time.perf_counter() - t0) / 200 * 1e6:.1f} us")
+
+# production loop (bench.py other_configs): refactor + async solve per step,
+# host time to enqueue vs. device time per step, config-0 size
+A0, f0 = psg.generate_config(0, 1 << 20, 1)
+x0 = torch.empty_like(f0)
+H = psg.parallel_factor(A0, 1024)
+for _ in range(20):
+    H.refactor(A0)
+    H.solve_async(f0, x0)
+H.sync()
+torch.cuda.synchronize()
+for timing in (False, True):
+    N = 200
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    t0 = time.perf_counter()
+    for _ in range(N):
+        H.refactor(A0)
+        H.solve_async(f0, x0, timing=timing)
+    t1 = time.perf_counter()
+    H.sync()
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"cfg0 refactor+solve_async (timing={timing}): host enqueue {(t1 - t0) / N * 1e6:.1f} us/step, "
+          f"device {e0.elapsed_time(e1) / N * 1e3:.1f} us/step")
