@@ -160,12 +160,31 @@ def _addr(t):
     return C.c_void_p(t.ctypes.data)
 
 
+_raw_stream = None  # torch's current-stream query, cached once CUDA is initialised
+
+
+def _ptr_of(t):
+    if t is None:
+        return 0
+    if hasattr(t, "data_ptr") and not isinstance(t, np.ndarray):
+        return t.data_ptr()
+    return t.ctypes.data
+
+
 def _stream_ptr(stream):
+    global _raw_stream
     if stream is None:
+        if _raw_stream is not None:
+            return C.c_void_p(_raw_stream())
         try:
             import torch
             if torch.cuda.is_available() and torch.cuda.is_initialized():
-                return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+                getraw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+                if getraw is not None:
+                    _raw_stream = lambda: getraw(torch.cuda.current_device())  # noqa: E731
+                else:
+                    _raw_stream = lambda: torch.cuda.current_stream().cuda_stream  # noqa: E731
+                return C.c_void_p(_raw_stream())
         except Exception:
             pass
         return None
@@ -199,9 +218,17 @@ class StructuredMatrix:
         return _is_cuda(self.data)
 
     def desc(self) -> _Desc:
+        # cached while the storage stays the same (refactor loops call this per step)
+        key = (id(self.data), id(self.corner), self.kind, self.n, self.m, self.s, self.r, self.corner_rows,
+               self.corner_cols, _ptr_of(self.data), _ptr_of(self.corner))
+        c = self.__dict__.get("_desc_cache")
+        if c is not None and c[0] == key:
+            return c[1]
         n_data = int(self.data.numel() if hasattr(self.data, "numel") else self.data.size)
-        return _Desc(int(self.kind), self.n, self.m, self.s, self.r, _addr(self.data), n_data,
-                     _addr(self.corner), self.corner_rows, self.corner_cols, 1 if self.on_device else 0)
+        d = _Desc(int(self.kind), self.n, self.m, self.s, self.r, _addr(self.data), n_data,
+                  _addr(self.corner), self.corner_rows, self.corner_cols, 1 if self.on_device else 0)
+        self.__dict__["_desc_cache"] = (key, d)
+        return d
 
 
 @dataclass
@@ -265,18 +292,24 @@ class ParallelFactorization:
     def solve(self, f, x=None, stats: SolveStats | None = None, stream=None):
         return solve(self, f, stats=stats, x=x, stream=stream)
 
+    def _errbuf(self):
+        e = self.__dict__.get("_err")
+        if e is None:
+            e = self.__dict__["_err"] = C.create_string_buffer(512)
+        return e
+
     def refactor(self, A: "StructuredMatrix | None" = None, stream=None):
         """New values, same structure (psg_refactor): refactor in place."""
         A = self.A if A is None else A
         d = A.desc()
-        err = C.create_string_buffer(512)
+        err = self._errbuf()
         _check(lib().psg_refactor(self.handle, C.byref(d), _stream_ptr(stream), err, 512), err)
         self.A = A
         return self
 
     def solve_async(self, f, x, timing: bool = False, stream=None):
         """Enqueue a device solve; x is final after sync() (psg_solve_async)."""
-        err = C.create_string_buffer(512)
+        err = self._errbuf()
         _check(lib().psg_solve_async(self.handle, _addr(f), _addr(x), 1 if timing else 0, _stream_ptr(stream),
                                      err, 512), err)
         return x
