@@ -101,3 +101,20 @@ def test_chain_async_and_refactor(cuda):
     x = psg.solve(F, dfs[1]).cpu().numpy()
     want, _ = O.parallel_solve(A2, p, f2)
     assert O.rel_err(x, want) <= 1e-10
+
+
+@pytest.mark.parametrize("m,nb", [(2, (1 << 20) + 3), (4, 70001), (8, 16 * 16 * 16 + 1), (2, 16 * 16 + 2)])
+def test_chain_hierarchy_depths(cuda, m, nb):
+    """Reduced hierarchies of 2..5 levels, exact multiples of the 16-block
+    chunk and ragged tails (the one-launch factor's arrival counters and the
+    per-CTA down sweep), against the oracle's sequential solve."""
+    A, f = random_bvp(m, nb, 100 + m)
+    want = O.solve_sequential(A, f)
+    x, st, F, _ = _gpu(cuda, A, 8, f)
+    assert st.speculative == 1
+    assert O.rel_err(x, want) <= 1e-10
+    assert O.residual(A, x, f) <= max(1e-13, 2.0 * O.residual(A, want, f))
+    # a second factor + solve on the same handle (self-resetting counters)
+    F.refactor()
+    x2 = psg.solve(F, _dev(cuda, f)).cpu().numpy()
+    assert np.array_equal(x, x2)
