@@ -95,8 +95,10 @@ int psg_factor(const psg_desc* A, int p, int strategy, double tol, void* stream,
 
 /* Three-phase solve (solve).  f and x are n-vectors, device pointers when
  * on_device = 1, else host pointers (copied through the handle's device
- * buffers; pinned host memory makes the copies fast).  Blocks until the
- * result and its certificate are known.  stats may be NULL. */
+ * buffers; pinned host memory makes the copies fast and, for large
+ * speculative tridiagonal solves without stats, lets f arrive and x leave in
+ * overlapping row chunks).  Blocks until the result and its certificate are
+ * known.  stats may be NULL. */
 int psg_solve(const psg_handle* h, const double* f, double* x, int on_device, void* stream,
               psg_stats* stats, char* err, size_t errlen);
 

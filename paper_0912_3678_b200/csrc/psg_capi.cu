@@ -375,6 +375,25 @@ EventPool& event_pool() {
   return *p;
 }
 
+// Process-wide copy streams per device (host-buffer pipelines): one for each
+// PCIe direction, non-blocking, ordered against the compute stream by events.
+void copy_streams(cudaStream_t& in, cudaStream_t& out) {
+  static std::mutex mu;
+  static std::map<int, std::pair<cudaStream_t, cudaStream_t>> by_dev;
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(mu);
+  auto it = by_dev.find(dev);
+  if (it == by_dev.end()) {
+    cudaStream_t a, b;
+    CUDA_TRY(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&b, cudaStreamNonBlocking));
+    it = by_dev.emplace(dev, std::make_pair(a, b)).first;
+  }
+  in = it->second.first;
+  out = it->second.second;
+}
+
 // ----------------------------------------------------------------------------
 // Tridiagonal solver: speculative single-level path + exact multi-level path
 // ----------------------------------------------------------------------------
@@ -457,6 +476,8 @@ struct TriSolver {
     S0 = S;
     maxlen0 = maxlen;
     minlen0 = minlen;
+    hstart0.clear();
+    if (st) hstart0 = *st;
     if (st) {
       start0.alloc(st->size());
       len0.alloc(ln->size());
@@ -506,7 +527,7 @@ struct TriSolver {
                   DevStatus* host_out = nullptr) {
     const int nsep = S0.nseg - 1;
     tri_spec_sep_kernel<<<blocks_for((long)blocks_for(nsep, kSepPerWarp) * 32, 256), 256, 0, s>>>(F, S0, wts.p,
-                                                                                                   xsep.p, st);
+                                                                                                   xsep.p, st, 0, nsep);
     LAUNCH_CHECK();
     launches += 1;
     if (ev) {  // the speculative reduced matrix is diagonal: phase 2 is fused into phase 1
@@ -515,6 +536,78 @@ struct TriSolver {
     }
     k3_and_cert(F, x, xsep.p, st, s, /*pdl=*/true, host_out);  // K3 stages its rows while the separators finish
   }
+
+  // ---- host buffers: chunked pipeline ---------------------------------------
+  // f arrives in row chunks on copy stream `ci`; the separators whose windows
+  // are complete and the segments between them are solved per chunk on `s`;
+  // each chunk of x leaves on copy stream `co` while later chunks of f are
+  // still arriving (both PCIe directions busy at once).  Same kernels and
+  // arithmetic as spec_solve; the certificate covers every separator.
+  void spec_solve_host(const double* hf, double* hx, double* df, double* dx, DevStatus* st, cudaStream_t s,
+                       cudaStream_t ci, cudaStream_t co, cudaEvent_t* evs, int nchunk, DevStatus* host_out) {
+    const int nsep = S0.nseg - 1;
+    auto seg_start = [&](int i) -> long {  // first row of segment i (n for i == nseg)
+      if (i >= S0.nseg) return n;
+      if (S0.start) return hstart0[i];
+      return (long)i * (S0.base + 1) + (i < S0.rem ? i : S0.rem);
+    };
+    // entry: the previous users of df / dx on s are done before the copies
+    CUDA_TRY(cudaEventRecord(evs[0], s));
+    CUDA_TRY(cudaStreamWaitEvent(ci, evs[0], 0));
+    CUDA_TRY(cudaStreamWaitEvent(co, evs[0], 0));
+    const RowArr F = make_rows(df, 0, n);
+    int ja = 0;  // separators done
+    for (int g = 0; g < nchunk; ++g) {
+      const long r0 = (long)n * g / nchunk, r1 = (long)n * (g + 1) / nchunk;
+      CUDA_TRY(cudaMemcpyAsync(df + r0, hf + r0, sizeof(double) * (r1 - r0), cudaMemcpyHostToDevice, ci));
+      CUDA_TRY(cudaEventRecord(evs[1 + 2 * g], ci));
+      CUDA_TRY(cudaStreamWaitEvent(s, evs[1 + 2 * g], 0));
+      // separators whose f window (t +- 32) lies in rows < r1; all of them at the end
+      int jb = ja;
+      if (g == nchunk - 1) {
+        jb = nsep;
+      } else {
+        while (jb < nsep && seg_start(jb + 1) - 1 + kHalo < r1) ++jb;
+      }
+      const int ib = g == nchunk - 1 ? S0.nseg : jb;  // segments with both separators known
+      const int ia = ja == 0 ? 0 : ja;
+      if (jb > ja) {
+        const int cnt = jb - ja;
+        tri_spec_sep_kernel<<<blocks_for((long)blocks_for(cnt, kSepPerWarp) * 32, 256), 256, 0, s>>>(
+            F, S0, wts.p, xsep.p, g == 0 ? st : nullptr, ja, jb);
+        LAUNCH_CHECK();
+        launches += 1;
+      } else if (g == 0) {
+        tri_spec_sep_kernel<<<1, 32, 0, s>>>(F, S0, wts.p, xsep.p, st, 0, 0);  // status reset only
+        LAUNCH_CHECK();
+        launches += 1;
+      }
+      if (ib > ia) {
+        TriSolveArgs a{};
+        a.A = A0;
+        a.F = F;
+        a.S = S0;
+        a.xsep = xsep.p;
+        a.x = dx;
+        a.crec = crec.p;
+        a.status = st;
+        a.seg0 = ia;
+        segment_solve(a, ib - ia, maxlen0, s, /*pdl=*/true);
+        launches += 1;
+        CUDA_TRY(cudaEventRecord(evs[2 + 2 * g], s));
+        CUDA_TRY(cudaStreamWaitEvent(co, evs[2 + 2 * g], 0));
+        const long x0 = seg_start(ia), x1 = seg_start(ib);
+        CUDA_TRY(cudaMemcpyAsync(hx + x0, dx + x0, sizeof(double) * (x1 - x0), cudaMemcpyDeviceToHost, co));
+      }
+      ja = jb;
+    }
+    launch_pdl(tri_cert_kernel, dim3(blocks_for(nsep, 256)), dim3(256), 0, s, nsep, (const double4*)crec.p, st,
+               host_out, cctr.p);
+    launches += 1;
+    CUDA_TRY(cudaEventRecord(evs[0], co));
+    CUDA_TRY(cudaStreamWaitEvent(s, evs[0], 0));  // x is on the host when s reaches this point
+  }
+  std::vector<int> hstart0;  // host copy of S0's explicit starts (refined maps)
 
   // ---- exact multi-level path ----------------------------------------------
   void build_levels(cudaStream_t s) {
@@ -1527,6 +1620,7 @@ struct psg_handle {
   DevBuf<DevStatus> d_status;
   DevStatus* h_status = nullptr;  // pinned slot
   DevBuf<double> d_f, d_x;        // host-path staging
+  std::vector<cudaEvent_t> host_evs;  // host-path chunk events
   cudaEvent_t ev_f0 = nullptr, ev_f1 = nullptr, ev_done = nullptr, ev[4] = {};
   std::mutex mu;
   int factor_launches = 0, solve_launches = 0;
@@ -1555,6 +1649,7 @@ struct psg_handle {
       for (int j = 0; j < 4; ++j)
         if (ring_t[i][j]) event_pool().put(ring_t[i][j]);
     }
+    for (cudaEvent_t e : host_evs) event_pool().put(e);
     if (h_status) pinned_slots().put(h_status);
     if (h_ring) cudaFreeHost(h_ring);
   }
@@ -2184,6 +2279,30 @@ int psg_solve(const psg_handle* hc, const double* f, double* x, int on_device, v
     const int n = h->A.n;
     const double* df = f;
     double* dx = x;
+    // host buffers, speculative tridiagonal path: chunked pipeline (x leaves
+    // while f still arrives); stats requests take the phase-timed path below
+    if (!on_device && !stats && !h->piv && !h->generic && h->use_spec() && h->spec_factored && n >= (1 << 22)) {
+      h->d_f.alloc(n);
+      h->d_x.alloc(n);
+      const int nchunk = std::min(16, std::max(2, n >> 22));
+      while ((int)h->host_evs.size() < 1 + 2 * nchunk) h->host_evs.push_back(event_pool().get());
+      cudaStream_t ci, co;
+      copy_streams(ci, co);
+      h->tri.launches = 0;
+      h->tri.spec_solve_host(f, x, h->d_f.p, h->d_x.p, h->d_status.p, s, ci, co, h->host_evs.data(), nchunk,
+                             h->h_status);
+      CUDA_TRY(cudaEventRecord(h->ev_done, s));
+      CUDA_TRY(cudaEventSynchronize(h->ev_done));
+      const Outcome o = read_status(*h->h_status);
+      h->solve_launches = h->tri.launches;
+      if (!o.bad && o.cert <= h->cert_tol) return 0;
+      h->speculative = false;  // speculative interface rejected: exact re-solve of the staged f
+      tri_solve_blocking(h, h->d_f.p, h->d_x.p, s, nullptr);
+      CUDA_TRY(cudaMemcpyAsync(x, h->d_x.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaStreamSynchronize(s));
+      CUDA_TRY(cudaEventRecord(h->ev_done, s));
+      return 0;
+    }
     if (!on_device) {
       h->d_f.alloc(n);
       h->d_x.alloc(n);

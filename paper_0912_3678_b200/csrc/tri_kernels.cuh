@@ -316,8 +316,10 @@ __global__ void __launch_bounds__(32) tri_spec_factor_kernel(TriRows A, SegMap S
 // before the first reduction so each warp keeps ~16 coalesced 256-byte
 // requests in flight.
 constexpr int kSepPerWarp = 4;
+// Separators [jbase, jend) only (the host path solves in row chunks).
 __global__ void __launch_bounds__(256) tri_spec_sep_kernel(RowArr F, SegMap S, const double* __restrict__ wts,
-                                                            double* __restrict__ xsep, DevStatus* reset) {
+                                                            double* __restrict__ xsep, DevStatus* reset, int jbase,
+                                                            int jend) {
   pdl_trigger();  // K3 may launch and stage its rows while the separators finish
   const int lane = threadIdx.x & 31;
   if (reset && blockIdx.x == 0 && threadIdx.x < kCertSlots + 2) {  // first kernel of the solve: fresh status
@@ -329,8 +331,8 @@ __global__ void __launch_bounds__(256) tri_spec_sep_kernel(RowArr F, SegMap S, c
       reset->pivot_seg = 0x7fffffff;
   }
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nsep = S.nseg - 1;
-  const int j0 = warp * kSepPerWarp;
+  const int nsep = jend;
+  const int j0 = jbase + warp * kSepPerWarp;
   if (j0 >= nsep) return;
   double w1[kSepPerWarp], w2[kSepPerWarp], f1[kSepPerWarp], f2[kSepPerWarp];
   long tt[kSepPerWarp];
@@ -386,6 +388,7 @@ struct TriSolveArgs {
   double* x;           // output, row r at x[r]
   double4* crec;       // per-segment certificate record (NULL: skip), see tri_cert_kernel
   DevStatus* status;
+  int seg0;            // first segment of this launch (the host path solves in row chunks)
 };
 
 template <int M>
@@ -404,7 +407,7 @@ __global__ void __launch_bounds__(32) tri_segment_solve_kernel(TriSolveArgs args
   __shared__ __align__(8) uint64_t bar;
   __shared__ double sepv[4];
   const int lane = threadIdx.x;
-  const int seg = blockIdx.x;
+  const int seg = args.seg0 + blockIdx.x;
   long s;
   int L;
   seg_of(args.S, seg, s, L);

@@ -264,3 +264,34 @@ def test_large_n_64bit_offsets(cuda):
         assert abs(lhs - f[r].item()) <= 1e-12 * (abs(a * xm) + abs(b * x[r].item()) + abs(c * xp) + abs(f[r].item()))
     del A, f, x, F
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("n,p", [((1 << 22) + 12345, 4096), (1 << 23, 1024), ((1 << 22) + 7, 2)])
+def test_host_buffer_pipeline(cuda, n, p):
+    """Host f / x without stats: f arrives in row chunks, x leaves per chunk
+    while later chunks still arrive (psg_solve's pipelined host path).  Same
+    result, bit for bit, as the device-resident solve."""
+    A, f = O.generate_config(0, n, 21)
+    GA = psg.StructuredMatrix(A.kind, A.n, A.m, A.s, A.r, _dev(cuda, A.data))
+    F = psg.parallel_factor(GA, p)
+    x_host = psg.solve(F, f)            # numpy in -> numpy out, pipelined
+    x_dev = psg.solve(F, _dev(cuda, f)).cpu().numpy()
+    assert np.array_equal(x_host, x_dev)
+    want = O.solve_sequential(A, f)
+    assert O.rel_err(x_host, want) <= 1e-12
+    assert O.residual(A, x_host, f) <= 1e-13
+
+
+def test_host_buffer_pipeline_fallback(cuda):
+    # weak dominance through the pipelined host path: certificate rejects, exact re-solve
+    n, p = (1 << 22) + 3, 512
+    A = _toeplitz(n, -1.0, 2.02, -1.0)
+    f = np.sin(np.arange(n) * 0.37)
+    GA = psg.StructuredMatrix(A.kind, A.n, A.m, A.s, A.r, _dev(cuda, A.data))
+    F = psg.parallel_factor(GA, p)
+    x = psg.solve(F, f)
+    assert O.residual(A, x, f) <= 1e-13
+    st = psg.SolveStats()
+    x2 = psg.solve(F, _dev(cuda, f), st).cpu().numpy()  # the handle stays exact
+    assert st.speculative == 0
+    assert O.rel_err(x, x2) <= 1e-12
