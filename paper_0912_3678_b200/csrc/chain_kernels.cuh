@@ -284,16 +284,19 @@ __global__ void __launch_bounds__(64) chain_tm_kernel(ChainLevelArgs g, ChainTre
         }
       }
     }
+    // M = R^-1 column by column (unit right-hand sides: the zeros above the
+    // unit fold away), kept in registers and stored over R
+    double Mi[MB * MB];
 #pragma unroll
-    for (int c = 0; c < 2 * MB; ++c) {
+    for (int c = 0; c < MB; ++c) {
       double y[MB];
 #pragma unroll
-      for (int i = 0; i < MB; ++i) y[i] = c < MB ? -slot[i * RW + c] : (i == c - MB ? 1.0 : 0.0);
+      for (int i = 0; i < MB; ++i) y[i] = i == c ? 1.0 : 0.0;
 #pragma unroll
       for (int i = 0; i < MB; ++i)
 #pragma unroll
         for (int k = 0; k < MB; ++k)
-          if (k < i) y[i] = fma(-R[i * MB + k], y[k], y[i]);
+          if (k < i && k >= c) y[i] = fma(-R[i * MB + k], y[k], y[i]);
 #pragma unroll
       for (int ii = 0; ii < MB; ++ii) {
         const int i = MB - 1 - ii;
@@ -303,7 +306,24 @@ __global__ void __launch_bounds__(64) chain_tm_kernel(ChainLevelArgs g, ChainTre
         y[i] *= R[i * MB + i];
       }
 #pragma unroll
-      for (int i = 0; i < MB; ++i) slot[i * RW + c] = y[i];  // T (c < MB) over S, M over R
+      for (int i = 0; i < MB; ++i) {
+        Mi[i * MB + c] = y[i];
+        slot[i * RW + MB + c] = y[i];
+      }
+    }
+    // T = -M S column by column (independent FMA chains), stored over S
+#pragma unroll
+    for (int c = 0; c < MB; ++c) {
+      double sc[MB];
+#pragma unroll
+      for (int l = 0; l < MB; ++l) sc[l] = slot[l * RW + c];
+#pragma unroll
+      for (int i = 0; i < MB; ++i) {
+        double acc = -Mi[i * MB] * sc[0];
+#pragma unroll
+        for (int l = 1; l < MB; ++l) acc = fma(-Mi[i * MB + l], sc[l], acc);
+        slot[i * RW + c] = acc;
+      }
     }
     // ---- pair-interleave the slot in place (double2 (i, q) <-> (q, i)), then
     // one TMA bulk store of the block: block b, double2 q*MB + i = row i,
