@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(64) chain_tm_kernel(ChainLevelArgs g, ChainTre
   __syncwarp();
   if (lane < nblk) bulk_g2s(sm + lane * SLOT, g.data + MB * MB + (bfirst - 1 + lane) * BW, BW * 8, bar);
   mbar_wait(bar, 0);
-  // ---- per lane: LU of R (no pivoting), then T = -R^-1 S and M = R^-1 column by column
+  // ---- per lane: M = R^-1 (Gauss-Jordan, no pivoting), then T = -M S
   double* slot = sm + lane * SLOT;
   if (lane < nblk) {
     double R[MB * MB];
@@ -269,48 +269,31 @@ __global__ void __launch_bounds__(64) chain_tm_kernel(ChainLevelArgs g, ChainTre
     for (int i = 0; i < MB; ++i)
 #pragma unroll
       for (int c = 0; c < MB; ++c) R[(i) * MB + (c)] = slot[i * RW + MB + c];
+    // M = R^-1 by in-place Gauss-Jordan (no pivoting, like the reference's Lu):
+    // MB dependent pivot steps of MB^2 independent updates; stored over R
 #pragma unroll
     for (int k = 0; k < MB; ++k) {
       const double p = fast_rcp(R[k * MB + k]);
-      R[k * MB + k] = p;  // keep the reciprocal pivot
+      double col[MB], row[MB];
 #pragma unroll
-      for (int i = 0; i < MB; ++i) {
-        if (i > k) {
-          const double l = R[i * MB + k] * p;
-          R[i * MB + k] = l;
+      for (int i = 0; i < MB; ++i) col[i] = R[i * MB + k];
 #pragma unroll
-          for (int c = 0; c < MB; ++c)
-            if (c > k) R[i * MB + c] = fma(-l, R[k * MB + c], R[i * MB + c]);
-        }
-      }
-    }
-    // M = R^-1 column by column (unit right-hand sides: the zeros above the
-    // unit fold away), kept in registers and stored over R
-    double Mi[MB * MB];
-#pragma unroll
-    for (int c = 0; c < MB; ++c) {
-      double y[MB];
-#pragma unroll
-      for (int i = 0; i < MB; ++i) y[i] = i == c ? 1.0 : 0.0;
+      for (int j = 0; j < MB; ++j) row[j] = R[k * MB + j] * p;
 #pragma unroll
       for (int i = 0; i < MB; ++i)
 #pragma unroll
-        for (int k = 0; k < MB; ++k)
-          if (k < i && k >= c) y[i] = fma(-R[i * MB + k], y[k], y[i]);
-#pragma unroll
-      for (int ii = 0; ii < MB; ++ii) {
-        const int i = MB - 1 - ii;
-#pragma unroll
-        for (int k = 0; k < MB; ++k)
-          if (k > i) y[i] = fma(-R[i * MB + k], y[k], y[i]);
-        y[i] *= R[i * MB + i];
-      }
-#pragma unroll
-      for (int i = 0; i < MB; ++i) {
-        Mi[i * MB + c] = y[i];
-        slot[i * RW + MB + c] = y[i];
-      }
+        for (int j = 0; j < MB; ++j) {
+          if (i == k)
+            R[i * MB + j] = j == k ? p : row[j];
+          else
+            R[i * MB + j] = j == k ? -col[i] * p : fma(-col[i], row[j], R[i * MB + j]);
+        }
     }
+    double (&Mi)[MB * MB] = R;
+#pragma unroll
+    for (int i = 0; i < MB; ++i)
+#pragma unroll
+      for (int c = 0; c < MB; ++c) slot[i * RW + MB + c] = Mi[i * MB + c];
     // T = -M S column by column (independent FMA chains), stored over S
 #pragma unroll
     for (int c = 0; c < MB; ++c) {
