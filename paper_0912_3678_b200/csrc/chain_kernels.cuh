@@ -180,7 +180,7 @@ __device__ __forceinline__ void chain_load_maps(double* sm, const double* src, i
 // recorded), the multipliers below the diagonal
 template <int MB>
 __device__ void chain_top_factor(const ChainLevelArgs& g, const ChainTree& t, double* sm, int lane) {
-  constexpr int SLOT = ChainSmem<MB>::SLOT, RW = 2 * MB, MM = MB * MB, GP = MB + 1;
+  constexpr int SLOT = ChainSmem<MB>::SLOT, MM = MB * MB, GP = MB + 1;
   chain_load_maps<MB>(sm, t.phi[t.T - 1], t.P[t.T - 1], lane);
   chain_tree16<MB>(sm, 1, lane);
   double* G = sm + SLOT;
@@ -221,7 +221,7 @@ __device__ void chain_top_factor(const ChainLevelArgs& g, const ChainTree& t, do
 // this warp is the last arriver of the enclosing chunk
 template <int MB>
 __device__ void chain_factor_up(const ChainLevelArgs& g, const ChainTree& t, double* sm, long w, int lane) {
-  constexpr int SLOT = ChainSmem<MB>::SLOT, RW = 2 * MB, MM = MB * MB;
+  constexpr int SLOT = ChainSmem<MB>::SLOT, MM = MB * MB;
   const long nw = ((long)t.P[0] + 1) / 2;  // factor warps (2 level-0 chunks each)
   long c = w;
   for (int l = 1;; ++l) {

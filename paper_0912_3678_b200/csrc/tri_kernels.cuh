@@ -245,8 +245,8 @@ __global__ void __launch_bounds__(32) tri_spec_factor_kernel(TriRows A, SegMap S
   if (lane == 0) mbar_init(&bar, 3 * kFacSeps);
   __syncwarp();
   for (int task = lane; task < 3 * kFacSeps; task += 32) {
-    const int x = task / kFacSeps, q = task % kFacSeps;
-    const long t = tme;  // q == lane & 15 for every task this lane issues
+    const int x = task / kFacSeps;  // separator task % kFacSeps == lane & 15
+    const long t = tme;
     const RowArr X = x == 0 ? A.a : x == 1 ? A.b : A.c;
     uint32_t tx = 0;
     shifts[task] = stage_issue(X, t - kHalo, t + kHalo + 1, tile + task * kFacPitch, &bar, &tx);
