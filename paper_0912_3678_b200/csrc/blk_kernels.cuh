@@ -1047,6 +1047,13 @@ __device__ __forceinline__ double dmul(double a, double b, int base, int u, int 
     acc = fma(__shfl_sync(0xffffffffu, a, base + u * 4 + l), __shfl_sync(0xffffffffu, b, base + l * 4 + v), acc);
   return acc;
 }
+// the same product with the left operand already held as row u in every
+// lane of that row (no shuffles for it): acc = sum_l arow[l] B(l, v)
+__device__ __forceinline__ double dmul_row(const double (&arow)[4], double b, int base, int v, int K) {
+  double acc = 0.0;
+  for (int l = 0; l < K; ++l) acc = fma(arow[l], __shfl_sync(0xffffffffu, b, base + l * 4 + v), acc);
+  return acc;
+}
 // in-place Gauss-Jordan inverse without pivoting
 __device__ __forceinline__ double dinv(double a, int base, int u, int v, int K, double* rsum) {
   for (int k = 0; k < K; ++k) {
@@ -1128,8 +1135,12 @@ __global__ void __launch_bounds__(128) blk_spec_factor_kernel(BlkSpecArgs g) {
       Nn = ld(r1, tN, oN, kN);
     }
     if (i > 0) {
-      D -= dmul(Fc, dmul(G, Ncp, base, u, v, K), base, u, v, K);
-      Np[i - 1] = dmul(Fc, G, base, u, v, K);
+      // Fc is the left operand of both products: its row u gathered once
+      double frow[4];
+#pragma unroll
+      for (int l = 0; l < 4; ++l) frow[l] = l < K ? __shfl_sync(0xffffffffu, Fc, base + u * 4 + l) : 0.0;
+      D -= dmul_row(frow, dmul(G, Ncp, base, u, v, K), base, v, K);
+      Np[i - 1] = dmul_row(frow, G, base, v, K);
     }
     const double Gi = dinv(D, base, u, v, K, &rsum);
     G = act ? Gi : 0.0;
