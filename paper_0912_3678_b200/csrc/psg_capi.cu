@@ -438,7 +438,46 @@ void launch_segment_solve(const TriSolveArgs& a, int nseg, cudaStream_t s, bool 
 // pdl: K3 stages A and F before waiting for its predecessor -- only valid
 // when neither is produced by the preceding kernel (the speculative solve:
 // user f, predecessor = the separator kernel)
-void segment_solve(const TriSolveArgs& a, int nseg, int maxlen, cudaStream_t s, bool pdl = false) {
+int sm_count() {
+  static int n = [] {
+    int dev = 0, c = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
+    return c > 0 ? c : 148;
+  }();
+  return n;
+}
+
+// persistent K3 (two staging buffers per warp) for 33-row chunks: segments
+// [a.seg0, a.seg0 + nseg) by sm_count() * per-SM warps
+void launch_segment_solve_persist(TriSolveArgs a, int nseg, cudaStream_t s, bool pdl) {
+  constexpr int bytes = 2 * TriWarpSmem<33>::BYTES;
+  ensure_smem(reinterpret_cast<const void*>(tri_segment_solve_kernel<33, true>), bytes);
+  static const int per_sm = [] {
+    const char* e = getenv("PSG_K3_PERSIST");
+    return e && atoi(e) > 0 ? atoi(e) : 3;
+  }();
+  const int grid = std::min(nseg, sm_count() * per_sm);
+  a.seg_end = a.seg0 + nseg;
+  if (pdl)
+    launch_pdl(tri_segment_solve_kernel<33, true>, dim3(grid), dim3(32), bytes, s, a);
+  else
+    tri_segment_solve_kernel<33, true><<<grid, 32, bytes, s>>>(a);
+}
+
+void segment_solve(const TriSolveArgs& a, int nseg, int maxlen, cudaStream_t s, bool pdl = false,
+                   bool persist = false) {
+  // off unless PSG_K3_PERSIST = warps per SM is set: measured slower (3 warps
+  // per SM: 0.558 ms/step against 0.451 for one warp per segment)
+  static const bool persist_on = [] {
+    const char* e = getenv("PSG_K3_PERSIST");
+    return e && atoi(e) > 0;
+  }();
+  if (persist && persist_on && maxlen > 32 * 17 && maxlen <= 32 * 33 && nseg > 4 * sm_count()) {
+    launch_segment_solve_persist(a, nseg, s, pdl);
+    LAUNCH_CHECK();
+    return;
+  }
   if (maxlen <= 32 * 5)
     launch_segment_solve<5>(a, nseg, s, pdl);
   else if (maxlen <= 32 * 9)
@@ -517,7 +556,7 @@ struct TriSolver {
     a.x = x;
     a.crec = crec.p;
     a.status = st;
-    segment_solve(a, S0.nseg, maxlen0, s, pdl);
+    segment_solve(a, S0.nseg, maxlen0, s, pdl, /*persist=*/true);
     launch_pdl(tri_cert_kernel, dim3(blocks_for(S0.nseg - 1, 256)), dim3(256), 0, s, S0.nseg - 1,
                (const double4*)crec.p, st, host_out, cctr.p);
     launches += 2;

@@ -389,6 +389,7 @@ struct TriSolveArgs {
   double4* crec;       // per-segment certificate record (NULL: skip), see tri_cert_kernel
   DevStatus* status;
   int seg0;            // first segment of this launch (the host path solves in row chunks)
+  int seg_end;         // persistent launch: segments [seg0 + blockIdx.x, seg_end) with stride gridDim.x
 };
 
 template <int M>
@@ -398,43 +399,61 @@ struct TriWarpSmem {
   static constexpr int BYTES = 4 * ROW * 8;
 };
 
-template <int M>
+// PERSIST: one warp per SM slot loops over segments seg0 + blockIdx.x,
+// + gridDim.x, ... with two staging buffers -- the next segment's rows are in
+// flight while this one is solved (continuous HBM traffic per warp).
+template <int M, bool PERSIST = false>
 __global__ void __launch_bounds__(32) tri_segment_solve_kernel(TriSolveArgs args) {
   static_assert(M % 2 == 1 && M >= 3, "M must be odd and >= 3");
   constexpr int ROW = TriWarpSmem<M>::ROW;
   constexpr unsigned FULL = 0xffffffffu;
   extern __shared__ __align__(128) double smem[];
-  __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t bars[2];
   __shared__ double sepv[4];
   const int lane = threadIdx.x;
-  const int seg = args.seg0 + blockIdx.x;
+  const int nseg = args.S.nseg;
+  const int seg_begin = args.seg0 + blockIdx.x;
+  const int seg_end = PERSIST ? args.seg_end : seg_begin + 1;
+  const int stride = PERSIST ? gridDim.x : 1;
+  const RowArr X = lane == 0 ? args.A.a : lane == 1 ? args.A.b : lane == 2 ? args.A.c : args.F;
+  if (lane == 0) {
+    mbar_init(&bars[0], 4);
+    if (PERSIST) mbar_init(&bars[1], 4);
+  }
+  __syncwarp();
+  // ---- staging: lanes 0..3 issue one bulk copy each (a, b, c, f rows s-1 .. s+L)
+  auto issue = [&](int sg, int buf) -> int {
+    long s0;
+    int L0;
+    seg_of(args.S, sg, s0, L0);
+    int sh = 0;
+    if (lane < 4) {
+      uint32_t tx = 0;
+      sh = stage_issue(X, s0 - 1, s0 + L0 + 1, smem + (buf * 4 + (lane & 3)) * ROW, &bars[buf], &tx);
+      mbar_arrive_expect_tx(&bars[buf], tx);
+    }
+    return sh;
+  };
+  int shift = seg_begin < seg_end ? issue(seg_begin, 0) : 0;
+  pdl_wait();  // the separator values come from the previous kernel (staging above overlaps it)
+  int k = 0;
+  for (int seg = seg_begin; seg < seg_end; seg += stride, ++k) {
+  const int buf = PERSIST ? (k & 1) : 0;
+  const int shift_next = (PERSIST && seg + stride < seg_end) ? issue(seg + stride, buf ^ 1) : 0;
   long s;
   int L;
   seg_of(args.S, seg, s, L);
-  const int nseg = args.S.nseg;
   const bool has_l = seg > 0, has_r = seg < nseg - 1;
-
-  // ---- staging: lanes 0..3 issue one bulk copy each (a, b, c, f rows s-1 .. s+L)
-  const RowArr X = lane == 0 ? args.A.a : lane == 1 ? args.A.b : lane == 2 ? args.A.c : args.F;
   const long lo = s - 1, hi = s + L + 1;
-  double* const base = smem + (lane & 3) * ROW;
-  if (lane == 0) mbar_init(&bar, 4);
-  __syncwarp();
-  int shift = 0;
-  if (lane < 4) {
-    uint32_t tx = 0;
-    shift = stage_issue(X, lo, hi, base, &bar, &tx);
-    mbar_arrive_expect_tx(&bar, tx);
-  }
+  double* const base = smem + (buf * 4 + (lane & 3)) * ROW;
   // sX[q] = body row q; sX[-1] / sX[L] = left / right separator rows
-  double* sA = smem + 0 * ROW + 2 + __shfl_sync(FULL, shift, 0);
-  double* sB = smem + 1 * ROW + 2 + __shfl_sync(FULL, shift, 1);
-  double* sC = smem + 2 * ROW + 2 + __shfl_sync(FULL, shift, 2);
-  double* sF = smem + 3 * ROW + 2 + __shfl_sync(FULL, shift, 3);
-  pdl_wait();  // the separator values come from the previous kernel (staging above overlaps it)
+  double* sA = smem + (buf * 4 + 0) * ROW + 2 + __shfl_sync(FULL, shift, 0);
+  double* sB = smem + (buf * 4 + 1) * ROW + 2 + __shfl_sync(FULL, shift, 1);
+  double* sC = smem + (buf * 4 + 2) * ROW + 2 + __shfl_sync(FULL, shift, 2);
+  double* sF = smem + (buf * 4 + 3) * ROW + 2 + __shfl_sync(FULL, shift, 3);
   const double xl = has_l ? args.xsep[seg - 1] : 0.0;
   const double xr = has_r ? args.xsep[seg] : 0.0;
-  mbar_wait(&bar, 0);
+  mbar_wait(&bars[buf], PERSIST ? ((k >> 1) & 1) : 0);
   if (lane < 4) stage_fixup(X, lo, hi, base + 1 + shift);
   __syncwarp();
   if (lane == 0) {
@@ -566,6 +585,12 @@ __global__ void __launch_bounds__(32) tri_segment_solve_kernel(TriSolveArgs args
     if (args.crec)
       args.crec[seg] = make_double4(has_r ? sepv[0] * sF[L - 1] : 0.0, has_r ? sepv[1] * xr : 0.0,
                                     has_r ? sepv[2] : 0.0, has_l ? sepv[3] * sF[0] : 0.0);
+  }
+  if (PERSIST) {  // this buffer is refilled by the next iteration's prefetch
+    fence_proxy_async_smem();
+    __syncwarp();
+  }
+  shift = shift_next;
   }
 }
 
