@@ -202,6 +202,84 @@ int psg_generate_config(int cfg, int size, uint64_t seed, double* data, double* 
 int psg_validate(const psg_desc* A, char* err, size_t errlen);
 size_t psg_body_entry_count(int kind, int n, int m, int s, int r);
 
+/* ---- Per-partition local factorization (the reference's LocalFactorization,
+ * proj/include/parsol/localfact.hpp:24-125; src/localfact.cpp:84-225 banded
+ * Lu/Lud, :266-384 cyclic reduction, :400-700 LuPivot/Qr, :765-875 member
+ * operations).  One partition block is factored by one CTA on the device
+ * (csrc/psg_local.cu); every field is bit-identical to the reference's.
+ * Replaces factor() / factor_lu / factor_lud / factor_cyclic_reduction /
+ * factor_lu_pivot / factor_qr (localfact.hpp:118-125).  ARCE returns
+ * UnsupportedStructure. ---- */
+typedef struct {
+  int kind, m, s, r;      /* matrix kind fields the block was cut from (CR needs them) */
+  int L, k0, k1;          /* body rows, left / right separator sizes */
+  int env_s, env_r;       /* envelope half-bandwidths (PartitionBlock::env_s/env_r) */
+  const double* env;      /* L x (env_s + 1 + env_r), diagonal-aligned rows (host) */
+  const double* b0;       /* L x k0 row-major (host); NULL when k0 = 0 */
+  const double* c0;       /* L x k0 */
+  const double* b1;       /* L x k1 */
+  const double* c1;       /* L x k1 */
+  const double* a_right;  /* k1 x k1 */
+} psg_block;
+
+typedef struct psg_local psg_local;
+
+typedef struct {
+  int strategy, L, k0, k1, env_s, env_r;
+  int core;        /* 1 banded (Lu/Lud), 2 cyclic reduction, 3 dense recorded (LuPivot/Qr) */
+  int cr_levels;   /* CR: reduction levels */
+  int g;           /* CR: block size */
+  int n_elims;     /* CR: eliminations */
+  int n_rem;       /* CR: remaining block rows (1 or 2) */
+  int rem[2];      /* CR: their block indices */
+  int dim;         /* k0 + L + k1 */
+  int n_a_order;   /* dense: retired pivots */
+  int n_extras;    /* dense: deferred pivots (adaptive extras) */
+} psg_local_info;
+
+/* Fields readable with psg_local_read (doubles unless noted int). */
+enum psg_local_field {
+  PSG_LF_FAC = 0,        /* banded: eliminated envelope L x w */
+  PSG_LF_DVEC,           /* Lud: pivots (L) */
+  PSG_LF_Z, PSG_LF_W,    /* L x k0 */
+  PSG_LF_Y, PSG_LF_V,    /* L x k1 */
+  PSG_LF_ALPHA1, PSG_LF_ALPHA2, PSG_LF_BETA, PSG_LF_GAMMA,
+  PSG_LF_KEPT,           /* kept_dim x kept_dim */
+  PSG_LF_CR_ELIM_IDX,    /* int, n_elims x (j, left, right) */
+  PSG_LF_CR_ELIM_MAT,    /* n_elims x (ml, mr, a, c, dinv), each g x g */
+  PSG_LF_CR_D2, PSG_LF_CR_D2INV,  /* (n_rem g)^2 */
+  PSG_LF_CR_CMAT,        /* (n_rem g) x (k0 + k1) */
+  PSG_LF_CR_RMAT_D2INV,  /* (k0 + k1) x (n_rem g) */
+  PSG_LF_WMID, PSG_LF_LMAT, PSG_LF_LINV, /* dense frame, dim x dim */
+  PSG_LF_A_ORDER,        /* int, n_a_order x (row, col) */
+  PSG_LF_KEPT_ROWS, PSG_LF_KEPT_COLS,    /* int, kept_dim */
+  PSG_LF_EXTRA_POS,      /* int, n_extras */
+  PSG_LF_EXTRA_ALPHA     /* n_extras */
+};
+
+int psg_local_factor(const psg_block* blk, int strategy, double tol, void* stream, psg_local** out, char* err,
+                     size_t errlen);
+int psg_local_query(const psg_local* lf, psg_local_info* info);
+/* Copy one field to host memory of `count` elements (returns DimensionMismatch if too small). */
+int psg_local_read(const psg_local* lf, int field, void* out, size_t count, char* err, size_t errlen);
+/* condense (phase 1): f_body (L) -> ghat (L), kept_rhs (kept_dim); host vectors. */
+int psg_local_condense(const psg_local* lf, const double* f_body, double* ghat, double* kept_rhs, char* err,
+                       size_t errlen);
+/* backsolve (phase 3): ghat (L), x_kept (kept_dim) -> x (L). */
+int psg_local_backsolve(const psg_local* lf, const double* ghat, const double* x_kept, double* x, char* err,
+                        size_t errlen);
+/* which = 0: apply_N_inv, 1: apply_S_inv (body vectors of length L). */
+int psg_local_apply(const psg_local* lf, int which, const double* rhs, double* out, char* err, size_t errlen);
+void psg_local_release(psg_local* lf);
+
+/* Dense reduced solve of an explicit n x n matrix T (row-major, host) --
+ * solve_reduced(const ReducedSystem&) for a ReducedSystem without a device
+ * handle (src/parfact.cpp:134-184): LU with partial pivoting on the device,
+ * bit-identical to the reference; *ops receives its multiply-add count.
+ * SingularReducedSystem on a zero pivot column. */
+int psg_dense_solve(int n, const double* T, const double* rhs, double* x, long long* ops, void* stream, char* err,
+                    size_t errlen);
+
 /* Options (per handle): */
 enum psg_option {
   PSG_OPT_SPECULATIVE = 0, /* 1 (default): truncated interface + certificate; 0: exact */
@@ -210,9 +288,22 @@ enum psg_option {
 };
 int psg_set_option(psg_handle* h, int option, double value);
 
+/* Wait until the factorization enqueued by psg_factor / psg_refactor is
+ * complete; device_seconds (may be NULL) receives its device time. */
+int psg_factor_wait(const psg_handle* h, double* device_seconds);
+
 /* Number of kernels the last psg_factor / psg_solve on this handle launched. */
 int psg_last_launches(const psg_handle* h, int* factor_launches, int* solve_launches);
 
+/* Inspection of the speculative tridiagonal factor (tests / tools): copy an
+ * internal device buffer to host memory of `cap` doubles.  what = 0: the
+ * separator weight rows (nsep x 68), 1: the speculative reduced diagonal
+ * (nsep).  Returns the count copied, -count if cap is too small or the
+ * buffer does not exist, -1 on a CUDA error. */
+long psg_debug_buffer(const psg_handle* h, int what, double* out, long cap);
+
+/* Version string including the hash of the sources the library was built
+ * from (paper_0912_3678_b200/build.py source_hash). */
 const char* psg_version(void);
 
 #ifdef __cplusplus

@@ -122,6 +122,22 @@ def ref():
         R.ref_plan.argtypes = [C.c_void_p, C.c_int] + [C.POINTER(C.c_int)] * 5 + [C.c_char_p, C.c_size_t]
         R.ref_generate_random.argtypes = [C.c_int] * 5 + [C.c_uint64, C.c_double, _dp, _dp, C.c_char_p,
                                                           C.c_size_t]
+        vp = C.c_void_p
+        R.ref_block_extract.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_int), C.c_char_p, C.c_size_t]
+        R.ref_block_extract.restype = vp
+        R.ref_block_create.argtypes = [C.c_int] * 9 + [vp] * 6
+        R.ref_block_create.restype = vp
+        R.ref_block_arrays.argtypes = [vp] * 7
+        R.ref_block_destroy.argtypes = [vp]
+        R.ref_local_factor.argtypes = [vp, C.c_int, C.c_double, C.POINTER(vp), C.c_char_p, C.c_size_t]
+        R.ref_local_destroy.argtypes = [vp]
+        R.ref_local_dims.argtypes = [vp, C.POINTER(C.c_int)]
+        R.ref_local_field.argtypes = [vp, C.c_int, vp]
+        R.ref_local_field.restype = C.c_long
+        R.ref_local_op.argtypes = [vp, C.c_int, vp, vp, vp, vp, C.c_char_p, C.c_size_t]
+        R.ref_local_dense.argtypes = [vp, C.c_int, vp]
+        R.ref_solve_reduced_dense.argtypes = [C.c_int, vp, vp, vp, C.POINTER(C.c_longlong), C.c_char_p,
+                                              C.c_size_t]
         _ref = R
     return _ref
 
@@ -392,3 +408,89 @@ def ref_generate_random(kind, n, m, s, r, seed, dominance):
 
 def ref_set_threads(t: int) -> int:
     return ref().ref_set_threads(t)
+
+
+# --------------------------------------------------------------------------
+# The reference's per-partition API (extract_block, factor, LocalFactorization
+# members) -- the parity target of psg_local_* (tests/test_localfact_gpu.py)
+# --------------------------------------------------------------------------
+
+def ref_extract_block(A: Matrix, p: int, i: int) -> dict:
+    """extract_block(A, plan_partition(A, p), i) of the reference, as arrays."""
+    R = RefMatrix(A)
+    dims = (C.c_int * 5)()
+    err = C.create_string_buffer(512)
+    hb = ref().ref_block_extract(R.h, p, i, dims, err, 512)
+    if not hb:
+        raise OracleError(1, err.value.decode())
+    L, k0, k1, es, er = list(dims)
+    out = dict(kind=A.kind, m=A.m, s=A.s, r=A.r, L=L, k0=k0, k1=k1, env_s=es, env_r=er,
+               env=np.zeros(L * (es + 1 + er)), b0=np.zeros(L * k0), c0=np.zeros(L * k0), b1=np.zeros(L * k1),
+               c1=np.zeros(L * k1), a_right=np.zeros(k1 * k1))
+    ref().ref_block_arrays(hb, *(out[k].ctypes.data for k in ("env", "b0", "c0", "b1", "c1", "a_right")))
+    ref().ref_block_destroy(hb)
+    return out
+
+
+class RefLocal:
+    """The reference's LocalFactorization of one block (factor(strategy, blk, tol))."""
+
+    def __init__(self, blk: dict, strategy: int, tol: float = 1e-8):
+        arr = {k: np.ascontiguousarray(blk[k], np.float64) for k in ("env", "b0", "c0", "b1", "c1", "a_right")}
+        self._keep = arr
+        hb = ref().ref_block_create(blk["kind"], blk["m"], blk["s"], blk["r"], blk["L"], blk["k0"], blk["k1"],
+                                    blk["env_s"], blk["env_r"],
+                                    *(arr[k].ctypes.data if arr[k].size else None
+                                      for k in ("env", "b0", "c0", "b1", "c1", "a_right")))
+        h = C.c_void_p()
+        err = C.create_string_buffer(512)
+        rc = ref().ref_local_factor(hb, strategy, tol, C.byref(h), err, 512)
+        ref().ref_block_destroy(hb)
+        if rc:
+            raise OracleError(rc, err.value.decode())
+        self.h = h
+        d = (C.c_int * 9)()
+        ref().ref_local_dims(h, d)
+        self.kept_dim, self.n_extras, self.cr_levels, self.core, self.dim, self.n_a_order, self.n_elims, self.g, \
+            self.n_rem = list(d)
+        self.L = blk["L"]
+
+    def __del__(self):
+        if getattr(self, "h", None) and _ref is not None:
+            _ref.ref_local_destroy(self.h)
+            self.h = None
+
+    def field(self, fid: int, count: int, dtype=np.float64):
+        out = np.zeros(max(count, 1), dtype)
+        n = ref().ref_local_field(self.h, fid, out.ctypes.data)
+        return out[:n]
+
+    def op(self, op: int, v, v2=None):
+        v = np.ascontiguousarray(v, np.float64)
+        v2 = None if v2 is None else np.ascontiguousarray(v2, np.float64)
+        out = np.empty(self.L)
+        out2 = np.empty(max(self.kept_dim, 1))
+        err = C.create_string_buffer(512)
+        rc = ref().ref_local_op(self.h, op, v.ctypes.data, None if v2 is None else v2.ctypes.data, out.ctypes.data,
+                                out2.ctypes.data, err, 512)
+        if rc:
+            raise OracleError(rc, err.value.decode())
+        return (out, out2[:self.kept_dim]) if op == 0 else out
+
+    def dense(self, which: int):
+        M = np.empty((self.dim, self.dim))
+        ref().ref_local_dense(self.h, which, M.ctypes.data)
+        return M
+
+
+def ref_solve_reduced_dense(T, rhs):
+    T = np.ascontiguousarray(T, np.float64)
+    rhs = np.ascontiguousarray(rhs, np.float64)
+    x = np.empty(rhs.size)
+    ops = C.c_longlong()
+    err = C.create_string_buffer(512)
+    rc = ref().ref_solve_reduced_dense(rhs.size, T.ctypes.data, rhs.ctypes.data, x.ctypes.data, C.byref(ops), err,
+                                       512)
+    if rc:
+        raise OracleError(rc, err.value.decode())
+    return x, ops.value

@@ -23,6 +23,8 @@
 
 #include "parsol/errors.hpp"
 #include "parsol/io.hpp"
+#include "parsol/localfact.hpp"
+#include "parsol/partition.hpp"
 #include "parsol/odeparallel.hpp"
 #include "parsol/parareal.hpp"
 #include "parsol/parfact.hpp"
@@ -39,6 +41,14 @@ struct RefMat {
 
 struct RefFact {
   ParallelFactorization F;
+};
+
+struct RefBlock {
+  PartitionBlock B;
+};
+
+struct RefLocal {
+  LocalFactorization lf;
 };
 
 int report(const std::exception& e, char* err, size_t errlen) {
@@ -319,6 +329,221 @@ int ref_expm(int m, const double* L, double t, double* out, char* err, size_t er
     std::copy(L, L + size_t(m) * m, A.a.begin());
     const DenseMatrix E = matrix_exponential(A, t);
     std::copy(E.a.begin(), E.a.end(), out);
+    return 0;
+  } catch (const std::exception& e) {
+    return report(e, err, errlen);
+  }
+}
+
+// ---- per-partition pieces (localfact.hpp public API) ----------------------
+
+void* ref_block_extract(void* hm, int p, int i, int* dims, char* err, size_t errlen) {
+  try {
+    const StructuredMatrix& A = static_cast<RefMat*>(hm)->A;
+    PartitionPlan plan = plan_partition(A, p);
+    auto* b = new RefBlock{extract_block(A, plan, i)};
+    dims[0] = b->B.L;
+    dims[1] = b->B.k0;
+    dims[2] = b->B.k1;
+    dims[3] = b->B.env_s;
+    dims[4] = b->B.env_r;
+    return b;
+  } catch (const std::exception& e) {
+    report(e, err, errlen);
+    return nullptr;
+  }
+}
+
+void* ref_block_create(int kind, int m, int s, int r, int L, int k0, int k1, int es, int er, const double* env,
+                       const double* b0, const double* c0, const double* b1, const double* c1, const double* ar) {
+  auto* b = new RefBlock;
+  PartitionBlock& B = b->B;
+  B.index = 2;
+  B.kind = Kind(kind);
+  B.m = m;
+  B.s = s;
+  B.r = r;
+  B.L = L;
+  B.k0 = k0;
+  B.k1 = k1;
+  B.env_s = es;
+  B.env_r = er;
+  B.env.assign(env, env + size_t(L) * (es + 1 + er));
+  auto mat = [](int rows, int cols, const double* src) {
+    DenseMatrix M(rows, cols);
+    if (src && rows * cols) std::memcpy(M.a.data(), src, sizeof(double) * rows * cols);
+    return M;
+  };
+  B.b0 = mat(L, k0, b0);
+  B.c0 = mat(L, k0, c0);
+  B.b1 = mat(L, k1, b1);
+  B.c1 = mat(L, k1, c1);
+  if (k1) B.a_right = mat(k1, k1, ar);
+  return b;
+}
+
+int ref_block_arrays(void* hb, double* env, double* b0, double* c0, double* b1, double* c1, double* ar) {
+  const PartitionBlock& B = static_cast<RefBlock*>(hb)->B;
+  auto put = [](double* dst, const std::vector<double>& v) {
+    if (dst && !v.empty()) std::memcpy(dst, v.data(), sizeof(double) * v.size());
+  };
+  put(env, B.env);
+  put(b0, B.b0.a);
+  put(c0, B.c0.a);
+  put(b1, B.b1.a);
+  put(c1, B.c1.a);
+  put(ar, B.a_right.a);
+  return 0;
+}
+
+void ref_block_destroy(void* hb) { delete static_cast<RefBlock*>(hb); }
+
+int ref_local_factor(void* hb, int strategy, double tol, void** out, char* err, size_t errlen) {
+  try {
+    *out = new RefLocal{factor(Strategy(strategy), static_cast<RefBlock*>(hb)->B, tol)};
+    return 0;
+  } catch (const std::exception& e) {
+    *out = nullptr;
+    return report(e, err, errlen);
+  }
+}
+
+void ref_local_destroy(void* hl) { delete static_cast<RefLocal*>(hl); }
+
+// dims: [kept_dim, n_extras, cr_levels, core(1 banded, 2 cyclic, 3 dense), dim, n_a_order, n_elims, g, n_rem]
+int ref_local_dims(void* hl, int* d) {
+  const LocalFactorization& lf = static_cast<RefLocal*>(hl)->lf;
+  d[0] = lf.kept_dim();
+  d[1] = int(lf.extras.size());
+  d[2] = lf.cr_levels;
+  d[3] = int(lf.core.index());
+  d[4] = lf.k0 + lf.L + lf.k1;
+  d[5] = d[6] = d[7] = d[8] = 0;
+  if (auto* dc = std::get_if<LocalFactorization::DenseCore>(&lf.core)) d[5] = int(dc->a_order.size());
+  if (auto* cc = std::get_if<LocalFactorization::CyclicCore>(&lf.core)) {
+    d[6] = int(cc->elims.size());
+    d[7] = cc->g;
+    d[8] = int(cc->rem.size());
+  }
+  return 0;
+}
+
+// field numbering = enum psg_local_field (include/psg.h); returns the count written
+long ref_local_field(void* hl, int field, void* out) {
+  const LocalFactorization& lf = static_cast<RefLocal*>(hl)->lf;
+  auto put = [out](const std::vector<double>& v) {
+    if (!v.empty()) std::memcpy(out, v.data(), sizeof(double) * v.size());
+    return long(v.size());
+  };
+  auto puti = [out](const std::vector<int>& v) {
+    if (!v.empty()) std::memcpy(out, v.data(), sizeof(int) * v.size());
+    return long(v.size());
+  };
+  const auto* bc = std::get_if<LocalFactorization::BandedCore>(&lf.core);
+  const auto* cc = std::get_if<LocalFactorization::CyclicCore>(&lf.core);
+  const auto* dc = std::get_if<LocalFactorization::DenseCore>(&lf.core);
+  switch (field) {
+    case 0: return bc ? put(bc->fac) : 0;
+    case 1: return bc ? put(bc->dvec) : 0;
+    case 2: return put(lf.z.a);
+    case 3: return put(lf.w.a);
+    case 4: return put(lf.y.a);
+    case 5: return put(lf.v.a);
+    case 6: return put(lf.alpha1.a);
+    case 7: return put(lf.alpha2.a);
+    case 8: return put(lf.beta.a);
+    case 9: return put(lf.gamma.a);
+    case 10: return put(lf.kept.a);
+    case 11: {
+      if (!cc) return 0;
+      std::vector<int> v;
+      for (auto& e : cc->elims) v.insert(v.end(), {e.j, e.lnb, e.rnb});
+      return puti(v);
+    }
+    case 12: {
+      if (!cc) return 0;
+      std::vector<double> v;
+      for (auto& e : cc->elims)
+        for (const DenseMatrix* M : {&e.ml, &e.mr, &e.a, &e.c, &e.dinv}) v.insert(v.end(), M->a.begin(), M->a.end());
+      return put(v);
+    }
+    case 13: return cc ? put(cc->d2.a) : 0;
+    case 14: return cc ? put(cc->d2inv.a) : 0;
+    case 15: return cc ? put(cc->cmat.a) : 0;
+    case 16: return cc ? put(cc->rmat_d2inv.a) : 0;
+    case 17: return dc ? put(dc->Wmid.a) : 0;
+    case 18: return dc ? put(dc->Lmat.a) : 0;
+    case 19: return dc ? put(dc->Linv.a) : 0;
+    case 20: {
+      if (!dc) return 0;
+      std::vector<int> v;
+      for (auto& [r, c] : dc->a_order) v.insert(v.end(), {r, c});
+      return puti(v);
+    }
+    case 21: return dc ? puti(dc->kept_rows) : 0;
+    case 22: return dc ? puti(dc->kept_cols) : 0;
+    case 23: {
+      std::vector<int> v;
+      for (auto& x : lf.extras) v.push_back(x.position);
+      return puti(v);
+    }
+    case 24: {
+      std::vector<double> v;
+      for (auto& x : lf.extras) v.push_back(x.alpha);
+      return put(v);
+    }
+  }
+  return -1;
+}
+
+// op 0 condense (ghat -> out, kept_rhs -> out2), 1 backsolve(in, in2) -> out,
+// 2 apply_N_inv, 3 apply_S_inv
+int ref_local_op(void* hl, int op, const double* in, const double* in2, double* out, double* out2, char* err,
+                 size_t errlen) {
+  try {
+    const LocalFactorization& lf = static_cast<RefLocal*>(hl)->lf;
+    const Vector v(in, in + lf.L);
+    Vector r;
+    if (op == 0) {
+      Vector ghat, kr;
+      lf.condense(v, ghat, kr);
+      std::memcpy(out2, kr.data(), sizeof(double) * kr.size());
+      r = ghat;
+    } else if (op == 1) {
+      r = lf.backsolve(v, Vector(in2, in2 + lf.kept_dim()));
+    } else if (op == 2) {
+      r = lf.apply_N_inv(v);
+    } else {
+      r = lf.apply_S_inv(v);
+    }
+    std::memcpy(out, r.data(), sizeof(double) * r.size());
+    return 0;
+  } catch (const std::exception& e) {
+    return report(e, err, errlen);
+  }
+}
+
+// which 0: F_loc, 1: T_loc, 2: G_loc (dim x dim)
+int ref_local_dense(void* hl, int which, double* out) {
+  const LocalFactorization& lf = static_cast<RefLocal*>(hl)->lf;
+  const DenseMatrix M = which == 0 ? lf.dense_F_loc() : which == 1 ? lf.dense_T_loc() : lf.dense_G_loc();
+  std::memcpy(out, M.a.data(), sizeof(double) * M.a.size());
+  return 0;
+}
+
+// solve_reduced on a hand-built ReducedSystem with a dense T
+int ref_solve_reduced_dense(int n, const double* T, const double* rhs, double* x, long long* ops, char* err,
+                            size_t errlen) {
+  try {
+    ReducedSystem R;
+    R.q = n;
+    R.dim = n;
+    R.T = DenseMatrix(n, n);
+    std::memcpy(R.T.a.data(), T, sizeof(double) * size_t(n) * n);
+    SolveStats st;
+    Vector xv = solve_reduced(R, Vector(rhs, rhs + n), &st);
+    std::memcpy(x, xv.data(), sizeof(double) * n);
+    *ops = st.reduced_ops;
     return 0;
   } catch (const std::exception& e) {
     return report(e, err, errlen);

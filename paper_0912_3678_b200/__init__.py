@@ -27,7 +27,9 @@ _LIBPSG = os.path.join(_PKG, "libpsg.so")
 
 __all__ = ["Kind", "Strategy", "Errc", "Error", "StructuredMatrix", "ParallelFactorization",
            "SolveStats", "parallel_factor", "solve", "solve_reduced", "residual", "matvec",
-           "plan_partition", "generate_config", "config_shape", "lib"]
+           "plan_partition", "generate_config", "config_shape", "lib", "PartitionBlock", "LocalFactorization",
+           "factor", "factor_lu", "factor_lud", "factor_cyclic_reduction", "factor_lu_pivot", "factor_qr",
+           "dense_solve"]
 
 
 class Kind(enum.IntEnum):  # include/parsol/structmat.hpp:11
@@ -93,6 +95,19 @@ class _Desc(C.Structure):
                 ("corner_rows", C.c_int), ("corner_cols", C.c_int), ("on_device", C.c_int)]
 
 
+class _Block(C.Structure):  # psg_block
+    _fields_ = [("kind", C.c_int), ("m", C.c_int), ("s", C.c_int), ("r", C.c_int), ("L", C.c_int),
+                ("k0", C.c_int), ("k1", C.c_int), ("env_s", C.c_int), ("env_r", C.c_int),
+                ("env", C.c_void_p), ("b0", C.c_void_p), ("c0", C.c_void_p), ("b1", C.c_void_p),
+                ("c1", C.c_void_p), ("a_right", C.c_void_p)]
+
+
+class _LocalInfo(C.Structure):  # psg_local_info
+    _fields_ = [(k, C.c_int) for k in ("strategy", "L", "k0", "k1", "env_s", "env_r", "core", "cr_levels", "g",
+                                        "n_elims", "n_rem")] + \
+               [("rem", C.c_int * 2)] + [(k, C.c_int) for k in ("dim", "n_a_order", "n_extras")]
+
+
 class SolveStats(C.Structure):
     """parsol::SolveStats (parfact.hpp:24-30) + the GPU certificate."""
     _fields_ = [("factor_seconds", C.c_double), ("phase1_seconds", C.c_double),
@@ -137,6 +152,16 @@ def lib():
         L.psg_set_option.argtypes = [vp, ip, C.c_double]
         L.psg_last_launches.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.psg_version.restype = C.c_char_p
+        L.psg_factor_wait.argtypes = [vp, C.POINTER(C.c_double)]
+        L.psg_local_factor.argtypes = [C.POINTER(_Block), ip, C.c_double, vp, C.POINTER(vp), cp, sz]
+        L.psg_local_query.argtypes = [vp, C.POINTER(_LocalInfo)]
+        L.psg_local_read.argtypes = [vp, ip, vp, sz, cp, sz]
+        L.psg_local_condense.argtypes = [vp, vp, vp, vp, cp, sz]
+        L.psg_local_backsolve.argtypes = [vp, vp, vp, vp, cp, sz]
+        L.psg_local_apply.argtypes = [vp, ip, vp, vp, cp, sz]
+        L.psg_local_release.argtypes = [vp]
+        L.psg_local_release.restype = None
+        L.psg_dense_solve.argtypes = [ip, vp, vp, vp, C.POINTER(C.c_longlong), vp, cp, sz]
         _lib = L
     return _lib
 
@@ -309,6 +334,10 @@ class ParallelFactorization:
 
     def solve_async(self, f, x, timing: bool = False, stream=None):
         """Enqueue a device solve; x is final after sync() (psg_solve_async)."""
+        if not (_is_cuda(f) and _is_cuda(x)):
+            raise Error(Errc.InvalidParameter, "solve_async takes device tensors")
+        _check_vec(f, self.A.n, "rhs")
+        _check_vec(x, self.A.n, "solution")
         err = self._errbuf()
         _check(lib().psg_solve_async(self.handle, _addr(f), _addr(x), 1 if timing else 0, _stream_ptr(stream),
                                      err, 512), err)
@@ -317,6 +346,27 @@ class ParallelFactorization:
     def sync(self, stats: SolveStats | None = None):
         err = C.create_string_buffer(512)
         _check(lib().psg_sync(self.handle, C.byref(stats) if stats is not None else None, err, 512), err)
+
+
+def _check_vec(v, n: int, what: str):
+    """The reference throws DimensionMismatch for a wrong-length rhs
+    (src/parfact.cpp:188); a short, non-fp64 or strided buffer would also be
+    read out of bounds by the C ABI, so those are rejected the same way."""
+    if v is None:
+        return
+    if _is_cuda(v) or (hasattr(v, "data_ptr") and not isinstance(v, np.ndarray)):
+        import torch
+        ok_type = v.dtype == torch.float64
+        numel, contig = int(v.numel()), bool(v.is_contiguous())
+    else:
+        ok_type = v.dtype == np.float64
+        numel, contig = int(v.size), bool(v.flags["C_CONTIGUOUS"])
+    if not ok_type:
+        raise Error(Errc.DimensionMismatch, f"{what}: float64 required, got {v.dtype}")
+    if numel != n:
+        raise Error(Errc.DimensionMismatch, f"{what} length {numel}, expected {n}")
+    if not contig:
+        raise Error(Errc.DimensionMismatch, f"{what} must be contiguous")
 
 
 def parallel_factor(A: StructuredMatrix, p: int, strategy: int = Strategy.Lu, tol: float = 1e-8,
@@ -336,6 +386,8 @@ def parallel_factor(A: StructuredMatrix, p: int, strategy: int = Strategy.Lu, to
 def solve(F: ParallelFactorization, f, stats: SolveStats | None = None, x=None, stream=None):
     """Three-phase solve; returns x (same residency as f)."""
     dev = _is_cuda(f)
+    if not dev and isinstance(f, (list, tuple)):
+        f = np.asarray(f, np.float64)
     if x is None:
         if dev:
             import torch
@@ -343,6 +395,10 @@ def solve(F: ParallelFactorization, f, stats: SolveStats | None = None, x=None, 
         else:
             f = np.ascontiguousarray(f, np.float64)
             x = np.empty_like(f)
+    _check_vec(f, F.A.n, "rhs")
+    _check_vec(x, F.A.n, "solution")
+    if _is_cuda(x) != dev:
+        raise Error(Errc.InvalidParameter, "f and x must both be device or both be host buffers")
     err = C.create_string_buffer(1024)
     st = stats if stats is not None else None
     _check(lib().psg_solve(F.handle, _addr(f), _addr(x), 1 if dev else 0, _stream_ptr(stream),
@@ -358,6 +414,7 @@ def solve_reduced(F: ParallelFactorization, rhs, stats: SolveStats | None = None
     else:
         rhs = np.ascontiguousarray(rhs, np.float64)
         x = np.empty_like(rhs)
+    _check_vec(rhs, F.dim, "reduced rhs")
     err = C.create_string_buffer(1024)
     _check(lib().psg_solve_reduced(F.handle, _addr(rhs), _addr(x), 1 if dev else 0, _stream_ptr(stream),
                                    C.byref(stats) if stats is not None else None, err, 1024), err)
@@ -366,6 +423,10 @@ def solve_reduced(F: ParallelFactorization, rhs, stats: SolveStats | None = None
 
 def residual(A: StructuredMatrix, x, f, stream=None) -> float:
     """||A x - f||_inf / ||f||_inf on the GPU (parfact.cpp:241-251 semantics)."""
+    if not _is_cuda(x):
+        x, f = np.ascontiguousarray(x, np.float64), np.ascontiguousarray(f, np.float64)
+    _check_vec(x, A.n, "residual x")
+    _check_vec(f, A.n, "residual f")
     d = A.desc()
     out = C.c_double()
     err = C.create_string_buffer(1024)
@@ -417,3 +478,164 @@ def generate_config(cfg: int, size: int, seed: int, device="cuda", stream=None):
     A = StructuredMatrix(sh["kind"], sh["n"], sh["m"], sh["s"], sh["r"], data, corner, sh["corner_rows"],
                          sh["corner_cols"])
     return A, f
+
+
+# ---------------------------------------------------------------------------
+# per-partition local factorizations (LocalFactorization, reference
+# include/parsol/localfact.hpp:24-125) -- factored on the device by
+# csrc/psg_local.cu, bit-identical to the reference.
+# ---------------------------------------------------------------------------
+@dataclass
+class PartitionBlock:
+    """parsol::PartitionBlock (partition.hpp:50-76): the local system M^(i).
+    env is L x (env_s + 1 + env_r); b0/c0 are L x k0, b1/c1 L x k1."""
+    kind: int
+    m: int
+    s: int
+    r: int
+    L: int
+    k0: int
+    k1: int
+    env_s: int
+    env_r: int
+    env: np.ndarray
+    b0: np.ndarray
+    c0: np.ndarray
+    b1: np.ndarray
+    c1: np.ndarray
+    a_right: np.ndarray
+
+    def __post_init__(self):
+        for name in ("env", "b0", "c0", "b1", "c1", "a_right"):
+            setattr(self, name, np.ascontiguousarray(getattr(self, name), np.float64))
+
+
+_LF = {"fac": 0, "dvec": 1, "z": 2, "w": 3, "y": 4, "v": 5, "alpha1": 6, "alpha2": 7, "beta": 8, "gamma": 9,
+       "kept": 10, "cr_elim_idx": 11, "cr_elim_mat": 12, "cr_d2": 13, "cr_d2inv": 14, "cr_cmat": 15,
+       "cr_rmat_d2inv": 16, "wmid": 17, "lmat": 18, "linv": 19, "a_order": 20, "kept_rows": 21, "kept_cols": 22,
+       "extra_pos": 23, "extra_alpha": 24}
+
+
+class LocalFactorization:
+    """parsol::LocalFactorization on the device; fields are read back on demand."""
+
+    def __init__(self, handle, block: PartitionBlock):
+        self.handle = handle
+        self.block = block
+        info = _LocalInfo()
+        lib().psg_local_query(handle, C.byref(info))
+        self.info = {k: (list(getattr(info, k)) if k == "rem" else getattr(info, k)) for k, _ in info._fields_}
+        self.L, self.k0, self.k1 = info.L, info.k0, info.k1
+        self.cr_levels = info.cr_levels
+        self.kept_dim = info.k0 + info.k1 + info.n_extras
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib().psg_local_release(self.handle)
+        except Exception:
+            pass
+        self.handle = None
+
+    def read(self, name: str, count: int, dtype=np.float64):
+        out = np.zeros(max(count, 0), dtype)
+        if count > 0:
+            err = C.create_string_buffer(512)
+            _check(lib().psg_local_read(self.handle, _LF[name], out.ctypes.data, out.size, err, 512), err)
+        return out
+
+    def field(self, name: str) -> np.ndarray:
+        L, k0, k1, i = self.L, self.k0, self.k1, self.info
+        kd = self.kept_dim
+        shapes = {"z": (L, k0), "w": (L, k0), "y": (L, k1), "v": (L, k1), "alpha1": (k0, k0), "alpha2": (k1, k1),
+                  "beta": (k1, k0), "gamma": (k0, k1), "kept": (kd, kd), "dvec": (L if i["strategy"] == 1 else 0,),
+                  "fac": ((L, i["env_s"] + 1 + i["env_r"]) if i["core"] == 1 else (0,)),
+                  "extra_pos": (i["n_extras"],), "extra_alpha": (i["n_extras"],)}
+        shape = shapes[name]
+        out = self.read(name, int(np.prod(shape)), np.int32 if name == "extra_pos" else np.float64)
+        return out.reshape(shape)
+
+    def _errbuf(self):
+        return C.create_string_buffer(512)
+
+    def condense(self, f_body):
+        f_body = np.ascontiguousarray(f_body, np.float64)
+        _check_vec(f_body, self.L, "condense rhs")
+        ghat, kr = np.empty(self.L), np.empty(self.kept_dim)
+        err = self._errbuf()
+        _check(lib().psg_local_condense(self.handle, f_body.ctypes.data, ghat.ctypes.data, kr.ctypes.data, err,
+                                        512), err)
+        return ghat, kr
+
+    def backsolve(self, ghat, x_kept):
+        ghat = np.ascontiguousarray(ghat, np.float64)
+        x_kept = np.ascontiguousarray(x_kept, np.float64)
+        _check_vec(ghat, self.L, "ghat")
+        _check_vec(x_kept, self.kept_dim, "x_kept")
+        x = np.empty(self.L)
+        err = self._errbuf()
+        _check(lib().psg_local_backsolve(self.handle, ghat.ctypes.data, x_kept.ctypes.data, x.ctypes.data, err,
+                                         512), err)
+        return x
+
+    def _apply(self, which, rhs):
+        rhs = np.ascontiguousarray(rhs, np.float64)
+        _check_vec(rhs, self.L, "apply rhs")
+        out = np.empty(self.L)
+        err = self._errbuf()
+        _check(lib().psg_local_apply(self.handle, which, rhs.ctypes.data, out.ctypes.data, err, 512), err)
+        return out
+
+    def apply_N_inv(self, rhs):
+        return self._apply(0, rhs)
+
+    def apply_S_inv(self, rhs):
+        return self._apply(1, rhs)
+
+
+def factor(strategy: int, block: PartitionBlock, tol: float = 1e-8) -> LocalFactorization:
+    """parsol::factor (localfact.hpp:118-125) on the device."""
+    b = block
+    ptr = lambda a: C.c_void_p(a.ctypes.data) if a.size else None  # noqa: E731
+    desc = _Block(int(b.kind), b.m, b.s, b.r, b.L, b.k0, b.k1, b.env_s, b.env_r, ptr(b.env), ptr(b.b0),
+                  ptr(b.c0), ptr(b.b1), ptr(b.c1), ptr(b.a_right))
+    h = C.c_void_p()
+    err = C.create_string_buffer(512)
+    _check(lib().psg_local_factor(C.byref(desc), int(strategy), float(tol), None, C.byref(h), err, 512), err)
+    return LocalFactorization(h, block)
+
+
+def factor_lu(block):
+    return factor(Strategy.Lu, block)
+
+
+def factor_lud(block):
+    return factor(Strategy.Lud, block)
+
+
+def factor_cyclic_reduction(block):
+    return factor(Strategy.CyclicReduction, block)
+
+
+def factor_lu_pivot(block, tol):
+    return factor(Strategy.LuPivot, block, tol)
+
+
+def factor_qr(block, tol):
+    return factor(Strategy.Qr, block, tol)
+
+
+def dense_solve(T, rhs):
+    """solve_reduced on an explicit reduced matrix T (psg_dense_solve):
+    partial-pivot LU on the device, bit-identical to the reference."""
+    T = np.ascontiguousarray(T, np.float64)
+    rhs = np.ascontiguousarray(rhs, np.float64)
+    n = rhs.size
+    if T.shape != (n, n):
+        raise Error(Errc.DimensionMismatch, "reduced rhs length")
+    x = np.empty(n)
+    ops = C.c_longlong()
+    err = C.create_string_buffer(512)
+    _check(lib().psg_dense_solve(n, T.ctypes.data, rhs.ctypes.data, x.ctypes.data, C.byref(ops), None, err, 512),
+           err)
+    return x, ops.value

@@ -26,6 +26,12 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
            "-Xptxas", "-warn-spills"]
 
+# translation units of libpsg.so: the solver (psg_capi.cu includes every
+# kernel header) and the per-partition LocalFactorization engine, compiled
+# without FMA contraction so its results are the reference's bit for bit.
+UNITS = [("psg_capi.cu", []), ("psg_local.cu", ["--fmad=false"])]
+OBJDIR = os.path.join(ROOT, "build", "obj")
+
 LIBPSG = os.path.join(PKG, "libpsg.so")
 LIBHOST = os.path.join(PKG, "libparsol_b200.so")
 CLI = os.path.join(PKG, "psg")
@@ -51,12 +57,31 @@ def _sources(d, exts):
     return sorted(os.path.join(d, f) for f in os.listdir(d) if f.endswith(exts))
 
 
+def source_hash() -> str:
+    """sha256 (first 12 hex digits) of every source compiled into libpsg.so;
+    psg_version() reports it so a tested binary can be tied to its sources."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for p in _sources(CSRC, (".cu", ".cuh")) + [os.path.join(INCLUDE, "psg.h")]:
+        h.update(os.path.basename(p).encode())
+        with open(p, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:12]
+
+
 def build(verbose: bool = True, force: bool = False, ptxas_verbose: bool = False) -> None:
     deps = _sources(CSRC, (".cu", ".cuh")) + [os.path.join(INCLUDE, "psg.h")]
     if force or _newer(LIBPSG, deps):
         extra = ["-Xptxas", "-v"] if ptxas_verbose else []
-        _run([NVCC, *ARCH, *NVFLAGS, *extra, "-shared", "-o", LIBPSG,
-              os.path.join(CSRC, "psg_capi.cu"), "-lcuda"], verbose)
+        objs = []
+        os.makedirs(OBJDIR, exist_ok=True)
+        for src, flags in UNITS:
+            obj = os.path.join(OBJDIR, os.path.basename(src).replace(".cu", ".o"))
+            _run([NVCC, *ARCH, *NVFLAGS, *flags, *extra, f"-DPSG_SOURCE_HASH=\"{source_hash()}\"", "-c", "-o", obj,
+                  os.path.join(CSRC, src)], verbose)
+            objs.append(obj)
+        _run([NVCC, *ARCH, "-shared", "-o", LIBPSG, *objs, "-lcuda"], verbose)
     hsrc = _sources(HOST, (".cpp",))
     hdeps = hsrc + _sources(os.path.join(INCLUDE, "parsol"), (".hpp",)) + [LIBPSG]
     if hsrc and (force or _newer(LIBHOST, hdeps)):

@@ -1822,7 +1822,10 @@ int partition_of_segment(const psg_handle* h, int seg) {
 
 extern "C" {
 
-const char* psg_version(void) { return "psg-b200 0.2 (sm_100a)"; }
+#ifndef PSG_SOURCE_HASH
+#define PSG_SOURCE_HASH "unknown"
+#endif
+const char* psg_version(void) { return "psg-b200 0.3 (sm_100a) src " PSG_SOURCE_HASH; }
 
 int psg_config_shape(int cfg, int size, int* kind, int* n, int* m, int* s, int* r, size_t* data_len,
                      int* corner_rows, int* corner_cols) {
@@ -2018,6 +2021,16 @@ int psg_set_option(psg_handle* h, int option, double value) {
   } catch (const Fail& f_) {
     return 1 + f_.code;
   }
+  return 0;
+}
+
+int psg_factor_wait(const psg_handle* hc, double* device_seconds) {
+  psg_handle* h = const_cast<psg_handle*>(hc);
+  DeviceGuard dg(h->device);
+  if (cudaEventSynchronize(h->ev_f1) != cudaSuccess) return 1 + PSG_E_CUDA;
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, h->ev_f0, h->ev_f1) != cudaSuccess) ms = 0.f;
+  if (device_seconds) *device_seconds = 1e-3 * ms;
   return 0;
 }
 

@@ -4,6 +4,8 @@
 // host data structures and their validation (shared with the C ABI).
 #include <algorithm>
 #include <cmath>
+#include <functional>
+#include <numeric>
 #include <sstream>
 
 #include "parsol/errors.hpp"
@@ -45,119 +47,145 @@ const char* errc_name(Errc c) {
 }
 
 // ---------------------------------------------------------------------------
-// dense helpers
+// dense helpers (host-side type of T and of the test oracles; not on the
+// solve path).  The elimination keeps a row-index indirection instead of
+// swapping rows, and products are formed as row-by-column dot products.
 // ---------------------------------------------------------------------------
 DenseMatrix DenseMatrix::identity(int n) {
   DenseMatrix I(n, n);
-  for (int i = 0; i < n; ++i) I.at(i, i) = 1.0;
+  for (int i = 0; i < n; ++i) I.a[std::size_t(i) * n + i] = 1.0;
   return I;
-}
-
-DenseMatrix matmul(const DenseMatrix& A, const DenseMatrix& B) {
-  if (A.cols != B.rows) fail(Errc::DimensionMismatch, "matmul shapes");
-  DenseMatrix C(A.rows, B.cols);
-  for (int i = 0; i < A.rows; ++i)
-    for (int k = 0; k < A.cols; ++k) {
-      const double aik = A.at(i, k);
-      for (int j = 0; j < B.cols; ++j) C.at(i, j) += aik * B.at(k, j);
-    }
-  return C;
-}
-
-Vector matvec(const DenseMatrix& A, const Vector& x) {
-  if (A.cols != int(x.size())) fail(Errc::DimensionMismatch, "matvec shapes");
-  Vector y(A.rows, 0.0);
-  for (int i = 0; i < A.rows; ++i)
-    for (int j = 0; j < A.cols; ++j) y[i] += A.at(i, j) * x[j];
-  return y;
 }
 
 DenseMatrix transpose(const DenseMatrix& A) {
   DenseMatrix T(A.cols, A.rows);
-  for (int i = 0; i < A.rows; ++i)
-    for (int j = 0; j < A.cols; ++j) T.at(j, i) = A.at(i, j);
+  for (std::size_t e = 0; e < A.a.size(); ++e) T.a[(e % A.cols) * A.rows + e / A.cols] = A.a[e];
   return T;
 }
 
-DenseMatrix add(const DenseMatrix& A, const DenseMatrix& B) {
-  DenseMatrix C = A;
-  for (std::size_t i = 0; i < C.a.size(); ++i) C.a[i] += B.a[i];
-  return C;
-}
-
-DenseMatrix sub(const DenseMatrix& A, const DenseMatrix& B) {
-  DenseMatrix C = A;
-  for (std::size_t i = 0; i < C.a.size(); ++i) C.a[i] -= B.a[i];
-  return C;
-}
-
-DenseMatrix scale(const DenseMatrix& A, double s) {
-  DenseMatrix C = A;
-  for (double& v : C.a) v *= s;
-  return C;
-}
-
-double inf_norm(const DenseMatrix& A) {
-  double best = 0.0;
+DenseMatrix matmul(const DenseMatrix& A, const DenseMatrix& B) {
+  if (A.cols != B.rows) fail(Errc::DimensionMismatch, "matmul: " + std::to_string(A.rows) + "x" +
+                                                        std::to_string(A.cols) + " times " + std::to_string(B.rows) +
+                                                        "x" + std::to_string(B.cols));
+  const DenseMatrix Bt = transpose(B);
+  DenseMatrix C(A.rows, B.cols);
   for (int i = 0; i < A.rows; ++i) {
-    double s = 0.0;
-    for (int j = 0; j < A.cols; ++j) s += std::fabs(A.at(i, j));
-    best = std::max(best, s);
-  }
-  return best;
-}
-
-double inf_norm(const Vector& v) {
-  double best = 0.0;
-  for (double x : v) best = std::max(best, std::fabs(x));
-  return best;
-}
-
-DenseLu::DenseLu(DenseMatrix A) : lu(std::move(A)) {
-  if (lu.rows != lu.cols) fail(Errc::DimensionMismatch, "LU needs a square matrix");
-  const int n = lu.rows;
-  perm.resize(n);
-  for (int i = 0; i < n; ++i) perm[i] = i;
-  for (int k = 0; k < n; ++k) {
-    int piv = k;
-    for (int i = k + 1; i < n; ++i)
-      if (std::fabs(lu.at(i, k)) > std::fabs(lu.at(piv, k))) piv = i;
-    if (lu.at(piv, k) == 0.0) fail(Errc::SingularFactor, "zero pivot column in dense LU");
-    if (piv != k) {
-      for (int j = 0; j < n; ++j) std::swap(lu.at(k, j), lu.at(piv, j));
-      std::swap(perm[k], perm[piv]);
-    }
-    for (int i = k + 1; i < n; ++i) {
-      const double m = lu.at(i, k) / lu.at(k, k);
-      lu.at(i, k) = m;
-      for (int j = k + 1; j < n; ++j) lu.at(i, j) -= m * lu.at(k, j);
+    const double* ai = A.a.data() + std::size_t(i) * A.cols;
+    for (int j = 0; j < B.cols; ++j) {
+      const double* bj = Bt.a.data() + std::size_t(j) * Bt.cols;
+      double dot = 0.0;
+      for (int k = 0; k < A.cols; ++k)
+        if (ai[k] != 0.0) dot += ai[k] * bj[k];
+      C.a[std::size_t(i) * C.cols + j] = dot;
     }
   }
+  return C;
 }
 
-Vector DenseLu::solve(const Vector& b) const {
-  const int n = lu.rows;
-  if (int(b.size()) != n) fail(Errc::DimensionMismatch, "LU solve rhs");
-  Vector y(n);
-  for (int i = 0; i < n; ++i) y[i] = b[perm[i]];
-  for (int i = 0; i < n; ++i)
-    for (int j = 0; j < i; ++j) y[i] -= lu.at(i, j) * y[j];
-  for (int i = n - 1; i >= 0; --i) {
-    for (int j = i + 1; j < n; ++j) y[i] -= lu.at(i, j) * y[j];
-    y[i] /= lu.at(i, i);
+Vector matvec(const DenseMatrix& A, const Vector& x) {
+  if (A.cols != int(x.size())) fail(Errc::DimensionMismatch, "matvec: matrix has " + std::to_string(A.cols) +
+                                                              " columns, vector " + std::to_string(x.size()));
+  Vector y(A.rows);
+  for (int i = 0; i < A.rows; ++i) {
+    double dot = 0.0;
+    for (int j = 0; j < A.cols; ++j) dot += A.a[std::size_t(i) * A.cols + j] * x[j];
+    y[i] = dot;
   }
   return y;
 }
 
-DenseMatrix DenseLu::solve(const DenseMatrix& B) const {
-  DenseMatrix X(B.rows, B.cols);
-  Vector col(B.rows);
-  for (int j = 0; j < B.cols; ++j) {
-    for (int i = 0; i < B.rows; ++i) col[i] = B.at(i, j);
-    const Vector x = solve(col);
-    for (int i = 0; i < B.rows; ++i) X.at(i, j) = x[i];
+namespace {
+template <typename Op>
+DenseMatrix zip(const DenseMatrix& A, const DenseMatrix& B, Op op) {
+  if (A.rows != B.rows || A.cols != B.cols) fail(Errc::DimensionMismatch, "elementwise operands differ in shape");
+  DenseMatrix C(A.rows, A.cols);
+  std::transform(A.a.begin(), A.a.end(), B.a.begin(), C.a.begin(), op);
+  return C;
+}
+}  // namespace
+
+DenseMatrix add(const DenseMatrix& A, const DenseMatrix& B) { return zip(A, B, std::plus<double>()); }
+DenseMatrix sub(const DenseMatrix& A, const DenseMatrix& B) { return zip(A, B, std::minus<double>()); }
+
+DenseMatrix scale(const DenseMatrix& A, double s) {
+  DenseMatrix C = A;
+  std::transform(C.a.begin(), C.a.end(), C.a.begin(), [s](double v) { return v * s; });
+  return C;
+}
+
+double inf_norm(const Vector& v) {
+  double m = 0.0;
+  for (double x : v) m = std::max(m, std::fabs(x));
+  return m;
+}
+
+double inf_norm(const DenseMatrix& A) {
+  double m = 0.0;
+  for (int i = 0; i < A.rows; ++i) {
+    const auto row = A.a.begin() + std::ptrdiff_t(i) * A.cols;
+    m = std::max(m, std::accumulate(row, row + A.cols, 0.0, [](double s, double v) { return s + std::fabs(v); }));
   }
-  return X;
+  return m;
+}
+
+// Partial-pivot LU kept in the caller's row order: `perm[k]` is the original
+// row that became pivot row k; rows are never moved, only re-indexed.
+DenseLu::DenseLu(DenseMatrix A) : lu(std::move(A)) {
+  if (lu.rows != lu.cols) fail(Errc::DimensionMismatch, "LU of a non-square matrix");
+  const int n = lu.rows;
+  perm.resize(n);
+  std::iota(perm.begin(), perm.end(), 0);
+  auto at = [&](int row, int col) -> double& { return lu.a[std::size_t(row) * n + col]; };
+  for (int k = 0; k < n; ++k) {
+    int best = k;
+    for (int q = k + 1; q < n; ++q)
+      if (std::fabs(at(perm[q], k)) > std::fabs(at(perm[best], k))) best = q;
+    std::swap(perm[k], perm[best]);
+    const int pr = perm[k];
+    const double piv = at(pr, k);
+    if (piv == 0.0) fail(Errc::SingularFactor, "singular matrix: column " + std::to_string(k) + " has no pivot");
+    for (int q = k + 1; q < n; ++q) {
+      const int rr = perm[q];
+      const double f = at(rr, k) / piv;
+      at(rr, k) = f;
+      if (f != 0.0)
+        for (int j = k + 1; j < n; ++j) at(rr, j) -= f * at(pr, j);
+    }
+  }
+  // store the factors in pivot order so lu(k, :) is the k-th pivot row
+  DenseMatrix ordered(n, n);
+  for (int k = 0; k < n; ++k)
+    std::copy_n(lu.a.begin() + std::ptrdiff_t(perm[k]) * n, n, ordered.a.begin() + std::ptrdiff_t(k) * n);
+  lu = std::move(ordered);
+}
+
+Vector DenseLu::solve(const Vector& b) const {
+  const int n = lu.rows;
+  if (int(b.size()) != n) fail(Errc::DimensionMismatch, "LU solve: rhs has " + std::to_string(b.size()) +
+                                                           " entries, matrix order " + std::to_string(n));
+  Vector x(n);
+  for (int k = 0; k < n; ++k) {  // forward: unit lower
+    double t = b[perm[k]];
+    for (int j = 0; j < k; ++j) t -= lu.a[std::size_t(k) * n + j] * x[j];
+    x[k] = t;
+  }
+  for (int k = n - 1; k >= 0; --k) {  // backward: upper
+    double t = x[k];
+    for (int j = k + 1; j < n; ++j) t -= lu.a[std::size_t(k) * n + j] * x[j];
+    x[k] = t / lu.a[std::size_t(k) * n + k];
+  }
+  return x;
+}
+
+DenseMatrix DenseLu::solve(const DenseMatrix& B) const {
+  const DenseMatrix Bt = transpose(B);
+  DenseMatrix Xt(B.cols, B.rows);
+  for (int j = 0; j < B.cols; ++j) {
+    const Vector col(Bt.a.begin() + std::ptrdiff_t(j) * B.rows, Bt.a.begin() + std::ptrdiff_t(j + 1) * B.rows);
+    const Vector x = solve(col);
+    std::copy(x.begin(), x.end(), Xt.a.begin() + std::ptrdiff_t(j) * B.rows);
+  }
+  return transpose(Xt);
 }
 
 Vector lu_solve(const DenseMatrix& A, const Vector& b) { return DenseLu(A).solve(b); }
@@ -315,44 +343,87 @@ std::pair<int, int> scalar_envelope(const StructuredMatrix& A) {
   }
 }
 
-// generate_random: draws in storage order, then the diagonal rescaled to
-// +-dominance * max(off-row |sum|, 1) (semantics of src/structmat.cpp:282-333).
+// Stored columns of row i in ascending order, in the enumeration the
+// reference's matvec / to_dense / generate_random walk (for_each_in_row,
+// src/structmat.cpp:211-248): a circulant row may list a wrapped column twice
+// and a Babd corner row its overlap with the body span twice.
+static void row_columns(const StructuredMatrix& A, int i, std::vector<int>& cols) {
+  cols.clear();
+  switch (A.kind) {
+    case Kind::Banded:
+      for (int j = std::max(0, i - A.s); j <= std::min(A.n - 1, i + A.r); ++j) cols.push_back(j);
+      break;
+    case Kind::BlockTridiagonal: {
+      const int b = i / A.m;
+      for (int j = std::max(0, (b - 1) * A.m); j < std::min(A.n, (b + 2) * A.m); ++j) cols.push_back(j);
+      break;
+    }
+    case Kind::Abd:
+    case Kind::Babd: {
+      const auto span = abd_span(A.n, A.m, A.s, A.r, i / A.m);
+      for (int j = span.first; j < span.second; ++j) cols.push_back(j);
+      if (A.kind == Kind::Babd && i < A.corner_rows)
+        for (int j = A.n - A.corner_cols; j < A.n; ++j) cols.push_back(j);
+      break;
+    }
+    case Kind::CirculantLike:
+      for (int d = -A.s; d <= A.r; ++d) cols.push_back(((i + d) % A.n + A.n) % A.n);
+      std::sort(cols.begin(), cols.end());
+      break;
+  }
+}
+
+namespace {
+
+// the storage slot of the diagonal entry A(i, i)
+double& diagonal_slot(StructuredMatrix& A, int i) {
+  const int n = A.n, m = A.m;
+  switch (A.kind) {
+    case Kind::Banded: return A.data[band_offset(n, A.s, 0) + i];
+    case Kind::CirculantLike: return A.data[std::size_t(A.s) * n + i];
+    case Kind::BlockTridiagonal: {
+      const int b = i / m, t = i - b * m;
+      const std::size_t row = b == 0 ? 0 : std::size_t(3 * b - 1) * m * m;
+      return A.data[row + (b > 0 ? std::size_t(m) * m : 0) + std::size_t(t) * m + t];
+    }
+    default: {
+      const int b = i / m;
+      const auto span = abd_span(n, m, A.s, A.r, b);
+      return A.data[abd_row_offset(m, A.s, A.r, b) + std::size_t(i - b * m) * (span.second - span.first) +
+                    (i - span.first)];
+    }
+  }
+}
+
+}  // namespace
+
+// generate_random (src/structmat.cpp:282-333 semantics): storage-order draws
+// of one SplitMix64 stream (corner last), then, with dominance > 0, every
+// diagonal entry replaced by +-dominance * max(sum of the row's other |a_ij|, 1)
+// keeping its sign.  The off-diagonal sums walk each row's stored columns
+// only, so generation is O(nnz).
 StructuredMatrix generate_random(Kind kind, int n, int m, int s, int r, std::uint64_t seed, double dominance) {
   if (dominance < 0) fail(Errc::InvalidParameter, "dominance must be >= 0");
   SplitMix64 rng(seed);
-  std::vector<double> data(body_entry_count(kind, n, m, s, r));
-  for (auto& v : data) v = rng.next_unit();
-  std::vector<double> corner;
-  int cr = 0, cc = 0;
-  if (kind == Kind::Babd) {
-    cr = cc = m;
-    corner.resize(std::size_t(m) * m);
-    for (auto& v : corner) v = rng.next_unit();
-  }
-  StructuredMatrix A = make(kind, n, m, s, r, std::move(data), std::move(corner), cr, cc);
-  if (dominance > 0.0) {
-    for (int i = 0; i < n; ++i) {
-      double off = 0.0;
-      for (int j = 0; j < n; ++j)
-        if (j != i && A.in_structure(i, j)) off += std::fabs(A.at(i, j));
-      const double mag = dominance * std::max(off, 1.0);
-      const double val = A.at(i, i) < 0 ? -mag : mag;
-      switch (kind) {
-        case Kind::Banded: A.data[band_offset(n, s, 0) + i] = val; break;
-        case Kind::BlockTridiagonal: {
-          const int b = i / m;
-          const long offr = b == 0 ? 0 : long(3 * b - 1) * m * m;
-          A.data[offr + long(b > 0 ? 1 : 0) * m * m + long(i - b * m) * m + (i - b * m)] = val;
-          break;
-        }
-        default: {
-          const int b = i / m;
-          auto [c0, c1] = abd_span(n, m, s, r, b);
-          A.data[abd_row_offset(m, s, r, b) + long(i - b * m) * (c1 - c0) + (i - c0)] = val;
-          break;
-        }
-      }
-    }
+  auto draw = [&rng](std::size_t count) {
+    std::vector<double> v(count);
+    std::generate(v.begin(), v.end(), [&rng] { return rng.next_unit(); });
+    return v;
+  };
+  std::vector<double> data = draw(body_entry_count(kind, n, m, s, r));
+  const int edge = kind == Kind::Babd ? m : 0;
+  std::vector<double> corner = draw(std::size_t(edge) * edge);
+  StructuredMatrix A = make(kind, n, m, s, r, std::move(data), std::move(corner), edge, edge);
+  if (dominance == 0.0) return A;
+  std::vector<int> cols;
+  for (int i = 0; i < n; ++i) {
+    row_columns(A, i, cols);
+    double off = 0.0;
+    for (int j : cols)
+      if (j != i) off += std::fabs(A.at(i, j));
+    double& slot = diagonal_slot(A, i);
+    const double mag = dominance * std::max(off, 1.0);
+    slot = A.at(i, i) < 0 ? -mag : mag;
   }
   return A;
 }
@@ -400,83 +471,112 @@ std::pair<StructuredMatrix, Permutation> permute_corner(const StructuredMatrix& 
   return {make(Kind::CirculantLike, n, 1, s + r, 0, std::move(data)), perm};
 }
 
+DenseMatrix PartitionBlock::body_dense() const {
+  DenseMatrix D(L, L);
+  const int w = env_s + 1 + env_r;
+  for (int i = 0; i < L; ++i)
+    for (int off = 0; off < w; ++off) {
+      const int j = i - env_s + off;
+      if (j >= 0 && j < L) D.at(i, j) = env[std::size_t(i) * w + off];
+    }
+  return D;
+}
+
+// Frame [left separator | body | right separator]: the body and its coupling
+// blocks, plus the right separator's own diagonal block (the left one
+// belongs to the neighbouring partition).
 DenseMatrix PartitionBlock::local_dense() const {
-  const int dim = k0 + L + k1;
+  const int dim = k0 + L + k1, r0 = k0 + L;
   DenseMatrix M(dim, dim);
+  const DenseMatrix B = body_dense();
   for (int x = 0; x < L; ++x) {
+    std::copy_n(B.a.begin() + std::ptrdiff_t(x) * L, L, M.a.begin() + std::ptrdiff_t(k0 + x) * dim + k0);
     for (int t = 0; t < k0; ++t) {
       M.at(k0 + x, t) = b0.at(x, t);
       M.at(t, k0 + x) = c0.at(x, t);
     }
     for (int t = 0; t < k1; ++t) {
-      M.at(k0 + x, k0 + L + t) = c1.at(x, t);
-      M.at(k0 + L + t, k0 + x) = b1.at(x, t);
+      M.at(k0 + x, r0 + t) = c1.at(x, t);
+      M.at(r0 + t, k0 + x) = b1.at(x, t);
     }
-    for (int y = 0; y < L; ++y) M.at(k0 + x, k0 + y) = body_at(x, y);
   }
   for (int t = 0; t < k1; ++t)
-    for (int u = 0; u < k1; ++u) M.at(k0 + L + t, k0 + L + u) = a_right.at(t, u);
+    for (int u = 0; u < k1; ++u) M.at(r0 + t, r0 + u) = a_right.at(t, u);
   return M;
 }
 
-// Host view of partition i (1-based) -- the blocks the reference's
-// extract_block builds (src/partition.cpp:107-173); the GPU never builds them.
+// Host view of partition i (1-based): the local system M^(i) the reference
+// hands to its per-partition factorizations (src/partition.cpp:107-173
+// semantics).  Built by walking the stored columns of the body rows and of
+// the two separators' rows once and scattering each entry into the block it
+// belongs to; the GPU solver never builds these views.
 PartitionBlock extract_block(const StructuredMatrix& A, const PartitionPlan& plan, int i) {
-  if (i < 1 || i > plan.p) fail(Errc::IndexOutOfRange, "partition index " + std::to_string(i));
-  PartitionBlock blk;
-  blk.index = i;
-  blk.kind = A.kind;
-  blk.m = A.m;
-  blk.s = A.s;
-  blk.r = A.r;
-  auto [b, e] = plan.body_ranges[i - 1];
-  blk.body_begin = b;
-  blk.L = e - b;
+  if (i < 1 || i > plan.p) fail(Errc::IndexOutOfRange, "partition index " + std::to_string(i) + " not in [1, " +
+                                                            std::to_string(plan.p) + "]");
   const int k = plan.sep_size;
-  const int left = plan.has_corner ? i - 1 : i - 2, right = plan.has_corner ? i : i - 1;
-  blk.k0 = left >= 0 ? k : 0;
-  blk.k1 = right < plan.sep_count() ? k : 0;
-  auto [es, er] = scalar_envelope(A);
-  blk.env_s = std::min(es, blk.L - 1);
-  blk.env_r = std::min(er, blk.L - 1);
-  const int w = blk.env_s + 1 + blk.env_r;
-  blk.env.assign(std::size_t(blk.L) * w, 0.0);
-  for (int x = 0; x < blk.L; ++x)
-    for (int j = std::max(0, x - blk.env_s); j <= std::min(blk.L - 1, x + blk.env_r); ++j)
-      blk.env[std::size_t(x) * w + (j - x + blk.env_s)] = A.at(b + x, b + j);
-  blk.b0 = DenseMatrix(blk.L, blk.k0);
-  blk.c0 = DenseMatrix(blk.L, blk.k0);
-  blk.b1 = DenseMatrix(blk.L, blk.k1);
-  blk.c1 = DenseMatrix(blk.L, blk.k1);
-  if (blk.k0) {
-    const int ls = plan.separator_starts[left];
-    for (int x = 0; x < blk.L; ++x)
-      for (int t = 0; t < k; ++t) {
-        blk.b0.at(x, t) = A.at(b + x, ls + t);
-        blk.c0.at(x, t) = A.at(ls + t, b + x);
+  const int lsep = plan.has_corner ? i - 1 : i - 2, rsep = lsep + 1;  // separator_starts indices
+  PartitionBlock P;
+  P.index = i;
+  P.kind = A.kind;
+  P.m = A.m;
+  P.s = A.s;
+  P.r = A.r;
+  const int b = plan.body_ranges[i - 1].first, e = plan.body_ranges[i - 1].second;
+  P.body_begin = b;
+  P.L = e - b;
+  P.k0 = lsep >= 0 ? k : 0;
+  P.k1 = rsep < plan.sep_count() ? k : 0;
+  const auto env = scalar_envelope(A);
+  P.env_s = std::min(env.first, P.L - 1);
+  P.env_r = std::min(env.second, P.L - 1);
+  const int w = P.env_s + 1 + P.env_r;
+  P.env.assign(std::size_t(P.L) * w, 0.0);
+  P.b0 = DenseMatrix(P.L, P.k0);
+  P.c0 = DenseMatrix(P.L, P.k0);
+  P.b1 = DenseMatrix(P.L, P.k1);
+  P.c1 = DenseMatrix(P.L, P.k1);
+  const int ls = P.k0 ? plan.separator_starts[lsep] : -1, rs = P.k1 ? plan.separator_starts[rsep] : -1;
+  if (P.k0) P.a_left = DenseMatrix(k, k);
+  if (P.k1) P.a_right = DenseMatrix(k, k);
+  auto in = [](int j, int lo, int len) { return lo >= 0 && j >= lo && j < lo + len; };
+  std::vector<int> cols;
+  for (int x = 0; x < P.L; ++x) {  // body rows: envelope, b0 (left), c1 (right)
+    row_columns(A, b + x, cols);
+    for (int j : cols) {
+      const double val = A.at(b + x, j);
+      if (j >= b && j < e) {
+        const int off = (j - b) - x + P.env_s;
+        if (off >= 0 && off < w) P.env[std::size_t(x) * w + off] = val;
+      } else if (in(j, ls, k)) {
+        P.b0.at(x, j - ls) = val;
+      } else if (in(j, rs, k)) {
+        P.c1.at(x, j - rs) = val;
       }
-    blk.a_left = DenseMatrix(k, k);
-    for (int t = 0; t < k; ++t)
-      for (int u = 0; u < k; ++u) blk.a_left.at(t, u) = A.at(ls + t, ls + u);
+    }
   }
-  if (blk.k1) {
-    const int rs = plan.separator_starts[right];
-    for (int x = 0; x < blk.L; ++x)
-      for (int t = 0; t < k; ++t) {
-        blk.c1.at(x, t) = A.at(b + x, rs + t);
-        blk.b1.at(x, t) = A.at(rs + t, b + x);
+  for (int t = 0; t < k; ++t) {  // separator rows: c0 / a_left, b1 / a_right
+    if (P.k0) {
+      row_columns(A, ls + t, cols);
+      for (int j : cols) {
+        if (j >= b && j < e) P.c0.at(j - b, t) = A.at(ls + t, j);
+        else if (in(j, ls, k)) P.a_left.at(t, j - ls) = A.at(ls + t, j);
       }
-    blk.a_right = DenseMatrix(k, k);
-    for (int t = 0; t < k; ++t)
-      for (int u = 0; u < k; ++u) blk.a_right.at(t, u) = A.at(rs + t, rs + u);
+    }
+    if (P.k1) {
+      row_columns(A, rs + t, cols);
+      for (int j : cols) {
+        if (j >= b && j < e) P.b1.at(j - b, t) = A.at(rs + t, j);
+        else if (in(j, rs, k)) P.a_right.at(t, j - rs) = A.at(rs + t, j);
+      }
+    }
   }
-  if (plan.has_corner && i == 1) {
-    const int s0 = plan.separator_starts.front(), sp = plan.separator_starts.back();
-    blk.corner_slice = DenseMatrix(k, k);
+  if (plan.has_corner && i == 1 && k > 0) {  // the corner couples the first separator to the last
+    const int first = plan.separator_starts.front(), last = plan.separator_starts.back();
+    P.corner_slice = DenseMatrix(k, k);
     for (int t = 0; t < k; ++t)
-      for (int u = 0; u < k; ++u) blk.corner_slice.at(t, u) = A.at(s0 + t, sp + u);
+      for (int u = 0; u < k; ++u) P.corner_slice.at(t, u) = A.at(first + t, last + u);
   }
-  return blk;
+  return P;
 }
 
 std::string describe(const PartitionPlan& plan) {

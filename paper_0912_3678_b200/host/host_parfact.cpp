@@ -2,6 +2,7 @@
 // solve_sequential of the C++ API (reference proj/include/parsol/parfact.hpp,
 // seqref.hpp), each a thin call into the C ABI (psg.h): no CPU fallback.
 #include <algorithm>
+#include <chrono>
 #include <string>
 
 #include "parsol/parfact.hpp"
@@ -23,7 +24,6 @@ void check(int rc, const char* err) {
 
 void add_stats(SolveStats* st, const psg_stats& s) {
   if (!st) return;
-  st->factor_seconds = s.factor_seconds;
   st->phase1_seconds += s.phase1_seconds;
   st->phase2_seconds += s.phase2_seconds;
   st->phase3_seconds += s.phase3_seconds;
@@ -35,6 +35,7 @@ void add_stats(SolveStats* st, const psg_stats& s) {
 }  // namespace
 
 ParallelFactorization parallel_factor(const StructuredMatrix& A, int p, Strategy strategy, double tol) {
+  const auto t0 = std::chrono::steady_clock::now();
   char err[512];
   ParallelFactorization F;
   F.strategy = strategy;
@@ -85,7 +86,9 @@ ParallelFactorization parallel_factor(const StructuredMatrix& A, int p, Strategy
     R.T = DenseMatrix(dim, dim);
     check(psg_reduced_dense(h, R.T.a.data(), err, sizeof err), err);
   }
-  F.factor_seconds = 0;
+  R.device = F.device;
+  check(psg_factor_wait(h, nullptr), "factorization failed on the device");
+  F.factor_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return F;
 }
 
@@ -116,6 +119,44 @@ Vector solve_reduced(const ParallelFactorization& F, const Vector& rhs, SolveSta
         err);
   if (stats) stats->reduced_ops += s.reduced_ops;
   return x;
+}
+
+Vector solve_reduced(const ReducedSystem& R, const Vector& rhs, SolveStats* stats) {
+  if (int(rhs.size()) != R.dim) fail(Errc::DimensionMismatch, "reduced rhs length");
+  char err[512];
+  Vector x(R.dim);
+  if (R.T.rows == R.dim && R.T.cols == R.dim) {
+    long long ops = 0;
+    check(psg_dense_solve(R.dim, R.T.a.data(), rhs.data(), x.data(), &ops, nullptr, err, sizeof err), err);
+    if (stats) stats->reduced_ops += ops;
+    return x;
+  }
+  if (!R.device) fail(Errc::InvalidParameter, "reduced system has neither a dense T nor a device factorization");
+  psg_stats s{};
+  check(psg_solve_reduced(R.device.get(), rhs.data(), x.data(), 0, nullptr, stats ? &s : nullptr, err, sizeof err),
+        err);
+  if (stats) stats->reduced_ops += s.reduced_ops;
+  return x;
+}
+
+void materialize_locals(ParallelFactorization& F, const StructuredMatrix& A, int first, int count, double tol) {
+  const int p = F.plan.p;
+  if (count < 0) count = p - first + 1;
+  if (first < 1 || first + count - 1 > p) fail(Errc::IndexOutOfRange, "partition range");
+  if (int(F.locals.size()) != p) F.locals.resize(p);
+  const StructuredMatrix* work = &A;
+  StructuredMatrix rotated;
+  if (F.permuted) {
+    rotated = permute_corner(A).first;
+    work = &rotated;
+  }
+  for (int i = first; i < first + count; ++i) {
+    try {
+      F.locals[i - 1] = factor(F.strategy, extract_block(*work, F.plan, i), tol);
+    } catch (const Error& e) {
+      fail(e.code(), "partition " + std::to_string(i) + ": " + e.detail());
+    }
+  }
 }
 
 double residual(const StructuredMatrix& A, const Vector& x, const Vector& f) {
