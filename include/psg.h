@@ -119,10 +119,16 @@ int psg_sync(const psg_handle* h, psg_stats* stats, char* err, size_t errlen);
 /* New matrix values with the structure the handle was factored for (kind, n,
  * m, s, r, corner shape, p): recompute the factorization in place, without
  * re-planning or re-allocating.  The equivalent of parallel_factor on a
- * matrix whose sparsity pattern is unchanged.  Pending asynchronous solves are
- * not drained (stream order keeps them on the old factor data) but are
- * certified at psg_sync against the values current then: call psg_sync before
- * overwriting A's values in place. */
+ * matrix whose sparsity pattern is unchanged.
+ * Pending asynchronous solves: when A comes in a different buffer than the
+ * handle's current one (or as host memory, copied into the handle), they are
+ * drained first -- certificates checked and failures repaired against the
+ * matrix they were enqueued for -- and their statistics are reported by the
+ * next psg_sync.  With the same device buffer they stay pending (stream order
+ * runs them on the old factor data) and are certified at psg_sync against the
+ * buffer's values then: call psg_sync before overwriting A's values in place.
+ * Calls on one handle from different streams are ordered: each entry point
+ * makes its stream wait for the work previously enqueued on the handle. */
 int psg_refactor(psg_handle* h, const psg_desc* A, void* stream, char* err, size_t errlen);
 
 /* Reduced system metadata (ReducedSystem, parfact.hpp:14-22): q kept blocks,

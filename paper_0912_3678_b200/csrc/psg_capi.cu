@@ -349,14 +349,19 @@ Plan make_plan(const psg_desc& A, int p) {
 // small pools: CUDA events
 // ----------------------------------------------------------------------------
 struct EventPool {
+  // events belong to the device that was current when they were created:
+  // the free lists are kept per device (a handle releases its events while
+  // its own device is current, psg_release's DeviceGuard)
   std::mutex mu;
-  std::vector<cudaEvent_t> free_;
+  std::map<int, std::vector<cudaEvent_t>> free_;
   cudaEvent_t get() {
+    const int dev = BlockCache::device();
     {
       std::lock_guard<std::mutex> g(mu);
-      if (!free_.empty()) {
-        cudaEvent_t e = free_.back();
-        free_.pop_back();
+      auto& fl = free_[dev];
+      if (!fl.empty()) {
+        cudaEvent_t e = fl.back();
+        fl.pop_back();
         return e;
       }
     }
@@ -365,8 +370,9 @@ struct EventPool {
     return e;
   }
   void put(cudaEvent_t e) {
+    const int dev = BlockCache::device();
     std::lock_guard<std::mutex> g(mu);
-    free_.push_back(e);
+    free_[dev].push_back(e);
   }
 };
 
@@ -1674,6 +1680,10 @@ struct psg_handle {
     int launches;
   };
   std::vector<Pending> pending;
+  psg_stats carried{};      // statistics of solves drained by psg_refactor, reported at the next psg_sync
+  bool has_carried = false;
+  cudaStream_t last_stream = nullptr;  // stream of the last enqueued work (see order_on)
+  bool used = false;
   DevBuf<DevStatus> d_ring;
   DevStatus* h_ring = nullptr;               // pinned mirror
   cudaEvent_t ring_done[kRing] = {}, ring_t[kRing][4] = {};
@@ -1763,6 +1773,17 @@ void check_strategy(const psg_desc& A, int strategy) {
 bool is_tridiag(const psg_desc& A) { return A.kind == PSG_BANDED && A.s == 1 && A.r == 1; }
 
 // (Re)compute the factor data for the current mode.
+// Calls on one handle may come from different streams; they share the
+// handle's scratch (status words, staging, reduced-system buffers), so a
+// stream that differs from the previous call's first waits for the work
+// already enqueued on the handle (ev_done is recorded at the end of every
+// entry point).
+void order_on(psg_handle* h, cudaStream_t s) {
+  if (h->used && s != h->last_stream) CUDA_TRY(cudaStreamWaitEvent(s, h->ev_done, 0));
+  h->last_stream = s;
+  h->used = true;
+}
+
 void run_factor(psg_handle* h, cudaStream_t s) {
   h->tri.launches = 0;
   CUDA_TRY(cudaEventRecord(h->ev_f0, s));
@@ -1949,6 +1970,8 @@ int psg_factor(const psg_desc* Ain, int p, int strategy, double tol, void* strea
       h->h_status = static_cast<DevStatus*>(pinned_slots().get());
       run_factor(h.get(), s);
       CUDA_TRY(cudaEventRecord(h->ev_done, s));
+      h->last_stream = s;
+      h->used = true;
       *out = h.release();
       return 0;
     }
@@ -1987,6 +2010,8 @@ int psg_factor(const psg_desc* Ain, int p, int strategy, double tol, void* strea
     h->h_status = static_cast<DevStatus*>(pinned_slots().get());
     run_factor(h.get(), s);
     CUDA_TRY(cudaEventRecord(h->ev_done, s));
+    h->last_stream = s;
+    h->used = true;
     *out = h.release();
     return 0;
   } catch (const Fail& f_) {
@@ -2008,8 +2033,8 @@ int psg_set_option(psg_handle* h, int option, double value) {
       case PSG_OPT_SPECULATIVE:
         h->speculative = value != 0.0;
         if ((h->spec_mode() && !h->spec_factored) || (!h->spec_mode() && !h->exact_factored)) {
-          run_factor(h, nullptr);
-          CUDA_TRY(cudaEventRecord(h->ev_done, nullptr));
+          run_factor(h, h->last_stream);
+          CUDA_TRY(cudaEventRecord(h->ev_done, h->last_stream));
         }
         break;
       case PSG_OPT_HALO:
@@ -2328,6 +2353,7 @@ int psg_solve(const psg_handle* hc, const double* f, double* x, int on_device, v
   std::lock_guard<std::mutex> g(h->mu);
   try {
     cudaStream_t s = (cudaStream_t)stream;
+    order_on(h, s);
     const int n = h->A.n;
     const double* df = f;
     double* dx = x;
@@ -2671,6 +2697,7 @@ int psg_solve_async(const psg_handle* hc, const double* f, double* x, int timing
   std::lock_guard<std::mutex> g(h->mu);
   try {
     cudaStream_t s = (cudaStream_t)stream;
+    order_on(h, s);
     if (h->piv) {  // pivoting handles certify by a residual pass: blocking
       piv_blocking(h, f, x, s, nullptr);
       CUDA_TRY(cudaEventRecord(h->ev_done, s));
@@ -2718,6 +2745,17 @@ int psg_sync(const psg_handle* hc, psg_stats* stats, char* err, size_t errlen) {
       stats->factor_seconds = tf * 1e-3;
     }
     drain(h, stats);
+    if (h->has_carried) {  // solves drained early by psg_refactor
+      if (stats) {
+        stats->phase1_seconds += h->carried.phase1_seconds;
+        stats->phase3_seconds += h->carried.phase3_seconds;
+        stats->reduced_ops += h->carried.reduced_ops;
+        stats->certificate = std::max(stats->certificate, h->carried.certificate);
+        stats->fallbacks += h->carried.fallbacks;
+      }
+      h->carried = psg_stats{};
+      h->has_carried = false;
+    }
     return 0;
   } catch (const Fail& f_) {
     return set_err(err, errlen, f_.code, f_.msg);
@@ -2736,6 +2774,21 @@ int psg_refactor(psg_handle* h, const psg_desc* A, void* stream, char* err, size
         A->corner_rows != h->A.corner_rows || A->corner_cols != h->A.corner_cols)
       throw Fail{PSG_E_DIMENSION_MISMATCH, "psg_refactor needs the factored structure"};
     cudaStream_t s = (cudaStream_t)stream;
+    order_on(h, s);
+    // Pending asynchronous solves were enqueued against the current matrix.
+    // When the new values arrive in another buffer (or through the handle's
+    // own copy of a host matrix) the old values are about to become
+    // unreachable, so those solves are drained -- a failed certificate is
+    // repaired against the matrix it was enqueued for -- before anything is
+    // replaced; their statistics are reported at the next psg_sync.  A
+    // refactor on the same device buffer keeps them pending (stream order
+    // runs them on the old factor data; psg.h: psg_sync before overwriting A
+    // in place).
+    if (!h->pending.empty() &&
+        (!A->on_device || A->data != h->A.data || A->corner != h->A.corner || h->piv)) {
+      drain(h, &h->carried);
+      h->has_carried = true;
+    }
     if (h->piv) {  // new values may defer other pivots: the reduced layout is rebuilt
       CUDA_TRY(cudaEventSynchronize(h->ev_done));
       piv_set_matrix(h, *A, s);
@@ -2746,10 +2799,6 @@ int psg_refactor(psg_handle* h, const psg_desc* A, void* stream, char* err, size
       CUDA_TRY(cudaEventRecord(h->ev_done, s));
       return 0;
     }
-    // Pending asynchronous solves are NOT drained here: the factor kernels run
-    // after them in stream order.  Their certificates are checked at psg_sync
-    // against the matrix values current then, so callers must psg_sync before
-    // changing A's values in place (psg.h).
     const double* data = A->data;
     const double* corner = A->corner;
     if (!A->on_device) {
@@ -2925,6 +2974,7 @@ int psg_solve_reduced(const psg_handle* hc, const double* rhs, double* x, int on
   std::lock_guard<std::mutex> g(h->mu);
   try {
     cudaStream_t s = (cudaStream_t)stream;
+    order_on(h, s);
     if (h->piv) {
       const int dim = h->piv->dim;
       DevBuf<double> dr, dxv;
