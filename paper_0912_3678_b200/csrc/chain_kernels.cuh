@@ -12,16 +12,19 @@
 //                                             src/localfact.cpp:182-225)
 //     phi_j = the chain from 0 with f         (condense, src/localfact.cpp:765-781)
 //
-//   factor  chain_tm_kernel (ONE launch): per block T_b and M_b = R_b^-1 (one
-//           block per lane, LU in registers), stored beside the data; Phi_j
-//           by a shared-memory tree product.  The reduced system in x_sigma is
-//           again a BVP-layout chain (maps Phi_j, R = I, same Ba / Bb); its
-//           chunk products Phi^(l) on every level are formed inside the same
-//           launch by the warp that completes each chunk, and the last one
-//           factors the top-level BC matrix (partial pivoting).
-//   solve   chain_solve_kernel<0/1/2> (three launches): condense + reduced
-//           levels up; top solve + x down + separator residuals up; the
-//           correction down + certificate (see the kernel comment below).
+//   factor + condense  chain_fc_kernel (ONE pass over A and f): per block
+//           T_b = -R_b^-1 S_b and c_b = R_b^-1 f_b by Gauss-Jordan on the
+//           augmented rows (MB lanes per block, row per lane), stored for the
+//           final pass; the chunk maps (Phi_j, phi_j) composed on the fly.
+//           The reduced system in x_sigma is again a BVP-layout chain (maps
+//           Phi_j, R = I, same Ba / Bb); its chunk maps on every level are
+//           composed inside the same launch by the CTA / composer that
+//           completes each chunk, and the last one factors the top-level BC
+//           matrix (partial pivoting).  The factor is lazy: a refactor
+//           followed by a solve runs this one fused launch.
+//   solve   chain_down_kernel (top solve + x down), chain_solve_kernel<1>
+//           (x through every block, separator residuals up), chain_down_kernel
+//           (the correction down), chain_solve_kernel<2> (x += d, certificate).
 //
 #pragma once
 
@@ -36,7 +39,8 @@ struct ChainLevelArgs {
   int nb;                // block rows
   const double* f;       // rhs (nb * MB)
   double* x;             // solution
-  double* tm;            // factor output / solve input: per block [T | M] (T = -R^-1 S, M = R^-1), row pairs interleaved (see the factor)
+  double* tm;            // per block T_b = -R_b^-1 S_b (MB x MB, double2 (row i, columns 2q, 2q+1) at q MB + i)
+  double* cv;            // condense output: per block c_b = R_b^-1 f_b (nb x MB, block 0 unused)
   DevStatus* status;
 };
 
@@ -62,29 +66,7 @@ __device__ __forceinline__ void cert_push(DevStatus* st, double num, double den)
   if ((threadIdx.x & 31) == 0 && om > 0) status_cert(st, om);
 }
 
-// ---------------------------------------------------------------------------
-// factor: per block b the transfer T_b = -R_b^-1 S_b and M_b = R_b^-1, stored
-// row-interleaved like the data ([T row i | M row i], 2 MB doubles per row),
-// and per chunk Phi_j = T_last ... T_first by a shared-memory tree product.
-// One lane per block (LU in registers, no communication); a warp owns 32
-// consecutive blocks = kChainC0-block chunks, staged through shared memory with
-// a padded slot pitch (2 MB^2 + 2 doubles: conflict-free LDS.128 phases).
-// ---------------------------------------------------------------------------
 constexpr int kChainC0 = 16;  // chunk length (blocks) on every level
-
-template <int MB>
-struct ChainSmem {
-  static constexpr int SLOT = 2 * MB * MB + 2;
-  static constexpr int WARP = 32 * SLOT;  // doubles per warp
-};
-
-// [T | M] of a block in the pair-interleaved order of the global tm array
-// (and of a slot once its block is factored): element (i, c) at
-// (c / 2) * 2 MB + 2 i + c % 2 -- double2 (i, c/2) transposed
-template <int MB>
-__host__ __device__ constexpr int tix(int i, int c) {
-  return (c >> 1) * 2 * MB + 2 * i + (c & 1);
-}
 
 // ---------------------------------------------------------------------------
 // The reduced-system hierarchy.  Level 0 is the user's chain (N + 1 block
@@ -130,72 +112,117 @@ __device__ __forceinline__ bool warp_last_arrive(int* ctr, int expected, int lan
   return last != 0;
 }
 
-// tree of products P = later * earlier over the kChainC0 slots of each of
-// `nch` chunks (T parts of the padded slots); the product lands in the
-// chunk's LAST slot.  One lane per (product, row): the result row overwrites
-// that row of the later factor, which only this lane reads; the earlier
-// factor is a previous round's result (read-only in this round).
+// ---------------------------------------------------------------------------
+// chain_fc_kernel: the level-0 factor and condense of the chain in ONE pass
+// over A (and f), plus the whole reduced hierarchy.
+//
+// A subgroup of MB lanes owns one level-0 chunk (16 consecutive block rows),
+// lane i = row i of every block.  Per block: [S | R] arrives by cp.async
+// (16-byte pieces, coalesced, XOR-swizzled so each lane reads its row
+// conflict-free), two blocks in flight per subgroup; Gauss-Jordan on the
+// augmented rows [R | S | f] with the pivot row broadcast through shared
+// memory leaves R diagonal, so T_b = -D^-1 S' and c_b = D^-1 f' (no pivoting,
+// like the reference's Lu); lane i stores row i of T_b (pair-interleaved, the
+// final pass reads it coalesced) and c_b.  The chunk's affine map
+//     (Phi_j, phi_j) = (T_16, c_16) o ... o (T_1, c_1)
+// accumulates as it goes: lane i keeps column i of Phi (Phi <- T_b Phi) and
+// the whole phi (phi <- T_b phi + c_b), T_b read back from shared memory.
+//
+// A CTA (4 warps) holds 128 / MB chunks = 8 / MB level-1 chunks, which warp 0
+// composes right away (maps from L2); higher levels and the top BC matrix
+// G = Ba + Bb Phi_total (factored with partial pivoting) are done by the last
+// arriving CTA / composer (self-resetting counters), all inside the launch.
+//
+// STORE_T: store T_b and the maps Phi (factor); WITH_F: c_b and phi (condense).
+//   <true, true>   refactor + first solve fused (the production step)
+//   <true, false>  factor alone
+//   <false, true>  condense alone (a further right-hand side): A is read again
+//                  instead of keeping R^-1 (same bytes as storing it)
+// ---------------------------------------------------------------------------
 template <int MB>
-__device__ __forceinline__ void chain_tree16(double* sm, int nch, int lane) {
-  constexpr int SLOT = ChainSmem<MB>::SLOT;
+struct FcCfg {
+  static constexpr int SG = 32 / MB;                                  // subgroups (chunks) per warp
+  static constexpr int NW = 4;                                        // warps per CTA
+  static constexpr int CPC = NW * SG;                                 // level-0 chunks per CTA
+  static constexpr int L1C = CPC / kChainC0;                          // level-1 chunks per CTA (8 / MB)
+  static constexpr int BLK = 2 * MB * MB;                             // [S | R] doubles per block row
+  static constexpr int TP = MB + 2;                                   // row pitch of the published T_b
+  static constexpr int PIV = 2 * MB + 2;                              // pivot row buffer
+  static constexpr int TBS = MB * TP + MB;                            // published T_b + phi
+  static constexpr int SUB = 2 * BLK + TBS + 2 * PIV;                 // doubles per subgroup
+  static constexpr int SMEM = NW * SG * SUB * 8;                      // bytes per CTA
+};
+
+template <int MB>
+__device__ __forceinline__ double pick(const double (&v)[MB], int i) {
+  double o = 0.0;
+#pragma unroll
+  for (int r = 0; r < MB; ++r) o = r == i ? v[r] : o;
+  return o;
+}
+
+// Combine the affine maps held by 16 consecutive subgroups of the CTA (map of
+// subgroup s covers chunk range s; later o earlier) into the first subgroup of
+// each group of 16: four rounds, the later partner publishes (Phi, phi) in its
+// shared buffer, the earlier one composes Phi_L Phi_E (lane i: column i) and
+// Phi_L phi_E + phi_L.  Every thread of the CTA calls it.
+template <int MB, bool VEC>
+__device__ __forceinline__ void fc_tree16(double* fsm, int gsub, int i, double (&pc)[MB], double (&ph)[MB]) {
+  using C = FcCfg<MB>;
+  const int s = gsub % kChainC0;
 #pragma unroll 1
   for (int h = 1; h < kChainC0; h <<= 1) {
-    const int pairs = kChainC0 / (2 * h);  // per chunk
-    const int tasks = nch * pairs * MB;
-    for (int task = lane; task < tasks; task += 32) {
-      const int i = task % MB, pk = task / MB, c = pk / pairs, k = pk % pairs;
-      const double* E = sm + (c * kChainC0 + 2 * k * h + h - 1) * SLOT;
-      double* L = sm + (c * kChainC0 + 2 * k * h + 2 * h - 1) * SLOT;
-      double a[MB], o[MB];
+    double* mine = fsm + gsub * C::SUB + 2 * C::BLK;  // TB region: MB x TP, then MB for phi
+    if (s % (2 * h) == h) {  // later partner of (s - h): publish
 #pragma unroll
-      for (int l = 0; l < MB; ++l) a[l] = L[tix<MB>(i, l)];
+      for (int r = 0; r < MB; ++r) mine[r * C::TP + i] = pc[r];
+      if (VEC) mine[MB * C::TP + i] = pick<MB>(ph, i);
+    }
+    __syncthreads();
+    if (s % (2 * h) == 0) {
+      const double* L = fsm + (gsub + h) * C::SUB + 2 * C::BLK;
+      double np[MB], nv[MB];
 #pragma unroll
-      for (int cc = 0; cc < MB; ++cc) {
-        double acc = a[0] * E[tix<MB>(0, cc)];
+      for (int r = 0; r < MB; ++r) {
+        double a = 0.0, v = VEC ? L[MB * C::TP + r] : 0.0;
 #pragma unroll
-        for (int l = 1; l < MB; ++l) acc = fma(a[l], E[tix<MB>(l, cc)], acc);
-        o[cc] = acc;
+        for (int c = 0; c < MB; c += 2) {
+          const double2 m = *reinterpret_cast<const double2*>(L + r * C::TP + c);
+          a = fma(m.y, pc[c + 1], fma(m.x, pc[c], a));
+          if (VEC) v = fma(m.y, ph[c + 1], fma(m.x, ph[c], v));
+        }
+        np[r] = a;
+        nv[r] = v;
       }
 #pragma unroll
-      for (int cc = 0; cc < MB; ++cc) L[tix<MB>(i, cc)] = o[cc];
+      for (int r = 0; r < MB; ++r) {
+        pc[r] = np[r];
+        if (VEC) ph[r] = nv[r];
+      }
     }
-    __syncwarp();
+    __syncthreads();
   }
 }
 
-// maps src[s] (s < len, written by another warp of this launch) into the T
-// parts of slots 0..15, identity beyond
+// top of the hierarchy: G = Ba + Bb Phi_total (lane i holds column i of
+// Phi_total), LU with partial pivoting (full-row swaps, pivot rows recorded)
+// into t.glu.  Lanes 0..MB-1 of one warp; G staged in `buf`.
 template <int MB>
-__device__ __forceinline__ void chain_load_maps(double* sm, const double* src, int len, int lane) {
-  constexpr int SLOT = ChainSmem<MB>::SLOT, MM = MB * MB;
-  for (int e = lane; e < kChainC0 * MM; e += 32) {
-    const int s = e / MM, r = e % MM, i = r / MB, k = r % MB;
-    sm[s * SLOT + tix<MB>(i, k)] = s < len ? __ldcg(src + (long)s * MM + r) : (i == k ? 1.0 : 0.0);
-  }
-  __syncwarp();
-}
-
-// top level: Phi_total = product of the top maps, G = Ba + Bb Phi_total, LU
-// of G with partial pivoting (LAPACK convention: full-row swaps, pivot rows
-// recorded), the multipliers below the diagonal
-template <int MB>
-__device__ void chain_top_factor(const ChainLevelArgs& g, const ChainTree& t, double* sm, int lane) {
-  constexpr int SLOT = ChainSmem<MB>::SLOT, MM = MB * MB, GP = MB + 1;
-  chain_load_maps<MB>(sm, t.phi[t.T - 1], t.P[t.T - 1], lane);
-  chain_tree16<MB>(sm, 1, lane);
-  double* G = sm + SLOT;
+__device__ void chain_fc_top(const ChainLevelArgs& g, const ChainTree& t, double* buf, int lane, const double (&pc)[MB]) {
+  constexpr int MM = MB * MB, GP = MB + 1;
+  const int i = lane % MB;
   if (lane < MB) {
-    const int i = lane;
 #pragma unroll
-    for (int c = 0; c < MB; ++c) {
-      double v = __ldg(g.data + i * MB + c);
+    for (int r = 0; r < MB; ++r) {
+      double v = __ldg(g.data + r * MB + i);
 #pragma unroll
-      for (int l = 0; l < MB; ++l) v = fma(__ldg(g.corner + i * MB + l), sm[(kChainC0 - 1) * SLOT + tix<MB>(l, c)], v);
-      G[i * GP + c] = v;
+      for (int l = 0; l < MB; ++l) v = fma(__ldg(g.corner + r * MB + l), pc[l], v);
+      buf[r * GP + i] = v;
     }
   }
   __syncwarp();
   if (lane == 0) {
+    double* G = buf;
     for (int k = 0; k < MB; ++k) {
       int p = k;
       for (int r = k + 1; r < MB; ++r)
@@ -215,132 +242,250 @@ __device__ void chain_top_factor(const ChainLevelArgs& g, const ChainTree& t, do
     }
     for (int e = 0; e < MM; ++e) t.glu[e] = G[(e / MB) * GP + e % MB];
   }
-}
-
-// after the level-0 chunk maps of warp w are stored: climb the hierarchy while
-// this warp is the last arriver of the enclosing chunk
-template <int MB>
-__device__ void chain_factor_up(const ChainLevelArgs& g, const ChainTree& t, double* sm, long w, int lane) {
-  constexpr int SLOT = ChainSmem<MB>::SLOT, MM = MB * MB;
-  const long nw = ((long)t.P[0] + 1) / 2;  // factor warps (2 level-0 chunks each)
-  long c = w;
-  for (int l = 1;; ++l) {
-    if (l == t.T) {
-      const int expected = t.T == 1 ? (int)nw : t.P[t.T - 1];
-      if (warp_last_arrive(t.cnt + t.coff[t.T], expected, lane)) chain_top_factor<MB>(g, t, sm, lane);
-      return;
-    }
-    const long cc = l == 1 ? c / 8 : c / kChainC0;
-    const int expected = l == 1 ? (int)min(8L, nw - 8 * cc) : (int)min((long)kChainC0, t.P[l - 1] - kChainC0 * cc);
-    if (!warp_last_arrive(t.cnt + t.coff[l] + cc, expected, lane)) return;
-    const int len = (int)min((long)kChainC0, t.P[l - 1] - kChainC0 * cc);
-    chain_load_maps<MB>(sm, t.phi[l - 1] + kChainC0 * cc * MM, len, lane);
-    chain_tree16<MB>(sm, 1, lane);
-    for (int e = lane; e < MM; e += 32) t.phi[l][cc * MM + e] = sm[(kChainC0 - 1) * SLOT + tix<MB>(e / MB, e % MB)];
-    c = cc;
-  }
-}
-
-template <int MB>
-__global__ void __launch_bounds__(64) chain_tm_kernel(ChainLevelArgs g, ChainTree t) {
-  constexpr int SLOT = ChainSmem<MB>::SLOT, RW = 2 * MB, BW = 2 * MB * MB;
-  extern __shared__ __align__(16) double csm[];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  double* sm = csm + wib * ChainSmem<MB>::WARP;
-  const long w = (long)blockIdx.x * (blockDim.x >> 5) + wib;
-  const long bfirst = 32 * w + 1;  // blocks bfirst .. bfirst + 31 (chunks 2w, 2w + 1)
-  if (bfirst > g.nb - 1) return;   // warp-uniform
-  const int nblk = (int)min(32L, g.nb - bfirst);
-  // ---- stage the warp's blocks into padded slots: one TMA bulk copy per lane
-  __shared__ __align__(8) uint64_t tbar[2];
-  uint64_t* bar = tbar + wib;
-  if (lane == 0) {
-    mbar_init(bar, 1);
-    mbar_arrive_expect_tx(bar, (uint32_t)nblk * BW * 8);
-  }
   __syncwarp();
-  if (lane < nblk) bulk_g2s(sm + lane * SLOT, g.data + MB * MB + (bfirst - 1 + lane) * BW, BW * 8, bar);
-  mbar_wait(bar, 0);
-  // ---- per lane: M = R^-1 (Gauss-Jordan, no pivoting), then T = -M S
-  double* slot = sm + lane * SLOT;
-  if (lane < nblk) {
-    double R[MB * MB];
+}
+
+// CTA-level arrival: true (for every thread) in the CTA that completes the count
+__device__ __forceinline__ bool cta_last_arrive(int* ctr, int expected) {
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int last = atomicAdd(ctr, 1) == expected - 1;
+    if (last) atomicExch(ctr, 0);  // reset for the next launch
+    s_last = last;
+  }
+  __syncthreads();
+  const bool last = s_last != 0;
+  if (last) __threadfence();
+  return last;
+}
+
+template <int MB, bool STORE_T, bool WITH_F>
+__global__ void __launch_bounds__(128) chain_fc_kernel(ChainLevelArgs g, ChainTree t) {
+  using C = FcCfg<MB>;
+  constexpr int MM = MB * MB, RW = 2 * MB;
+  extern __shared__ __align__(16) double fsm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, sg = lane / MB, i = lane % MB;
+  double* sub = fsm + (wid * C::SG + sg) * C::SUB;
+  double* stage = sub;                       // 2 x BLK
+  double* TB = sub + 2 * C::BLK;             // MB x TP published T_b, then phi
+  double* PB = TB + C::TBS;                  // 2 pivot rows
+  const long P0 = t.P[0];
+  const long j = (long)blockIdx.x * C::CPC + wid * C::SG + sg;  // level-0 chunk
+  const bool live = j < P0;
+  const long nblk = (long)g.nb - 1;                             // blocks after the BC row
+  const int len = live ? (int)min((long)kChainC0, nblk - kChainC0 * j) : 0;
+  const long b0 = kChainC0 * j + 1;                             // first block row of the chunk
+  auto issue = [&](int tt) {  // cp.async of block row b0 + tt into stage buffer tt & 1
+    if (tt < len) {
+      const double* src = g.data + MM + (b0 + tt - 1) * C::BLK;
+      double* dst = stage + (tt & 1) * C::BLK;
 #pragma unroll
-    for (int i = 0; i < MB; ++i)
+      for (int q = 0; q < MB; ++q) cp_async16(dst + q * RW + 2 * (i ^ q), src + q * RW + 2 * i);
+    }
+    cp_async_commit();
+  };
+  double pc[MB], ph[MB];
 #pragma unroll
-      for (int c = 0; c < MB; ++c) R[(i) * MB + (c)] = slot[i * RW + MB + c];
-    // M = R^-1 by in-place Gauss-Jordan (no pivoting, like the reference's Lu):
-    // MB dependent pivot steps of MB^2 independent updates; stored over R
+  for (int r = 0; r < MB; ++r) {
+    pc[r] = r == i ? 1.0 : 0.0;
+    ph[r] = 0.0;
+  }
+  issue(0);
+#pragma unroll 1
+  for (int tt = 0; tt < kChainC0; ++tt) {
+    issue(tt + 1);
+    cp_async_wait<1>();
+    __syncwarp();
+    const bool act = tt < len;
+    double R[MB], S[MB], fv = 0.0;
+    {
+      const double* row = stage + (tt & 1) * C::BLK + i * RW;
+#pragma unroll
+      for (int q = 0; q < MB; ++q) {  // 16-byte piece q of the row sits at q ^ i
+        const double2 v = *reinterpret_cast<const double2*>(row + 2 * (q ^ i));
+        if (2 * q < MB) {
+          S[2 * q] = v.x;
+          S[2 * q + 1] = v.y;
+        } else {
+          R[2 * q - MB] = v.x;
+          R[2 * q - MB + 1] = v.y;
+        }
+      }
+      if (WITH_F && act) fv = __ldg(g.f + (b0 + tt) * MB + i);
+    }
+    // Gauss-Jordan on [R | S | f]: pivot row k broadcast through PB as
+    // 16-byte pairs (two alternating buffers: one __syncwarp per pivot)
+    double dg = 1.0;
 #pragma unroll
     for (int k = 0; k < MB; ++k) {
-      const double p = fast_rcp(R[k * MB + k]);
-      double col[MB], row[MB];
+      double2* pb = reinterpret_cast<double2*>(PB + (k & 1) * C::PIV);
+      if (i == k) {  // the pivot lane publishes its row and the pivot's reciprocal
 #pragma unroll
-      for (int i = 0; i < MB; ++i) col[i] = R[i * MB + k];
+        for (int c = 2 * (k / 2); c < MB; c += 2) pb[c / 2] = make_double2(R[c], R[c + 1]);
 #pragma unroll
-      for (int j = 0; j < MB; ++j) row[j] = R[k * MB + j] * p;
+        for (int c = 0; c < MB; c += 2) pb[(MB + c) / 2] = make_double2(S[c], S[c + 1]);
+        pb[MB] = make_double2(fv, fast_rcp(R[k]));
+      }
+      __syncwarp();
+      double pr[MB], ps[MB];
 #pragma unroll
-      for (int i = 0; i < MB; ++i)
+      for (int c = 2 * (k / 2); c < MB; c += 2) {
+        const double2 v = pb[c / 2];
+        pr[c] = v.x;
+        pr[c + 1] = v.y;
+      }
 #pragma unroll
-        for (int j = 0; j < MB; ++j) {
-          if (i == k)
-            R[i * MB + j] = j == k ? p : row[j];
-          else
-            R[i * MB + j] = j == k ? -col[i] * p : fma(-col[i], row[j], R[i * MB + j]);
+      for (int c = 0; c < MB; c += 2) {
+        const double2 v = pb[(MB + c) / 2];
+        ps[c] = v.x;
+        ps[c + 1] = v.y;
+      }
+      const double2 frp = pb[MB];
+      // branch-free: the pivot lane applies a zero multiplier
+      const bool me = i == k;
+      dg = me ? pr[k] : dg;
+      const double m = me ? 0.0 : R[k] * frp.y;
+#pragma unroll
+      for (int c = k + 1; c < MB; ++c) R[c] = fma(-m, pr[c], R[c]);
+#pragma unroll
+      for (int c = 0; c < MB; ++c) S[c] = fma(-m, ps[c], S[c]);
+      if (WITH_F) fv = fma(-m, frp.x, fv);
+    }
+    const double rd = fast_rcp(dg);
+    double T[MB];
+#pragma unroll
+    for (int c = 0; c < MB; ++c) T[c] = -S[c] * rd;
+    const double ci = fv * rd;
+    // this block's phi component: phi_i <- T_b[i] . phi + c_i (phi of the
+    // previous block is in every lane)
+    double phi_i = ci;
+    if (WITH_F)
+#pragma unroll
+      for (int l = 0; l < MB; ++l) phi_i = fma(T[l], ph[l], phi_i);
+    if (act) {
+      if (STORE_T) {
+        double2* dst = reinterpret_cast<double2*>(g.tm + (b0 + tt - 1) * MM) + i;
+#pragma unroll
+        for (int q = 0; q < MB / 2; ++q) dst[q * MB] = make_double2(T[2 * q], T[2 * q + 1]);
+      }
+      if (WITH_F) g.cv[(b0 + tt) * MB + i] = ci;
+    }
+    // publish T_b (row i) and phi_i, then fold the block into the chunk map
+    double* TBk = TB;
+#pragma unroll
+    for (int c = 0; c < MB; c += 2) *reinterpret_cast<double2*>(TBk + i * C::TP + c) = make_double2(T[c], T[c + 1]);
+    if (WITH_F) TBk[MB * C::TP + i] = phi_i;
+    __syncwarp();
+    if (act) {
+      double np[MB];
+#pragma unroll
+      for (int r = 0; r < MB; ++r) {
+        double a = 0.0;
+#pragma unroll
+        for (int c = 0; c < MB; c += 2) {
+          const double2 m = *reinterpret_cast<const double2*>(TBk + r * C::TP + c);
+          a = fma(m.y, pc[c + 1], fma(m.x, pc[c], a));
+        }
+        np[r] = a;
+      }
+#pragma unroll
+      for (int r = 0; r < MB; ++r) pc[r] = np[r];
+      if (WITH_F)
+#pragma unroll
+        for (int r = 0; r < MB; r += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(TBk + MB * C::TP + r);
+          ph[r] = v.x;
+          ph[r + 1] = v.y;
         }
     }
-    double (&Mi)[MB * MB] = R;
+    __syncwarp();  // TB is published again by the next block
+  }
+  cp_async_wait<0>();
+  if (live) {
+    if (STORE_T)
 #pragma unroll
-    for (int i = 0; i < MB; ++i)
+      for (int r = 0; r < MB; ++r) t.phi[0][j * MM + r * MB + i] = pc[r];
+    if (WITH_F) {
+      t.fl[1][(j + 1) * MB + i] = pick<MB>(ph, i);
+      if (j == 0) t.fl[1][i] = __ldg(g.f + i);
+    }
+  }
+  // ---- level 1: the CTA's 8 / MB level-1 chunks by a shared-memory tree
+  const int T = t.T;
+  const int gsub = wid * C::SG + sg;  // subgroup index in the CTA
+  if (!live) {  // identity beyond the last chunk
 #pragma unroll
-      for (int c = 0; c < MB; ++c) slot[i * RW + MB + c] = Mi[i * MB + c];
-    // T = -M S column by column (independent FMA chains), stored over S
+    for (int r = 0; r < MB; ++r) {
+      pc[r] = r == i ? 1.0 : 0.0;
+      ph[r] = 0.0;
+    }
+  }
+  __syncthreads();
+  fc_tree16<MB, WITH_F>(fsm, gsub, i, pc, ph);
+  if (T == 1) {  // the level-0 maps were the top (one CTA)
+    if (STORE_T && gsub == 0) chain_fc_top<MB>(g, t, fsm, lane, pc);
+    return;
+  }
+  {
+    const long c1 = (long)blockIdx.x * C::L1C + gsub / kChainC0;
+    if (gsub % kChainC0 == 0 && c1 * kChainC0 < P0) {
+      if (STORE_T)
 #pragma unroll
-    for (int c = 0; c < MB; ++c) {
-      double sc[MB];
-#pragma unroll
-      for (int l = 0; l < MB; ++l) sc[l] = slot[l * RW + c];
-#pragma unroll
-      for (int i = 0; i < MB; ++i) {
-        double acc = -Mi[i * MB] * sc[0];
-#pragma unroll
-        for (int l = 1; l < MB; ++l) acc = fma(-Mi[i * MB + l], sc[l], acc);
-        slot[i * RW + c] = acc;
+        for (int r = 0; r < MB; ++r) t.phi[1][c1 * MM + r * MB + i] = pc[r];
+      if (WITH_F) {
+        t.fl[2][(c1 + 1) * MB + i] = pick<MB>(ph, i);
+        if (c1 == 0) t.fl[2][i] = __ldg(g.f + i);
       }
     }
-    // ---- pair-interleave the slot in place (double2 (i, q) <-> (q, i)), then
-    // one TMA bulk store of the block: block b, double2 q*MB + i = row i,
-    // columns 2q, 2q+1 of [T | M] -- the solve's MB lanes read one contiguous
-    // MB*16-byte run per load (coalesced)
-    double2* s2 = reinterpret_cast<double2*>(slot);
-#pragma unroll
-    for (int i = 0; i < MB; ++i)
-#pragma unroll
-      for (int q = i + 1; q < MB; ++q) {
-        const double2 x = s2[i * MB + q], y = s2[q * MB + i];
-        s2[i * MB + q] = y;
-        s2[q * MB + i] = x;
+  }
+  // ---- levels >= 2 and the top: the last arriving CTA composes (16 subgroups)
+  long cprev = (long)blockIdx.x;  // arrival unit at level 2: this CTA
+  for (int l = 2;; ++l) {
+    const bool top = l == T;
+    long cc;
+    int expected, len;
+    if (top) {
+      cc = 0;
+      expected = T == 2 ? (int)gridDim.x : t.P[T - 1];
+      len = t.P[T - 1];
+    } else {
+      cc = l == 2 ? cprev * C::L1C / kChainC0 : cprev / kChainC0;
+      if (l == 2) {
+        const long first_cta = cc * kChainC0 / C::L1C;
+        const long last_cta = min((long)gridDim.x, (cc + 1) * kChainC0 / C::L1C);
+        expected = (int)(last_cta - first_cta);
+      } else {
+        expected = (int)min((long)kChainC0, (long)t.P[l - 1] - kChainC0 * cc);
       }
-    fence_proxy_async_smem();
-    bulk_s2g(g.tm + (bfirst - 1 + lane) * BW, slot, BW * 8);
-    bulk_commit_and_wait_read();
-  } else {  // missing blocks of a short last chunk: T = I
+      len = (int)min((long)kChainC0, (long)t.P[l - 1] - kChainC0 * cc);
+    }
+    if (!cta_last_arrive(t.cnt + t.coff[l] + cc, expected)) return;
+    const double* maps = t.phi[l - 1] + cc * kChainC0 * MM;
+    const double* vecs = t.fl[l] + (cc * kChainC0 + 1) * MB;
 #pragma unroll
-    for (int i = 0; i < MB; ++i)
+    for (int r = 0; r < MB; ++r) {
+      const bool have = gsub < len;
+      pc[r] = have ? __ldcg(maps + (long)gsub * MM + r * MB + i) : (r == i ? 1.0 : 0.0);
+      ph[r] = have && WITH_F ? __ldcg(vecs + (long)gsub * MB + r) : 0.0;
+    }
+    fc_tree16<MB, WITH_F>(fsm, gsub, i, pc, ph);
+    if (top) {
+      if (STORE_T && gsub == 0) chain_fc_top<MB>(g, t, fsm, lane, pc);
+      return;
+    }
+    if (gsub == 0) {
+      if (STORE_T)
 #pragma unroll
-      for (int c = 0; c < MB; ++c) slot[tix<MB>(i, c)] = i == c ? 1.0 : 0.0;
+        for (int r = 0; r < MB; ++r) t.phi[l][cc * MM + r * MB + i] = pc[r];
+      if (WITH_F) {
+        t.fl[l + 1][(cc + 1) * MB + i] = pick<MB>(ph, i);
+        if (cc == 0) t.fl[l + 1][i] = __ldg(g.f + i);
+      }
+    }
+    cprev = cc;
   }
-  __syncwarp();
-  // ---- Phi of the two chunks: tree of products P = later * earlier, in the T slots
-  chain_tree16<MB>(sm, 2, lane);
-  // ---- Phi^(0) of this warp's chunks, then the upper levels of the hierarchy
-  const long P0 = t.P[0];
-  for (int e = lane; e < 2 * MB * MB; e += 32) {
-    const int c = e / (MB * MB), r = e % (MB * MB);
-    if (2 * w + c < P0)
-      t.phi[0][(2 * w + c) * MB * MB + r] = sm[(c * kChainC0 + kChainC0 - 1) * SLOT + tix<MB>(r / MB, r % MB)];
-  }
-  chain_factor_up<MB>(g, t, sm, w, lane);
 }
 
 // ---------------------------------------------------------------------------
@@ -414,29 +559,22 @@ template <int MB, int MODE>
 struct Pass0 {
   long b0 = 0;
   int len = 0;
-  double Tq[kPre][MB], Mq[kPre][MB], Fq[kPre], Xq[kPre];  // Fq: f_i of the block (row i; shuffled for M f)
+  double Tq[kPre][MB], Cq[kPre], Xq[kPre];  // row i of T_b, c_b[i] (final) or x_b[i] (correction)
 
   __device__ __forceinline__ void fetch(const ChainLevelArgs& g, int i, int t, int slot) {
-    constexpr int BW = 2 * MB * MB;
+    constexpr int MM = MB * MB;
     if (t < len) {
-      const double2* row = reinterpret_cast<const double2*>(g.tm + (b0 + t - 1) * BW) + i;
+      const double2* row = reinterpret_cast<const double2*>(g.tm + (b0 + t - 1) * MM) + i;
 #pragma unroll
       for (int c = 0; c < MB / 2; ++c) {
         const double2 tv = __ldg(row + c * MB);
         Tq[slot][2 * c] = tv.x;
         Tq[slot][2 * c + 1] = tv.y;
       }
-      if (MODE != 2) {
-#pragma unroll
-        for (int c = 0; c < MB / 2; ++c) {
-          const double2 mv = __ldg(row + (MB / 2 + c) * MB);
-          Mq[slot][2 * c] = mv.x;
-          Mq[slot][2 * c + 1] = mv.y;
-        }
-        Fq[slot] = __ldg(g.f + (b0 + t) * MB + i);
-      } else {
+      if (MODE != 2)
+        Cq[slot] = __ldg(g.cv + (b0 + t) * MB + i);
+      else
         Xq[slot] = g.x[(b0 + t) * MB + i];
-      }
     }
   }
 
@@ -457,10 +595,7 @@ struct Pass0 {
     for (int t = 0; t < kChainC0; ++t) {
       const int sl = t % kPre;
       const bool act = t < len, last = t == len - 1;
-      double a = 0.0;
-      if (MODE != 2)
-#pragma unroll
-        for (int l = 0; l < MB; ++l) a = fma(Mq[sl][l], gshfl<MB>(Fq[sl], l), a);
+      double a = MODE != 2 ? Cq[sl] : 0.0;
 #pragma unroll
       for (int l = 0; l < MB; ++l) a = fma(Tq[sl][l], gshfl<MB>(y, l), a);
       const double xold = MODE == 2 ? Xq[sl] : 0.0;
@@ -672,24 +807,7 @@ __global__ void __launch_bounds__(16 * MB) chain_solve_kernel(ChainLevelArgs g, 
   bool finite = true;
   (void)MM;
 
-  if constexpr (KM == 0) {
-    Pass0<MB, 0> ps;
-    ps.start(g, j, live, i);
-    if (T >= 2) chain_stage<MB, false>(reg1, t.phi[0], kChainC0 * c, len1, nullptr, 0, 0, tid, NT);
-    const double y = ps.run(g, j, live, i, 0.0, 0.0, 0.0, 0.0, corr, num, den, finite);
-    if (live) {
-      t.fl[1][(j + 1) * MB + i] = y;
-      rr1[(grp + 1) * MB + i] = y;
-      if (j == 0) {
-        const double f0 = __ldg(g.f + i);
-        t.fl[1][i] = f0;
-        rr1[i] = f0;
-      }
-    }
-    if (T < 2) return;
-    __syncthreads();
-    if (tid < 32) chain_up<MB>(t, t.fl, reg1, c, len1, lane);
-  } else {
+  {
     constexpr int SEL = KM == 1 ? 0 : 1;
     double* const* Fd = SEL ? t.cfl : t.fl;  // rhs of the level-1 chain
     Pass0<MB, KM> ps;

@@ -1009,7 +1009,8 @@ struct ChainSolver {
   const double* corner = nullptr;
   long N = 0;              // block rows after the BC row
   std::vector<long> P;     // chunks per level (P[l], l < T)
-  DevBuf<double> tm, glu, x1, xlev[2], xtop[2];
+  DevBuf<double> tm, cv, glu, x1, xlev[2], xtop[2];
+  bool factor_pending = false;  // lazy factor: fused into the next solve's condense pass
   std::vector<std::unique_ptr<DevBuf<double>>> phi, fl, cfl;
   DevBuf<int> cnt;
   int coff[kChainMaxLev + 1] = {};
@@ -1034,7 +1035,8 @@ struct ChainSolver {
     const int T = (int)P.size();
     if (T > kChainMaxLev) return;
     const size_t MM = (size_t)MB * MB;
-    tm.alloc((size_t)N * 2 * MM);
+    tm.alloc((size_t)N * MM);
+    cv.alloc((size_t)(N + 1) * MB);
     phi.clear();
     fl.clear();
     cfl.clear();
@@ -1075,6 +1077,7 @@ struct ChainSolver {
     g.f = f;
     g.x = x;
     g.tm = tm.p;
+    g.cv = cv.p;
     g.status = st;
     return g;
   }
@@ -1099,12 +1102,12 @@ struct ChainSolver {
     return t;
   }
 
-  template <int M>
-  void factor_t(cudaStream_t s) {
-    constexpr int bytes = ChainSmem<M>::WARP * 8;
-    ensure_smem(reinterpret_cast<const void*>(chain_tm_kernel<M>), bytes);
-    const long warps = (N + 31) / 32;
-    chain_tm_kernel<M><<<(int)warps, 32, bytes, s>>>(args(nullptr, nullptr, nullptr), tree());
+  template <int M, bool STORE_T, bool WITH_F>
+  void fc_launch(const double* f, cudaStream_t s) {
+    constexpr int bytes = FcCfg<M>::SMEM;
+    ensure_smem(reinterpret_cast<const void*>(chain_fc_kernel<M, STORE_T, WITH_F>), bytes);
+    const int ctas = (int)((P[0] + FcCfg<M>::CPC - 1) / FcCfg<M>::CPC);
+    chain_fc_kernel<M, STORE_T, WITH_F><<<ctas, 128, bytes, s>>>(args(f, nullptr, nullptr), tree());
     LAUNCH_CHECK();
     ++launches;
   }
@@ -1130,7 +1133,11 @@ struct ChainSolver {
   template <int M>
   void solve_t(const double* f, double* x, DevStatus* st, cudaStream_t s, cudaEvent_t* ev) {
     const ChainTree t = tree();
-    solve_launch<M, 0>(args(f, x, nullptr), t, s);  // condense, reduced levels up
+    if (factor_pending)  // refactor + solve: one pass over A for both
+      fc_launch<M, true, true>(f, s);
+    else                 // condense only (the factor of an earlier solve stays)
+      fc_launch<M, false, true>(f, s);
+    factor_pending = false;
     down_launch<M>(args(f, x, nullptr), t, 0, s);   // top solve, x down to level 2
     if (ev) {
       CUDA_TRY(cudaEventRecord(ev[1], s));
@@ -1141,10 +1148,15 @@ struct ChainSolver {
     solve_launch<M, 2>(args(f, x, st), t, s);       // x += d, certificate
   }
 
-  void factor(cudaStream_t s) {
-    if (MB == 8) factor_t<8>(s);
-    else if (MB == 4) factor_t<4>(s);
-    else factor_t<2>(s);
+  // lazy: the factor runs fused with the next solve's condense pass; force()
+  // runs it alone (a caller that wants the factor data without a solve)
+  void factor(cudaStream_t) { factor_pending = true; }
+  void force(cudaStream_t s) {
+    if (!factor_pending) return;
+    if (MB == 8) fc_launch<8, true, false>(nullptr, s);
+    else if (MB == 4) fc_launch<4, true, false>(nullptr, s);
+    else fc_launch<2, true, false>(nullptr, s);
+    factor_pending = false;
   }
   // status slot must be reset by the caller
   void solve(const double* f, double* x, DevStatus* st, cudaStream_t s, cudaEvent_t* ev) {

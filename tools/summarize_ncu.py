@@ -17,10 +17,9 @@ import subprocess
 import sys
 from collections import defaultdict
 
-OUT = sys.argv[1] if len(sys.argv) > 1 else "profiles"
-TAG = sys.argv[2] if len(sys.argv) > 2 else "r01"
+OUT = sys.argv[1] if len(sys.argv) > 1 and __name__ == "__main__" else "profiles"
+TAG = sys.argv[2] if len(sys.argv) > 2 and __name__ == "__main__" else "r01"
 G = "gpurun_out"
-os.makedirs(OUT, exist_ok=True)
 
 CMD = {
     "": "ncu --metrics gpu__time_duration.sum --clock-control none python bench.py --steps 2 --warmup 3 "
@@ -92,26 +91,32 @@ def val(s):
     return float(num) * mult
 
 
-if os.path.exists(os.path.join(G, "launches.csv")):
-    launch_list(os.path.join(G, "launches.csv"), os.path.join(OUT, f"{TAG}_launches.txt"), CMD[""])
-for c in (0, 2, 3, 4):
-    src = os.path.join(G, f"launches_cfg{c}.csv")
-    if os.path.exists(src):
-        launch_list(src, os.path.join(OUT, f"{TAG}_launches_cfg{c}.txt"),
-                    f"ncu --metrics gpu__time_duration.sum --clock-control none python tools/cfg_step.py {c} 3")
+def main():
+    os.makedirs(OUT, exist_ok=True)
+    if os.path.exists(os.path.join(G, "launches.csv")):
+        launch_list(os.path.join(G, "launches.csv"), os.path.join(OUT, f"{TAG}_launches.txt"), CMD[""])
+    for c in (0, 2, 3, 4):
+        src = os.path.join(G, f"launches_cfg{c}.csv")
+        if os.path.exists(src):
+            launch_list(src, os.path.join(OUT, f"{TAG}_launches_cfg{c}.txt"),
+                        f"ncu --metrics gpu__time_duration.sum --clock-control none python tools/cfg_step.py {c} 3")
 
-rep = os.path.join(G, "full.ncu-rep")
-if os.path.exists(rep):
-    res = full_capture(rep, os.path.join(OUT, f"{TAG}_ncu_full.txt"),
-                       "tools/profile_step.py: cfg1 n=2^26 p=65536, second factor+solve")
-    for d in res:  # traffic of the dominant kernel for bench.py
-        if "segment_solve" in d.get("Kernel Name", ""):
-            t = val(d["dram__bytes_read.sum"]) + val(d["dram__bytes_write.sum"])
-            json.dump({"kernel": d["Kernel Name"], "dram_bytes_per_launch": t,
-                       "source": f"profiles/{TAG}_ncu_full.txt"}, open(os.path.join(OUT, "k3_traffic.json"), "w"),
-                      indent=1)
-for c in (2, 3, 4):
-    rep = os.path.join(G, f"full_cfg{c}.ncu-rep")
+    rep = os.path.join(G, "full.ncu-rep")
     if os.path.exists(rep):
-        full_capture(rep, os.path.join(OUT, f"{TAG}_ncu_full_cfg{c}.txt"),
-                     f"tools/cfg_step.py {c}: refactor + async solve, one launch per kernel")
+        res = full_capture(rep, os.path.join(OUT, f"{TAG}_ncu_full.txt"),
+                           "tools/profile_step.py: cfg1 n=2^26 p=65536, second factor+solve")
+        for d in res:  # traffic of the dominant kernel for bench.py
+            if "segment_solve" in d.get("Kernel Name", ""):
+                t = val(d["dram__bytes_read.sum"]) + val(d["dram__bytes_write.sum"])
+                json.dump({"kernel": d["Kernel Name"], "dram_bytes_per_launch": t,
+                           "source": f"profiles/{TAG}_ncu_full.txt"}, open(os.path.join(OUT, "k3_traffic.json"), "w"),
+                          indent=1)
+    for c in (2, 3, 4):
+        rep = os.path.join(G, f"full_cfg{c}.ncu-rep")
+        if os.path.exists(rep):
+            full_capture(rep, os.path.join(OUT, f"{TAG}_ncu_full_cfg{c}.txt"),
+                         f"tools/cfg_step.py {c}: refactor + async solve, one launch per kernel")
+
+
+if __name__ == "__main__":
+    main()
