@@ -148,6 +148,14 @@ int psg_reduced_dense(const psg_handle* h, double* T, char* err, size_t errlen);
 int psg_reduced_blocks(const psg_handle* h, double* diag, double* sub, double* super, char* err,
                        size_t errlen);
 
+/* The reduced right-hand side of f on the reference plan (the rrhs that
+ * solve() hands to solve_reduced, src/parfact.cpp:205-214): f at the
+ * separator rows plus every partition's condensed contribution kept_rhs
+ * (LocalFactorization::condense, src/localfact.cpp:765-781), computed by the
+ * exact phase-1 kernels; out has dim entries.  Not for LuPivot / Qr handles. */
+int psg_reduced_rhs(const psg_handle* h, const double* f, double* out, int on_device, void* stream, char* err,
+                    size_t errlen);
+
 /* Solve T x = rhs for the handle's reduced system (solve_reduced), device
  * or host vectors of length dim. */
 int psg_solve_reduced(const psg_handle* h, const double* rhs, double* x, int on_device,

@@ -415,9 +415,11 @@ def ref_set_threads(t: int) -> int:
 # members) -- the parity target of psg_local_* (tests/test_localfact_gpu.py)
 # --------------------------------------------------------------------------
 
-def ref_extract_block(A: Matrix, p: int, i: int) -> dict:
-    """extract_block(A, plan_partition(A, p), i) of the reference, as arrays."""
-    R = RefMatrix(A)
+def ref_extract_block(A, p: int, i: int) -> dict:
+    """extract_block(A, plan_partition(A, p), i) of the reference, as arrays
+    (A: a Matrix, or a RefMatrix to reuse its reference copy)."""
+    R = A if isinstance(A, RefMatrix) else RefMatrix(A)
+    A = R._keep
     dims = (C.c_int * 5)()
     err = C.create_string_buffer(512)
     hb = ref().ref_block_extract(R.h, p, i, dims, err, 512)

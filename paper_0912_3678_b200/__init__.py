@@ -153,6 +153,7 @@ def lib():
         L.psg_last_launches.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.psg_version.restype = C.c_char_p
         L.psg_factor_wait.argtypes = [vp, C.POINTER(C.c_double)]
+        L.psg_reduced_rhs.argtypes = [vp, vp, vp, ip, vp, cp, sz]
         L.psg_local_factor.argtypes = [C.POINTER(_Block), ip, C.c_double, vp, C.POINTER(vp), cp, sz]
         L.psg_local_query.argtypes = [vp, C.POINTER(_LocalInfo)]
         L.psg_local_read.argtypes = [vp, ip, vp, sz, cp, sz]
@@ -306,6 +307,22 @@ class ParallelFactorization:
         size = np.empty(self.q, np.int32)
         lib().psg_reduced_layout(self.handle, pos.ctypes.data, size.ctypes.data)
         return pos, size
+
+    def reduced_rhs(self, f, stream=None):
+        """Reduced right-hand side of f on the reference plan (psg_reduced_rhs):
+        f at the separators plus the partitions' condensed contributions."""
+        dev = _is_cuda(f)
+        if dev:
+            import torch
+            out = torch.empty(self.dim, dtype=torch.float64, device=f.device)
+        else:
+            f = np.ascontiguousarray(f, np.float64)
+            out = np.empty(self.dim)
+        _check_vec(f, self.A.n, "rhs")
+        err = C.create_string_buffer(512)
+        _check(lib().psg_reduced_rhs(self.handle, _addr(f), _addr(out), 1 if dev else 0, _stream_ptr(stream), err,
+                                     512), err)
+        return out
 
     def reduced_dense(self):
         """Dense image of the reduced matrix T (psg_reduced_dense)."""

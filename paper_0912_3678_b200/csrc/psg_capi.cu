@@ -742,6 +742,20 @@ struct TriSolver {
     }
   }
 
+  // phase 1 of the exact path alone: the level-0 reduced right-hand side
+  // (f at the separators plus every body's condensed contribution) lands in
+  // lv[0]->rhs_next
+  const double* exact_condense(const RowArr& F0, cudaStream_t s) {
+    TriLevel& L = *lv[0];
+    L.F = F0;
+    tri_interface_kernel<false, true><<<blocks_for(2L * L.S.nseg, 128), 128, 0, s>>>(L.A, L.F, L.S, 0, nullptr,
+                                                                                    L.rhsv.p);
+    LAUNCH_CHECK();
+    tri_assemble_rhs_kernel<<<blocks_for(L.S.nseg - 1, 256), 256, 0, s>>>(L.A, L.F, L.S, L.rhsv.p, L.rhs_next.p);
+    LAUNCH_CHECK();
+    return L.rhs_next.p;
+  }
+
 };
 
 // ----------------------------------------------------------------------------
@@ -1302,6 +1316,19 @@ struct GenSolver {
       LAUNCH_CHECK();
       launches += 2;
     }
+  }
+
+  // phase 1 of level 0 alone (the reduced right-hand side into lv[0]->rhs_next)
+  const double* condense(const double* f0, cudaStream_t s) {
+    GenLevel& L = *lv[0];
+    L.f = f0;
+    GenArgs g = args_of(L, nullptr);
+    gen_ends_kernel<1><<<2 * L.p, 32, 0, s>>>(g);
+    LAUNCH_CHECK();
+    const long ent = (long)L.q * L.k;
+    gen_assemble_rhs_kernel<<<(int)((ent + 255) / 256), 256, 0, s>>>(g, L.sep.p, L.rhs_next.p);
+    LAUNCH_CHECK();
+    return L.rhs_next.p;
   }
 
   void solve(const double* f0, double* x0, DevStatus* st, cudaStream_t s, cudaEvent_t* ev, size_t from = 0) {
@@ -3051,6 +3078,51 @@ int psg_solve_reduced(const psg_handle* hc, const double* rhs, double* x, int on
     CUDA_TRY(cudaStreamSynchronize(s));
     CUDA_TRY(cudaEventRecord(h->ev_done, s));
     if (stats) stats->reduced_ops += reduced_ops_of(h, false);
+    return 0;
+  } catch (const Fail& f_) {
+    return set_err(err, errlen, f_.code, f_.msg);
+  }
+}
+
+int psg_reduced_rhs(const psg_handle* hc, const double* f, double* out, int on_device, void* stream, char* err,
+                    size_t errlen) {
+  psg_handle* h = const_cast<psg_handle*>(hc);
+  DeviceGuard dg(h->device);
+  std::lock_guard<std::mutex> g(h->mu);
+  try {
+    cudaStream_t s = (cudaStream_t)stream;
+    order_on(h, s);
+    if (h->piv) throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "reduced rhs of a pivoting factorization: use solve"};
+    if (h->rot) throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "reduced rhs of a row-rotated (circulant) system"};
+    const int n = h->A.n;
+    const double* df = f;
+    DevBuf<double> dfb, dob;
+    if (!on_device) {
+      dfb.alloc(n);
+      CUDA_TRY(cudaMemcpyAsync(dfb.p, f, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+      df = dfb.p;
+    }
+    const double* rr = nullptr;
+    size_t dim = 0;
+    if (h->generic) {
+      if (h->gen.lv.size() < 2) throw Fail{PSG_E_INVALID_PARAMETER, "no reduced system"};
+      ensure_exact_generic(h, s);
+      rr = h->gen.condense(df, s);
+      dim = (size_t)h->gen.lv[0]->q * h->gen.lv[0]->k;
+    } else {
+      if (h->refined) throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "reduced system was refined internally (bodies > 1056 rows)"};
+      if (!h->exact_factored) {
+        h->tri.launches = 0;
+        h->tri.exact_factor(s);
+        h->exact_factored = true;
+      }
+      rr = h->tri.exact_condense(make_rows(df, 0, n), s);
+      dim = (size_t)h->tri.S0.nseg - 1;
+    }
+    CUDA_TRY(cudaMemcpyAsync(out, rr, sizeof(double) * dim, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                             s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    CUDA_TRY(cudaEventRecord(h->ev_done, s));
     return 0;
   } catch (const Fail& f_) {
     return set_err(err, errlen, f_.code, f_.msg);

@@ -19,3 +19,21 @@ def cuda():
         pytest.skip("no CUDA device")
     torch.cuda.init()
     return torch
+
+
+# Achieved parity values of the -m gpu run, merged into profiles/r02_parity.json
+# (and gpurun_out/) as they are recorded.
+def record_parity(key, values):
+    import json
+    for d in (os.path.join(ROOT, "profiles"), os.path.join(ROOT, "gpurun_out")):
+        os.makedirs(d, exist_ok=True)
+        path = os.path.join(d, "r02_parity.json")
+        old = {}
+        if os.path.exists(path):
+            try:
+                old = json.load(open(path))
+            except Exception:
+                old = {}
+        old[key] = values
+        with open(path, "w") as fh:
+            json.dump(old, fh, indent=1, sort_keys=True)

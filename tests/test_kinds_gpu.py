@@ -10,6 +10,7 @@ import pytest
 
 import oracle as O
 import paper_0912_3678_b200 as psg
+from conftest import record_parity
 
 pytestmark = pytest.mark.gpu
 
@@ -79,8 +80,14 @@ def test_generic_matches_reference_golden(cuda, path):
     g = np.load(path)
     A, f = O.generate_config(int(g["cfg"]), int(g["size"]), int(g["seed"]))
     got, st, F, _ = _gpu(cuda, A, int(g["p"]), f)
-    tol = 1e-12 if int(g["cfg"]) != 4 else 1e-10
-    assert O.rel_err(got, g["x"]) <= tol
+    # config 4: 10x the reference's own parallel-vs-sequential spread on the
+    # golden (x vs x_seq, both written by the unmodified reference)
+    spread = O.rel_err(g["x"], g["x_seq"]) if "x_seq" in g.files else 0.0
+    tol = 1e-12 if int(g["cfg"]) != 4 else 10 * max(spread, 1e-14)
+    d = O.rel_err(got, g["x"])
+    record_parity("golden_" + os.path.basename(path)[:-4], {"gpu_vs_ref_parallel": d, "ref_spread": spread,
+                                                          "bound": tol, "residual_gpu": O.residual(A, got, f)})
+    assert d <= tol
     assert O.residual(A, got, f) <= 1e-13
     assert F.q == int(g["q"]) and F.dim == int(g["dim"])
 
@@ -97,5 +104,5 @@ def test_full_size_configs(cuda, cfg, size, p):
     Ah = O.Matrix(A.kind, A.n, A.m, A.s, A.r, A.data.cpu().numpy(),
                   None if A.corner is None else A.corner.cpu().numpy(), A.corner_rows, A.corner_cols)
     want = O.solve_sequential(Ah, f.cpu().numpy())
-    tol = 1e-12 if cfg != 4 else 1e-10
+    tol = 1e-12 if cfg != 4 else 5e-11  # cfg 4: measured 1.67e-11 (tests/test_parity_pin_gpu.py, x up to 30)
     assert O.rel_err(x.cpu().numpy(), want) <= tol
