@@ -35,7 +35,6 @@ METRIC = "solved unknowns/s and % of HBM roofline, fp64 partitioned tridiagonal 
 UNIT = "unknowns/s"
 N_CFG1 = 1 << 26
 P_CFG1 = 65536
-CPU_SAMPLE_N = 1 << 24  # bounded CPU sample (rows of the same distribution)
 
 
 def peaks():
@@ -61,56 +60,75 @@ def cpu_model():
 
 # ---------------------------------------------------------------------------
 # CPU reference (oracle/_ref or the oracle port) -- baseline, never the product
+# BASELINE.md §3 / SURVEY.md §8(d): all host threads, 1 warm-up + median of 5,
+# parallel_factor(A, p_cpu, Lu) + solve with p_cpu = the config's own p for
+# config 0 and p_cpu = #threads for configs 1-3 (the reference's dense reduced
+# solve needs a dim^2 matrix: 34 GB at config 1's p = 65536); config 4 at
+# N = 2^12, p = 64 (the reference's Babd entry access is O(block row), so full
+# N takes hours); plus solve_sequential on one thread.
 # ---------------------------------------------------------------------------
-def run_cpu_reference(n: int, reps: int, warmup: int = 1):
-    import numpy as np
+CPU_CFG = {0: (1 << 20, 1024), 1: (N_CFG1, None), 2: (1 << 20, None), 3: (1 << 24, None), 4: (1 << 12, 64)}
+
+
+def run_cpu_reference(cfg: int, reps: int = 5, warmup: int = 1, sequential: bool = False):
     import oracle as O
 
     threads = os.cpu_count() or 1
-    A, f = O.generate_config(1, n, 2)
+    size, p = CPU_CFG[cfg]
+    A, f = O.generate_config(cfg, size, cfg + 1)
+    n = A.n
+    times = []
     if O.ref_available():
-        O.ref_set_threads(threads)
+        kind = "reference"
+        cores = 1 if sequential else threads
+        O.ref_set_threads(cores)
+        p = p or threads
         R = O.RefMatrix(A)
-        kind, cores, p = "reference", threads, threads
-        times = []
         for it in range(warmup + reps):
             t0 = time.perf_counter()
-            F = R.factor(p)
-            x, _, _ = F.solve(f)
-            dt = time.perf_counter() - t0
-            del F
+            if sequential:
+                R.solve_sequential(f)
+            else:
+                F = R.factor(p)
+                F.solve(f)
+                del F
             if it >= warmup:
-                times.append(dt)
+                times.append(time.perf_counter() - t0)
+        O.ref_set_threads(threads)
     else:  # oracle port (single thread)
-        kind, cores, p = "port", 1, 64
-        times = []
+        kind, cores, p = "port", 1, p or 64
         for it in range(warmup + reps):
             t0 = time.perf_counter()
-            x, _ = O.parallel_solve(A, p, f)
-            dt = time.perf_counter() - t0
+            if sequential:
+                O.solve_sequential(A, f)
+            else:
+                O.parallel_solve(A, p, f)
             if it >= warmup:
-                times.append(dt)
+                times.append(time.perf_counter() - t0)
     med = statistics.median(times)
-    sample = (f"cfg1 distribution, n=2^{n.bit_length() - 1} ({n} rows), p={p}, "
-              f"parallel_factor+solve (Strategy::Lu), median of {reps}; host: {cpu_model()}")
-    return dict(value=n / med, unit=UNIT, cores=cores, kind=kind, sample=sample,
-                seconds_per_sample=med), times
+    what = "solve_sequential (1 thread)" if sequential else f"parallel_factor+solve (Strategy::Lu), p={p}"
+    sample = (f"cfg{cfg}, n={n}, {what}, {warmup} warm-up + median of {reps}; "
+              f"host: {cpu_model()}, {cores} thread(s)")
+    return dict(value=n / med, unit=UNIT, cores=cores, kind=kind, sample=sample, seconds_per_sample=med, n=n,
+                p=None if sequential else p), times
 
 
 def impl_reference(args, rank, world):
     if rank != 0:
         return 0
     steps = max(1, args.steps)
-    info, times = run_cpu_reference(CPU_SAMPLE_N, steps, warmup=max(0, min(args.warmup, 1)))
+    info, times = run_cpu_reference(1, steps, warmup=max(0, min(args.warmup, 1)))
     ms = 1e3 * sum(times) / len(times)
     line = {
         "metric": METRIC, "value": info["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SplitMix64, BASELINE cfg1 distribution)",
         "impl": "reference",
-        "config": {"workload": "cfg1: tridiagonal fp64, CPU reference on a bounded sample",
-                   "n": CPU_SAMPLE_N, "p": info["sample"].split("p=")[1].split(",")[0],
-                   "threads": info["cores"]},
+        "config": {"workload": "cfg1: tridiagonal fp64 n=2^26, factor+solve per step (the unmodified reference, "
+                               "oracle/_ref, all host threads)",
+                   "n": info["n"], "p": info["p"], "threads": info["cores"],
+                   "p_note": "p = #threads: the reference's reduced solve is a dense dim^2 LU (34 GB at the "
+                             "config's p = 65536, SURVEY.md §0.3); p is the paper's processor count"},
         "cpu_baseline": {k: info[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": info["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -211,21 +229,38 @@ def other_configs(psg, torch, peak, dev, steps=20):
             H.solve_async(f, x)
         H.sync()
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         st = psg.SolveStats()
-        e0.record()
-        for _ in range(steps):  # no per-phase events inside the bracket (as the headline)
-            H.refactor(A)
-            H.solve_async(f, x)
-        H.sync(st)
-        e1.record()
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / steps
         corner = 0 if A.corner is None else A.corner.numel()
-        min_bytes = (A.data.numel() + corner + 2 * A.n) * 8
+        in_bytes = (A.data.numel() + corner + 2 * A.n) * 8
+        if in_bytes < 4 * (126 << 20):  # fits in L2: flush it before every step, time each step alone
+            flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+            for e0, e1 in evs:
+                flush.random_(0, 255)
+                e0.record()
+                H.refactor(A)
+                H.solve_async(f, x)
+                H.sync(st)
+                e1.record()
+            torch.cuda.synchronize()
+            ms = sum(e0.elapsed_time(e1) for e0, e1 in evs) / steps
+            l2 = "L2 flushed (512 MB write) before each step; each step timed alone, incl. its certificate sync"
+            del flush
+        else:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(steps):  # no per-phase events inside the bracket (as the headline)
+                H.refactor(A)
+                H.solve_async(f, x)
+            H.sync(st)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / steps
+            l2 = "inputs larger than L2; back-to-back steps"
+        min_bytes = in_bytes
         out.append({"cfg": cfg, "n": A.n, "p": p, "ms_per_step": ms, "unknowns_per_s": A.n / (ms / 1e3),
                     "hbm_roofline_frac": min_bytes / (ms / 1e3) / 1e9 / peak, "min_bytes": min_bytes,
-                    "residual": psg.residual(A, x, f), "certificate": st.certificate,
+                    "residual": psg.residual(A, x, f), "certificate": st.certificate, "l2": l2,
                     "path": "speculative" if st.speculative else "exact", "fallbacks": st.fallbacks})
         H.close()
         del A, f, x
@@ -376,11 +411,18 @@ def impl_ours(args, rank, world, local_rank):
 
     cpu = None
     if not args.no_cpu_baseline:
-        try:
-            cpu, _ = run_cpu_reference(CPU_SAMPLE_N, 3)
-            cpu.pop("seconds_per_sample", None)
-        except Exception as e:  # baseline is informative only
-            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable", "sample": str(e)}
+        def cpu_fig(cfg, sequential=False):
+            try:
+                d, _ = run_cpu_reference(cfg, sequential=sequential)
+                d.pop("seconds_per_sample", None)
+                return d
+            except Exception as e:  # baseline is informative only
+                return {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable", "sample": str(e)}
+
+        cpu = cpu_fig(1)
+        cpu["single_core_solve_sequential"] = cpu_fig(1, sequential=True)
+        for oc in other or []:
+            oc["cpu_baseline"] = cpu_fig(oc["cfg"])
 
     value = units / (ms_step / 1e3)
     line = {
