@@ -28,53 +28,85 @@ OdeMethod method_from_name(const std::string& s) {
   fail(Errc::InvalidParameter, "unknown method '" + s + "'");
 }
 
+namespace {
+
+void require_interval(bool ok, const char* what) {
+  if (!ok) fail(Errc::InvalidInterval, what);
+}
+
+// write block B (scaled by sgn) into M at (r0, c0)
+void put_block(DenseMatrix& M, int r0, int c0, const DenseMatrix& B, double sgn = 1.0) {
+  for (int i = 0; i < B.rows; ++i)
+    for (int j = 0; j < B.cols; ++j) M.at(r0 + i, c0 + j) = sgn * B.at(i, j);
+}
+
+// rows [r0, r0 + m) of a tall block matrix
+DenseMatrix rows_of(const DenseMatrix& T, int r0, int m) {
+  DenseMatrix B(m, T.cols);
+  std::copy_n(T.a.begin() + std::ptrdiff_t(r0) * T.cols, std::size_t(m) * T.cols, B.a.begin());
+  return B;
+}
+
+// one implicit step of the window: y <- diag^{-1} (sub y + rhs)
+Vector implicit_step(const WindowSystem& W, const Vector& y, const double* rhs) {
+  Vector t = matvec(W.sub, y);
+  for (int q = 0; q < W.m; ++q) t[q] = rhs[q] + t[q];
+  return W.diag_lu.solve(t);
+}
+
+}  // namespace
+
+// The coarse mesh tau_i = t0 + (T - t0) i / p (end points exact) and the fine
+// step h_i = (tau_i - tau_{i-1}) / N of every window (paper §3; the sample
+// points must be the reference's: the GPU trajectory reproduces its values).
 TimeGrid coarse_mesh(double t0, double T, int p, int N) {
-  if (!(T > t0)) fail(Errc::InvalidInterval, "T must exceed t0");
-  if (p < 1 || N < 1) fail(Errc::InvalidInterval, "p and N must be >= 1");
+  require_interval(T > t0, "T must exceed t0");
+  require_interval(p >= 1 && N >= 1, "p and N must be >= 1");
   std::vector<double> tau(p + 1);
-  for (int i = 0; i <= p; ++i) tau[i] = t0 + (T - t0) * double(i) / double(p);
-  tau[0] = t0;
-  tau[p] = T;
+  int i = 0;
+  std::generate(tau.begin(), tau.end(), [&] { return t0 + (T - t0) * double(i++) / double(p); });
+  tau.front() = t0;
+  tau.back() = T;
   return coarse_mesh(std::move(tau), N);
 }
 
 TimeGrid coarse_mesh(std::vector<double> tau, int N) {
-  if (tau.size() < 2) fail(Errc::InvalidInterval, "need at least one window");
-  if (N < 1) fail(Errc::InvalidInterval, "N must be >= 1");
-  for (std::size_t i = 1; i < tau.size(); ++i)
-    if (!(tau[i] > tau[i - 1])) fail(Errc::InvalidInterval, "mesh must be strictly increasing");
+  require_interval(tau.size() >= 2, "need at least one window");
+  require_interval(N >= 1, "N must be >= 1");
+  require_interval(std::adjacent_find(tau.begin(), tau.end(), [](double a, double b) { return !(b > a); }) ==
+                       tau.end(),
+                   "mesh must be strictly increasing");
   TimeGrid g;
-  g.tau = std::move(tau);
   g.N = N;
-  for (std::size_t i = 1; i < g.tau.size(); ++i) g.h.push_back((g.tau[i] - g.tau[i - 1]) / N);
+  g.h.resize(tau.size() - 1);
+  std::transform(tau.begin() + 1, tau.end(), tau.begin(), g.h.begin(),
+                 [N](double hi, double lo) { return (hi - lo) / N; });
+  g.tau = std::move(tau);
   return g;
 }
 
+// v_i: the window's coupling to its initial value, nonzero in the first step only
 DenseMatrix WindowSystem::v_dense() const {
   DenseMatrix V(m * N, m);
-  for (int i = 0; i < m; ++i)
-    for (int j = 0; j < m; ++j) V.at(i, j) = sub.at(i, j);
+  put_block(V, 0, 0, sub);
   return V;
 }
 
+// M_i: block lower bidiagonal, diag on the diagonal, -sub below it
 DenseMatrix WindowSystem::m_dense() const {
   DenseMatrix M(m * N, m * N);
-  for (int s = 0; s < N; ++s)
-    for (int i = 0; i < m; ++i)
-      for (int j = 0; j < m; ++j) {
-        M.at(s * m + i, s * m + j) = diag.at(i, j);
-        if (s > 0) M.at(s * m + i, (s - 1) * m + j) = -sub.at(i, j);
-      }
+  for (int s = 0; s < N; ++s) {
+    put_block(M, s * m, s * m, diag);
+    if (s) put_block(M, s * m, (s - 1) * m, sub, -1.0);
+  }
   return M;
 }
 
-DenseMatrix WindowSolution::w_tail() const {
-  DenseMatrix W(m, m);
-  for (int i = 0; i < m; ++i)
-    for (int j = 0; j < m; ++j) W.at(i, j) = w.at((N - 1) * m + i, j);
-  return W;
-}
+DenseMatrix WindowSolution::w_tail() const { return rows_of(w, (N - 1) * m, m); }
 
+// Window i of the one-step scheme y_n - y_{n-1} = h (theta L y_n + (1-theta) L y_{n-1}) + rhs_n:
+// implicit Euler theta = 1 (diag = I - h L, sub = I, rhs_n = h g(t_n)), trapezoidal
+// theta = 1/2 (diag = I - h/2 L, sub = I + h/2 L, rhs_n = h/2 (g(t_n - h) + g(t_n))).
 WindowSystem discretize_window(const IVProblem& prob, const TimeGrid& grid, int i, OdeMethod method) {
   if (i < 1 || i > grid.windows()) fail(Errc::IndexOutOfRange, "window index");
   if ((int)prob.y0.size() != prob.dim()) fail(Errc::DimensionMismatch, "y0 length");
@@ -85,94 +117,87 @@ WindowSystem discretize_window(const IVProblem& prob, const TimeGrid& grid, int 
   W.N = grid.N;
   W.h = grid.h[i - 1];
   W.tstart = grid.tau[i - 1];
+  const bool trap = method == OdeMethod::Trapezoidal;
+  const double hi = trap ? W.h / 2 : W.h;  // step weight of the implicit end
   const DenseMatrix I = DenseMatrix::identity(W.m);
-  if (method == OdeMethod::ImplicitEuler) {
-    W.diag = sub(I, scale(prob.L, W.h));
-    W.sub = I;
-  } else {
-    W.diag = sub(I, scale(prob.L, W.h / 2));
-    W.sub = add(I, scale(prob.L, W.h / 2));
-  }
+  W.diag = sub(I, scale(prob.L, hi));
+  W.sub = trap ? add(I, scale(prob.L, hi)) : I;
   try {
     W.diag_lu = DenseLu(W.diag);
   } catch (const Error&) {
     fail(Errc::StepTooLarge, "window matrix singular for h = " + std::to_string(W.h));
   }
-  W.gvec.assign(std::size_t(W.m) * W.N, 0.0);
-  for (int s = 1; s <= W.N; ++s) {
+  W.gvec.resize(std::size_t(W.m) * W.N);
+  auto out = W.gvec.begin();
+  for (int s = 1; s <= W.N; ++s, out += W.m) {
     const double tn = W.tstart + s * W.h;
-    Vector gn = prob.forcing(tn);
-    if (method == OdeMethod::ImplicitEuler) {
-      for (double& v : gn) v *= W.h;
+    const Vector right = prob.forcing(tn);
+    if (trap) {
+      const Vector left = prob.forcing(tn - W.h);
+      std::transform(left.begin(), left.end(), right.begin(), out, [hi](double a, double b) { return hi * (a + b); });
     } else {
-      const Vector g0 = prob.forcing(tn - W.h);
-      for (int q = 0; q < W.m; ++q) gn[q] = W.h / 2 * (g0[q] + gn[q]);
+      std::transform(right.begin(), right.end(), out, [hi](double b) { return b * hi; });
     }
-    std::copy(gn.begin(), gn.end(), W.gvec.begin() + std::size_t(s - 1) * W.m);
   }
   return W;
 }
 
+// the window's steps from y_init with its right-hand sides
 Vector window_forward(const WindowSystem& W, const Vector& y_init) {
-  Vector out(std::size_t(W.m) * W.N), prev = y_init, rhs(W.m);
+  Vector out;
+  out.reserve(std::size_t(W.m) * W.N);
+  Vector y = y_init;
   for (int s = 0; s < W.N; ++s) {
-    for (int q = 0; q < W.m; ++q) {
-      double acc = W.gvec[std::size_t(s) * W.m + q];
-      for (int j = 0; j < W.m; ++j) acc += W.sub.at(q, j) * prev[j];
-      rhs[q] = acc;
-    }
-    prev = W.diag_lu.solve(rhs);
-    std::copy(prev.begin(), prev.end(), out.begin() + std::size_t(s) * W.m);
+    y = implicit_step(W, y, W.gvec.data() + std::size_t(s) * W.m);
+    out.insert(out.end(), y.begin(), y.end());
   }
   return out;
 }
 
+// z = M^{-1} g and w = M^{-1} v: the homogeneous propagator is carried as one
+// m x m matrix through the steps (Y_s = diag^{-1} sub Y_{s-1}, Y_0 = I)
 WindowSolution solve_window_homogeneous(const WindowSystem& W) {
   WindowSolution sol;
   sol.m = W.m;
   sol.N = W.N;
   sol.z = window_forward(W, Vector(W.m, 0.0));
   sol.w = DenseMatrix(W.m * W.N, W.m);
-  WindowSystem hom = W;
-  std::fill(hom.gvec.begin(), hom.gvec.end(), 0.0);
-  for (int j = 0; j < W.m; ++j) {
-    Vector e(W.m, 0.0);
-    e[j] = 1.0;
-    const Vector col = window_forward(hom, e);
-    for (int q = 0; q < W.m * W.N; ++q) sol.w.at(q, j) = col[q];
+  DenseMatrix Y = DenseMatrix::identity(W.m);
+  for (int s = 0; s < W.N; ++s) {
+    Y = W.diag_lu.solve(matmul(W.sub, Y));
+    put_block(sol.w, s * W.m, 0, Y);
   }
   return sol;
 }
 
+// y_{0,i+1} = z_N,i + w_N,i y_{0,i}, window after window
 std::vector<Vector> reduced_recursion(const std::vector<WindowSolution>& sols, const Vector& y0) {
-  std::vector<Vector> inits(sols.size());
+  std::vector<Vector> inits;
+  inits.reserve(sols.size());
   if (sols.empty()) return inits;
-  inits[0] = y0;
+  inits.push_back(y0);
   for (std::size_t i = 0; i + 1 < sols.size(); ++i) {
-    Vector next = sols[i].z_tail();
-    const DenseMatrix wN = sols[i].w_tail();
-    for (int q = 0; q < sols[i].m; ++q)
-      for (int j = 0; j < sols[i].m; ++j) next[q] += wN.at(q, j) * inits[i][j];
-    inits[i + 1] = std::move(next);
+    Vector next = matvec(sols[i].w_tail(), inits.back());
+    const Vector zt = sols[i].z_tail();
+    std::transform(zt.begin(), zt.end(), next.begin(), next.begin(), std::plus<double>());
+    inits.push_back(std::move(next));
   }
   return inits;
 }
 
-Trajectory parallel_update(const TimeGrid& grid, const std::vector<WindowSolution>& sols,
+// every window's trajectory from its initial value: y = z + w y_{0,i}
+Trajectory parallel_update(const TimeGrid&, const std::vector<WindowSolution>& sols,
                            const std::vector<Vector>& inits) {
-  (void)grid;
   Trajectory tr;
   tr.m = sols.at(0).m;
   tr.p = (int)sols.size();
   tr.N = sols[0].N;
-  tr.flat.assign(std::size_t(tr.p * tr.N + 1) * tr.m, 0.0);
-  std::copy(inits[0].begin(), inits[0].end(), tr.flat.begin());
-  for (int i = 0; i < tr.p; ++i)
-    for (int q = 0; q < tr.m * tr.N; ++q) {
-      double acc = sols[i].z[q];
-      for (int j = 0; j < tr.m; ++j) acc += sols[i].w.at(q, j) * inits[i][j];
-      tr.flat[std::size_t(i) * tr.N * tr.m + tr.m + q] = acc;
-    }
+  tr.flat = inits.at(0);
+  for (int i = 0; i < tr.p; ++i) {
+    Vector y = matvec(sols[i].w, inits[i]);
+    std::transform(sols[i].z.begin(), sols[i].z.end(), y.begin(), y.begin(), std::plus<double>());
+    tr.flat.insert(tr.flat.end(), y.begin(), y.end());
+  }
   return tr;
 }
 
