@@ -298,7 +298,9 @@ int psg_dense_solve(int n, const double* T, const double* rhs, double* x, long l
 enum psg_option {
   PSG_OPT_SPECULATIVE = 0, /* 1 (default): truncated interface + certificate; 0: exact */
   PSG_OPT_HALO = 1,        /* truncation depth H in rows (default 32) */
-  PSG_OPT_CERT_TOL = 2     /* certificate threshold (default 1e-14) */
+  PSG_OPT_CERT_TOL = 2,    /* certificate threshold (default 1e-14) */
+  PSG_OPT_BODY_CERT = 3    /* 1: the tridiagonal certificate also covers every body row (componentwise
+                              backward error from the rows K3 already holds; default 0: separator rows) */
 };
 int psg_set_option(psg_handle* h, int option, double value);
 

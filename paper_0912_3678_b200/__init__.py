@@ -283,7 +283,7 @@ class ParallelFactorization:
             pass
 
     def set_option(self, option: str, value: float):
-        code = {"speculative": 0, "halo": 1, "cert_tol": 2}[option]
+        code = {"speculative": 0, "halo": 1, "cert_tol": 2, "body_cert": 3}[option]
         _check(lib().psg_set_option(self.handle, code, float(value)), C.create_string_buffer(b"bad option"))
 
     def launches(self):

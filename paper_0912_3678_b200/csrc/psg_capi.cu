@@ -432,13 +432,21 @@ SegMap segment_uniform(int q, int& maxlen) {
   return SegMap{p, base, rem, nullptr, nullptr};
 }
 
-template <int M>
-void launch_segment_solve(const TriSolveArgs& a, int nseg, cudaStream_t s, bool pdl) {
+template <int M, bool BODY>
+void launch_segment_solve_t(const TriSolveArgs& a, int nseg, cudaStream_t s, bool pdl) {
   constexpr int bytes = TriWarpSmem<M>::BYTES;
   if (pdl)
-    launch_pdl(tri_segment_solve_kernel<M>, dim3(nseg), dim3(32), bytes, s, a);
+    launch_pdl(tri_segment_solve_kernel<M, false, BODY>, dim3(nseg), dim3(32), bytes, s, a);
   else
-    tri_segment_solve_kernel<M><<<nseg, 32, bytes, s>>>(a);
+    tri_segment_solve_kernel<M, false, BODY><<<nseg, 32, bytes, s>>>(a);
+}
+
+template <int M>
+void launch_segment_solve(const TriSolveArgs& a, int nseg, cudaStream_t s, bool pdl) {
+  if (a.body)
+    launch_segment_solve_t<M, true>(a, nseg, s, pdl);
+  else
+    launch_segment_solve_t<M, false>(a, nseg, s, pdl);
 }
 
 // pdl: K3 stages A and F before waiting for its predecessor -- only valid
@@ -479,7 +487,7 @@ void segment_solve(const TriSolveArgs& a, int nseg, int maxlen, cudaStream_t s, 
     const char* e = getenv("PSG_K3_PERSIST");
     return e && atoi(e) > 0;
   }();
-  if (persist && persist_on && maxlen > 32 * 17 && maxlen <= 32 * 33 && nseg > 4 * sm_count()) {
+  if (persist && persist_on && !a.body && maxlen > 32 * 17 && maxlen <= 32 * 33 && nseg > 4 * sm_count()) {
     launch_segment_solve_persist(a, nseg, s, pdl);
     LAUNCH_CHECK();
     return;
@@ -510,6 +518,7 @@ struct TriSolver {
   DevBuf<double> wts, Tdiag, xsep;
   DevBuf<double4> crec;  // per-segment certificate records
   DevBuf<unsigned> cctr;  // certificate kernel: finished-block counter (last block publishes the status)
+  bool body_cert = false; // K3 also certifies every body row (PSG_OPT_BODY_CERT)
   // exact multi-level path (built on demand)
   std::vector<std::unique_ptr<TriLevel>> lv;
   int launches = 0;
@@ -562,6 +571,12 @@ struct TriSolver {
     a.x = x;
     a.crec = crec.p;
     a.status = st;
+    a.body = body_cert ? 1 : 0;
+    // the separator certificate stays a separate PDL-chained kernel: folding it
+    // into K3 (each segment's arrival at its two separators, the later one
+    // evaluating omega, the last segment publishing the status) held every K3
+    // warp for its fences and atomics -- config 1 0.455 -> 0.694 ms/step
+    //
     segment_solve(a, S0.nseg, maxlen0, s, pdl, /*persist=*/true);
     launch_pdl(tri_cert_kernel, dim3(blocks_for(S0.nseg - 1, 256)), dim3(256), 0, s, S0.nseg - 1,
                (const double4*)crec.p, st, host_out, cctr.p);
@@ -637,6 +652,7 @@ struct TriSolver {
         a.crec = crec.p;
         a.status = st;
         a.seg0 = ia;
+        a.body = body_cert ? 1 : 0;
         segment_solve(a, ib - ia, maxlen0, s, /*pdl=*/true);
         launches += 1;
         CUDA_TRY(cudaEventRecord(evs[2 + 2 * g], s));
@@ -2080,6 +2096,7 @@ int psg_set_option(psg_handle* h, int option, double value) {
         if ((int)value != kHalo) return 1 + PSG_E_INVALID_PARAMETER;  // fixed to the warp width
         break;
       case PSG_OPT_CERT_TOL: h->cert_tol = value; break;
+      case PSG_OPT_BODY_CERT: h->tri.body_cert = value != 0.0; break;
       default: return 1 + PSG_E_INVALID_PARAMETER;
     }
   } catch (const Fail& f_) {

@@ -390,6 +390,7 @@ struct TriSolveArgs {
   DevStatus* status;
   int seg0;            // first segment of this launch (the host path solves in row chunks)
   int seg_end;         // persistent launch: segments [seg0 + blockIdx.x, seg_end) with stride gridDim.x
+  int body;            // 1: also the componentwise backward error of every body row (K3 <.., BODY = true>)
 };
 
 template <int M>
@@ -402,7 +403,7 @@ struct TriWarpSmem {
 // PERSIST: one warp per SM slot loops over segments seg0 + blockIdx.x,
 // + gridDim.x, ... with two staging buffers -- the next segment's rows are in
 // flight while this one is solved (continuous HBM traffic per warp).
-template <int M, bool PERSIST = false>
+template <int M, bool PERSIST = false, bool BODY = false>
 __global__ void __launch_bounds__(32) tri_segment_solve_kernel(TriSolveArgs args) {
   static_assert(M % 2 == 1 && M >= 3, "M must be odd and >= 3");
   constexpr int ROW = TriWarpSmem<M>::ROW;
@@ -544,13 +545,47 @@ __global__ void __launch_bounds__(32) tri_segment_solve_kernel(TriSolveArgs args
   if (lane == 31) Fn = 0.0;
   const double Ev = dE - aE * Fv - cE * Fn;
 
-  // ---- chunk back-substitution, finite check, stage y over f
+  // ---- chunk back-substitution, finite check, stage y over f.  BODY: the
+  // componentwise backward error of every body row too (the row's f is read
+  // before y overwrites it; separator couplings are folded into f, which only
+  // shrinks the denominator: a conservative bound), no extra HBM traffic.
   bool finite = true;
+  double wnum = 0.0, wden = 1.0;  // largest num / den so far, compared by cross products (no division per row)
+  double ym2 = BODY ? __shfl_up_sync(FULL, Ev, 1) : 0.0, ym1 = 0.0, fm1 = 0.0;  // y_{q0-1}: previous chunk's last
+  if (BODY && lane == 0) ym2 = 0.0;
 #pragma unroll
   for (int j = 0; j < M; ++j) {
     const double y = (j == 0) ? Fv : (j == M - 1) ? Ev : dp[j] - ap[j] * Fv - cp[j] * Ev;
     if (q0 + j < L) finite &= isfinite(y);
+    if (BODY) {
+      const double fj = sF[q0 + j];
+      if (j > 0) {  // row q0 + j - 1: a y_{j-2} + b y_{j-1} + c y_j = f
+        const int q = q0 + j - 1;
+        const double ta = sA[q] * ym2, tb = sB[q] * ym1, tc = sC[q] * y;
+        const double num = fabs(((fm1 - ta) - tb) - tc), den = fabs(fm1) + fabs(ta) + fabs(tb) + fabs(tc);
+        if (q < L && !(num * wden <= wnum * den)) {  // NaN-safe: a non-finite row always wins
+          wnum = num;
+          wden = den;
+        }
+      }
+      ym2 = j > 0 ? ym1 : ym2;
+      ym1 = y;
+      fm1 = fj;
+    }
     sF[q0 + j] = y;
+  }
+  if (BODY) {  // the chunk's last row: its right neighbour is the next chunk's first (Fn)
+    const int q = q0 + M - 1;
+    const double ta = sA[q] * ym2, tb = sB[q] * ym1, tc = sC[q] * Fn;
+    const double num = fabs(((fm1 - ta) - tb) - tc), den = fabs(fm1) + fabs(ta) + fabs(tb) + fabs(tc);
+    if (q < L && !(num * wden <= wnum * den)) {
+      wnum = num;
+      wden = den;
+    }
+    double wbody = wden > 0.0 ? wnum / wden : (wnum > 0.0 ? __longlong_as_double(0x7ff0000000000000ll) : 0.0);
+    if (!(wbody <= 1.0e300)) wbody = __longlong_as_double(0x7ff0000000000000ll);
+    for (int o = 16; o > 0; o >>= 1) wbody = fmax(wbody, __shfl_xor_sync(FULL, wbody, o));
+    if (lane == 0 && wbody > 0.0 && args.status) status_cert(args.status, wbody);
   }
   if (args.status) {
     const bool piv_ok = __all_sync(FULL, isfinite(rsum));
@@ -582,9 +617,10 @@ __global__ void __launch_bounds__(32) tri_segment_solve_kernel(TriSolveArgs args
     if (has_r) args.x[s + L] = xr;
     // certificate record: right separator t = s+L: (a_t y_{t-1}, b_t x_t, f_t),
     // left separator: c_{s-1} y_s
-    if (args.crec)
+    if (args.crec) {
       args.crec[seg] = make_double4(has_r ? sepv[0] * sF[L - 1] : 0.0, has_r ? sepv[1] * xr : 0.0,
                                     has_r ? sepv[2] : 0.0, has_l ? sepv[3] * sF[0] : 0.0);
+    }
   }
   if (PERSIST) {  // this buffer is refilled by the next iteration's prefetch
     fence_proxy_async_smem();

@@ -295,3 +295,58 @@ def test_host_buffer_pipeline_fallback(cuda):
     x2 = psg.solve(F, _dev(cuda, f), st).cpu().numpy()  # the handle stays exact
     assert st.speculative == 0
     assert O.rel_err(x, x2) <= 1e-12
+
+
+def _planted_unstable(torch, n, p, body, offset):
+    """Config-0 distribution with one body made unstable for the no-pivot
+    elimination: a 2x2 block [[eps, 1], [1, 1]] (a_r = 0, b_r = 1e-12) deep
+    inside body `body`, far from both separators."""
+    A, f = O.generate_config(0, n, 5)
+    d = A.data.copy()
+    plan = O.RefMatrix(A).plan(p) if O.ref_available() else None
+    b0 = plan["body"][body][0] if plan else body * (n // p)
+    r = b0 + offset
+    d[r - 1] = 0.0           # a_r (sub-diagonal of row r)
+    d[n - 1 + r] = 1e-12     # b_r
+    d[2 * n - 1 + r] = 1.0   # c_r
+    d[r] = 1.0               # a_{r+1}
+    d[n - 1 + r + 1] = 1.0   # b_{r+1}
+    A2 = O.Matrix(A.kind, A.n, A.m, A.s, A.r, d)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    return A2, f, psg.StructuredMatrix(A2.kind, A2.n, A2.m, A2.s, A2.r, dev(d)), dev(f)
+
+
+def test_body_certificate_catches_planted_instability(cuda):
+    """The separator-row certificate cannot see an inaccurate body solve; with
+    PSG_OPT_BODY_CERT the certificate covers every body row (componentwise
+    backward error from the rows K3 already holds) and rejects it."""
+    torch = cuda
+    n, p = 1 << 16, 64
+    A, f, GA, df = _planted_unstable(torch, n, p, body=10, offset=33 * 3 + 10)
+    F = psg.parallel_factor(GA, p)
+    st = psg.SolveStats()
+    x = psg.solve(F, df, st)
+    sep_only = st.certificate
+    res_sep_only = psg.residual(GA, x, df)
+    F2 = psg.parallel_factor(GA, p)
+    F2.set_option("body_cert", 1)
+    st2 = psg.SolveStats()
+    x2 = psg.solve(F2, df, st2)
+    from conftest import record_parity
+    record_parity("planted_unstable_body", {"separator_certificate": sep_only, "residual": res_sep_only,
+                                            "body_certificate": st2.certificate, "fallbacks": st2.fallbacks})
+    assert sep_only <= 1e-14 and res_sep_only > 1e-10  # the separator rows alone pass a wrong solution
+    assert st2.certificate > 1e-14                      # the body certificate catches it
+    assert st2.fallbacks == 1                           # and the speculative result is re-solved exactly
+
+
+def test_body_certificate_passes_dominant_systems(cuda):
+    torch = cuda
+    A, f = psg.generate_config(0, 1 << 20, 1)
+    F = psg.parallel_factor(A, 1024)
+    F.set_option("body_cert", 1)
+    st = psg.SolveStats()
+    x = psg.solve(F, f, st)
+    assert st.speculative == 1 and st.fallbacks == 0
+    assert st.certificate <= 1e-15
+    assert psg.residual(A, x, f) <= 1e-13

@@ -19,6 +19,8 @@ size, p = CFG[cfg]
 A, f = psg.generate_config(cfg, size, cfg + 1)
 x = torch.empty_like(f)
 F = psg.parallel_factor(A, p)
+if os.environ.get("BODY_CERT"):
+    F.set_option("body_cert", 1)
 for _ in range(3):
     F.refactor(A)
     F.solve_async(f, x)
