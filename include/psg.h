@@ -312,10 +312,10 @@ int psg_factor_wait(const psg_handle* h, double* device_seconds);
 int psg_last_launches(const psg_handle* h, int* factor_launches, int* solve_launches);
 
 /* Inspection of the speculative tridiagonal factor (tests / tools): copy an
- * internal device buffer to host memory of `cap` doubles.  what = 0: the
- * separator weight rows (nsep x 68), 1: the speculative reduced diagonal
- * (nsep).  Returns the count copied, -count if cap is too small or the
- * buffer does not exist, -1 on a CUDA error. */
+ * internal device buffer to host memory of `cap` doubles.  what = 1: the
+ * speculative reduced diagonal (nsep); other values: -1 (the separator
+ * weights of earlier versions are no longer formed).  Returns the count
+ * copied, -count if cap is too small, -1 on a CUDA error. */
 long psg_debug_buffer(const psg_handle* h, int what, double* out, long cap);
 
 /* Version string including the hash of the sources the library was built

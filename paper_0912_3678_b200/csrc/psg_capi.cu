@@ -515,7 +515,7 @@ struct TriSolver {
   int maxlen0 = 0, minlen0 = 0;
   DevBuf<int> start0, len0;  // refined maps
   // speculative path buffers
-  DevBuf<double> wts, Tdiag, xsep;
+  DevBuf<double> Tdiag, xsep;
   DevBuf<double4> crec;  // per-segment certificate records
   DevBuf<unsigned> cctr;  // certificate kernel: finished-block counter (last block publishes the status)
   bool body_cert = false; // K3 also certifies every body row (PSG_OPT_BODY_CERT)
@@ -550,11 +550,27 @@ struct TriSolver {
   bool spec_possible() const { return minlen0 >= kMinSpecSeg && S0.nseg > 1; }
 
   // ---- speculative path ----------------------------------------------------
-  void spec_factor(cudaStream_t s) {
+  // The speculative factor is lazy: its sweeps run inside the next solve's
+  // separator kernel (tri_spec_fused_kernel, one pass over the windows of
+  // a, b, c and f).  tdiag_current: Tdiag matches the current matrix.
+  bool tdiag_current = false;
+  void spec_factor(cudaStream_t) {
+    Tdiag.alloc(S0.nseg - 1);
+    tdiag_current = false;
+  }
+  // the factor alone (Tdiag for psg_reduced_blocks, no solve)
+  void spec_tdiag(cudaStream_t s) {
+    if (tdiag_current) return;
     const int nsep = S0.nseg - 1;
-    wts.alloc((size_t)kWRow * nsep);
-    Tdiag.alloc(nsep);
-    tri_spec_factor_kernel<<<blocks_for(nsep, kFacSeps), 32, 0, s>>>(A0, S0, wts.p, Tdiag.p);
+    tri_spec_fused_kernel<false><<<blocks_for(nsep, kFacSeps), 32, 0, s>>>(A0, RowArr{}, S0, nullptr, Tdiag.p,
+                                                                          nullptr, 0, nsep);
+    LAUNCH_CHECK();
+    launches += 1;
+    tdiag_current = true;
+  }
+  void fused_sep(const RowArr& F, DevStatus* st, int ja, int jb, cudaStream_t s) {
+    tri_spec_fused_kernel<true><<<std::max(1, blocks_for(jb - ja, kFacSeps)), 32, 0, s>>>(A0, F, S0, xsep.p, Tdiag.p,
+                                                                                          st, ja, jb);
     LAUNCH_CHECK();
     launches += 1;
   }
@@ -586,10 +602,8 @@ struct TriSolver {
   void spec_solve(const RowArr& F, double* x, DevStatus* st, cudaStream_t s, cudaEvent_t* ev,
                   DevStatus* host_out = nullptr) {
     const int nsep = S0.nseg - 1;
-    tri_spec_sep_kernel<<<blocks_for((long)blocks_for(nsep, kSepPerWarp) * 32, 256), 256, 0, s>>>(F, S0, wts.p,
-                                                                                                   xsep.p, st, 0, nsep);
-    LAUNCH_CHECK();
-    launches += 1;
+    fused_sep(F, st, 0, nsep, s);  // factor sweeps + separator values in one pass
+    tdiag_current = true;
     if (ev) {  // the speculative reduced matrix is diagonal: phase 2 is fused into phase 1
       CUDA_TRY(cudaEventRecord(ev[1], s));
       CUDA_TRY(cudaEventRecord(ev[2], s));
@@ -631,17 +645,7 @@ struct TriSolver {
       }
       const int ib = g == nchunk - 1 ? S0.nseg : jb;  // segments with both separators known
       const int ia = ja == 0 ? 0 : ja;
-      if (jb > ja) {
-        const int cnt = jb - ja;
-        tri_spec_sep_kernel<<<blocks_for((long)blocks_for(cnt, kSepPerWarp) * 32, 256), 256, 0, s>>>(
-            F, S0, wts.p, xsep.p, g == 0 ? st : nullptr, ja, jb);
-        LAUNCH_CHECK();
-        launches += 1;
-      } else if (g == 0) {
-        tri_spec_sep_kernel<<<1, 32, 0, s>>>(F, S0, wts.p, xsep.p, st, 0, 0);  // status reset only
-        LAUNCH_CHECK();
-        launches += 1;
-      }
+      if (jb > ja || g == 0) fused_sep(F, g == 0 ? st : nullptr, ja, jb, s);  // chunk 0 also resets the status
       if (ib > ia) {
         TriSolveArgs a{};
         a.A = A0;
@@ -665,6 +669,7 @@ struct TriSolver {
     launch_pdl(tri_cert_kernel, dim3(blocks_for(nsep, 256)), dim3(256), 0, s, nsep, (const double4*)crec.p, st,
                host_out, cctr.p);
     launches += 1;
+    tdiag_current = true;
     CUDA_TRY(cudaEventRecord(evs[0], co));
     CUDA_TRY(cudaStreamWaitEvent(s, evs[0], 0));  // x is on the host when s reaches this point
   }
@@ -3008,6 +3013,8 @@ int psg_reduced_blocks(const psg_handle* hc, double* diag, double* sub, double* 
     const int ns = h->tri.S0.nseg - 1;
     if (h->use_spec() && h->spec_factored) {
       // speculative reduced matrix: diagonal (beta = gamma = 0 below rho^L)
+      h->tri.spec_tdiag(nullptr);
+      CUDA_TRY(cudaDeviceSynchronize());
       if (diag) CUDA_TRY(cudaMemcpy(diag, h->tri.Tdiag.p, sizeof(double) * ns, cudaMemcpyDeviceToHost));
       if (sub) std::fill(sub, sub + ns, 0.0);
       if (super) std::fill(super, super + ns, 0.0);
@@ -3153,9 +3160,18 @@ long psg_debug_buffer(const psg_handle* hc, int what, double* out, long cap) {
   DeviceGuard dg(h->device);
   std::lock_guard<std::mutex> g(h->mu);
   if (cudaEventSynchronize(h->ev_done) != cudaSuccess) return -1;
-  const DevBuf<double>& b = what == 0 ? h->tri.wts : h->tri.Tdiag;
+  if (what != 1) return -1;  // the separator weights are no longer formed (tri_spec_fused_kernel)
+  if (h->use_spec() && h->spec_factored) {
+    try {
+      h->tri.spec_tdiag(nullptr);
+    } catch (const Fail&) {
+      return -1;
+    }
+    if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+  }
+  const DevBuf<double>& b = h->tri.Tdiag;
   const long nsep = h->tri.S0.nseg - 1;
-  const long cnt = what == 0 ? nsep * kWRow : nsep;
+  const long cnt = nsep;
   if (!b.p || cnt > cap) return -cnt;
   if (cudaMemcpy(out, b.p, sizeof(double) * cnt, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
   return cnt;

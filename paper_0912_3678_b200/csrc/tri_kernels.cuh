@@ -203,53 +203,63 @@ __device__ __forceinline__ double warp_tri_pcr(double lo, double di, double up, 
   return r;
 }
 
-// Weight row of separator j (kWRow doubles):
-//   [0, 32)  -a_t v_i / Tdiag   v = last row of the inverse of segment j's trailing 32-row block
-//   [32, 64) -c_t w_i / Tdiag   w = first row of the inverse of segment j+1's leading block
-//   64: 1/Tdiag   65: Tdiag   66: kR = a_t c_{t-1} v_31   67: kL = c_t a_{t+1} w_0
-// (Tdiag = b_t - kR - kL).  Trailing block: top-down sweep d_k = b_k - l_k c_{k-1},
-// l_k = a_k / d_{k-1}, v_31 = 1/d_31, v_i = -l_{i+1} v_{i+1}.  Leading block:
-// bottom-up sweep e_k = b_k - mu_k a_{k+1}, mu_k = c_k / e_{k+1}, w_0 = 1/e_0,
-// w_i = -mu_{i-1} w_{i-1}.  Both are the same recurrence read in opposite row
-// orders, which is how one warp runs them on its two half-warps at once.
-constexpr int kWRow = 68;
+// Speculative separators in one pass over the 65-row window of every
+// separator t (rows t-32 .. t+32 of a, b, c and, when the right-hand side is
+// known, f).  Trailing block (rows t-32 .. t-1): the top-down Thomas sweep
+//   d_k = b_k - l_k c_{k-1},  l_k = a_k / d_{k-1},  g_k = f_k - l_k g_{k-1}
+// gives v_31 = 1/d_31 and v . f = g_31 / d_31 (v = last row of the block's
+// inverse: the forward sweep IS the dot product, no weights are formed).
+// Leading block (rows t+1 .. t+32): the same sweep bottom-up,
+//   e_k = b_k - mu_k a_{k+1},  mu_k = c_k / e_{k+1},  h_k = f_k - mu_k h_{k+1}
+// gives w_0 = 1/e_0 and w . f = h_0 / e_0.  Then
+//   Tdiag_t = b_t - a_t c_{t-1} / d_31 - c_t a_{t+1} / e_0
+//   x_t     = (f_t - a_t g_31 / d_31 - c_t h_0 / e_0) / Tdiag_t.
+// One warp = 16 separators: lanes < 16 sweep the trailing blocks, lanes >= 16
+// the leading ones (the same recurrence read in opposite row orders); every
+// (array, separator) window is one TMA bulk copy, all in flight on one
+// mbarrier.  WITH_F = false: Tdiag only (the factor alone).  Separators
+// [jbase, jend) (the host path solves in row chunks).  The factor is lazy:
+// a refactor followed by a solve is this single launch.
 constexpr int kFacSeps = 16;             // separators per warp (one per half-warp lane pair)
 constexpr int kWin = 2 * kHalo + 1;      // window rows t-32 .. t+32
 constexpr int kFacPitch = 70;            // per-(array, separator) window slot: 65 rows + staging slack,
                                          // 16-byte multiple; 70 = 6 mod 16 keeps lane conflicts 2-way
 
-// One warp = 16 consecutive separators.  Every (array, separator) window is
-// one TMA bulk copy (48 per warp, all in flight on one mbarrier); each lane
-// then sweeps its own window in shared memory, lanes < 16 the trailing block
-// (top-down LU) and lanes >= 16 the leading block (bottom-up UL) of the same
-// separator; the weight rows leave through one TMA bulk store.
-__global__ void __launch_bounds__(32) tri_spec_factor_kernel(TriRows A, SegMap S, double* __restrict__ wts,
-                                                             double* __restrict__ Tdiag) {
+template <bool WITH_F>
+__global__ void __launch_bounds__(32) tri_spec_fused_kernel(TriRows A, RowArr F, SegMap S, double* __restrict__ xsep,
+                                                            double* __restrict__ Tdiag, DevStatus* reset, int jbase,
+                                                            int jend) {
   constexpr unsigned FULL = 0xffffffffu;
-  __shared__ __align__(16) double tile[3 * kFacSeps * kFacPitch];
+  constexpr int NA = WITH_F ? 4 : 3;
+  __shared__ __align__(16) double tile[NA * kFacSeps * kFacPitch];
   __shared__ __align__(8) uint64_t bar;
-  __shared__ int shifts[3 * kFacSeps];
+  __shared__ int shifts[NA * kFacSeps];
+  if (WITH_F) pdl_trigger();  // K3 may launch and stage its rows while the separators finish
   const int lane = threadIdx.x;
-  const int nsep = S.nseg - 1;
-  const int j0 = blockIdx.x * kFacSeps;
-  const int nj = min(kFacSeps, nsep - j0);
+  if (reset && blockIdx.x == 0 && lane < kCertSlots) reset->cert_bits[lane] = 0ull;  // first kernel of the solve
+  if (reset && blockIdx.x == 0 && lane == 0) {
+    reset->bad_seg = 0x7fffffff;
+    reset->pivot_seg = 0x7fffffff;
+  }
+  const int j0 = jbase + blockIdx.x * kFacSeps;
+  if (j0 >= jend) return;
+  const int nj = min(kFacSeps, jend - j0);
   const int jj = lane & (kFacSeps - 1);
   long tme;
   {
     long s0;
     int L0;
-    seg_of(S, min(j0 + jj, nsep - 1), s0, L0);
+    seg_of(S, min(j0 + jj, jend - 1), s0, L0);
     tme = s0 + L0;
   }
   // ---- windows -> shared: task = (array x, separator q), one bulk copy each
-  if (lane == 0) mbar_init(&bar, 3 * kFacSeps);
+  if (lane == 0) mbar_init(&bar, NA * kFacSeps);
   __syncwarp();
-  for (int task = lane; task < 3 * kFacSeps; task += 32) {
+  for (int task = lane; task < NA * kFacSeps; task += 32) {
     const int x = task / kFacSeps;  // separator task % kFacSeps == lane & 15
-    const long t = tme;
-    const RowArr X = x == 0 ? A.a : x == 1 ? A.b : A.c;
+    const RowArr X = x == 0 ? A.a : x == 1 ? A.b : x == 2 ? A.c : F;
     uint32_t tx = 0;
-    shifts[task] = stage_issue(X, t - kHalo, t + kHalo + 1, tile + task * kFacPitch, &bar, &tx);
+    shifts[task] = stage_issue(X, tme - kHalo, tme + kHalo + 1, tile + task * kFacPitch, &bar, &tx);
     mbar_arrive_expect_tx(&bar, tx);
   }
   __syncwarp();
@@ -257,6 +267,7 @@ __global__ void __launch_bounds__(32) tri_spec_factor_kernel(TriRows A, SegMap S
   const double* wA = tile + (0 * kFacSeps + jj) * kFacPitch + 1 + shifts[0 * kFacSeps + jj];
   const double* wB = tile + (1 * kFacSeps + jj) * kFacPitch + 1 + shifts[1 * kFacSeps + jj];
   const double* wC = tile + (2 * kFacSeps + jj) * kFacPitch + 1 + shifts[2 * kFacSeps + jj];
+  const double* wF = WITH_F ? tile + (3 * kFacSeps + jj) * kFacPitch + 1 + shifts[3 * kFacSeps + jj] : nullptr;
   // ---- one sweep per lane: lanes < 16 the trailing block (window rows 0..31
   //      downwards), lanes >= 16 the leading block (rows 64..33 upwards)
   const bool trail = lane < kFacSeps;
@@ -266,105 +277,25 @@ __global__ void __launch_bounds__(32) tri_spec_factor_kernel(TriRows A, SegMap S
   int off = trail ? 0 : kWin - 1;
   double piv = wB[off];
   double qprev = Qc[off];
-  double m[kHalo];
+  double g = WITH_F ? wF[off] : 0.0;
 #pragma unroll
   for (int k = 1; k < kHalo; ++k) {
     off += dw;
     const double l = Nm[off] * fast_rcp(piv);
-    m[k] = l;
     piv = fma(-l, qprev, wB[off]);
     qprev = Qc[off];
+    if (WITH_F) g = fma(-l, g, wF[off]);
   }
-  const double u31 = fast_rcp(piv);  // v_31 (trailing) or w_0 (leading)
-  const double other = __shfl_xor_sync(FULL, u31, kFacSeps);
-  const double v31 = trail ? u31 : other, w0 = trail ? other : u31;
+  const double u = fast_rcp(piv);  // v_31 (trailing) or w_0 (leading)
+  const double ug = g * u;         // v . f (trailing) or w . f (leading)
+  const double ou = __shfl_xor_sync(FULL, u, kFacSeps), oug = __shfl_xor_sync(FULL, ug, kFacSeps);
+  if (!trail || jj >= nj) return;
   const double at = wA[kHalo], bt = wB[kHalo], ct = wC[kHalo];  // separator row t
-  const double kR = at * wC[kHalo - 1] * v31;
-  const double kL = ct * wA[kHalo + 1] * w0;
+  const double kR = at * wC[kHalo - 1] * u;
+  const double kL = ct * wA[kHalo + 1] * ou;
   const double td = b_minus(bt, kR, kL);
-  const double it = 1.0 / td;
-  __syncwarp();
-  // ---- weight rows -> shared (reusing the tile) -> one bulk store
-  double* wout = tile;
-  const double sc = (trail ? -at : -ct) * it;
-  double u = u31;
-  wout[jj * kWRow + (trail ? kHalo - 1 : kHalo)] = sc * u;
-#pragma unroll
-  for (int k = kHalo - 2; k >= 0; --k) {
-    u = -m[k + 1] * u;
-    wout[jj * kWRow + (trail ? k : 2 * kHalo - 1 - k)] = sc * u;
-  }
-  if (trail) {
-    wout[jj * kWRow + 64] = it;
-    wout[jj * kWRow + 65] = td;
-    wout[jj * kWRow + 66] = kR;
-    wout[jj * kWRow + 67] = kL;
-    if (jj < nj) Tdiag[j0 + jj] = td;
-  }
-  fence_proxy_async_smem();
-  __syncwarp();
-  if (lane == 0) {
-    bulk_s2g(wts + (long)j0 * kWRow, wout, (uint32_t)(nj * kWRow * sizeof(double)));
-    bulk_commit_and_wait_read();
-  }
-}
-
-// Speculative separator values (phase 1 + phase 2 fused): with the weight row
-// W of separator j and the f rows t-32 .. t+32 around its row t,
-//   x_t = f_t / Tdiag + sum_i W[i] f(t-32+i) + sum_i W[32+i] f(t+1+i).
-// One warp evaluates kSepPerWarp separators; all their loads are issued
-// before the first reduction so each warp keeps ~16 coalesced 256-byte
-// requests in flight.
-constexpr int kSepPerWarp = 4;
-// Separators [jbase, jend) only (the host path solves in row chunks).
-__global__ void __launch_bounds__(256) tri_spec_sep_kernel(RowArr F, SegMap S, const double* __restrict__ wts,
-                                                            double* __restrict__ xsep, DevStatus* reset, int jbase,
-                                                            int jend) {
-  pdl_trigger();  // K3 may launch and stage its rows while the separators finish
-  const int lane = threadIdx.x & 31;
-  if (reset && blockIdx.x == 0 && threadIdx.x < kCertSlots + 2) {  // first kernel of the solve: fresh status
-    if (threadIdx.x < kCertSlots)
-      reset->cert_bits[threadIdx.x] = 0ull;
-    else if (threadIdx.x == kCertSlots)
-      reset->bad_seg = 0x7fffffff;
-    else
-      reset->pivot_seg = 0x7fffffff;
-  }
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nsep = jend;
-  const int j0 = jbase + warp * kSepPerWarp;
-  if (j0 >= nsep) return;
-  double w1[kSepPerWarp], w2[kSepPerWarp], f1[kSepPerWarp], f2[kSepPerWarp];
-  long tt[kSepPerWarp];
-#pragma unroll
-  for (int k = 0; k < kSepPerWarp; ++k) {
-    const int j = min(j0 + k, nsep - 1);
-    long s0;
-    int L0;
-    seg_of(S, j, s0, L0);
-    tt[k] = s0 + L0;
-    const double* W = wts + (long)j * kWRow;
-    w1[k] = __ldg(W + lane);
-    w2[k] = __ldg(W + kHalo + lane);
-    f1[k] = row_at(F, tt[k] - kHalo + lane);
-    f2[k] = row_at(F, tt[k] + 1 + lane);
-  }
-  double mine = 0.0, ft = 0.0, it = 0.0;
-  if (lane < kSepPerWarp && j0 + lane < nsep) {
-    long s0;
-    int L0;
-    seg_of(S, j0 + lane, s0, L0);
-    ft = row_at(F, s0 + L0);
-    it = __ldg(wts + (long)(j0 + lane) * kWRow + 2 * kHalo);
-  }
-#pragma unroll
-  for (int k = 0; k < kSepPerWarp; ++k) {
-    double acc = fma(w1[k], f1[k], w2[k] * f2[k]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == k) mine = acc;
-  }
-  if (lane < kSepPerWarp && j0 + lane < nsep) xsep[j0 + lane] = fma(ft, it, mine);
+  Tdiag[j0 + jj] = td;
+  if (WITH_F) xsep[j0 + jj] = ((wF[kHalo] - at * ug) - ct * oug) / td;
 }
 
 // ----------------------------------------------------------------------------
