@@ -4,14 +4,16 @@
 // K = 2..4.  The scalar tridiagonal path (tri_kernels.cuh) is the K = 1 case
 // of the same design:
 //
-//   factor (blk_spec_factor_kernel): per separator block S (K rows), the
-//     Schur complement T = A_SS - B1 [B_T^-1]_{near} C_T - C0 [B_L^-1]_{near} A_L
-//     of the TRUNCATED neighbouring bodies (HB block rows each side), and the
-//     weights that give x_S = T^-1 f_S + sum W^T_d f(S-(d+1)K) + sum W^L_d f(S+K+dK)
+//   factor + separators (blk_spec_fused_kernel, lazy: one launch per
+//     refactor + solve): per separator block S (K rows), the Schur complement
+//     T = A_SS - B1 [B_T^-1]_{near} C_T - C0 [B_L^-1]_{near} A_L of the
+//     TRUNCATED neighbouring bodies (HB block rows each side) and, carried by
+//     the same far -> near block sweeps, the condensed right-hand sides, so
+//     x_S = T^-1 (f_S - B1 [B_T^-1 f_T]_{near} - C0 [B_L^-1 f_L]_{near})
 //     -- the separator row of F T G restricted to the truncation window
-//     (src/localfact.cpp:84-225 computes the same blocks on full bodies);
+//     (src/localfact.cpp:84-225, 765-781 compute the same blocks on full
+//     bodies); no weights are formed;
 //   solve:
-//     blk_spec_sep_kernel      x_S from the weights (warp per separator);
 //     blk_segment_solve_kernel the bodies, exact given x_S (warp per body, block
 //                              chunk elimination + block PCR across lanes);
 //     blk_cert_kernel          componentwise backward error of every separator
@@ -1019,8 +1021,10 @@ struct BlkSpecArgs {
   int layout;
   int nsep;
   const int* sep;  // separator start rows
-  double* W;       // out: per separator (1 + 2 HB) K*K: T^-1 | W^T_0..HB-1 | W^L_0..HB-1
+  const double* f; // right-hand side
+  double* xsep;    // out: per separator its K values
   double* Tdiag;   // out: per separator the K*K block A_SS (certificate)
+  DevStatus* reset;  // the solve's status slot (reset by block 0)
   long boff[9];    // banded: A(row, row + d) = data[boff[d + K] + row]
 };
 
@@ -1075,14 +1079,24 @@ __device__ __forceinline__ double dinv(double a, int base, int u, int v, int K, 
 }
 
 template <int K, int HB>
-__global__ void __launch_bounds__(128) blk_spec_factor_kernel(BlkSpecArgs g) {
+__global__ void __launch_bounds__(128) blk_spec_fused_kernel(BlkSpecArgs g) {
+  pdl_trigger();  // the body kernel may launch and stage its rows early
   const int lane = threadIdx.x & 31;
   const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (g.reset && blockIdx.x == 0 && threadIdx.x < kCertSlots + 2) {  // first kernel of the solve: fresh status
+    if (threadIdx.x < kCertSlots)
+      g.reset->cert_bits[threadIdx.x] = 0ull;
+    else if (threadIdx.x == kCertSlots)
+      g.reset->bad_seg = INT_MAX;
+    else
+      g.reset->pivot_seg = INT_MAX;
+  }
   if (j >= g.nsep) return;  // warp-uniform
   constexpr int KK = K * K;
   const int h = lane >> 4, e = lane & 15, u = e >> 2, v = e & 3;
   const int base = h << 4;
   const bool act = u < K && v < K;
+  const bool vec = u < K && v == 0;  // block vectors live in column 0
   const double eye = (u == v) ? 1.0 : 0.0;
   const long S = g.sep[j];
   const long n = g.n;
@@ -1112,27 +1126,30 @@ __global__ void __launch_bounds__(128) blk_spec_factor_kernel(BlkSpecArgs g) {
     const long col = r0 + v + (t - 1) * K;
     return (col >= 0 && col < n) ? __ldg(g.data + off + r0) : 0.0;
   };
+  auto ldf = [&](long r0) -> double { return vec ? __ldg(g.f + r0 + u) : 0.0; };
   // couplings with the separator: B1 = A(S+u, S-K+v) / C0 = A(S+u, S+K+v);
   // near block -> separator: A(S-K+u, S+v) / A(S+K+u, S+v)
   const double Bc = act ? blk_at(g, K, S + u, h == 0 ? S - K + v : S + K + v) : 0.0;
   const double Cc = act ? blk_at(g, K, h == 0 ? S - K + u : S + K + u, S + v) : 0.0;
   const double Dss = act ? blk_at(g, K, S + u, S + v) : eye;
+  const double fS = ldf(S);
   double rsum = 0.0;
-  // far -> near sweep with the next block's loads in flight; only the
-  // transfer products Np[i] = Fc[i+1] G_i stay in registers
+  // far -> near sweep with the next block's loads in flight:
+  //   D'_i = D_i - Fc_i G_{i-1} Nc_{i-1},  G_i = D'_i^-1,  y_i = f_i - Fc_i G_{i-1} y_{i-1}
   auto row0 = [&](int i) -> long { return h == 0 ? S - (long)(HB - i) * K : S + K + (long)(HB - 1 - i) * K; };
   double Dn = act ? ld(row0(0), 1, oD, kD) : eye, Fn = ld(row0(0), tF, oF, kF), Nn = ld(row0(0), tN, oN, kN);
-  double G = 0.0, Ncp = 0.0;  // previous block's inverse pivot and its coupling toward this block
-  double Np[HB];
+  double fn = ldf(row0(0));
+  double G = 0.0, Ncp = 0.0, y = 0.0;  // previous block's inverse pivot, its coupling toward this block, rhs
 #pragma unroll
   for (int i = 0; i < HB; ++i) {
     double D = Dn;
-    const double Fc = Fn, Nc = Nn;
+    const double Fc = Fn, Nc = Nn, fi = fn;
     if (i + 1 < HB) {
       const long r1 = row0(i + 1);
       Dn = act ? ld(r1, 1, oD, kD) : eye;
       Fn = ld(r1, tF, oF, kF);
       Nn = ld(r1, tN, oN, kN);
+      fn = ldf(r1);
     }
     if (i > 0) {
       // Fc is the left operand of both products: its row u gathered once
@@ -1140,72 +1157,27 @@ __global__ void __launch_bounds__(128) blk_spec_factor_kernel(BlkSpecArgs g) {
 #pragma unroll
       for (int l = 0; l < 4; ++l) frow[l] = l < K ? __shfl_sync(0xffffffffu, Fc, base + u * 4 + l) : 0.0;
       D -= dmul_row(frow, dmul(G, Ncp, base, u, v, K), base, v, K);
-      Np[i - 1] = dmul_row(frow, G, base, v, K);
+      y = fi - dmul_row(frow, dmul(G, y, base, u, v, K), base, v, K);
+    } else {
+      y = fi;
     }
     const double Gi = dinv(D, base, u, v, K, &rsum);
     G = act ? Gi : 0.0;
     Ncp = Nc;
   }
-  const double Xn = G;  // near diagonal block of the truncated inverse
-  const double part = dmul(Bc, dmul(Xn, Cc, base, u, v, K), base, u, v, K);
+  // near diagonal block of the truncated inverse Xn = G: this side's Schur
+  // term B Xn C and condensed rhs B Xn y
+  const double part = dmul(Bc, dmul(G, Cc, base, u, v, K), base, u, v, K);
+  const double rpart = dmul(Bc, dmul(G, y, base, u, v, K), base, u, v, K);
   const double other = __shfl_xor_sync(0xffffffffu, part, 16);
+  const double rother = __shfl_xor_sync(0xffffffffu, rpart, 16);
   double Ti = dinv(Dss - part - other, base, u, v, K, &rsum);
   if (!act) Ti = 0.0;
-  double* out = g.W + (long)j * (1 + 2 * HB) * KK;
-  if (h == 0 && act) {
-    out[u * K + v] = Ti;
-    g.Tdiag[(long)j * KK + u * K + v] = Dss;
-  }
-  // weights near to far: W_0 = -T^-1 Bc G_near, W_d = -W_{d-1} Np[HB-1-d]
-  double w = -dmul(dmul(Ti, Bc, base, u, v, K), Xn, base, u, v, K);
-#pragma unroll
-  for (int d = 0; d < HB; ++d) {
-    if (d > 0) w = -dmul(w, Np[HB - 1 - d], base, u, v, K);
-    if (act) out[(long)(1 + h * HB + d) * KK + u * K + v] = w;
-  }
-  (void)rsum;  // a vanished pivot leaves non-finite weights: the certificate rejects them
-}
-
-// x_S = T^-1 f_S + sum_d W^T_d f(S-(d+1)K ..) + sum_d W^L_d f(S+K+dK ..):
-// warp per separator; block 0 also resets the solve's status slot.
-template <int K, int HB>
-__global__ void __launch_bounds__(128) blk_spec_sep_kernel(const double* __restrict__ W, const int* __restrict__ sep,
-                                                           int nsep, const double* __restrict__ f,
-                                                           double* __restrict__ xsep, DevStatus* reset) {
-  constexpr int KK = K * K, NBK = 1 + 2 * HB, BPI = 32 / KK;
-  pdl_trigger();  // the body kernel may launch and stage its rows early
-  const int lane = threadIdx.x & 31;
-  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (reset && blockIdx.x == 0 && threadIdx.x < kCertSlots + 2) {
-    if (threadIdx.x < kCertSlots)
-      reset->cert_bits[threadIdx.x] = 0ull;
-    else if (threadIdx.x == kCertSlots)
-      reset->bad_seg = INT_MAX;
-    else
-      reset->pivot_seg = INT_MAX;
-  }
-  if (j >= nsep) return;
-  const long S = sep[j];
-  const double* w = W + (long)j * NBK * KK;
-  const int e = lane % KK, slot = lane / KK;
-  const int v = e % K;
-  double acc = 0.0;
-  if (slot < BPI) {
-#pragma unroll 4
-    for (int blk = slot; blk < NBK; blk += BPI) {
-      const long row = blk == 0 ? S : (blk <= HB ? S - (long)blk * K : S + K + (long)(blk - 1 - HB) * K);
-      acc = fma(__ldg(w + (long)blk * KK + e), __ldg(f + row + v), acc);
-    }
-  }
-  __shared__ double red[4][32];
-  red[threadIdx.x >> 5][lane] = acc;
-  __syncwarp();
-  if (lane < K) {
-    double s = 0.0;
-    for (int t = 0; t < BPI * KK; ++t)
-      if ((t % KK) / K == lane) s += red[threadIdx.x >> 5][t];
-    xsep[(long)j * K + lane] = s;
-  }
+  const double rhs = vec ? (fS - rpart) - rother : 0.0;
+  const double xs = dmul(Ti, rhs, base, u, v, K);
+  if (h == 0 && act) g.Tdiag[(long)j * KK + u * K + v] = Dss;
+  if (h == 0 && vec) g.xsep[(long)j * K + u] = xs;
+  (void)rsum;  // a vanished pivot leaves non-finite separator values: the certificate rejects them
 }
 
 // omega = max over separator rows of |f - A_SS x_S - left - right| / (|f| + sum |terms|).

@@ -890,7 +890,7 @@ struct BlkSolver {
   std::vector<int> hsep;
   DevBuf<GPart> part;
   DevBuf<int> sep;
-  DevBuf<double> W, Tdiag, xsep, rec;
+  DevBuf<double> Tdiag, xsep, rec;
   int nseg = 0, nsep = 0, launches = 0;
 
   void init(const psg_desc& A, const Plan& P) {
@@ -957,7 +957,6 @@ struct BlkSolver {
     sep.alloc(nsep);
     CUDA_TRY(cudaMemcpy(part.p, hpart.data(), sizeof(GPart) * nseg, cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(sep.p, hsep.data(), sizeof(int) * nsep, cudaMemcpyHostToDevice));
-    W.alloc((size_t)nsep * (1 + 2 * blk_hb(K)) * K * K);
     Tdiag.alloc((size_t)nsep * K * K);
     xsep.alloc((size_t)nsep * K);
     rec.alloc((size_t)nseg * 4 * K);
@@ -973,7 +972,12 @@ struct BlkSolver {
 
   void set_data(const double* d) { base.data = d; }
 
-  void spec_factor(cudaStream_t s) {
+  // the factor is lazy: its block sweeps run inside the next solve's fused
+  // separator kernel (blk_spec_fused_kernel), which also condenses f
+  void spec_factor(cudaStream_t) {}
+
+  // fused factor + separators -> bodies -> certificate; the first kernel resets the status slot.
+  void spec_solve(const double* f, double* x, DevStatus* st, cudaStream_t s, cudaEvent_t* ev) {
     BlkSpecArgs g{};
     g.data = base.data;
     g.n = base.n;
@@ -982,29 +986,18 @@ struct BlkSolver {
     g.layout = layout;
     g.nsep = nsep;
     g.sep = sep.p;
-    g.W = W.p;
+    g.f = f;
+    g.xsep = xsep.p;
     g.Tdiag = Tdiag.p;
+    g.reset = st;
     for (int t = 0; t < 9; ++t) g.boff[t] = base.boff[t];
     const int grid = (nsep + 3) / 4;
     if (K == 4)
-      blk_spec_factor_kernel<4, blk_hb(4)><<<grid, 128, 0, s>>>(g);
+      blk_spec_fused_kernel<4, blk_hb(4)><<<grid, 128, 0, s>>>(g);
     else if (K == 3)
-      blk_spec_factor_kernel<3, blk_hb(3)><<<grid, 128, 0, s>>>(g);
+      blk_spec_fused_kernel<3, blk_hb(3)><<<grid, 128, 0, s>>>(g);
     else
-      blk_spec_factor_kernel<2, blk_hb(2)><<<grid, 128, 0, s>>>(g);
-    LAUNCH_CHECK();
-    launches += 1;
-  }
-
-  // sep -> bodies -> certificate; the first kernel resets the status slot.
-  void spec_solve(const double* f, double* x, DevStatus* st, cudaStream_t s, cudaEvent_t* ev) {
-    const int grid = (nsep + 3) / 4;
-    if (K == 4)
-      blk_spec_sep_kernel<4, blk_hb(4)><<<grid, 128, 0, s>>>(W.p, sep.p, nsep, f, xsep.p, st);
-    else if (K == 3)
-      blk_spec_sep_kernel<3, blk_hb(3)><<<grid, 128, 0, s>>>(W.p, sep.p, nsep, f, xsep.p, st);
-    else
-      blk_spec_sep_kernel<2, blk_hb(2)><<<grid, 128, 0, s>>>(W.p, sep.p, nsep, f, xsep.p, st);
+      blk_spec_fused_kernel<2, blk_hb(2)><<<grid, 128, 0, s>>>(g);
     LAUNCH_CHECK();
     if (ev) {
       CUDA_TRY(cudaEventRecord(ev[1], s));
