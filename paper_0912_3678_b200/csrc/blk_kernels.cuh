@@ -1078,11 +1078,11 @@ __device__ __forceinline__ double dinv(double a, int base, int u, int v, int K, 
   return a;
 }
 
-template <int K, int HB>
+template <int K, int HB, int NS = 2>
 __global__ void __launch_bounds__(128) blk_spec_fused_kernel(BlkSpecArgs g) {
   pdl_trigger();  // the body kernel may launch and stage its rows early
   const int lane = threadIdx.x & 31;
-  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int j0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * NS;
   if (g.reset && blockIdx.x == 0 && threadIdx.x < kCertSlots + 2) {  // first kernel of the solve: fresh status
     if (threadIdx.x < kCertSlots)
       g.reset->cert_bits[threadIdx.x] = 0ull;
@@ -1091,17 +1091,18 @@ __global__ void __launch_bounds__(128) blk_spec_fused_kernel(BlkSpecArgs g) {
     else
       g.reset->pivot_seg = INT_MAX;
   }
-  if (j >= g.nsep) return;  // warp-uniform
+  if (j0 >= g.nsep) return;  // warp-uniform
   constexpr int KK = K * K;
   const int h = lane >> 4, e = lane & 15, u = e >> 2, v = e & 3;
   const int base = h << 4;
   const bool act = u < K && v < K;
   const bool vec = u < K && v == 0;  // block vectors live in column 0
   const double eye = (u == v) ? 1.0 : 0.0;
-  const long S = g.sep[j];
   const long n = g.n;
-  // Both halves run the same far -> near elimination (no divergence around the
-  // shuffles).  Block i = 0 (far) .. HB-1 (near) of side h starts at row
+  // NS separators per warp, their block chains interleaved (independent
+  // shuffle / FP64 dependency chains in flight together).  Both halves run
+  // the same far -> near elimination (no divergence around the shuffles).
+  // Block i = 0 (far) .. HB-1 (near) of side h starts at row
   //   trailing (h = 0): S - (HB - i) K      leading (h = 1): S + K + (HB - 1 - i) K
   // and couples to its farther neighbour through Fc (trailing: sub, leading:
   // super) and to its nearer neighbour through Nc.  Element (u, v) of the
@@ -1127,56 +1128,76 @@ __global__ void __launch_bounds__(128) blk_spec_fused_kernel(BlkSpecArgs g) {
     return (col >= 0 && col < n) ? __ldg(g.data + off + r0) : 0.0;
   };
   auto ldf = [&](long r0) -> double { return vec ? __ldg(g.f + r0 + u) : 0.0; };
-  // couplings with the separator: B1 = A(S+u, S-K+v) / C0 = A(S+u, S+K+v);
-  // near block -> separator: A(S-K+u, S+v) / A(S+K+u, S+v)
-  const double Bc = act ? blk_at(g, K, S + u, h == 0 ? S - K + v : S + K + v) : 0.0;
-  const double Cc = act ? blk_at(g, K, h == 0 ? S - K + u : S + K + u, S + v) : 0.0;
-  const double Dss = act ? blk_at(g, K, S + u, S + v) : eye;
-  const double fS = ldf(S);
+  long S[NS];
+  double Bc[NS], Cc[NS], Dss[NS], fS[NS], Dn[NS], Fn[NS], Nn[NS], fn[NS], G[NS], Ncp[NS], y[NS];
+  auto row0 = [&](int q, int i) -> long {
+    return h == 0 ? S[q] - (long)(HB - i) * K : S[q] + K + (long)(HB - 1 - i) * K;
+  };
+#pragma unroll
+  for (int q = 0; q < NS; ++q) {
+    S[q] = g.sep[min(j0 + q, g.nsep - 1)];
+    // couplings with the separator: B1 = A(S+u, S-K+v) / C0 = A(S+u, S+K+v);
+    // near block -> separator: A(S-K+u, S+v) / A(S+K+u, S+v)
+    Bc[q] = act ? blk_at(g, K, S[q] + u, h == 0 ? S[q] - K + v : S[q] + K + v) : 0.0;
+    Cc[q] = act ? blk_at(g, K, h == 0 ? S[q] - K + u : S[q] + K + u, S[q] + v) : 0.0;
+    Dss[q] = act ? blk_at(g, K, S[q] + u, S[q] + v) : eye;
+    fS[q] = ldf(S[q]);
+    const long r = row0(q, 0);
+    Dn[q] = act ? ld(r, 1, oD, kD) : eye;
+    Fn[q] = ld(r, tF, oF, kF);
+    Nn[q] = ld(r, tN, oN, kN);
+    fn[q] = ldf(r);
+    G[q] = Ncp[q] = y[q] = 0.0;
+  }
   double rsum = 0.0;
   // far -> near sweep with the next block's loads in flight:
   //   D'_i = D_i - Fc_i G_{i-1} Nc_{i-1},  G_i = D'_i^-1,  y_i = f_i - Fc_i G_{i-1} y_{i-1}
-  auto row0 = [&](int i) -> long { return h == 0 ? S - (long)(HB - i) * K : S + K + (long)(HB - 1 - i) * K; };
-  double Dn = act ? ld(row0(0), 1, oD, kD) : eye, Fn = ld(row0(0), tF, oF, kF), Nn = ld(row0(0), tN, oN, kN);
-  double fn = ldf(row0(0));
-  double G = 0.0, Ncp = 0.0, y = 0.0;  // previous block's inverse pivot, its coupling toward this block, rhs
 #pragma unroll
   for (int i = 0; i < HB; ++i) {
-    double D = Dn;
-    const double Fc = Fn, Nc = Nn, fi = fn;
-    if (i + 1 < HB) {
-      const long r1 = row0(i + 1);
-      Dn = act ? ld(r1, 1, oD, kD) : eye;
-      Fn = ld(r1, tF, oF, kF);
-      Nn = ld(r1, tN, oN, kN);
-      fn = ldf(r1);
-    }
-    if (i > 0) {
-      // Fc is the left operand of both products: its row u gathered once
-      double frow[4];
 #pragma unroll
-      for (int l = 0; l < 4; ++l) frow[l] = l < K ? __shfl_sync(0xffffffffu, Fc, base + u * 4 + l) : 0.0;
-      D -= dmul_row(frow, dmul(G, Ncp, base, u, v, K), base, v, K);
-      y = fi - dmul_row(frow, dmul(G, y, base, u, v, K), base, v, K);
-    } else {
-      y = fi;
+    for (int q = 0; q < NS; ++q) {
+      double D = Dn[q];
+      const double Fc = Fn[q], Nc = Nn[q], fi = fn[q];
+      if (i + 1 < HB) {
+        const long r1 = row0(q, i + 1);
+        Dn[q] = act ? ld(r1, 1, oD, kD) : eye;
+        Fn[q] = ld(r1, tF, oF, kF);
+        Nn[q] = ld(r1, tN, oN, kN);
+        fn[q] = ldf(r1);
+      }
+      if (i > 0) {
+        // Fc is the left operand of both products: its row u gathered once
+        double frow[4];
+#pragma unroll
+        for (int l = 0; l < 4; ++l) frow[l] = l < K ? __shfl_sync(0xffffffffu, Fc, base + u * 4 + l) : 0.0;
+        D -= dmul_row(frow, dmul(G[q], Ncp[q], base, u, v, K), base, v, K);
+        y[q] = fi - dmul_row(frow, dmul(G[q], y[q], base, u, v, K), base, v, K);
+      } else {
+        y[q] = fi;
+      }
+      const double Gi = dinv(D, base, u, v, K, &rsum);
+      G[q] = act ? Gi : 0.0;
+      Ncp[q] = Nc;
     }
-    const double Gi = dinv(D, base, u, v, K, &rsum);
-    G = act ? Gi : 0.0;
-    Ncp = Nc;
   }
-  // near diagonal block of the truncated inverse Xn = G: this side's Schur
-  // term B Xn C and condensed rhs B Xn y
-  const double part = dmul(Bc, dmul(G, Cc, base, u, v, K), base, u, v, K);
-  const double rpart = dmul(Bc, dmul(G, y, base, u, v, K), base, u, v, K);
-  const double other = __shfl_xor_sync(0xffffffffu, part, 16);
-  const double rother = __shfl_xor_sync(0xffffffffu, rpart, 16);
-  double Ti = dinv(Dss - part - other, base, u, v, K, &rsum);
-  if (!act) Ti = 0.0;
-  const double rhs = vec ? (fS - rpart) - rother : 0.0;
-  const double xs = dmul(Ti, rhs, base, u, v, K);
-  if (h == 0 && act) g.Tdiag[(long)j * KK + u * K + v] = Dss;
-  if (h == 0 && vec) g.xsep[(long)j * K + u] = xs;
+#pragma unroll
+  for (int q = 0; q < NS; ++q) {
+    // near diagonal block of the truncated inverse Xn = G: this side's Schur
+    // term B Xn C and condensed rhs B Xn y
+    const double part = dmul(Bc[q], dmul(G[q], Cc[q], base, u, v, K), base, u, v, K);
+    const double rpart = dmul(Bc[q], dmul(G[q], y[q], base, u, v, K), base, u, v, K);
+    const double other = __shfl_xor_sync(0xffffffffu, part, 16);
+    const double rother = __shfl_xor_sync(0xffffffffu, rpart, 16);
+    double Ti = dinv(Dss[q] - part - other, base, u, v, K, &rsum);
+    if (!act) Ti = 0.0;
+    const double rhs = vec ? (fS[q] - rpart) - rother : 0.0;
+    const double xs = dmul(Ti, rhs, base, u, v, K);
+    const int j = j0 + q;
+    if (j < g.nsep) {
+      if (h == 0 && act) g.Tdiag[(long)j * KK + u * K + v] = Dss[q];
+      if (h == 0 && vec) g.xsep[(long)j * K + u] = xs;
+    }
+  }
   (void)rsum;  // a vanished pivot leaves non-finite separator values: the certificate rejects them
 }
 

@@ -991,13 +991,14 @@ struct BlkSolver {
     g.Tdiag = Tdiag.p;
     g.reset = st;
     for (int t = 0; t < 9; ++t) g.boff[t] = base.boff[t];
-    const int grid = (nsep + 3) / 4;
+    constexpr int NS = 2;  // separators per warp
+    const int grid = (nsep + 4 * NS - 1) / (4 * NS);
     if (K == 4)
-      blk_spec_fused_kernel<4, blk_hb(4)><<<grid, 128, 0, s>>>(g);
+      blk_spec_fused_kernel<4, blk_hb(4), NS><<<grid, 128, 0, s>>>(g);
     else if (K == 3)
-      blk_spec_fused_kernel<3, blk_hb(3)><<<grid, 128, 0, s>>>(g);
+      blk_spec_fused_kernel<3, blk_hb(3), NS><<<grid, 128, 0, s>>>(g);
     else
-      blk_spec_fused_kernel<2, blk_hb(2)><<<grid, 128, 0, s>>>(g);
+      blk_spec_fused_kernel<2, blk_hb(2), NS><<<grid, 128, 0, s>>>(g);
     LAUNCH_CHECK();
     if (ev) {
       CUDA_TRY(cudaEventRecord(ev[1], s));
@@ -1710,6 +1711,8 @@ struct psg_handle {
   DevBuf<unsigned long long> d_norm;
   std::vector<int> seg_start, seg_len;  // level-0 segmentation when refined
   bool refined = false;
+  const double* gen_ref_data = nullptr;  // refined tridiagonal: gen holds the reference plan's reduced system
+  bool gen_ref_factored = false;
   // options
   bool speculative = true;
   double cert_tol = 1e-14;
@@ -1783,13 +1786,23 @@ SegMap plan_segments(const Plan& P, std::vector<int>& st, std::vector<int>& ln, 
   refined = false;
   maxlen = int(P.base + (P.rem ? 1 : 0));
   minlen = int(P.base);
-  if (maxlen <= kMaxSeg) return SegMap{P.p, int(P.base), int(P.rem), nullptr, nullptr};
+  // few long bodies (small p): split them further so that K3 gets enough
+  // warps to hide its latency (one warp per segment; the fused separator
+  // kernel's cost per extra separator is one 65-row window)
+  static const int target = [] {
+    const char* e = getenv("PSG_SEG_TARGET");
+    return e ? atoi(e) : 2048;
+  }();
+  int par = 1;
+  if (P.p < target && (long)P.p * maxlen >= (1L << 18))
+    par = std::max(1, std::min((target + P.p - 1) / P.p, minlen / 256));
+  if (maxlen <= kMaxSeg && par == 1) return SegMap{P.p, int(P.base), int(P.rem), nullptr, nullptr};
   refined = true;
   maxlen = 0;
   minlen = INT_MAX;
   for (int i = 0; i < P.p; ++i) {
     const int b = P.body_begin(i), L = P.body_end(i) - b;
-    const int t = (L + 1 + kMaxSeg) / (kMaxSeg + 1);  // sub-bodies
+    const int t = std::max(par, (L + 1 + kMaxSeg) / (kMaxSeg + 1));  // sub-bodies
     const long body = (long)L - (t - 1);
     const long base = body / t, rem = body % t;
     long cur = b;
@@ -2203,6 +2216,30 @@ void ensure_exact_generic(psg_handle* h, cudaStream_t s) {
   h->gen.launches = 0;
   h->gen.factor(s);
   h->exact_factored = true;
+}
+
+// The reference plan's reduced system (ReducedSystem, psg_reduced_* and
+// psg_solve_reduced).  Generic handles have it on their exact path; a
+// tridiagonal handle whose bodies were refined internally (bodies > 1056
+// rows: its own levels carry extra separators) gets it from the generic
+// exact path built on demand over the same matrix and plan.
+void ensure_reduced_gen(psg_handle* h, cudaStream_t s) {
+  if (h->generic) {
+    ensure_exact_generic(h, s);
+    return;
+  }
+  if (h->gen.lv.empty() || h->gen_ref_data != h->A.data) {
+    SMView V{PSG_BANDED, h->A.n, 1, 1, 1, h->A.data, nullptr, 0, 0};
+    CUDA_TRY(cudaStreamSynchronize(s));
+    h->gen.build(V, h->plan.p);
+    h->gen_ref_data = h->A.data;
+    h->gen_ref_factored = false;
+  }
+  if (!h->gen_ref_factored) {
+    h->gen.launches = 0;
+    h->gen.factor(s);
+    h->gen_ref_factored = true;
+  }
 }
 
 // Block kinds: enqueue one speculative solve whose status lands in device
@@ -2883,6 +2920,7 @@ int psg_refactor(psg_handle* h, const psg_desc* A, void* stream, char* err, size
       if (!h->tri.lv.empty()) h->tri.lv[0]->A = h->tri.A0;
     }
     h->spec_factored = h->exact_factored = false;
+    h->gen_ref_factored = false;
     h->speculative = true;  // a new matrix gets a fresh speculation
     run_factor(h, s);
     CUDA_TRY(cudaEventRecord(h->ev_done, s));
@@ -2963,11 +3001,9 @@ int psg_reduced_blocks(const psg_handle* hc, double* diag, double* sub, double* 
   try {
     CUDA_TRY(cudaEventSynchronize(h->ev_done));
     if (h->piv) throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "reduced system has adaptive extras: use psg_reduced_dense"};
-    if (h->generic) {
-      if (!h->exact_factored) {  // parallel_factor's ReducedSystem comes from the exact path
-        ensure_exact_generic(h, nullptr);
-        CUDA_TRY(cudaDeviceSynchronize());
-      }
+    if (h->generic || h->refined) {  // parallel_factor's ReducedSystem comes from the exact path
+      ensure_reduced_gen(h, nullptr);
+      CUDA_TRY(cudaDeviceSynchronize());
       GenLevel& L = *h->gen.lv[0];
       const int q = L.q, k = L.k, kk = k * k;
       std::vector<double> T(L.Tdata.n), C(kk, 0.0);
@@ -3002,7 +3038,6 @@ int psg_reduced_blocks(const psg_handle* hc, double* diag, double* sub, double* 
       }
       return 0;
     }
-    if (h->refined) throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "reduced system was refined internally (bodies > 1056 rows)"};
     const int ns = h->tri.S0.nseg - 1;
     if (h->use_spec() && h->spec_factored) {
       // speculative reduced matrix: diagonal (beta = gamma = 0 below rho^L)
@@ -3050,9 +3085,9 @@ int psg_solve_reduced(const psg_handle* hc, const double* rhs, double* x, int on
       if (stats) stats->reduced_ops += h->piv->reduced_ops();
       return 0;
     }
-    if (h->generic) {
+    if (h->generic || h->refined) {
+      ensure_reduced_gen(h, s);
       if (h->gen.lv.size() < 2) throw Fail{PSG_E_INVALID_PARAMETER, "no reduced system"};
-      ensure_exact_generic(h, s);
       const int dim = h->gen.lv[0]->q * h->gen.lv[0]->k;
       DevBuf<double> dr, dxv;
       const double* r = rhs;
@@ -3072,7 +3107,6 @@ int psg_solve_reduced(const psg_handle* hc, const double* rhs, double* x, int on
       if (stats) stats->reduced_ops += reduced_ops_of(h, false);
       return 0;
     }
-    if (h->refined) throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "reduced system was refined internally (bodies > 1056 rows)"};
     if (!h->exact_factored) {  // the exact reduced matrix T (parallel_factor's ReducedSystem)
       h->tri.launches = 0;
       h->tri.exact_factor(s);
@@ -3121,13 +3155,12 @@ int psg_reduced_rhs(const psg_handle* hc, const double* f, double* out, int on_d
     }
     const double* rr = nullptr;
     size_t dim = 0;
-    if (h->generic) {
+    if (h->generic || h->refined) {
+      ensure_reduced_gen(h, s);
       if (h->gen.lv.size() < 2) throw Fail{PSG_E_INVALID_PARAMETER, "no reduced system"};
-      ensure_exact_generic(h, s);
       rr = h->gen.condense(df, s);
       dim = (size_t)h->gen.lv[0]->q * h->gen.lv[0]->k;
     } else {
-      if (h->refined) throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "reduced system was refined internally (bodies > 1056 rows)"};
       if (!h->exact_factored) {
         h->tri.launches = 0;
         h->tri.exact_factor(s);

@@ -350,3 +350,29 @@ def test_body_certificate_passes_dominant_systems(cuda):
     assert st.speculative == 1 and st.fallbacks == 0
     assert st.certificate <= 1e-15
     assert psg.residual(A, x, f) <= 1e-13
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_refined_plan_reduced_system_matches_reference(cuda):
+    """Bodies longer than one K3 warp (small p) are refined internally; the
+    ReducedSystem the API reports is still the reference plan's (built from
+    the generic exact path): T, solve_reduced and the reduced rhs against the
+    unmodified reference."""
+    torch = cuda
+    n, p = 70001, 16
+    A, f = O.generate_config(0, n, 7)
+    R = O.RefMatrix(A)
+    RF = R.factor(p)
+    Tr = RF.T()
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    GA = psg.StructuredMatrix(A.kind, A.n, A.m, A.s, A.r, dev(A.data))
+    F = psg.parallel_factor(GA, p)
+    assert F.q == Tr.shape[0] == p - 1
+    Tg = F.reduced_dense()
+    assert np.max(np.abs(Tg - Tr)) <= 1e-14 * np.max(np.abs(Tr))
+    rhs = O.random_vector(p - 1, 3)
+    xr = psg.solve_reduced(F, rhs)
+    assert O.rel_err(xr, np.linalg.solve(Tr, rhs)) <= 1e-13
+    x = psg.solve(F, dev(f)).cpu().numpy()
+    want, _, _ = RF.solve(f)
+    assert O.rel_err(x, want) <= 1e-12
