@@ -991,7 +991,7 @@ struct BlkSolver {
     g.Tdiag = Tdiag.p;
     g.reset = st;
     for (int t = 0; t < 9; ++t) g.boff[t] = base.boff[t];
-    constexpr int NS = 2;  // separators per warp
+    constexpr int NS = 1;  // separators per warp (2, chains interleaved: config 2 82 -> 123 us, config 3 217 -> 332 us)
     const int grid = (nsep + 4 * NS - 1) / (4 * NS);
     if (K == 4)
       blk_spec_fused_kernel<4, blk_hb(4), NS><<<grid, 128, 0, s>>>(g);
@@ -1786,12 +1786,12 @@ SegMap plan_segments(const Plan& P, std::vector<int>& st, std::vector<int>& ln, 
   refined = false;
   maxlen = int(P.base + (P.rem ? 1 : 0));
   minlen = int(P.base);
-  // few long bodies (small p): split them further so that K3 gets enough
-  // warps to hide its latency (one warp per segment; the fused separator
-  // kernel's cost per extra separator is one 65-row window)
+  // few long bodies (small p): optionally split them further so that K3
+  // gets more warps (PSG_SEG_TARGET = segments wanted; off by default:
+  // config 0 measured 0.056-0.060 ms/step with targets 1, 2048 and 4096)
   static const int target = [] {
     const char* e = getenv("PSG_SEG_TARGET");
-    return e ? atoi(e) : 2048;
+    return e ? atoi(e) : 0;
   }();
   int par = 1;
   if (P.p < target && (long)P.p * maxlen >= (1L << 18))
