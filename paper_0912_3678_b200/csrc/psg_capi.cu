@@ -515,7 +515,7 @@ struct TriSolver {
   int maxlen0 = 0, minlen0 = 0;
   DevBuf<int> start0, len0;  // refined maps
   // speculative path buffers
-  DevBuf<double> Tdiag, xsep;
+  DevBuf<double> Tdiag, xsep, xsep_alt;  // two separator buffers: consecutive solves alternate (see spec_solve)
   DevBuf<double4> crec;  // per-segment certificate records
   DevBuf<unsigned> cctr;  // certificate kernel: finished-block counter (last block publishes the status)
   bool body_cert = false; // K3 also certifies every body row (PSG_OPT_BODY_CERT)
@@ -544,7 +544,10 @@ struct TriSolver {
     crec.alloc(S0.nseg);
     cctr.alloc(1);
     CUDA_TRY(cudaMemsetAsync(cctr.p, 0, sizeof(unsigned), s));
-    if (S0.nseg > 1) xsep.alloc(S0.nseg - 1);
+    if (S0.nseg > 1) {
+      xsep.alloc(S0.nseg - 1);
+      xsep_alt.alloc(S0.nseg - 1);
+    }
   }
 
   bool spec_possible() const { return minlen0 >= kMinSpecSeg && S0.nseg > 1; }
@@ -568,9 +571,13 @@ struct TriSolver {
     launches += 1;
     tdiag_current = true;
   }
-  void fused_sep(const RowArr& F, DevStatus* st, int ja, int jb, cudaStream_t s) {
-    tri_spec_fused_kernel<true><<<std::max(1, blocks_for(jb - ja, kFacSeps)), 32, 0, s>>>(A0, F, S0, xsep.p, Tdiag.p,
-                                                                                          st, ja, jb);
+  // pdl: may overlap the previous solve's certificate kernel (see the kernel)
+  void fused_sep(const RowArr& F, DevStatus* st, int ja, int jb, cudaStream_t s, bool pdl = false) {
+    const dim3 grid(std::max(1, blocks_for(jb - ja, kFacSeps)));
+    if (pdl)
+      launch_pdl(tri_spec_fused_kernel<true>, grid, dim3(32), 0, s, A0, F, S0, xsep.p, Tdiag.p, st, ja, jb);
+    else
+      tri_spec_fused_kernel<true><<<grid, 32, 0, s>>>(A0, F, S0, xsep.p, Tdiag.p, st, ja, jb);
     LAUNCH_CHECK();
     launches += 1;
   }
@@ -602,7 +609,13 @@ struct TriSolver {
   void spec_solve(const RowArr& F, double* x, DevStatus* st, cudaStream_t s, cudaEvent_t* ev,
                   DevStatus* host_out = nullptr) {
     const int nsep = S0.nseg - 1;
-    fused_sep(F, st, 0, nsep, s);  // factor sweeps + separator values in one pass
+    // consecutive solves alternate separator buffers: the next solve's
+    // separator kernel may run while this solve's K3 drains (K3 and the
+    // certificate kernel trigger their dependents early; the separator kernel
+    // completes only after the previous certificate, so the next K3 -- which
+    // waits on it -- never overlaps this one's writes)
+    std::swap(xsep.p, xsep_alt.p);
+    fused_sep(F, st, 0, nsep, s, /*pdl=*/true);  // factor sweeps + separator values in one pass
     tdiag_current = true;
     if (ev) {  // the speculative reduced matrix is diagonal: phase 2 is fused into phase 1
       CUDA_TRY(cudaEventRecord(ev[1], s));

@@ -242,7 +242,10 @@ __global__ void __launch_bounds__(32) tri_spec_fused_kernel(TriRows A, RowArr F,
     reset->pivot_seg = 0x7fffffff;
   }
   const int j0 = jbase + blockIdx.x * kFacSeps;
-  if (j0 >= jend) return;
+  if (j0 >= jend) {
+    pdl_wait();
+    return;
+  }
   const int nj = min(kFacSeps, jend - j0);
   const int jj = lane & (kFacSeps - 1);
   long tme;
@@ -289,13 +292,18 @@ __global__ void __launch_bounds__(32) tri_spec_fused_kernel(TriRows A, RowArr F,
   const double u = fast_rcp(piv);  // v_31 (trailing) or w_0 (leading)
   const double ug = g * u;         // v . f (trailing) or w . f (leading)
   const double ou = __shfl_xor_sync(FULL, u, kFacSeps), oug = __shfl_xor_sync(FULL, ug, kFacSeps);
-  if (!trail || jj >= nj) return;
-  const double at = wA[kHalo], bt = wB[kHalo], ct = wC[kHalo];  // separator row t
-  const double kR = at * wC[kHalo - 1] * u;
-  const double kL = ct * wA[kHalo + 1] * ou;
-  const double td = b_minus(bt, kR, kL);
-  Tdiag[j0 + jj] = td;
-  if (WITH_F) xsep[j0 + jj] = ((wF[kHalo] - at * ug) - ct * oug) / td;
+  if (trail && jj < nj) {
+    const double at = wA[kHalo], bt = wB[kHalo], ct = wC[kHalo];  // separator row t
+    const double kR = at * wC[kHalo - 1] * u;
+    const double kL = ct * wA[kHalo + 1] * ou;
+    const double td = b_minus(bt, kR, kL);
+    Tdiag[j0 + jj] = td;
+    if (WITH_F) xsep[j0 + jj] = ((wF[kHalo] - at * ug) - ct * oug) / td;
+  }
+  // launched programmatically after the previous solve's certificate kernel:
+  // this grid completes only after it (so K3, which waits on this grid, never
+  // overwrites the certificate records the previous solve is still reading)
+  pdl_wait();
 }
 
 // ----------------------------------------------------------------------------
@@ -367,7 +375,8 @@ __global__ void __launch_bounds__(32) tri_segment_solve_kernel(TriSolveArgs args
     return sh;
   };
   int shift = seg_begin < seg_end ? issue(seg_begin, 0) : 0;
-  pdl_wait();  // the separator values come from the previous kernel (staging above overlaps it)
+  pdl_wait();     // the separator values come from the previous kernel (staging above overlaps it)
+  pdl_trigger();  // the certificate kernel may launch (it waits for this grid before reading the records)
   int k = 0;
   for (int seg = seg_begin; seg < seg_end; seg += stride, ++k) {
   const int buf = PERSIST ? (k & 1) : 0;
@@ -578,7 +587,9 @@ __device__ __forceinline__ double tri_omega(const double4& R, const double4& N) 
 
 __global__ void tri_cert_kernel(int nsep, const double4* __restrict__ crec, DevStatus* st, DevStatus* host_out,
                                 unsigned* done_ctr) {
-  pdl_wait();
+  pdl_trigger();  // the next solve's separator kernel may start: it touches nothing K3 or this kernel
+                  // reads or writes (other separator buffer, other status slot) and completes only after us
+  pdl_wait();     // K3 (records) complete
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   double w = 0.0;
   if (j < nsep) w = tri_omega(crec[j], crec[j + 1]);
