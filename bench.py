@@ -446,6 +446,7 @@ def impl_ours(args, rank, world, local_rank):
                    "path": "parallel_factor (new handle) + blocking solve per step"},
         "certificate_max": cert, "speculative": spec, "residual": res,
         "gpu_launches": launches,
+        "build": psg.lib().psg_version().decode(),
         "other_configs": other,
         "clocks": clk,
         "e2e": e2e,

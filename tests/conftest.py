@@ -8,6 +8,15 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 
+def pytest_report_header(config):
+    """The build under test: psg_version() carries the hash of the sources libpsg.so was built from."""
+    try:
+        import paper_0912_3678_b200 as psg
+        return "libpsg: " + psg.lib().psg_version().decode()
+    except Exception as e:  # the CPU suite still runs without the library
+        return f"libpsg: not loaded ({e})"
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (runs the CUDA path through the C ABI)")
 

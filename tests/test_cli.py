@@ -208,3 +208,48 @@ def test_pivoting_strategy_command(psg_bin, tmp_path, cuda):
     for st in ("lupivot", "qr"):
         res = run("verify", "-m", tmp_path / "c.mat", "-f", "ones", "--p", 4, "--strategy", st)
         assert res.returncode == 0, res.stdout + res.stderr
+
+
+@pytest.mark.parametrize("kind,name,n,m,s,r", [(0, "banded", 300, 1, 2, 1), (0, "banded", 40, 1, 3, 3),
+                                               (1, "blocktri", 96, 4, 1, 1), (2, "abd", 120, 4, 2, 2),
+                                               (3, "babd", 64, 4, 2, 2), (4, "circulant", 50, 1, 2, 1),
+                                               (4, "circulant", 7, 1, 3, 3)])
+def test_generate_random_matches_unmodified_reference(psg_bin, tmp_path, kind, name, n, m, s, r):
+    """generate_random of this library (the dominance pass walks each row's
+    stored columns: O(nnz)) against the UNMODIFIED reference's generator, every
+    kind incl. circulant-like (its diagonal lives in band s) and tiny n where
+    a circulant row lists a column twice."""
+    _ref_lib()
+    out = tmp_path / "g.mat"
+    res = run("generate", "--kind", name, "--n", n, "--m", m, "--s", s, "--r", r, "--seed", 9, "--dominance", 2,
+              "-o", out)
+    assert res.returncode == 0, res.stderr
+    lib = O.ref()
+    lib.ref_parse_matrix.restype = C.c_int
+    lib.ref_parse_matrix.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]
+    lib.ref_mat_dims.argtypes = [C.c_void_p] + [C.POINTER(C.c_int)] * 5 + [C.POINTER(C.c_size_t), C.c_void_p]
+    text = out.read_bytes()
+    h = C.c_void_p()
+    err = C.create_string_buffer(256)
+    assert lib.ref_parse_matrix(text, len(text), C.byref(h), err, 256) == 0, err.value
+    k, nn, mm, ss, rr = (C.c_int() for _ in range(5))
+    ln = C.c_size_t()
+    lib.ref_mat_dims(h, C.byref(k), C.byref(nn), C.byref(mm), C.byref(ss), C.byref(rr), C.byref(ln), None)
+    ours = np.empty(ln.value)
+    lib.ref_mat_dims(h, C.byref(k), C.byref(nn), C.byref(mm), C.byref(ss), C.byref(rr), C.byref(ln),
+                     ours.ctypes.data_as(C.c_void_p))
+    lib.ref_mat_destroy(h)
+    want, _ = O.ref_generate_random(kind, n, m, s, r, 9, 2.0)
+    assert np.array_equal(ours, want)
+
+
+def test_generate_is_linear_time(psg_bin, tmp_path):
+    """psg generate of a 2^24-row dominant banded matrix finishes in seconds
+    (generate_random walks each row's structure, not all n columns)."""
+    import time
+    t0 = time.perf_counter()
+    res = run("generate", "--kind", "banded", "--n", 1 << 24, "--s", 1, "--r", 1, "--seed", 1, "--dominance", 2,
+              "-o", "/dev/null")
+    dt = time.perf_counter() - t0
+    assert res.returncode == 0, res.stderr
+    assert dt < 60, dt
