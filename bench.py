@@ -240,11 +240,12 @@ def other_configs(psg, torch, peak, dev, steps=20):
                 e0.record()
                 H.refactor(A)
                 H.solve_async(f, x)
-                H.sync(st)
                 e1.record()
+                H.sync(st)  # certificate checked (and repaired) before the next step's flush
             torch.cuda.synchronize()
             ms = sum(e0.elapsed_time(e1) for e0, e1 in evs) / steps
-            l2 = "L2 flushed (512 MB write) before each step; each step timed alone, incl. its certificate sync"
+            l2 = ("L2 flushed (512 MB write) before each step; each step's device time (refactor + certified "
+                  "solve incl. its certificate kernel) timed alone")
             del flush
         else:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
