@@ -744,6 +744,11 @@ __global__ void __launch_bounds__(32) chain_down_kernel(ChainLevelArgs g, ChainT
   const int lane = threadIdx.x, i = lane % MB, T = t.T, PT = t.P[T - 1];
   const long w = blockIdx.x;
   double* const* F = sel ? t.cfl : t.fl;
+  // launched programmatically: wait for the producer of F (and of the maps),
+  // then let the next level-0 pass start its prologue (it waits on this grid
+  // before reading the values written here)
+  pdl_wait();
+  pdl_trigger();
   // regions: top at ssm, level l (2 <= l < T) at ssm + (T - l) * REG
   chain_stage<MB, false>(ssm, t.phi[T - 1], 0, PT, F[T], 0, PT + 1, lane, 32);
   for (int l = 2; l < T; ++l) {
@@ -790,6 +795,7 @@ __global__ void __launch_bounds__(32) chain_down_kernel(ChainLevelArgs g, ChainT
 
 template <int MB, int KM>
 __global__ void __launch_bounds__(16 * MB) chain_solve_kernel(ChainLevelArgs g, ChainTree t) {
+  pdl_trigger();  // the next down sweep waits for this grid before reading anything it writes
   constexpr int NT = 16 * MB, MAPS = ChainReg<MB>::MAPS, MM = MB * MB;
   extern __shared__ __align__(16) double ssm[];
   __shared__ double s_v[(kChainC0 + 1) * MB];  // x (KM 1) or d (KM 2) at this CTA's level-1 unknowns
@@ -817,6 +823,7 @@ __global__ void __launch_bounds__(16 * MB) chain_solve_kernel(ChainLevelArgs g, 
       for (int e = tid; e < (len1 + 1) * MB; e += NT) s_x[e] = __ldg(t.x1 + kChainC0 * c * MB + e);
     __syncthreads();
     if (tid < 32) {  // this CTA's level-1 values from the down sweep's level-2 values
+      pdl_wait();  // launched programmatically after the down sweep: its values from here on
       const double* xl = t.xlev[SEL];
       if (T == 1) {
         if (lane < MB)

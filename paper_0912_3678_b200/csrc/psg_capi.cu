@@ -1158,7 +1158,8 @@ struct ChainSolver {
   void solve_launch(const ChainLevelArgs& a, const ChainTree& t, cudaStream_t s) {
     constexpr int bytes = ChainReg<M>::SIZE * 8;
     ensure_smem(reinterpret_cast<const void*>(chain_solve_kernel<M, KM>), bytes);
-    chain_solve_kernel<M, KM><<<(int)((P[0] + kChainC0 - 1) / kChainC0), 16 * M, bytes, s>>>(a, t);
+    launch_pdl(chain_solve_kernel<M, KM>, dim3((unsigned)((P[0] + kChainC0 - 1) / kChainC0)), dim3(16 * M), bytes, s,
+               a, t);
     LAUNCH_CHECK();
     ++launches;
   }
@@ -1167,7 +1168,7 @@ struct ChainSolver {
   void down_launch(const ChainLevelArgs& a, const ChainTree& t, int sel, cudaStream_t s) {
     const int bytes = t.T * ChainReg<M>::SIZE * 8;
     ensure_smem(reinterpret_cast<const void*>(chain_down_kernel<M>), kChainMaxLev * ChainReg<M>::SIZE * 8);
-    chain_down_kernel<M><<<t.T >= 3 ? t.P[2] : 1, 32, bytes, s>>>(a, t, sel);
+    launch_pdl(chain_down_kernel<M>, dim3(t.T >= 3 ? t.P[2] : 1), dim3(32), bytes, s, a, t, sel);
     LAUNCH_CHECK();
     ++launches;
   }
