@@ -287,7 +287,8 @@ __global__ void __launch_bounds__(32 * NW) blk_segment_solve_kernel(BlkArgs g) {
     }
   }
   Vec<K> xl, xrv;
-  pdl_wait();  // separator values from the previous kernel (the staging above overlaps it)
+  pdl_wait();     // separator values from the previous kernel (the staging above overlaps it)
+  pdl_trigger();  // the certificate kernel may launch (it waits for this grid before reading the records)
 #pragma unroll
   for (int u = 0; u < K; ++u) {
     xl.v[u] = Pt.ls >= 0 ? __ldg(g.xsep + (long)lsi * K + u) : 0.0;
@@ -709,7 +710,8 @@ __global__ void __launch_bounds__(32) blk_body_narrow_kernel(BlkArgs g) {
   const long B0 = b / K, NBall = g.n / K;
   const bool hasl = live && Pt.ls >= 0, hasr = live && Pt.rs >= 0;
   Vec<K> xl, xrv;
-  pdl_wait();  // separator values from the previous kernel
+  pdl_wait();     // separator values from the previous kernel
+  pdl_trigger();  // the certificate kernel may launch (it waits for this grid before reading the records)
 #pragma unroll
   for (int u = 0; u < K; ++u) {
     xl.v[u] = hasl ? __ldg(g.xsep + (long)(seg - 1) * K + u) : 0.0;

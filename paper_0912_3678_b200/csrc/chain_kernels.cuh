@@ -263,6 +263,7 @@ __device__ __forceinline__ bool cta_last_arrive(int* ctr, int expected) {
 
 template <int MB, bool STORE_T, bool WITH_F>
 __global__ void __launch_bounds__(128) chain_fc_kernel(ChainLevelArgs g, ChainTree t) {
+  pdl_trigger();  // the down sweep may launch (it waits for this grid before reading anything)
   using C = FcCfg<MB>;
   constexpr int MM = MB * MB, RW = 2 * MB;
   extern __shared__ __align__(16) double fsm[];
