@@ -1028,6 +1028,7 @@ struct BlkSpecArgs {
   double* Tdiag;   // out: per separator the K*K block A_SS (certificate)
   DevStatus* reset;  // the solve's status slot (reset by block 0)
   long boff[9];    // banded: A(row, row + d) = data[boff[d + K] + row]
+  long data_len;   // entries in data (staging over-read bound)
 };
 
 // A(i, j) for the block kinds (0 outside the structure)

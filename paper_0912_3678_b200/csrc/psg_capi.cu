@@ -25,6 +25,7 @@
 #include "psg_common.cuh"
 #include "tri_kernels.cuh"
 #include "blk_kernels.cuh"
+#include "band_kernels.cuh"
 #include "chain_kernels.cuh"
 #include "ode_kernels.cuh"
 #include "piv_kernels.cuh"
@@ -892,11 +893,31 @@ bool launch_blk_segments(int K, int NB, int layout, const BlkArgs& a, cudaStream
 // truncation depth in block rows per side (about 64 scalar rows)
 constexpr int blk_hb(int K) { return K == 2 ? 32 : 16; }
 
+// Banded s, r <= K in scalar band arithmetic (band_kernels.cuh): longest
+// body of one body kernel (rows; smem (2K + 2) x (L + 4) doubles per warp).
+// PSG_BAND_OLD=1 keeps the K x K block kernels for banded matrices.
+int band_max_rows() {
+  static const int v = [] {
+    const char* e = getenv("PSG_BAND_MAXL");
+    return e && atoi(e) > 0 ? atoi(e) : 576;
+  }();
+  return v;
+}
+bool band_scalar_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("PSG_BAND_OLD");
+    return !(e && atoi(e) > 0);
+  }();
+  return v;
+}
+
 // Speculative solver for the K x K block kinds.  Its bodies are the
 // reference plan's, each split into equal sub-bodies (extra K-row separators)
 // when longer than one warp's 32 M block rows.
 struct BlkSolver {
   int K = 0, layout = 0, NB = 0;
+  bool band = false;  // scalar band kernels (band_kernels.cuh)
+  int RB = 0;         // band: smem rows per array
   bool possible = false;
   BlkArgs base{};
   std::vector<GPart> hpart;
@@ -919,6 +940,9 @@ struct BlkSolver {
       return;
     }
     const int unit = layout == kBlkBlockTri ? K : 1, ku = K / unit;
+    band = layout == kBlkBanded && band_scalar_enabled();
+    // longest body of one kernel, in block rows of K
+    const int maxnb = band ? band_max_rows() / K : blk_max_nb(K);
     hpart.clear();
     hsep.clear();
     int maxL = 0, minL = INT_MAX;
@@ -931,7 +955,7 @@ struct BlkSolver {
       if (!bodies.empty()) {
         auto& c = bodies.back();
         const int merged = c.second + K + L;
-        if ((merged + K - 1) / K <= blk_max_nb(K)) {
+        if ((merged + K - 1) / K <= maxnb) {
           c.second = merged;
           continue;
         }
@@ -943,7 +967,7 @@ struct BlkSolver {
       const int Lu = L / unit;
       auto nb_of = [&](int t) { return (((Lu - (t - 1) * ku) + t - 1) / t * unit + K - 1) / K; };
       int t = 1;
-      while (t < Lu && nb_of(t) > blk_max_nb(K)) ++t;
+      while (t < Lu && nb_of(t) > maxnb) ++t;
       const int body = Lu - (t - 1) * ku, bs = body / t, br = body % t;
       int cur = b;
       for (int u = 0; u < t; ++u) {
@@ -965,7 +989,13 @@ struct BlkSolver {
       hpart[g].rs = g < nsep ? hsep[g] : -1;
     }
     NB = (maxL + K - 1) / K;
-    if (minL < blk_hb(K) * K || minL < 2 * K || blk_shape(K, NB).M == 0 || nsep < 1) return;
+    if (minL < blk_hb(K) * K || minL < 2 * K || nsep < 1) return;
+    if (band) {
+      if (minL < 4 * K || maxL > band_max_rows()) return;
+      RB = (maxL + 4) & ~1;
+    } else if (blk_shape(K, NB).M == 0) {
+      return;
+    }
     part.alloc(nseg);
     sep.alloc(nsep);
     CUDA_TRY(cudaMemcpy(part.p, hpart.data(), sizeof(GPart) * nseg, cudaMemcpyHostToDevice));
@@ -984,6 +1014,36 @@ struct BlkSolver {
   }
 
   void set_data(const double* d) { base.data = d; }
+
+  template <int KK>
+  void band_spec_launch_k(const BlkSpecArgs& g, cudaStream_t s) {
+    constexpr int W = blk_hb(KK) * KK;
+    const int grid = (nsep + 31) / 32;
+    band_spec_kernel<KK, W><<<grid, kBandSpecThreads, 0, s>>>(g);
+  }
+  void band_spec_launch(const BlkSpecArgs& g, cudaStream_t s) {
+    if (K == 4)
+      band_spec_launch_k<4>(g, s);
+    else if (K == 3)
+      band_spec_launch_k<3>(g, s);
+    else
+      band_spec_launch_k<2>(g, s);
+  }
+  template <int KK>
+  void band_body_launch_k(const BlkArgs& a, cudaStream_t s) {
+    const int bytes = 8 * (2 * KK + 2) * RB;
+    ensure_smem(reinterpret_cast<const void*>(band_body_kernel<KK>), 200 * 1024);
+    launch_pdl(band_body_kernel<KK>, dim3(a.nseg), dim3(32), bytes, s, a, RB);
+  }
+  void band_body_launch(const BlkArgs& a, cudaStream_t s) {
+    if (K == 4)
+      band_body_launch_k<4>(a, s);
+    else if (K == 3)
+      band_body_launch_k<3>(a, s);
+    else
+      band_body_launch_k<2>(a, s);
+    LAUNCH_CHECK();
+  }
 
   // the factor is lazy: its block sweeps run inside the next solve's fused
   // separator kernel (blk_spec_fused_kernel), which also condenses f
@@ -1004,9 +1064,12 @@ struct BlkSolver {
     g.Tdiag = Tdiag.p;
     g.reset = st;
     for (int t = 0; t < 9; ++t) g.boff[t] = base.boff[t];
+    g.data_len = base.data_len;
     constexpr int NS = 1;  // separators per warp (2, chains interleaved: config 2 82 -> 123 us, config 3 217 -> 332 us)
     const int grid = (nsep + 4 * NS - 1) / (4 * NS);
-    if (K == 4)
+    if (band) {
+      band_spec_launch(g, s);
+    } else if (K == 4)
       blk_spec_fused_kernel<4, blk_hb(4), NS><<<grid, 128, 0, s>>>(g);
     else if (K == 3)
       blk_spec_fused_kernel<3, blk_hb(3), NS><<<grid, 128, 0, s>>>(g);
@@ -1023,7 +1086,9 @@ struct BlkSolver {
     a.xsep = xsep.p;
     a.rec = rec.p;
     a.status = st;
-    if (!launch_blk_segments(K, NB, layout, a, s, /*pdl=*/true))
+    if (band)
+      band_body_launch(a, s);
+    else if (!launch_blk_segments(K, NB, layout, a, s, /*pdl=*/true))
       throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "block body too long"};
     const int cg = std::min(148 * 8, (nsep * K + 255) / 256);
     const double* Td = Tdiag.p;
