@@ -122,6 +122,21 @@ __global__ void __launch_bounds__(32) band_body_kernel(BlkArgs g, int RB) {
     mbar_arrive_expect_tx(&bar, tx);
     boffs[lane] = lane * RB + 1 + shift;
   }
+  // certificate couplings, loaded while the rows stage: lanes u < K: A(ls + u, b + t),
+  // lanes 16 + u: A(rs + u, b + L - 1 - t), t < K (blk_cert_kernel record format)
+  double cpl[K];
+  {
+    const bool left = lane < K, right = lane >= 16 && lane < 16 + K;
+    const int u = left ? lane : lane - 16;
+    const long row = left ? (long)Pt.ls + u : (long)Pt.rs + u;
+    const bool has = (left && Pt.ls >= 0) || (right && Pt.rs >= 0);
+#pragma unroll
+    for (int t = 0; t < K; ++t) {
+      const long col = left ? b + t : b + L - 1 - t;
+      const int d = (int)(col - row);
+      cpl[t] = (has && g.rec && t < L && d >= -g.s && d <= g.r) ? __ldg(g.data + g.boff[d + K] + row) : 0.0;
+    }
+  }
   Vec<K> xl, xrv;
   pdl_wait();     // separator values from the separator kernel (the staging above overlaps it)
   pdl_trigger();  // the certificate kernel may launch (it waits for this grid before reading the records)
@@ -354,9 +369,40 @@ __global__ void __launch_bounds__(32) band_body_kernel(BlkArgs g, int RB) {
   blk_inv_short<K>(Bb, &rsum);
   Blk<K> al = blk_mul<K>(Bb, Ab), ga = blk_mul<K>(Bb, Cb);
   Vec<K> de = blk_mv<K>(Bb, Fv);
+  //      Strongly coupled-down rows (the common case: kappa = max row sum of
+  //      |al| + |ga| tiny) are solved by block Jacobi sweeps instead, X <-
+  //      de - al X_{t-1} - ga X_{t+1} from X = de: after it sweeps the error is
+  //      below kappa^(it+1) |X|, so it is chosen with kappa^(it+1) <= 2^-64
+  //      (config 3: kappa ~ 1e-7, 2 sweeps of 2 K x K mat-vecs instead of 2
+  //      PCR steps of 6 K x K products and an inverse).
   constexpr double kDecoupled = 5.421010862427522e-20;  // 2^-64
+  double kap = 0.0;
+#pragma unroll
+  for (int u = 0; u < K; ++u) {
+    double rsu = 0.0;
+#pragma unroll
+    for (int v = 0; v < K; ++v) rsu += fabs(al.v[u][v]) + fabs(ga.v[u][v]);
+    kap = fmax(kap, rsu);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) kap = fmax(kap, __shfl_xor_sync(FULL, kap, o));
+  const bool jacobi = kap <= 1.0 / 4096.0;  // NaN: PCR
+  if (jacobi) {
+    int nit = 0;
+    for (double pw = kap; pw > kDecoupled; pw *= kap) ++nit;
+    const Vec<K> d0 = de;
 #pragma unroll 1
-  for (int st = 1; st < NL; st <<= 1) {
+    for (int it = 0; it < nit; ++it) {
+      const Vec<K> xlft = vec_shfl<K>(de, lane > 0 ? lane - 1 : lane);
+      const Vec<K> xrgt = vec_shfl<K>(de, lane < 31 ? lane + 1 : lane);
+      Vec<K> nx = d0;
+      blk_mv_sub<K>(nx, al, xlft);
+      blk_mv_sub<K>(nx, ga, xrgt);
+      de = nx;
+    }
+  }
+#pragma unroll 1
+  for (int st = 1; st < (jacobi ? 1 : NL); st <<= 1) {
     if (__all_sync(FULL, fmax(blk_maxabs<K>(al), blk_maxabs<K>(ga)) < kDecoupled)) break;
     const bool hl = lane >= st, hh = lane + st < 32;
     const int sl = hl ? lane - st : lane, sh = hh ? lane + st : lane;
@@ -460,39 +506,19 @@ __global__ void __launch_bounds__(32) band_body_kernel(BlkArgs g, int RB) {
 #pragma unroll
     for (int u = 0; u < K; ++u) g.x[Pt.rs + u] = xrv.v[u];
   // ---- certificate records: the separator rows' couplings to this body (blk_cert_kernel format)
-  if (g.rec) {
-    double* rc = g.rec + (long)seg * 4 * K;
-    auto at = [&](long row, long col) -> double {  // global A(row, col), row inside the matrix
-      const int d = (int)(col - row);
-      if (d < -g.s || d > g.r || col < 0 || col >= n) return 0.0;
-      return __ldg(g.data + g.boff[d + K] + row);
-    };
-    if (lane < K) {
-      double sg = 0.0, ab = 0.0;
-      if (Pt.ls >= 0) {
-        const long row = Pt.ls + lane;
-        for (int t = 0; t < 2 * K && t < L; ++t) {
-          const double pr = at(row, b + t) * sx[t];
-          sg += pr;
-          ab += fabs(pr);
-        }
-      }
-      rc[lane] = sg;
-      rc[K + lane] = ab;
-    } else if (lane >= 16 && lane < 16 + K) {
-      const int u = lane - 16;
-      double sg = 0.0, ab = 0.0;
-      if (Pt.rs >= 0) {
-        const long row = Pt.rs + u;
-        for (int t = 1; t <= 2 * K && t <= L; ++t) {
-          const double pr = at(row, b + L - t) * sx[L - t];
-          sg += pr;
-          ab += fabs(pr);
-        }
-      }
-      rc[2 * K + u] = sg;
-      rc[3 * K + u] = ab;
+  if (g.rec && (lane < K || (lane >= 16 && lane < 16 + K))) {
+    const bool left = lane < K;
+    const int u = left ? lane : lane - 16;
+    double sg = 0.0, ab = 0.0;
+#pragma unroll
+    for (int t = 0; t < K; ++t) {
+      const double pr = t < L ? cpl[t] * sx[left ? t : L - 1 - t] : 0.0;
+      sg += pr;
+      ab += fabs(pr);
     }
+    double* rc = g.rec + (long)seg * 4 * K + (left ? 0 : 2 * K);
+    rc[u] = sg;
+    rc[K + u] = ab;
   }
   if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
