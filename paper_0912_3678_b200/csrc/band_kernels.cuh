@@ -153,20 +153,18 @@ __global__ void __launch_bounds__(32) band_body_kernel(BlkArgs g, int RB) {
   for (int a = 0; a < NA; ++a) bo[a] = boffs[a];
   auto S = [&](int a, int i) -> double& { return sm[bo[a] + i]; };
 
-  // ---- lane chunks: [lo, hi); lane t >= 1: separator S_t = rows [lo, lo + K), sub-body [lo + K, hi);
-  //      lane 0: sub-body [0, hi), S_0 = the body's left separator (known)
-  //      chunks of an ODD number R of rows (lane t starts at t R: the lanes' rows
-  //      fall in distinct shared-memory banks), the last one takes the rest
+  // ---- lane chunks: lane t's sub-body is [t R, (t + 1) R - K) (the last lane: up to L),
+  //      its separator S_t the K rows before it (lane 0: the body's left
+  //      separator, known); R odd, so the lanes' rows at the same step fall in
+  //      distinct shared-memory banks
   int R = ((L + 31) / 32) | 1;
   if (R < 2 * K) R = (2 * K) | 1;
   int NL = (L + R - 1) / R;
-  if (NL > 1 && L - (NL - 1) * R < 2 * K) --NL;  // too short a tail: the previous lane takes it
+  if (NL > 1 && L - (NL - 1) * R < K) --NL;  // too short a tail: the previous lane takes it
   const bool act = lane < NL;
-  const int lo = act ? lane * R : L;
-  const int hi = act ? (lane + 1 == NL ? L : (lane + 1) * R) : L;
-  const int bl = lane == 0 ? 0 : lo + K;  // sub-body start
-  const int sS = bl - K;                  // S_t start (lane 0: -K, the left separator)
-  const int len = hi - bl;                // >= K for active lanes
+  const int bl = act ? lane * R : L;                          // sub-body start
+  const int hi = act ? (lane + 1 == NL ? L : (lane + 1) * R - K) : L;
+  const int sS = bl - K;                                      // S_t start (lane 0: -K, the left separator)
   double rsum = 0.0;
 
   // ---- forward sweep: no-pivot band LU carrying v = [f | spike of S_t];
@@ -241,8 +239,8 @@ __global__ void __launch_bounds__(32) band_body_kernel(BlkArgs g, int RB) {
 #pragma unroll
         for (int a = 0; a < NA; ++a) cur[a] = nxt[a];
       }
-#pragma unroll 1
-      for (int i = bl + K; i < hi; ++i) {  // row hi is read ahead (inside the region; unused)
+#pragma unroll (K)
+      for (int i = bl + K; i < hi; ++i) {  // row hi is read ahead (inside the region; unused); unrolled by K: the window rotates by renaming
 #pragma unroll
         for (int a = 0; a < NA; ++a) nxt[a] = S(a, i + 1);
         step(i, -1, cur);
@@ -301,8 +299,8 @@ __global__ void __launch_bounds__(32) band_body_kernel(BlkArgs g, int RB) {
 #pragma unroll
         for (int a = 0; a < NA; ++a) cur[a] = nxt[a];
       }
-#pragma unroll 1
-      for (int i = hi - 1 - K; i >= bl; --i) {  // row bl - 1 is read ahead (inside the region; unused)
+#pragma unroll (K)
+      for (int i = hi - 1 - K; i >= bl; --i) {  // row bl - 1 is read ahead (inside the region; unused); unrolled by K
 #pragma unroll
         for (int a = 0; a < NA; ++a) nxt[a] = S(a, i - 1);
         step(i, -1, cur);
@@ -443,7 +441,10 @@ __global__ void __launch_bounds__(32) band_body_kernel(BlkArgs g, int RB) {
   if (lane == NL - 1) Xn = xrv;
   bool finite = true;
   if (act) {
-    double cur[C], nxt[C];  // [c | P | Q] of row i, loaded one row ahead
+    // independent rows, RU at a time: all loads of the group before its stores
+    // (the stores may alias later loads, so the compiler would not hoist them),
+    // x as a two-level sum (short dependency chain)
+    constexpr int RU = 4;
     auto ld = [&](double (&f)[C], int i) {
       f[0] = S(FA, i);
 #pragma unroll
@@ -452,20 +453,27 @@ __global__ void __launch_bounds__(32) band_body_kernel(BlkArgs g, int RB) {
         f[1 + K + v] = S(K + 1 + v, i);
       }
     };
-    ld(cur, bl);
 #pragma unroll 1
-    for (int i = bl; i < hi; ++i) {
-      ld(nxt, i + 1);
-      double x = cur[0];
+    for (int i0 = bl; i0 < hi; i0 += RU) {
+      double fr[RU][C];
 #pragma unroll
-      for (int v = 0; v < K; ++v) {
-        x = fma(cur[1 + v], de.v[v], x);
-        x = fma(cur[1 + K + v], Xn.v[v], x);
+      for (int u = 0; u < RU; ++u) ld(fr[u], i0 + u < hi ? i0 + u : hi - 1);
+#pragma unroll
+      for (int u = 0; u < RU; ++u) {
+        double p = fr[u][1] * de.v[0], q = fr[u][1 + K] * Xn.v[0];
+#pragma unroll
+        for (int v = 1; v < K; ++v) {
+          p = fma(fr[u][1 + v], de.v[v], p);
+          q = fma(fr[u][1 + K + v], Xn.v[v], q);
+        }
+        fr[u][0] += p + q;
       }
-      finite &= isfinite(x);
-      S(FA, i) = x;
 #pragma unroll
-      for (int q = 0; q < C; ++q) cur[q] = nxt[q];
+      for (int u = 0; u < RU; ++u)
+        if (i0 + u < hi) {
+          finite &= isfinite(fr[u][0]);
+          S(FA, i0 + u) = fr[u][0];
+        }
     }
     if (lane > 0)
 #pragma unroll
