@@ -367,38 +367,10 @@ __global__ void __launch_bounds__(32) band_body_kernel(BlkArgs g, int RB) {
   blk_inv_short<K>(Bb, &rsum);
   Blk<K> al = blk_mul<K>(Bb, Ab), ga = blk_mul<K>(Bb, Cb);
   Vec<K> de = blk_mv<K>(Bb, Fv);
-  //      Strongly coupled-down rows (the common case: kappa = max row sum of
-  //      |al| + |ga| tiny) are solved by block Jacobi sweeps instead, X <-
-  //      de - al X_{t-1} - ga X_{t+1} from X = de: after it sweeps the error is
-  //      below kappa^(it+1) |X|, so it is chosen with kappa^(it+1) <= 2^-64
-  //      (config 3: kappa ~ 1e-7, 2 sweeps of 2 K x K mat-vecs instead of 2
-  //      PCR steps of 6 K x K products and an inverse).
+  //      Strongly decoupled rows (the common case) take block Jacobi sweeps
+  //      instead (blk_jacobi: config 3 kappa ~ 1e-7, 2 sweeps).
   constexpr double kDecoupled = 5.421010862427522e-20;  // 2^-64
-  double kap = 0.0;
-#pragma unroll
-  for (int u = 0; u < K; ++u) {
-    double rsu = 0.0;
-#pragma unroll
-    for (int v = 0; v < K; ++v) rsu += fabs(al.v[u][v]) + fabs(ga.v[u][v]);
-    kap = fmax(kap, rsu);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) kap = fmax(kap, __shfl_xor_sync(FULL, kap, o));
-  const bool jacobi = kap <= 1.0 / 4096.0;  // NaN: PCR
-  if (jacobi) {
-    int nit = 0;
-    for (double pw = kap; pw > kDecoupled; pw *= kap) ++nit;
-    const Vec<K> d0 = de;
-#pragma unroll 1
-    for (int it = 0; it < nit; ++it) {
-      const Vec<K> xlft = vec_shfl<K>(de, lane > 0 ? lane - 1 : lane);
-      const Vec<K> xrgt = vec_shfl<K>(de, lane < 31 ? lane + 1 : lane);
-      Vec<K> nx = d0;
-      blk_mv_sub<K>(nx, al, xlft);
-      blk_mv_sub<K>(nx, ga, xrgt);
-      de = nx;
-    }
-  }
+  const bool jacobi = blk_jacobi<K>(al, ga, de, lane, 32);
 #pragma unroll 1
   for (int st = 1; st < (jacobi ? 1 : NL); st <<= 1) {
     if (__all_sync(FULL, fmax(blk_maxabs<K>(al), blk_maxabs<K>(ga)) < kDecoupled)) break;

@@ -162,6 +162,12 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// 32-byte aligned load of 4 doubles (one LDG.256: one sector per request
+// instead of four for a lane walking its own contiguous rows)
+__device__ __forceinline__ void ldg256(const double* p, double& a, double& b, double& c, double& d) {
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+
 // Reciprocal: MUFU approximation + two Newton steps (<= 1 ulp; no slow-path
 // branch).  0 -> inf and inf/NaN -> NaN propagate to the non-finite check.
 // Programmatic dependent launch (sm_90+): a kernel launched with the
