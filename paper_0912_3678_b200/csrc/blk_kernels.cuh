@@ -1277,6 +1277,163 @@ __global__ void __launch_bounds__(128) blk_spec_fused_kernel(BlkSpecArgs g) {
   (void)rsum;  // a vanished pivot leaves non-finite separator values: the certificate rejects them
 }
 
+// ---------------------------------------------------------------------------
+// speculative factor, block tridiagonal, ONE THREAD PER SEPARATOR SIDE with the
+// K x K algebra in registers (blktri_spec_kernel).  The side's HB block rows
+// stream straight from memory, one block row per step; K = 4 / 2 block
+// rows are 128 / 32-byte multiples, read by 256-bit loads (one sector per
+// request: the lanes of a warp walk different bodies, so the requests do not
+// coalesce and the sector count is what the L1 pays for), after an L2 prefetch
+// of the whole side.  Far -> near block
+// elimination (src/localfact.cpp:84-100 order):
+//   D'_i = D_i - F_i X_{i-1},  X_i = D'_i^-1 N_i,  z_i = D'_i^-1 (f_i - F_i z_{i-1})
+// with F the coupling away from the separator, N toward it; the near block row
+// then is x_near = z_n - X_n x_S, and the separator block row gives
+//   (A_SS - A_S,above X_above - C_S,below X_below) x_S = f_S - A_S,above z_above - C_S,below z_below.
+// CTA = 2 warps over 32 separators: warp 0 the sides above, warp 1 below.
+// ---------------------------------------------------------------------------
+template <int K>
+__device__ __forceinline__ void blktri_ld(const double* p, bool vec, Blk<K>& X) {
+  if constexpr (K == 4) {
+    if (vec) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) ldg256(p + 4 * u, X.v[u][0], X.v[u][1], X.v[u][2], X.v[u][3]);
+      return;
+    }
+  } else if constexpr (K == 2) {
+    if (vec) {
+      ldg256(p, X.v[0][0], X.v[0][1], X.v[1][0], X.v[1][1]);
+      return;
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < K; ++u)
+#pragma unroll
+    for (int v = 0; v < K; ++v) X.v[u][v] = __ldg(p + u * K + v);
+}
+
+template <int K, int HB, int H>
+__device__ __forceinline__ void blktri_side(const BlkSpecArgs& g, bool live, long BS, Blk<K>& T, Vec<K>& rr) {
+  constexpr int KK = K * K;
+  const long NBall = g.n / K;
+  const bool vec = ((reinterpret_cast<uintptr_t>(g.data) | reinterpret_cast<uintptr_t>(g.f)) & 31) == 0;
+  // block row Bi of step i (far -> near): H = 0: BS - HB + i, H = 1: BS + HB - i
+  auto brow = [&](int i) -> long { return H == 0 ? BS - HB + i : BS + HB - i; };
+  const bool ok = live && BS - HB >= 1 && BS + HB + 1 < NBall;  // interior (the host guarantees it)
+  struct Row {
+    Blk<K> F, D, N;
+    Vec<K> f;
+  };
+  auto load = [&](int i, Row& R) {
+    const long B = ok ? brow(i) : 1;
+    const double* p = g.data + (3 * B - 1) * KK;  // sub | diag | super
+    blktri_ld<K>(p + (H == 0 ? 0 : 2 * KK), vec, R.F);
+    blktri_ld<K>(p + KK, vec, R.D);
+    blktri_ld<K>(p + (H == 0 ? 2 * KK : 0), vec, R.N);
+    if (K == 4 && vec) {
+      ldg256(g.f + B * K, R.f.v[0], R.f.v[1], R.f.v[2], R.f.v[3]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < K; ++u) R.f.v[u] = __ldg(g.f + B * K + u);
+    }
+  };
+  // every block row of the side into L2 up front (the whole side is one wave of
+  // a few threads per SM: the sweep then waits on L2, not HBM, per block row)
+  if (ok) {
+#pragma unroll 1
+    for (int i = 0; i < HB; ++i) {
+      const char* p0 = reinterpret_cast<const char*>(g.data + (3 * brow(i) - 1) * KK);
+      for (int o = 0; o < 3 * KK * 8; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(p0 + o));
+    }
+  }
+  Row cur;
+  Blk<K> X;
+  Vec<K> z;
+  blk_set_zero<K>(X);
+#pragma unroll
+  for (int u = 0; u < K; ++u) z.v[u] = 0.0;
+  double rsum = 0.0;
+#pragma unroll 1
+  for (int i = 0; i < HB; ++i) {
+    load(i, cur);
+    Blk<K> D = cur.D;
+    Vec<K> y = cur.f;
+    if (i > 0) {  // step 0: the truncation drops the coupling to the far side
+      blk_mul_sub<K>(D, cur.F, X);
+      blk_mv_sub<K>(y, cur.F, z);
+    }
+    blk_inv<K>(D, &rsum);
+    X = blk_mul<K>(D, cur.N);
+    z = blk_mv<K>(D, y);
+  }
+  // the separator block row's coupling to this side's near block row
+  const double* ps = g.data + (3 * (ok ? BS : 1) - 1) * KK;
+  Blk<K> As;
+  blktri_ld<K>(ps + (H == 0 ? 0 : 2 * KK), vec, As);
+  T = blk_mul<K>(As, X);
+  rr = blk_mv<K>(As, z);
+  if (!ok || !isfinite(rsum))
+#pragma unroll
+    for (int u = 0; u < K; ++u) rr.v[u] = __longlong_as_double(0x7ff8000000000000ll);
+}
+
+template <int K, int HB>
+__global__ void __launch_bounds__(64) blktri_spec_kernel(BlkSpecArgs g) {
+  constexpr int KK = K * K;
+  __shared__ double xch[32][KK + K];
+  const int tid = threadIdx.x;
+  if (g.reset && blockIdx.x == 0)  // first kernel of the solve: fresh status
+    for (int q = tid; q < kCertSlots + 2; q += blockDim.x) {
+      if (q < kCertSlots)
+        g.reset->cert_bits[q] = 0ull;
+      else if (q == kCertSlots)
+        g.reset->bad_seg = INT_MAX;
+      else
+        g.reset->pivot_seg = INT_MAX;
+    }
+  pdl_trigger();  // the body kernel may launch and start loading
+  const int lane = tid & 31, h = tid >> 5;
+  const int j = blockIdx.x * 32 + lane;
+  const bool live = j < g.nsep;
+  const long BS = live ? g.sep[j] / K : 0;
+  Blk<K> T;
+  Vec<K> rr;
+  if (h == 0)
+    blktri_side<K, HB, 0>(g, live, BS, T, rr);
+  else
+    blktri_side<K, HB, 1>(g, live, BS, T, rr);
+  if (h == 1) {
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+      xch[lane][KK + u] = rr.v[u];
+#pragma unroll
+      for (int v = 0; v < K; ++v) xch[lane][u * K + v] = T.v[u][v];
+    }
+  }
+  __syncthreads();
+  if (h == 0 && live) {
+    const double* ps = g.data + (3 * BS - 1) * KK;
+    Blk<K> A;
+    Vec<K> rhs;
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+      rhs.v[u] = (__ldg(g.f + BS * K + u) - rr.v[u]) - xch[lane][KK + u];
+#pragma unroll
+      for (int v = 0; v < K; ++v) {
+        const double ass = __ldg(ps + KK + u * K + v);
+        A.v[u][v] = (ass - T.v[u][v]) - xch[lane][u * K + v];
+        g.Tdiag[(long)j * KK + u * K + v] = ass;
+      }
+    }
+    double rsum = 0.0;
+    blk_inv<K>(A, &rsum);
+    const Vec<K> xs = blk_mv<K>(A, rhs);
+#pragma unroll
+    for (int u = 0; u < K; ++u) g.xsep[(long)j * K + u] = xs.v[u];
+  }
+  // a vanished pivot leaves non-finite separator values: the certificate rejects them
+}
+
 // omega = max over separator rows of |f - A_SS x_S - left - right| / (|f| + sum |terms|).
 template <int K>
 __global__ void blk_cert_kernel(const double* __restrict__ Tdiag, const int* __restrict__ sep, int nsep,

@@ -1067,8 +1067,20 @@ struct BlkSolver {
     g.data_len = base.data_len;
     constexpr int NS = 1;  // separators per warp (2, chains interleaved: config 2 82 -> 123 us, config 3 217 -> 332 us)
     const int grid = (nsep + 4 * NS - 1) / (4 * NS);
+    static const bool warp_spec = [] {  // PSG_BLK_SPEC_WARP=1: the round-1/2 warp-per-separator kernel
+      const char* e = getenv("PSG_BLK_SPEC_WARP");
+      return e && atoi(e) > 0;
+    }();
     if (band) {
       band_spec_launch(g, s);
+    } else if (!warp_spec) {
+      const int g2 = (nsep + 31) / 32;
+      if (K == 4)
+        blktri_spec_kernel<4, blk_hb(4)><<<g2, 64, 0, s>>>(g);
+      else if (K == 3)
+        blktri_spec_kernel<3, blk_hb(3)><<<g2, 64, 0, s>>>(g);
+      else
+        blktri_spec_kernel<2, blk_hb(2)><<<g2, 64, 0, s>>>(g);
     } else if (K == 4)
       blk_spec_fused_kernel<4, blk_hb(4), NS><<<grid, 128, 0, s>>>(g);
     else if (K == 3)
