@@ -1102,6 +1102,7 @@ struct BlkSpecArgs {
   DevStatus* reset;  // the solve's status slot (reset by block 0)
   long boff[9];    // banded: A(row, row + d) = data[boff[d + K] + row]
   long data_len;   // entries in data (staging over-read bound)
+  int prefetch;    // blktri_spec_kernel: L2-prefetch each side before its sweep
 };
 
 // A(i, j) for the block kinds (0 outside the structure)
@@ -1277,6 +1278,279 @@ __global__ void __launch_bounds__(128) blk_spec_fused_kernel(BlkSpecArgs g) {
   (void)rsum;  // a vanished pivot leaves non-finite separator values: the certificate rejects them
 }
 
+// K x K block at p (row-major) into registers: 256-bit loads for K = 4 / 2 when
+// the data is 32-byte aligned
+template <int K>
+__device__ __forceinline__ void blktri_ld(const double* p, bool vec, Blk<K>& X, unsigned long long pol = 0) {
+  if constexpr (K == 4) {
+    if (vec) {
+      if (pol) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) ldg256h(p + 4 * u, pol, X.v[u][0], X.v[u][1], X.v[u][2], X.v[u][3]);
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) ldg256(p + 4 * u, X.v[u][0], X.v[u][1], X.v[u][2], X.v[u][3]);
+      }
+      return;
+    }
+  } else if constexpr (K == 2) {
+    if (vec) {
+      ldg256(p, X.v[0][0], X.v[0][1], X.v[1][0], X.v[1][1]);
+      return;
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < K; ++u)
+#pragma unroll
+    for (int v = 0; v < K; ++v) X.v[u][v] = __ldg(p + u * K + v);
+}
+
+// ---------------------------------------------------------------------------
+// body solver, block tridiagonal, TWO THREADS PER BODY (blktri_body_kernel):
+// exact given the separators.  The top thread eliminates block rows 0..m-1
+// top-down (block Thomas / LU without pivoting, src/localfact.cpp:84-100),
+//   D'_i = D_i - A_i G_{i-1},  G_i = D'_i^-1 C_i,  z_i = D'_i^-1 (f_i - A_i z_{i-1}),
+// the bottom thread block rows NB-1..m bottom-up (the mirror image, UL),
+//   D''_i = D_i - C_i H_{i+1}, H_i = D''_i^-1 A_i, w_i = D''_i^-1 (f_i - C_i w_{i+1});
+// they meet at rows m-1 / m: (I - G_{m-1} H_m) x_{m-1} = z_{m-1} - G_{m-1} w_m,
+// x_m = w_m - H_m x_{m-1}, and back-substitute outwards from the (G, z) / (H, w)
+// they parked in a global scratch (one 20-double record per block row, written
+// and read by the same thread moments apart: mostly L2).  Block rows arrive by
+// 256-bit loads (K = 4, aligned data) with an L2 prefetch 4 block rows ahead.
+// No shared memory beyond the 2 x 32 meeting records: every body of config 2
+// is in flight at once (2 threads x 16384 bodies), and there is no lane-level
+// reduced system at all.  The separator couplings of the first / last block
+// rows are folded into f.  CTA = 2 warps over 32 bodies: warp 0 the top
+// halves, warp 1 the bottom halves.
+// ---------------------------------------------------------------------------
+#ifndef PSG_BLKTRI_PREFETCH
+#define PSG_BLKTRI_PREFETCH 0
+#endif
+constexpr bool kBlktriPrefetch = PSG_BLKTRI_PREFETCH;
+template <int K, int H>
+__device__ __forceinline__ void blktri_half(const BlkArgs& g, double* scr, bool live, int seg, const GPart& Pt,
+                                            Blk<K>& Gm, Vec<K>& zm, double& rsum) {
+  constexpr int KK = K * K, SR = KK + K;
+  const long b = Pt.b;
+  const int NB = Pt.L / K, m = NB / 2;
+  const long B0 = b / K, NBall = g.n / K;
+  const bool vec = ((reinterpret_cast<uintptr_t>(g.data) | reinterpret_cast<uintptr_t>(g.f) |
+                     reinterpret_cast<uintptr_t>(scr)) & 31) == 0;
+  const int i0 = H == 0 ? 0 : NB - 1, cnt = H == 0 ? m : NB - m;
+  auto rowB = [&](int s) -> long { return B0 + (H == 0 ? i0 + s : i0 - s); };
+  auto prefetch = [&](int s) {
+    if (kBlktriPrefetch && live && s < cnt) {
+      const long B = rowB(s);
+      const char* p0 = reinterpret_cast<const char*>(g.data + (B == 0 ? 0 : (3 * B - 1) * KK));
+      for (int o = 0; o < 3 * KK * 8; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(p0 + o));
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < 4; ++s) prefetch(s);
+  pdl_wait();  // separator values from the separator kernel
+  Vec<K> xs;   // this half's outer separator (top: left, bottom: right)
+  const bool hs = live && (H == 0 ? Pt.ls >= 0 : Pt.rs >= 0);
+#pragma unroll
+  for (int u = 0; u < K; ++u) xs.v[u] = hs ? __ldg(g.xsep + (long)(H == 0 ? seg - 1 : seg) * K + u) : 0.0;
+  // L2: the rows stream through once (evict_first); the parked records come
+  // back within the same body sweep (evict_last: keep them out of DRAM)
+  const unsigned long long pin = l2_evict_first(), pkeep = l2_evict_last();
+  Blk<K> P;  // previous step's G (top) / H (bottom)
+  Vec<K> q;  // previous step's z / w
+  blk_set_zero<K>(P);
+#pragma unroll
+  for (int u = 0; u < K; ++u) q.v[u] = 0.0;
+#pragma unroll 1
+  for (int s = 0; s < (live ? cnt : 0); ++s) {
+    prefetch(s + 4);
+    const long B = rowB(s);
+    const double* p = g.data + (3 * B - 1) * KK;  // sub | diag | super (B >= 1 unless s == 0 at the top)
+    Blk<K> Fc, D, Nc;  // coupling to the previous step's row (F), toward the meeting point (N)
+    Vec<K> y;
+    const bool first = B == 0;  // block row 0 of the matrix: [diag | super] at 0
+    const double* pd = first ? g.data : p + KK;
+    blktri_ld<K>(pd, vec, D, pin);
+    const bool hasF = H == 0 ? B > 0 : B + 1 < NBall;  // the far coupling block exists
+    const bool hasN = H == 0 ? B + 1 < NBall : B > 0;
+    if (hasF) blktri_ld<K>(H == 0 ? p : p + 2 * KK, vec, Fc, pin); else blk_set_zero<K>(Fc);
+    if (hasN) blktri_ld<K>(H == 0 ? pd + KK : p, vec, Nc, pin); else blk_set_zero<K>(Nc);
+    if (K == 4 && vec) {
+      ldg256h(g.f + B * K, pin, y.v[0], y.v[1], y.v[2], y.v[3]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < K; ++u) y.v[u] = __ldg(g.f + B * K + u);
+    }
+    if (s == 0) {  // the outer separator's coupling to the rhs
+      if (hs) blk_mv_sub<K>(y, Fc, xs);
+    } else {
+      blk_mul_sub<K>(D, Fc, P);
+      blk_mv_sub<K>(y, Fc, q);
+    }
+    blk_inv<K>(D, &rsum);
+    P = blk_mul<K>(D, Nc);
+    q = blk_mv<K>(D, y);
+    if (s + 1 < cnt) {  // park (G, z) / (H, w) for the back-substitution
+      double* r = scr + B * SR;
+      if (K == 4 && vec) {  // 160-byte records, 32-byte aligned: five 256-bit stores
+#pragma unroll
+        for (int u = 0; u < K; ++u) stg256h(r + 4 * u, pkeep, P.v[u][0], P.v[u][1 % K], P.v[u][2 % K], P.v[u][3 % K]);
+        stg256h(r + KK, pkeep, q.v[0], q.v[1 % K], q.v[2 % K], q.v[3 % K]);
+      } else {
+#pragma unroll
+        for (int u = 0; u < K; ++u) {
+#pragma unroll
+          for (int v = 0; v < K; ++v) r[u * K + v] = P.v[u][v];
+          r[KK + u] = q.v[u];
+        }
+      }
+    }
+  }
+  Gm = P;
+  zm = q;
+}
+
+template <int K, int H>
+__device__ __forceinline__ void blktri_back(const BlkArgs& g, const double* scr, bool live, const GPart& Pt,
+                                            Vec<K> x, bool& finite) {
+  constexpr int KK = K * K, SR = KK + K;
+  const long b = Pt.b;
+  const int NB = Pt.L / K, m = NB / 2;
+  const long B0 = b / K;
+  const bool vec = ((reinterpret_cast<uintptr_t>(g.x) | reinterpret_cast<uintptr_t>(scr)) & 31) == 0;
+  const unsigned long long pgone = l2_evict_first();  // parked records: last use; x: streamed out
+  // x holds the meeting row's value (top: m-1, bottom: m); walk outwards
+  const int i0 = H == 0 ? m - 1 : m, cnt = H == 0 ? m : NB - m;
+#pragma unroll 1
+  for (int s = 0; s < (live ? cnt : 0); ++s) {
+    const long B = B0 + (H == 0 ? i0 - s : i0 + s);
+    if (s > 0) {
+      const double* r = scr + B * SR;
+      Blk<K> Pr;
+      Vec<K> y;
+      if (K == 4 && vec) {
+#pragma unroll
+        for (int u = 0; u < K; ++u) ldg256h(r + 4 * u, pgone, Pr.v[u][0], Pr.v[u][1 % K], Pr.v[u][2 % K], Pr.v[u][3 % K]);
+        ldg256h(r + KK, pgone, y.v[0], y.v[1 % K], y.v[2 % K], y.v[3 % K]);
+      } else {
+#pragma unroll
+        for (int u = 0; u < K; ++u) {
+          y.v[u] = r[KK + u];
+#pragma unroll
+          for (int v = 0; v < K; ++v) Pr.v[u][v] = r[u * K + v];
+        }
+      }
+      blk_mv_sub<K>(y, Pr, x);
+      x = y;
+    }
+#pragma unroll
+    for (int u = 0; u < K; ++u) finite &= isfinite(x.v[u]);
+    if (K == 4 && vec)
+      stg256h(g.x + B * K, pgone, x.v[0], x.v[1 % K], x.v[2 % K], x.v[3 % K]);
+    else
+#pragma unroll
+      for (int u = 0; u < K; ++u) g.x[B * K + u] = x.v[u];
+  }
+}
+
+template <int K>
+__global__ void __launch_bounds__(64) blktri_body_kernel(BlkArgs g, double* scr) {
+  constexpr int KK = K * K;
+  __shared__ double meet[32][KK + K];
+  const int tid = threadIdx.x, lane = tid & 31, h = tid >> 5;
+  const int seg = blockIdx.x * 32 + lane;
+  const bool live = seg < g.nseg;
+  const GPart Pt = g.part[live ? seg : g.nseg - 1];
+  pdl_trigger();  // the certificate kernel may launch (it waits for this grid)
+  double rsum = 0.0;
+  Blk<K> Gm;
+  Vec<K> zm;
+  if (h == 0)
+    blktri_half<K, 0>(g, scr, live, seg, Pt, Gm, zm, rsum);
+  else
+    blktri_half<K, 1>(g, scr, live, seg, Pt, Gm, zm, rsum);
+  if (h == 1) {  // (H_m, w_m) to the top thread
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+      meet[lane][KK + u] = zm.v[u];
+#pragma unroll
+      for (int v = 0; v < K; ++v) meet[lane][u * K + v] = Gm.v[u][v];
+    }
+  }
+  __syncthreads();
+  Vec<K> xm;
+  if (h == 0) {  // (I - G_{m-1} H_m) x_{m-1} = z_{m-1} - G_{m-1} w_m
+    Blk<K> Hm, M;
+    Vec<K> wm;
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+      wm.v[u] = meet[lane][KK + u];
+#pragma unroll
+      for (int v = 0; v < K; ++v) Hm.v[u][v] = meet[lane][u * K + v];
+    }
+    blk_set_eye<K>(M);
+    blk_mul_sub<K>(M, Gm, Hm);
+    blk_inv<K>(M, &rsum);
+    Vec<K> rhs = zm;
+    blk_mv_sub<K>(rhs, Gm, wm);
+    xm = blk_mv<K>(M, rhs);
+  }
+  __syncthreads();
+  if (h == 0)
+#pragma unroll
+    for (int u = 0; u < K; ++u) meet[lane][u] = xm.v[u];
+  __syncthreads();
+  if (h == 1) {  // x_m = w_m - H_m x_{m-1}
+    Vec<K> xt;
+#pragma unroll
+    for (int u = 0; u < K; ++u) xt.v[u] = meet[lane][u];
+    xm = zm;
+    blk_mv_sub<K>(xm, Gm, xt);
+  }
+  bool finite = true;
+  if (h == 0)
+    blktri_back<K, 0>(g, scr, live, Pt, xm, finite);
+  else
+    blktri_back<K, 1>(g, scr, live, Pt, xm, finite);
+  if (g.status && live) {
+    if (!isfinite(rsum)) status_pivot(g.status, seg);
+    if (!finite) status_nonfinite(g.status, seg);
+  }
+  if (!live) return;
+  const long B0 = Pt.b / K;
+  const int NB = Pt.L / K;
+  if (h == 1 && Pt.rs >= 0)
+#pragma unroll
+    for (int u = 0; u < K; ++u) g.x[Pt.rs + u] = __ldg(g.xsep + (long)seg * K + u);
+  // certificate records (blk_cert_kernel format): the separator block rows'
+  // couplings to this body's first (left) / last (right) block row
+  if (g.rec) {
+    double* rc = g.rec + (long)seg * 4 * K;
+    const bool has = h == 0 ? Pt.ls >= 0 : Pt.rs >= 0;
+    const long BB = h == 0 ? B0 : B0 + NB - 1;  // this body's boundary block row
+    Vec<K> y;
+#pragma unroll
+    for (int u = 0; u < K; ++u) y.v[u] = g.x[BB * K + u];  // written by this thread above
+    const double* cp = nullptr;
+    if (has) {
+      const long BS = h == 0 ? B0 - 1 : B0 + NB;  // the separator block row
+      cp = h == 0 ? g.data + (BS == 0 ? KK : (3 * BS - 1) * KK + 2 * KK) : g.data + (3 * BS - 1) * KK;
+    }
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+      double sg = 0.0, ab = 0.0;
+      if (has)
+#pragma unroll
+        for (int v = 0; v < K; ++v) {
+          const double pr = __ldg(cp + u * K + v) * y.v[v];
+          sg += pr;
+          ab += fabs(pr);
+        }
+      rc[(h == 0 ? 0 : 2 * K) + u] = sg;
+      rc[(h == 0 ? K : 3 * K) + u] = ab;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // speculative factor, block tridiagonal, ONE THREAD PER SEPARATOR SIDE with the
 // K x K algebra in registers (blktri_spec_kernel).  The side's HB block rows
@@ -1292,26 +1566,6 @@ __global__ void __launch_bounds__(128) blk_spec_fused_kernel(BlkSpecArgs g) {
 //   (A_SS - A_S,above X_above - C_S,below X_below) x_S = f_S - A_S,above z_above - C_S,below z_below.
 // CTA = 2 warps over 32 separators: warp 0 the sides above, warp 1 below.
 // ---------------------------------------------------------------------------
-template <int K>
-__device__ __forceinline__ void blktri_ld(const double* p, bool vec, Blk<K>& X) {
-  if constexpr (K == 4) {
-    if (vec) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u) ldg256(p + 4 * u, X.v[u][0], X.v[u][1], X.v[u][2], X.v[u][3]);
-      return;
-    }
-  } else if constexpr (K == 2) {
-    if (vec) {
-      ldg256(p, X.v[0][0], X.v[0][1], X.v[1][0], X.v[1][1]);
-      return;
-    }
-  }
-#pragma unroll
-  for (int u = 0; u < K; ++u)
-#pragma unroll
-    for (int v = 0; v < K; ++v) X.v[u][v] = __ldg(p + u * K + v);
-}
-
 template <int K, int HB, int H>
 __device__ __forceinline__ void blktri_side(const BlkSpecArgs& g, bool live, long BS, Blk<K>& T, Vec<K>& rr) {
   constexpr int KK = K * K;
@@ -1339,7 +1593,7 @@ __device__ __forceinline__ void blktri_side(const BlkSpecArgs& g, bool live, lon
   };
   // every block row of the side into L2 up front (the whole side is one wave of
   // a few threads per SM: the sweep then waits on L2, not HBM, per block row)
-  if (ok) {
+  if (ok && g.prefetch) {
 #pragma unroll 1
     for (int i = 0; i < HB; ++i) {
       const char* p0 = reinterpret_cast<const char*>(g.data + (3 * brow(i) - 1) * KK);

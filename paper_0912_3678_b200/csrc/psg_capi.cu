@@ -903,6 +903,15 @@ int band_max_rows() {
   }();
   return v;
 }
+// Block tridiagonal bodies: two threads per body (blktri_body_kernel) unless
+// PSG_BLK_BODY_NARROW=1 (the warp-per-body lane-chunk kernels).
+bool blktri_thread_bodies() {
+  static const bool v = [] {
+    const char* e = getenv("PSG_BLK_BODY_NARROW");
+    return !(e && atoi(e) > 0);
+  }();
+  return v;
+}
 bool band_scalar_enabled() {
   static const bool v = [] {
     const char* e = getenv("PSG_BAND_OLD");
@@ -917,7 +926,9 @@ bool band_scalar_enabled() {
 struct BlkSolver {
   int K = 0, layout = 0, NB = 0;
   bool band = false;  // scalar band kernels (band_kernels.cuh)
+  bool tbody = false; // block tridiagonal: two threads per body (blktri_body_kernel)
   int RB = 0;         // band: smem rows per array
+  DevBuf<double> scr; // tbody: the bodies' parked (G, z) records, (K^2 + K) per block row
   bool possible = false;
   BlkArgs base{};
   std::vector<GPart> hpart;
@@ -941,8 +952,11 @@ struct BlkSolver {
     }
     const int unit = layout == kBlkBlockTri ? K : 1, ku = K / unit;
     band = layout == kBlkBanded && band_scalar_enabled();
-    // longest body of one kernel, in block rows of K
-    const int maxnb = band ? band_max_rows() / K : blk_max_nb(K);
+    tbody = layout == kBlkBlockTri && blktri_thread_bodies();
+    // longest body of one kernel, in block rows of K (two-thread bodies: the
+    // reference plan's own bodies, not merged -- twice the threads in flight)
+    const int maxnb = band ? band_max_rows() / K : (tbody ? INT_MAX : blk_max_nb(K));
+    const int mergenb = tbody ? 0 : maxnb;
     hpart.clear();
     hsep.clear();
     int maxL = 0, minL = INT_MAX;
@@ -955,7 +969,7 @@ struct BlkSolver {
       if (!bodies.empty()) {
         auto& c = bodies.back();
         const int merged = c.second + K + L;
-        if ((merged + K - 1) / K <= maxnb) {
+        if ((merged + K - 1) / K <= mergenb) {
           c.second = merged;
           continue;
         }
@@ -993,6 +1007,9 @@ struct BlkSolver {
     if (band) {
       if (minL < 4 * K || maxL > band_max_rows()) return;
       RB = (maxL + 4) & ~1;
+    } else if (tbody) {
+      if (minL < 2 * K) return;
+      scr.alloc((size_t)(A.n / K) * (K * K + K) + 8);
     } else if (blk_shape(K, NB).M == 0) {
       return;
     }
@@ -1065,6 +1082,11 @@ struct BlkSolver {
     g.reset = st;
     for (int t = 0; t < 9; ++t) g.boff[t] = base.boff[t];
     g.data_len = base.data_len;
+    static const int spec_prefetch = [] {
+      const char* e = getenv("PSG_BLKTRI_SPEC_PREFETCH");  // measured: off 70 us, on 85 us (config 2)
+      return e ? atoi(e) : 0;
+    }();
+    g.prefetch = spec_prefetch;
     constexpr int NS = 1;  // separators per warp (2, chains interleaved: config 2 82 -> 123 us, config 3 217 -> 332 us)
     const int grid = (nsep + 4 * NS - 1) / (4 * NS);
     static const bool warp_spec = [] {  // PSG_BLK_SPEC_WARP=1: the round-1/2 warp-per-separator kernel
@@ -1098,9 +1120,18 @@ struct BlkSolver {
     a.xsep = xsep.p;
     a.rec = rec.p;
     a.status = st;
-    if (band)
+    if (band) {
       band_body_launch(a, s);
-    else if (!launch_blk_segments(K, NB, layout, a, s, /*pdl=*/true))
+    } else if (tbody) {
+      const dim3 grid((nseg + 31) / 32);
+      if (K == 4)
+        launch_pdl(blktri_body_kernel<4>, grid, dim3(64), 0, s, a, scr.p);
+      else if (K == 3)
+        launch_pdl(blktri_body_kernel<3>, grid, dim3(64), 0, s, a, scr.p);
+      else
+        launch_pdl(blktri_body_kernel<2>, grid, dim3(64), 0, s, a, scr.p);
+      LAUNCH_CHECK();
+    } else if (!launch_blk_segments(K, NB, layout, a, s, /*pdl=*/true))
       throw Fail{PSG_E_UNSUPPORTED_STRUCTURE, "block body too long"};
     const int cg = std::min(148 * 8, (nsep * K + 255) / 256);
     const double* Td = Tdiag.p;

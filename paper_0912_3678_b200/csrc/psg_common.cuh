@@ -168,6 +168,34 @@ __device__ __forceinline__ void ldg256(const double* p, double& a, double& b, do
   asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
 }
 
+// L2 eviction-priority policies (createpolicy) and the hinted 256-bit forms:
+// streamed-once data evict_first, a scratch written and read back soon evict_last
+__device__ __forceinline__ unsigned long long l2_evict_first() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ unsigned long long l2_evict_last() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void ldg256h(const double* p, unsigned long long pol, double& a, double& b, double& c,
+                                        double& d) {
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+      : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
+      : "l"(p), "l"(pol));
+}
+__device__ __forceinline__ void stg256h(double* p, unsigned long long pol, double a, double b, double c, double d) {
+  asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "d"(a), "d"(b), "d"(c),
+               "d"(d), "l"(pol)
+               : "memory");
+}
+
+__device__ __forceinline__ void stg256(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+
 // Reciprocal: MUFU approximation + two Newton steps (<= 1 ulp; no slow-path
 // branch).  0 -> inf and inf/NaN -> NaN propagate to the non-finite check.
 // Programmatic dependent launch (sm_90+): a kernel launched with the
