@@ -1102,7 +1102,6 @@ struct BlkSpecArgs {
   DevStatus* reset;  // the solve's status slot (reset by block 0)
   long boff[9];    // banded: A(row, row + d) = data[boff[d + K] + row]
   long data_len;   // entries in data (staging over-read bound)
-  int prefetch;    // blktri_spec_kernel: L2-prefetch each side before its sweep
 };
 
 // A(i, j) for the block kinds (0 outside the structure)
@@ -1316,17 +1315,14 @@ __device__ __forceinline__ void blktri_ld(const double* p, bool vec, Blk<K>& X, 
 // x_m = w_m - H_m x_{m-1}, and back-substitute outwards from the (G, z) / (H, w)
 // they parked in a global scratch (one 20-double record per block row, written
 // and read by the same thread moments apart: mostly L2).  Block rows arrive by
-// 256-bit loads (K = 4, aligned data) with an L2 prefetch 4 block rows ahead.
+// 256-bit loads (K = 4, aligned data; an L2 prefetch 4 block rows ahead or an
+// L1 prefetch of the next one measured no better or worse).
 // No shared memory beyond the 2 x 32 meeting records: every body of config 2
 // is in flight at once (2 threads x 16384 bodies), and there is no lane-level
 // reduced system at all.  The separator couplings of the first / last block
 // rows are folded into f.  CTA = 2 warps over 32 bodies: warp 0 the top
 // halves, warp 1 the bottom halves.
 // ---------------------------------------------------------------------------
-#ifndef PSG_BLKTRI_PREFETCH
-#define PSG_BLKTRI_PREFETCH 0
-#endif
-constexpr bool kBlktriPrefetch = PSG_BLKTRI_PREFETCH;
 template <int K, int H>
 __device__ __forceinline__ void blktri_half(const BlkArgs& g, double* scr, bool live, int seg, const GPart& Pt,
                                             Blk<K>& Gm, Vec<K>& zm, double& rsum) {
@@ -1338,15 +1334,6 @@ __device__ __forceinline__ void blktri_half(const BlkArgs& g, double* scr, bool 
                      reinterpret_cast<uintptr_t>(scr)) & 31) == 0;
   const int i0 = H == 0 ? 0 : NB - 1, cnt = H == 0 ? m : NB - m;
   auto rowB = [&](int s) -> long { return B0 + (H == 0 ? i0 + s : i0 - s); };
-  auto prefetch = [&](int s) {
-    if (kBlktriPrefetch && live && s < cnt) {
-      const long B = rowB(s);
-      const char* p0 = reinterpret_cast<const char*>(g.data + (B == 0 ? 0 : (3 * B - 1) * KK));
-      for (int o = 0; o < 3 * KK * 8; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(p0 + o));
-    }
-  };
-#pragma unroll
-  for (int s = 0; s < 4; ++s) prefetch(s);
   pdl_wait();  // separator values from the separator kernel
   Vec<K> xs;   // this half's outer separator (top: left, bottom: right)
   const bool hs = live && (H == 0 ? Pt.ls >= 0 : Pt.rs >= 0);
@@ -1362,7 +1349,6 @@ __device__ __forceinline__ void blktri_half(const BlkArgs& g, double* scr, bool 
   for (int u = 0; u < K; ++u) q.v[u] = 0.0;
 #pragma unroll 1
   for (int s = 0; s < (live ? cnt : 0); ++s) {
-    prefetch(s + 4);
     const long B = rowB(s);
     const double* p = g.data + (3 * B - 1) * KK;  // sub | diag | super (B >= 1 unless s == 0 at the top)
     Blk<K> Fc, D, Nc;  // coupling to the previous step's row (F), toward the meeting point (N)
@@ -1557,8 +1543,7 @@ __global__ void __launch_bounds__(64) blktri_body_kernel(BlkArgs g, double* scr)
 // stream straight from memory, one block row per step; K = 4 / 2 block
 // rows are 128 / 32-byte multiples, read by 256-bit loads (one sector per
 // request: the lanes of a warp walk different bodies, so the requests do not
-// coalesce and the sector count is what the L1 pays for), after an L2 prefetch
-// of the whole side.  Far -> near block
+// coalesce and the sector count is what the L1 pays for).  Far -> near block
 // elimination (src/localfact.cpp:84-100 order):
 //   D'_i = D_i - F_i X_{i-1},  X_i = D'_i^-1 N_i,  z_i = D'_i^-1 (f_i - F_i z_{i-1})
 // with F the coupling away from the separator, N toward it; the near block row
@@ -1591,15 +1576,6 @@ __device__ __forceinline__ void blktri_side(const BlkSpecArgs& g, bool live, lon
       for (int u = 0; u < K; ++u) R.f.v[u] = __ldg(g.f + B * K + u);
     }
   };
-  // every block row of the side into L2 up front (the whole side is one wave of
-  // a few threads per SM: the sweep then waits on L2, not HBM, per block row)
-  if (ok && g.prefetch) {
-#pragma unroll 1
-    for (int i = 0; i < HB; ++i) {
-      const char* p0 = reinterpret_cast<const char*>(g.data + (3 * brow(i) - 1) * KK);
-      for (int o = 0; o < 3 * KK * 8; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(p0 + o));
-    }
-  }
   Row cur;
   Blk<K> X;
   Vec<K> z;

@@ -1082,11 +1082,6 @@ struct BlkSolver {
     g.reset = st;
     for (int t = 0; t < 9; ++t) g.boff[t] = base.boff[t];
     g.data_len = base.data_len;
-    static const int spec_prefetch = [] {
-      const char* e = getenv("PSG_BLKTRI_SPEC_PREFETCH");  // measured: off 70 us, on 85 us (config 2)
-      return e ? atoi(e) : 0;
-    }();
-    g.prefetch = spec_prefetch;
     constexpr int NS = 1;  // separators per warp (2, chains interleaved: config 2 82 -> 123 us, config 3 217 -> 332 us)
     const int grid = (nsep + 4 * NS - 1) / (4 * NS);
     static const bool warp_spec = [] {  // PSG_BLK_SPEC_WARP=1: the round-1/2 warp-per-separator kernel
