@@ -7,7 +7,7 @@
 set -u
 cd "$(dirname "$0")/.."
 O=gpurun_out
-TAG=${TAG:-r02}
+export TAG=${TAG:-r02}
 mkdir -p $O
 Q=${1:-}
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > $O/gpu.txt 2>&1
@@ -27,12 +27,12 @@ python - <<'PY'
 import sys
 sys.path.insert(0, "tools")
 from summarize_ncu import launch_list
-launch_list("gpurun_out/_l1.csv", "gpurun_out/r02_launches.txt",
+launch_list("gpurun_out/_l1.csv", f"gpurun_out/{__import__('os').environ.get('TAG', 'r02')}_launches.txt",
             "ncu --metrics gpu__time_duration.sum --clock-control none python bench.py --steps 2 --warmup 3 "
             "--no-e2e --no-cpu-baseline --no-other-configs")
 PY
 declare -A KER=([0]="tri_spec_fused|tri_segment_solve|tri_cert" [1]="tri_spec_fused|tri_segment_solve|tri_cert"
-                [2]="blk_spec_fused|blk_body_narrow|blk_segment|blk_cert" [3]="blk_spec_fused|blk_body_narrow|blk_segment|blk_cert"
+                [2]="blktri_spec|blktri_body|blk_cert" [3]="band_spec|band_body|blk_cert"
                 [4]="chain_")
 declare -A CNT=([0]=3 [1]=3 [2]=3 [3]=3 [4]=5)
 for c in 0 1 2 3 4; do
@@ -44,7 +44,7 @@ import sys
 sys.path.insert(0, "tools")
 from summarize_ncu import launch_list
 c = sys.argv[1]
-launch_list("gpurun_out/_l.csv", f"gpurun_out/r02_launches_cfg{c}.txt",
+launch_list("gpurun_out/_l.csv", f"gpurun_out/{__import__('os').environ.get('TAG', 'r02')}_launches_cfg{c}.txt",
             f"ncu --metrics gpu__time_duration.sum --clock-control none python tools/cfg_step.py {c} 3")
 PY
   # the second step's kernels (the first one builds plans and warms caches)
