@@ -167,13 +167,14 @@ __global__ void __launch_bounds__(32) band_body_kernel(BlkArgs g, int RB) {
   const int sS = bl - K;                                      // S_t start (lane 0: -K, the left separator)
   double rsum = 0.0;
 
-  // ---- forward sweep: no-pivot band LU carrying v = [f | spike of S_t];
-  //      row i stores: diag slot 1/u_ii, super slots u_i,i+k, sub slots spike, f slot g
+  // ---- forward sweep: no-pivot band LU carrying v = [f | spike of S_t]; the
+  //      eliminated row is stored NORMALISED (divided by its pivot: no
+  //      reciprocal to keep) in place of its staged entries: super slots
+  //      u'_i,i+k, sub slots spike', f slot g'.  7 values per row (K = 3).
   {
-    double wr[K], wu[K][K], wv[K][K + 1];  // window: [0] = row i-1, ..., [K-1] = row i-K
+    double wu[K][K], wv[K][K + 1];  // window of normalised rows: [0] = row i-1, ..., [K-1] = row i-K
 #pragma unroll
     for (int w = 0; w < K; ++w) {
-      wr[w] = 0.0;
 #pragma unroll
       for (int k = 0; k < K; ++k) wu[w][k] = 0.0;
 #pragma unroll
@@ -196,9 +197,9 @@ __global__ void __launch_bounds__(32) band_body_kernel(BlkArgs g, int RB) {
           }
       }
 #pragma unroll
-      for (int c = -K; c < 0; ++c) {
+      for (int c = -K; c < 0; ++c) {  // the multiplier is the entry itself (rows normalised)
         const int w = -c - 1;
-        const double l = e[c + K] * wr[w];
+        const double l = e[c + K];
 #pragma unroll
         for (int k = 1; k <= K; ++k)
           if (c + k <= K) e[c + k + K] = fma(-l, wu[w][k - 1], e[c + k + K]);
@@ -207,25 +208,22 @@ __global__ void __launch_bounds__(32) band_body_kernel(BlkArgs g, int RB) {
       }
       const double r = fast_rcp(e[K]);
       rsum += fabs(r);
-      S(K, i) = r;
-#pragma unroll
-      for (int k = 1; k <= K; ++k) S(K + k, i) = e[K + k];
-#pragma unroll
-      for (int q = 1; q <= K; ++q) S(q - 1, i) = v[q];
-      S(FA, i) = v[0];
 #pragma unroll
       for (int w = K - 1; w > 0; --w) {
-        wr[w] = wr[w - 1];
 #pragma unroll
         for (int k = 0; k < K; ++k) wu[w][k] = wu[w - 1][k];
 #pragma unroll
         for (int q = 0; q <= K; ++q) wv[w][q] = wv[w - 1][q];
       }
-      wr[0] = r;
 #pragma unroll
-      for (int k = 0; k < K; ++k) wu[0][k] = e[K + 1 + k];
+      for (int k = 0; k < K; ++k) wu[0][k] = e[K + 1 + k] * r;
 #pragma unroll
-      for (int q = 0; q <= K; ++q) wv[0][q] = v[q];
+      for (int q = 0; q <= K; ++q) wv[0][q] = v[q] * r;
+#pragma unroll
+      for (int k = 1; k <= K; ++k) S(K + k, i) = wu[0][k - 1];
+#pragma unroll
+      for (int q = 1; q <= K; ++q) S(q - 1, i) = wv[0][q];
+      S(FA, i) = wv[0][0];
     };
     if (act) {
       double cur[NA], nxt[NA];
@@ -249,37 +247,40 @@ __global__ void __launch_bounds__(32) band_body_kernel(BlkArgs g, int RB) {
       }
     }
   }
-  // ---- backward sweep: every sub-body row as x_i = c + P X_{S_t} + Q X_{S_{t+1}};
-  //      row i stores: f slot c, sub slots P, super slots Q
-  {
-    double wx[K][C];  // [0] = row i+1, ...
-    // in[]: row i's stored forward results (slots as staged), loaded one row ahead
-    auto step = [&](int i, int mpeel, const double (&in)[NA]) {  // mpeel: rows below i in the sub-body when < K
-      const double r = in[K];
-      double u[K + 1], x[C];
+  // normalised row i: u' (K), then [g' | spike' (K)]
+  auto ldrow = [&](double (&f)[2 * K + 1], int i) {
 #pragma unroll
-      for (int k = 1; k <= K; ++k) u[k] = in[K + k];
-      x[0] = in[FA];
+    for (int k = 1; k <= K; ++k) f[k - 1] = S(K + k, i);
+    f[K] = S(FA, i);
 #pragma unroll
-      for (int q = 1; q <= K; ++q) x[q] = in[q - 1];
+    for (int q = 1; q <= K; ++q) f[K + q] = S(q - 1, i);
+  };
+  // ---- backward sweep 1, in registers only: the affine forms
+  //      x_i = c + P X_{S_t} + Q X_{S_{t+1}} of the rows the lane-level reduced
+  //      system needs -- the K lowest (bot[m] = row hi-1-m, from the first K
+  //      steps) and the K highest (wx[w] = row bl + w, what the window holds at
+  //      the end).  Nothing is stored: backward sweep 2 recomputes x from the
+  //      normalised rows once X is known (7 loads and 1 store per row instead
+  //      of 7 stores and 7 loads of forms).
+  double wx[K][C], bot[K][C];  // wx: [0] = row i+1, ...
+  if (act) {
+    auto step = [&](int mpeel, const double (&in)[2 * K + 1]) {  // mpeel: rows below i in the sub-body when < K
+      double x[C];
+      x[0] = in[K];
+#pragma unroll
+      for (int q = 1; q <= K; ++q) x[q] = in[K + q];
 #pragma unroll
       for (int q = K + 1; q < C; ++q) x[q] = 0.0;
 #pragma unroll
       for (int k = 1; k <= K; ++k) {
+        const double u = in[k - 1];
         if (mpeel < 0 || k <= mpeel) {
 #pragma unroll
-          for (int q = 0; q < C; ++q) x[q] = fma(-u[k], wx[k - 1][q], x[q]);
+          for (int q = 0; q < C; ++q) x[q] = fma(-u, wx[k - 1][q], x[q]);
         } else {  // row i + k = hi + (k - 1 - mpeel): row k - 1 - mpeel of S_{t+1}
-          x[K + 1 + (k - 1 - mpeel)] -= u[k];
+          x[K + 1 + (k - 1 - mpeel)] -= u;
         }
       }
-#pragma unroll
-      for (int q = 0; q < C; ++q) x[q] *= r;
-      S(FA, i) = x[0];
-#pragma unroll
-      for (int q = 1; q <= K; ++q) S(q - 1, i) = x[q];
-#pragma unroll
-      for (int q = 1; q <= K; ++q) S(K + q, i) = x[K + q];
 #pragma unroll
       for (int w = K - 1; w > 0; --w)
 #pragma unroll
@@ -287,29 +288,36 @@ __global__ void __launch_bounds__(32) band_body_kernel(BlkArgs g, int RB) {
 #pragma unroll
       for (int q = 0; q < C; ++q) wx[0][q] = x[q];
     };
-    if (act) {
-      double cur[NA], nxt[NA];
+    double cur[2 * K + 1], nxt[2 * K + 1];
+    ldrow(cur, hi - 1);
 #pragma unroll
-      for (int a = 0; a < NA; ++a) cur[a] = S(a, hi - 1);
+    for (int m = 0; m < K; ++m) {
+      ldrow(nxt, hi - 2 - m);
+      step(m, cur);
 #pragma unroll
-      for (int m = 0; m < K; ++m) {
+      for (int q = 0; q < C; ++q) bot[m][q] = wx[0][q];
 #pragma unroll
-        for (int a = 0; a < NA; ++a) nxt[a] = S(a, hi - 2 - m);
-        step(hi - 1 - m, m, cur);
-#pragma unroll
-        for (int a = 0; a < NA; ++a) cur[a] = nxt[a];
-      }
-#pragma unroll (K)
-      for (int i = hi - 1 - K; i >= bl; --i) {  // row bl - 1 is read ahead (inside the region; unused); unrolled by K
-#pragma unroll
-        for (int a = 0; a < NA; ++a) nxt[a] = S(a, i - 1);
-        step(i, -1, cur);
-#pragma unroll
-        for (int a = 0; a < NA; ++a) cur[a] = nxt[a];
-      }
+      for (int a = 0; a < 2 * K + 1; ++a) cur[a] = nxt[a];
     }
+#pragma unroll (K)
+    for (int i = hi - 1 - K; i >= bl; --i) {  // row bl - 1 is read ahead (inside the region; unused); unrolled by K
+      ldrow(nxt, i - 1);
+      step(-1, cur);
+#pragma unroll
+      for (int a = 0; a < 2 * K + 1; ++a) cur[a] = nxt[a];
+    }
+  } else {
+#pragma unroll
+    for (int w = 0; w < K; ++w)
+#pragma unroll
+      for (int q = 0; q < C; ++q) wx[w][q] = bot[w][q] = 0.0;
   }
-  __syncwarp();
+  // the previous lane's lowest forms (rows sS-1-m)
+  double pbot[K][C];
+#pragma unroll
+  for (int m = 0; m < K; ++m)
+#pragma unroll
+    for (int q = 0; q < C; ++q) pbot[m][q] = __shfl_sync(FULL, bot[m][q], lane > 0 ? lane - 1 : 0);
 
   // ---- lane-level reduced system: the K rows of S_t,
   //      Ab X_{S_{t-1}} + Bb X_{S_t} + Cb X_{S_{t+1}} = Fv
@@ -331,15 +339,15 @@ __global__ void __launch_bounds__(32) band_body_kernel(BlkArgs g, int RB) {
 #pragma unroll
       for (int c = -K; c <= K; ++c) {
         const double a = S(c + K, rho);
-        const int j = rho + c;
         if (u + c >= 0 && u + c < K) {
           Bb.v[u][u + c] += a;
         } else {  // a sub-body row: the previous lane's (P: S_{t-1}, Q: S_t) or ours (P: S_t, Q: S_{t+1})
           const bool prev = u + c < 0;
-          fv = fma(-a, S(FA, j), fv);
+          const double* fm = prev ? pbot[-(u + c) - 1] : wx[u + c - K];  // compile-time indices
+          fv = fma(-a, fm[0], fv);
 #pragma unroll
           for (int v = 0; v < K; ++v) {
-            const double P = S(v, j), Q = S(K + 1 + v, j);
+            const double P = fm[1 + v], Q = fm[1 + K + v];
             if (prev) {
               Ab.v[u][v] = fma(a, P, Ab.v[u][v]);
               Bb.v[u][v] = fma(a, Q, Bb.v[u][v]);
@@ -357,18 +365,14 @@ __global__ void __launch_bounds__(32) band_body_kernel(BlkArgs g, int RB) {
       blk_set_zero<K>(Cb);
     }
   }
-  __syncwarp();  // the neighbours' forms are read; the final pass overwrites them
-  // ---- normalise and block PCR across the lanes (al = B^-1 A, ga = B^-1 C, de = B^-1 F)
-  //      The rows are block diagonally dominant for the bodies this path
-  //      certifies, so the couplings shrink geometrically with every step;
-  //      once every |al|, |ga| entry is below 2^-64 the remaining couplings
-  //      change X by less than 1e-19 relative and the system is taken as
-  //      decoupled (deterministic; a non-dominant body runs all the steps).
+  // ---- normalise and solve the lane-level system (al = B^-1 A, ga = B^-1 C,
+  //      de = B^-1 F).  It is block diagonally dominant for the bodies this
+  //      path certifies: strongly decoupled rows take block Jacobi sweeps
+  //      (blk_jacobi: config 3 kappa ~ 1e-7, 2 sweeps), otherwise block PCR,
+  //      left once every coupling is below 2^-64 (X changes by < 1e-19 relative).
   blk_inv_short<K>(Bb, &rsum);
   Blk<K> al = blk_mul<K>(Bb, Ab), ga = blk_mul<K>(Bb, Cb);
   Vec<K> de = blk_mv<K>(Bb, Fv);
-  //      Strongly decoupled rows (the common case) take block Jacobi sweeps
-  //      instead (blk_jacobi: config 3 kappa ~ 1e-7, 2 sweeps).
   constexpr double kDecoupled = 5.421010862427522e-20;  // 2^-64
   const bool jacobi = blk_jacobi<K>(al, ga, de, lane, 32);
 #pragma unroll 1
@@ -408,44 +412,37 @@ __global__ void __launch_bounds__(32) band_body_kernel(BlkArgs g, int RB) {
     blk_neg<K>(ga);
     de = blk_mv<K>(nb, nd);
   }
-  // ---- x = c + P X_t + Q X_{t+1} over the sub-body; S_t rows get X_t
+  // ---- backward sweep 2: x_i = g'_i + spike'_i . X_t - sum_k u'_ik x_{i+k}
+  //      (x_{i+k} of rows >= hi: X_{t+1}) over the sub-body, in place of g';
+  //      the S_t rows get X_t
   Vec<K> Xn = vec_shfl<K>(de, lane < 31 ? lane + 1 : lane);
   if (lane == NL - 1) Xn = xrv;
   bool finite = true;
   if (act) {
-    // independent rows, RU at a time: all loads of the group before its stores
-    // (the stores may alias later loads, so the compiler would not hoist them),
-    // x as a two-level sum (short dependency chain)
-    constexpr int RU = 4;
-    auto ld = [&](double (&f)[C], int i) {
-      f[0] = S(FA, i);
+    double xw[K];  // [0] = x_{i+1}, ...
 #pragma unroll
-      for (int v = 0; v < K; ++v) {
-        f[1 + v] = S(v, i);
-        f[1 + K + v] = S(K + 1 + v, i);
-      }
+    for (int k = 0; k < K; ++k) xw[k] = Xn.v[k];  // rows hi.. hi+K-1 (for the last rows of the sub-body)
+    // the window starts at row hi: x_{hi + k} = Xn[k]; shift it so that xw[k] = x_{i+1+k}
+    double cur[2 * K + 1], nxt[2 * K + 1];
+    ldrow(cur, hi - 1);
+    auto step = [&](int i, const double (&in)[2 * K + 1]) {
+      double x = in[K];
+#pragma unroll
+      for (int q = 0; q < K; ++q) x = fma(in[K + 1 + q], de.v[q], x);
+#pragma unroll
+      for (int k = K; k >= 1; --k) x = fma(-in[k - 1], xw[k - 1], x);  // x_{i+1} last: shortest chain
+      finite &= isfinite(x);
+      S(FA, i) = x;
+#pragma unroll
+      for (int k = K - 1; k > 0; --k) xw[k] = xw[k - 1];
+      xw[0] = x;
     };
-#pragma unroll 1
-    for (int i0 = bl; i0 < hi; i0 += RU) {
-      double fr[RU][C];
+#pragma unroll (K)
+    for (int i = hi - 1; i >= bl; --i) {
+      ldrow(nxt, i - 1);
+      step(i, cur);
 #pragma unroll
-      for (int u = 0; u < RU; ++u) ld(fr[u], i0 + u < hi ? i0 + u : hi - 1);
-#pragma unroll
-      for (int u = 0; u < RU; ++u) {
-        double p = fr[u][1] * de.v[0], q = fr[u][1 + K] * Xn.v[0];
-#pragma unroll
-        for (int v = 1; v < K; ++v) {
-          p = fma(fr[u][1 + v], de.v[v], p);
-          q = fma(fr[u][1 + K + v], Xn.v[v], q);
-        }
-        fr[u][0] += p + q;
-      }
-#pragma unroll
-      for (int u = 0; u < RU; ++u)
-        if (i0 + u < hi) {
-          finite &= isfinite(fr[u][0]);
-          S(FA, i0 + u) = fr[u][0];
-        }
+      for (int a = 0; a < 2 * K + 1; ++a) cur[a] = nxt[a];
     }
     if (lane > 0)
 #pragma unroll
