@@ -1561,15 +1561,20 @@ __device__ __forceinline__ void blktri_side(const BlkSpecArgs& g, bool live, lon
   const bool vec = ((reinterpret_cast<uintptr_t>(g.data) | reinterpret_cast<uintptr_t>(g.f)) & 31) == 0;
   // block row Bi of step i (far -> near): H = 0: BS - HB + i, H = 1: BS + HB - i
   auto brow = [&](int i) -> long { return H == 0 ? BS - HB + i : BS + HB - i; };
-  const bool ok = live && BS - HB >= 1 && BS + HB + 1 < NBall;  // interior (the host guarantees it)
+  const bool ok = live && BS - HB >= 0 && BS + HB < NBall;  // the window inside the matrix
   struct Row {
     Blk<K> F, D, N;
     Vec<K> f;
   };
   auto load = [&](int i, Row& R) {
     const long B = ok ? brow(i) : 1;
-    const double* p = g.data + (3 * B - 1) * KK;  // sub | diag | super
-    blktri_ld<K>(p + (H == 0 ? 0 : 2 * KK), vec, R.F);
+    const double* p = g.data + (3 * B - 1) * KK;  // sub | diag | super (block row 0: diag | super at 0)
+    // the far coupling of the farthest block row is dropped by the truncation
+    // (and absent at the matrix ends): not read
+    if (i > 0)
+      blktri_ld<K>(p + (H == 0 ? 0 : 2 * KK), vec, R.F);
+    else
+      blk_set_zero<K>(R.F);
     blktri_ld<K>(p + KK, vec, R.D);
     blktri_ld<K>(p + (H == 0 ? 2 * KK : 0), vec, R.N);
     if (K == 4 && vec) {
