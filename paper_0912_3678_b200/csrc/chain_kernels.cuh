@@ -490,6 +490,440 @@ __global__ void __launch_bounds__(128) chain_fc_kernel(ChainLevelArgs g, ChainTr
 }
 
 // ---------------------------------------------------------------------------
+// chain_fc2_kernel (m = 8): chain_fc_kernel with TWO rows per lane -- MB / 2
+// lanes per block, lane i = rows i and i + MB/2 of every block and columns i
+// and i + MB/2 of Phi.  Same arithmetic, element by element, as
+// chain_fc_kernel (bit-identical results).  The row-per-lane kernel is bound
+// by the shared-memory data pipe (profiles/r02_ncu_full_cfg4.txt: 15 M load +
+// 10 M store wavefronts, MIO throttle the first stall); what changes:
+//  * the pivot row reaches the other lanes of its subgroup by shuffles (one
+//    LSU wavefront each; the shared-memory broadcast cost ~4.5 wavefronts per
+//    sparse 16-byte store plus the read-back, a divergent publish and a
+//    __syncwarp per pivot), and it serves two rows per lane;
+//  * the read-back of T_b for the composition serves two columns per lane;
+//  * two shared regions with their own pitch per subgroup (rows: 64 bytes mod
+//    128, T_b: 16 bytes mod 128), so neither the row reads nor the broadcast
+//    reads of the 8 subgroups of a warp conflict;
+//  * f one block ahead in registers, the next pivot's reciprocal started by
+//    every lane as soon as its column is updated;
+//  * CTAs of 16 chunks (one level-1 chunk, 2 warps): 1024 small CTAs balance
+//    over the SMs where 512 large ones left a 30 % tail.
+// Measured (config 4): 161 -> 122 us.  Not kept: the block by
+// COLUMNS (pivot column = 8 values per pivot instead of 17, no swizzle, bulk
+// copies: 15 M instead of 20 M wavefronts but 38 M instead of 31 M
+// instructions and f / phi replicated: 155 us), rows by 128-byte bulk copies
+// at a 144-byte pitch (183 us: the small copies and the mbarrier polls), one
+// stage buffer for 6 CTAs per SM (126 us) or 7 with 128 registers (129 us:
+// the SM's shared-memory pipe, not its occupancy, sets the pace; 4 CTAs per SM
+// also spread the 1024 CTAs more evenly).
+// ---------------------------------------------------------------------------
+template <int MB>
+struct Fc2Cfg {
+  static constexpr int LPB = MB / 2;                                  // lanes per block (chunk)
+  static constexpr int SG = 32 / LPB;                                 // subgroups (chunks) per warp
+  static constexpr int NW = kChainC0 / SG;                            // warps per CTA: 16 chunks = one level-1 chunk
+  static constexpr int CPC = NW * SG;                                 // level-0 chunks per CTA
+  static constexpr int L1C = CPC / kChainC0;                          // level-1 chunks per CTA
+  static constexpr int BLK = 2 * MB * MB;                             // [S | R] doubles per block row
+  static constexpr int TP = MB + 2;                                   // row pitch of the published T_b
+  static constexpr int TBS = MB * TP + MB;                            // published T_b + phi
+  static constexpr int STG = ((2 * BLK + 15) / 16) * 16 + 8;          // stage pitch: 64 bytes mod 128
+  static constexpr int SUB = ((TBS + 15) / 16) * 16 + 2;              // T_b pitch: 16 bytes mod 128
+  static constexpr int NSUB = NW * SG;
+  static constexpr int SMEM = NSUB * (STG + SUB) * 8;                 // bytes per CTA
+};
+
+// fc_tree16 for two columns per lane (pa: column i, pb: column i + MB/2)
+template <int MB, bool VEC>
+__device__ __forceinline__ void fc2_tree16(double* fsm, int gsub, int i, double (&pa)[MB], double (&pb)[MB],
+                                           double (&ph)[MB]) {
+  using C = Fc2Cfg<MB>;
+  constexpr int H = C::LPB;
+  const int s = gsub % kChainC0;
+#pragma unroll 1
+  for (int h = 1; h < kChainC0; h <<= 1) {
+    double* mine = fsm + C::NSUB * C::STG + gsub * C::SUB;  // TB region: MB x TP, then MB for phi
+    if (s % (2 * h) == h) {  // later partner of (s - h): publish
+#pragma unroll
+      for (int r = 0; r < MB; ++r) {
+        mine[r * C::TP + i] = pa[r];
+        mine[r * C::TP + i + H] = pb[r];
+      }
+      if (VEC) {
+        mine[MB * C::TP + i] = pick<MB>(ph, i);
+        mine[MB * C::TP + i + H] = pick<MB>(ph, i + H);
+      }
+    }
+    __syncthreads();
+    if (s % (2 * h) == 0) {
+      const double* L = fsm + C::NSUB * C::STG + (gsub + h) * C::SUB;
+      double na[MB], nb[MB], nv[MB];
+#pragma unroll
+      for (int r = 0; r < MB; ++r) {
+        double a = 0.0, b = 0.0, v = VEC ? L[MB * C::TP + r] : 0.0;
+#pragma unroll
+        for (int c = 0; c < MB; c += 2) {
+          const double2 m = *reinterpret_cast<const double2*>(L + r * C::TP + c);
+          a = fma(m.y, pa[c + 1], fma(m.x, pa[c], a));
+          b = fma(m.y, pb[c + 1], fma(m.x, pb[c], b));
+          if (VEC) v = fma(m.y, ph[c + 1], fma(m.x, ph[c], v));
+        }
+        na[r] = a;
+        nb[r] = b;
+        nv[r] = v;
+      }
+#pragma unroll
+      for (int r = 0; r < MB; ++r) {
+        pa[r] = na[r];
+        pb[r] = nb[r];
+        if (VEC) ph[r] = nv[r];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// chain_fc_top for the two-columns-per-lane layout (lanes 0..MB/2-1 of warp 0)
+template <int MB>
+__device__ void chain_fc2_top(const ChainLevelArgs& g, const ChainTree& t, double* buf, int lane, const double (&pa)[MB],
+                              const double (&pb)[MB]) {
+  constexpr int MM = MB * MB, GP = MB + 1, H = MB / 2;
+  if (lane < H) {
+#pragma unroll
+    for (int r = 0; r < MB; ++r) {
+      double va = __ldg(g.data + r * MB + lane), vb = __ldg(g.data + r * MB + lane + H);
+#pragma unroll
+      for (int l = 0; l < MB; ++l) {
+        const double bb = __ldg(g.corner + r * MB + l);
+        va = fma(bb, pa[l], va);
+        vb = fma(bb, pb[l], vb);
+      }
+      buf[r * GP + lane] = va;
+      buf[r * GP + lane + H] = vb;
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    double* G = buf;
+    for (int k = 0; k < MB; ++k) {
+      int p = k;
+      for (int r = k + 1; r < MB; ++r)
+        if (fabs(G[r * GP + k]) > fabs(G[p * GP + k])) p = r;
+      if (p != k)
+        for (int c = 0; c < MB; ++c) {
+          const double tmp = G[k * GP + c];
+          G[k * GP + c] = G[p * GP + c];
+          G[p * GP + c] = tmp;
+        }
+      t.glu[MM + k] = (double)p;
+      for (int r = k + 1; r < MB; ++r) {
+        const double l = G[r * GP + k] / G[k * GP + k];
+        G[r * GP + k] = l;
+        for (int c = k + 1; c < MB; ++c) G[r * GP + c] = fma(-l, G[k * GP + c], G[r * GP + c]);
+      }
+    }
+    for (int e = 0; e < MM; ++e) t.glu[e] = G[(e / MB) * GP + e % MB];
+  }
+  __syncwarp();
+}
+
+template <int MB, bool STORE_T, bool WITH_F>
+__global__ void __launch_bounds__(Fc2Cfg<MB>::NW * 32) chain_fc2_kernel(ChainLevelArgs g, ChainTree t) {
+  pdl_trigger();  // the down sweep may launch (it waits for this grid before reading anything)
+  using C = Fc2Cfg<MB>;
+  constexpr int MM = MB * MB, RW = 2 * MB, H = C::LPB, NP = RW / 2;  // NP 16-byte pieces per row
+  extern __shared__ __align__(16) double fsm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, sg = lane / H, i = lane % H;
+  double* stage = fsm + (wid * C::SG + sg) * C::STG;                     // 2 x BLK
+  double* TB = fsm + C::NSUB * C::STG + (wid * C::SG + sg) * C::SUB;    // MB x TP published T_b, then phi
+  const long P0 = t.P[0];
+  const long j = (long)blockIdx.x * C::CPC + wid * C::SG + sg;  // level-0 chunk
+  const bool live = j < P0;
+  const long nblk = (long)g.nb - 1;                             // blocks after the BC row
+  const int len = live ? (int)min((long)kChainC0, nblk - kChainC0 * j) : 0;
+  const long b0 = kChainC0 * j + 1;                             // first block row of the chunk
+  // block row b0 + tt into stage buffer tt & 1: 16-byte cp.async pieces, piece
+  // c of row q at c ^ q (lane i then reads its rows conflict-free)
+  auto issue = [&](int tt) {
+    if (tt < len) {
+      const double* src = g.data + MM + (b0 + tt - 1) * C::BLK;
+      double* dst = stage + (tt & 1) * C::BLK;
+#pragma unroll
+      for (int q = 0; q < MB; ++q)
+#pragma unroll
+        for (int hh = 0; hh < NP / H; ++hh) {
+          const int c = hh * H + i;
+          cp_async16(dst + q * RW + 2 * (c ^ q), src + q * RW + 2 * c);
+        }
+    }
+    cp_async_commit();
+  };
+  double pa[MB], pq[MB], ph[MB];  // columns i and i + H of Phi, the whole phi
+#pragma unroll
+  for (int r = 0; r < MB; ++r) {
+    pa[r] = r == i ? 1.0 : 0.0;
+    pq[r] = r == i + H ? 1.0 : 0.0;
+    ph[r] = 0.0;
+  }
+  issue(0);
+  double fn0 = 0.0, fn1 = 0.0;  // f of the next block (one step ahead)
+  if (WITH_F && len > 0) {
+    fn0 = __ldg(g.f + b0 * MB + i);
+    fn1 = __ldg(g.f + b0 * MB + i + H);
+  }
+#pragma unroll 1
+  for (int tt = 0; tt < kChainC0; ++tt) {
+    issue(tt + 1);
+    cp_async_wait<1>();
+    __syncwarp();
+    const bool act = tt < len;
+    double R0[MB], S0[MB], R1[MB], S1[MB], f0 = fn0, f1 = fn1;
+    if (WITH_F) {
+      const bool nx = tt + 1 < len;
+      fn0 = nx ? __ldg(g.f + (b0 + tt + 1) * MB + i) : 0.0;
+      fn1 = nx ? __ldg(g.f + (b0 + tt + 1) * MB + i + H) : 0.0;
+    }
+    {
+      const double* row0 = stage + (tt & 1) * C::BLK + i * RW;
+      const double* row1 = row0 + H * RW;
+#pragma unroll
+      for (int q = 0; q < NP; ++q) {  // 16-byte piece q of row r sits at q ^ r
+        const double2 v = *reinterpret_cast<const double2*>(row0 + 2 * (q ^ i));
+        const double2 w = *reinterpret_cast<const double2*>(row1 + 2 * (q ^ (i + H)));
+        if (2 * q < MB) {
+          S0[2 * q] = v.x;
+          S0[2 * q + 1] = v.y;
+          S1[2 * q] = w.x;
+          S1[2 * q + 1] = w.y;
+        } else {
+          R0[2 * q - MB] = v.x;
+          R0[2 * q - MB + 1] = v.y;
+          R1[2 * q - MB] = w.x;
+          R1[2 * q - MB + 1] = w.y;
+        }
+      }
+    }
+    // Gauss-Jordan on [R | S | f]; the next pivot's reciprocal is started by
+    // every lane as soon as its column is updated
+    double dg0 = 1.0, dg1 = 1.0;
+    double rc = fast_rcp(R0[0]);
+#pragma unroll
+    for (int k = 0; k < MB; ++k) {
+      // pivot row k lives in lane k % H (slot k / H): its entries reach the
+      // other lanes of the subgroup by shuffles (one LSU wavefront each; the
+      // shared-memory broadcast cost ~4.5 wavefronts per sparse 16-byte store
+      // plus the read-back, and a divergent publish + __syncwarp per pivot)
+      const bool own = i == k % H;
+      double pr[MB], ps[MB];
+#pragma unroll
+      for (int c = k + 1; c < MB; ++c) pr[c] = gshfl<H>(k < H ? R0[c] : R1[c], k % H);
+#pragma unroll
+      for (int c = 0; c < MB; ++c) ps[c] = gshfl<H>(k < H ? S0[c] : S1[c], k % H);
+      double2 frp;
+      frp.x = WITH_F ? gshfl<H>(k < H ? f0 : f1, k % H) : 0.0;
+      frp.y = gshfl<H>(rc, k % H);
+      pr[k] = k < H ? R0[k] : R1[k];  // read by the pivot lane only (its own diagonal entry)
+      // branch-free: the pivot row itself takes a zero multiplier
+      const bool me0 = own && k < H, me1 = own && k >= H;
+      dg0 = me0 ? pr[k] : dg0;
+      dg1 = me1 ? pr[k] : dg1;
+      const double m0 = me0 ? 0.0 : R0[k] * frp.y;
+      const double m1 = me1 ? 0.0 : R1[k] * frp.y;
+#pragma unroll
+      for (int c = k + 1; c < MB; ++c) {
+        R0[c] = fma(-m0, pr[c], R0[c]);
+        R1[c] = fma(-m1, pr[c], R1[c]);
+      }
+      if (k + 1 < MB) rc = fast_rcp(k + 1 < H ? R0[k + 1] : R1[k + 1]);
+#pragma unroll
+      for (int c = 0; c < MB; ++c) {
+        S0[c] = fma(-m0, ps[c], S0[c]);
+        S1[c] = fma(-m1, ps[c], S1[c]);
+      }
+      if (WITH_F) {
+        f0 = fma(-m0, frp.x, f0);
+        f1 = fma(-m1, frp.x, f1);
+      }
+    }
+    const double rd0 = fast_rcp(dg0), rd1 = fast_rcp(dg1);
+#pragma unroll
+    for (int c = 0; c < MB; ++c) {  // S becomes T_b = -D^-1 S'
+      S0[c] = -S0[c] * rd0;
+      S1[c] = -S1[c] * rd1;
+    }
+    const double ci0 = f0 * rd0, ci1 = f1 * rd1;
+    // this block's phi components: phi_r <- T_b[r] . phi + c_r
+    double phi0 = ci0, phi1 = ci1;
+    if (WITH_F)
+#pragma unroll
+      for (int l = 0; l < MB; ++l) {
+        phi0 = fma(S0[l], ph[l], phi0);
+        phi1 = fma(S1[l], ph[l], phi1);
+      }
+    if (act) {
+      if (STORE_T) {
+        double2* dst = reinterpret_cast<double2*>(g.tm + (b0 + tt - 1) * MM) + i;
+#pragma unroll
+        for (int q = 0; q < MB / 2; ++q) {
+          dst[q * MB] = make_double2(S0[2 * q], S0[2 * q + 1]);
+          dst[q * MB + H] = make_double2(S1[2 * q], S1[2 * q + 1]);
+        }
+      }
+      if (WITH_F) {
+        g.cv[(b0 + tt) * MB + i] = ci0;
+        g.cv[(b0 + tt) * MB + i + H] = ci1;
+      }
+    }
+    // publish T_b (rows i, i + H) and phi, then fold the block into the chunk map
+#pragma unroll
+    for (int c = 0; c < MB; c += 2) {
+      *reinterpret_cast<double2*>(TB + i * C::TP + c) = make_double2(S0[c], S0[c + 1]);
+      *reinterpret_cast<double2*>(TB + (i + H) * C::TP + c) = make_double2(S1[c], S1[c + 1]);
+    }
+    if (WITH_F) {
+      TB[MB * C::TP + i] = phi0;
+      TB[MB * C::TP + i + H] = phi1;
+    }
+    __syncwarp();
+    if (act) {
+      double na[MB], nq[MB];
+#pragma unroll
+      for (int r = 0; r < MB; ++r) {
+        double a = 0.0, b = 0.0;
+#pragma unroll
+        for (int c = 0; c < MB; c += 2) {
+          const double2 m = *reinterpret_cast<const double2*>(TB + r * C::TP + c);
+          a = fma(m.y, pa[c + 1], fma(m.x, pa[c], a));
+          b = fma(m.y, pq[c + 1], fma(m.x, pq[c], b));
+        }
+        na[r] = a;
+        nq[r] = b;
+      }
+#pragma unroll
+      for (int r = 0; r < MB; ++r) {
+        pa[r] = na[r];
+        pq[r] = nq[r];
+      }
+      if (WITH_F)
+#pragma unroll
+        for (int r = 0; r < MB; r += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(TB + MB * C::TP + r);
+          ph[r] = v.x;
+          ph[r + 1] = v.y;
+        }
+    }
+    __syncwarp();  // TB is published again by the next block
+  }
+  cp_async_wait<0>();
+  if (live) {
+    if (STORE_T)
+#pragma unroll
+      for (int r = 0; r < MB; ++r) {
+        t.phi[0][j * MM + r * MB + i] = pa[r];
+        t.phi[0][j * MM + r * MB + i + H] = pq[r];
+      }
+    if (WITH_F) {
+      t.fl[1][(j + 1) * MB + i] = pick<MB>(ph, i);
+      t.fl[1][(j + 1) * MB + i + H] = pick<MB>(ph, i + H);
+      if (j == 0) {
+        t.fl[1][i] = __ldg(g.f + i);
+        t.fl[1][i + H] = __ldg(g.f + i + H);
+      }
+    }
+  }
+  // ---- level 1: the CTA's level-1 chunk by a shared-memory tree
+  const int T = t.T;
+  const int gsub = wid * C::SG + sg;  // subgroup index in the CTA
+  if (!live) {  // identity beyond the last chunk
+#pragma unroll
+    for (int r = 0; r < MB; ++r) {
+      pa[r] = r == i ? 1.0 : 0.0;
+      pq[r] = r == i + H ? 1.0 : 0.0;
+      ph[r] = 0.0;
+    }
+  }
+  __syncthreads();
+  fc2_tree16<MB, WITH_F>(fsm, gsub, i, pa, pq, ph);
+  if (T == 1) {  // the level-0 maps were the top (one CTA)
+    if (STORE_T && gsub == 0) chain_fc2_top<MB>(g, t, fsm, lane, pa, pq);
+    return;
+  }
+  {
+    const long c1 = (long)blockIdx.x * C::L1C + gsub / kChainC0;
+    if (gsub % kChainC0 == 0 && c1 * kChainC0 < P0) {
+      if (STORE_T)
+#pragma unroll
+        for (int r = 0; r < MB; ++r) {
+          t.phi[1][c1 * MM + r * MB + i] = pa[r];
+          t.phi[1][c1 * MM + r * MB + i + H] = pq[r];
+        }
+      if (WITH_F) {
+        t.fl[2][(c1 + 1) * MB + i] = pick<MB>(ph, i);
+        t.fl[2][(c1 + 1) * MB + i + H] = pick<MB>(ph, i + H);
+        if (c1 == 0) {
+          t.fl[2][i] = __ldg(g.f + i);
+          t.fl[2][i + H] = __ldg(g.f + i + H);
+        }
+      }
+    }
+  }
+  // ---- levels >= 2 and the top: the last arriving CTA composes (16 subgroups)
+  long cprev = (long)blockIdx.x;  // arrival unit at level 2: this CTA
+  for (int l = 2;; ++l) {
+    const bool top = l == T;
+    long cc;
+    int expected, len2;
+    if (top) {
+      cc = 0;
+      expected = T == 2 ? (int)gridDim.x : t.P[T - 1];
+      len2 = t.P[T - 1];
+    } else {
+      cc = l == 2 ? cprev * C::L1C / kChainC0 : cprev / kChainC0;
+      if (l == 2) {
+        const long first_cta = cc * kChainC0 / C::L1C;
+        const long last_cta = min((long)gridDim.x, (cc + 1) * kChainC0 / C::L1C);
+        expected = (int)(last_cta - first_cta);
+      } else {
+        expected = (int)min((long)kChainC0, (long)t.P[l - 1] - kChainC0 * cc);
+      }
+      len2 = (int)min((long)kChainC0, (long)t.P[l - 1] - kChainC0 * cc);
+    }
+    if (!cta_last_arrive(t.cnt + t.coff[l] + cc, expected)) return;
+    const double* maps = t.phi[l - 1] + cc * kChainC0 * MM;
+    const double* vecs = t.fl[l] + (cc * kChainC0 + 1) * MB;
+#pragma unroll
+    for (int r = 0; r < MB; ++r) {
+      const bool have = gsub < len2;
+      pa[r] = have ? __ldcg(maps + (long)gsub * MM + r * MB + i) : (r == i ? 1.0 : 0.0);
+      pq[r] = have ? __ldcg(maps + (long)gsub * MM + r * MB + i + H) : (r == i + H ? 1.0 : 0.0);
+      ph[r] = have && WITH_F ? __ldcg(vecs + (long)gsub * MB + r) : 0.0;
+    }
+    fc2_tree16<MB, WITH_F>(fsm, gsub, i, pa, pq, ph);
+    if (top) {
+      if (STORE_T && gsub == 0) chain_fc2_top<MB>(g, t, fsm, lane, pa, pq);
+      return;
+    }
+    if (gsub == 0) {
+      if (STORE_T)
+#pragma unroll
+        for (int r = 0; r < MB; ++r) {
+          t.phi[l][cc * MM + r * MB + i] = pa[r];
+          t.phi[l][cc * MM + r * MB + i + H] = pq[r];
+        }
+      if (WITH_F) {
+        t.fl[l + 1][(cc + 1) * MB + i] = pick<MB>(ph, i);
+        t.fl[l + 1][(cc + 1) * MB + i + H] = pick<MB>(ph, i + H);
+        if (cc == 0) {
+          t.fl[l + 1][i] = __ldg(g.f + i);
+          t.fl[l + 1][i + H] = __ldg(g.f + i + H);
+        }
+      }
+    }
+    cprev = cc;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // solve: three launches of chain_solve_kernel<MB, KM>, one CTA per level-1
 // chunk c (16 level-0 chunks, MB lanes each: lane i = row i of every block).
 //   KM 0 (condense)   level-0 chunks: phi_j = chain from zero with f; the CTA

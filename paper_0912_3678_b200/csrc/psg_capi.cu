@@ -1249,6 +1249,23 @@ struct ChainSolver {
 
   template <int M, bool STORE_T, bool WITH_F>
   void fc_launch(const double* f, cudaStream_t s) {
+    // m = 8: two rows per lane (half the shared-memory traffic per block;
+    // bit-identical results).  PSG_CHAIN_FC1 = 1 keeps the row-per-lane kernel.
+    static const bool fc1 = [] {
+      const char* e = getenv("PSG_CHAIN_FC1");
+      return e && atoi(e) > 0;
+    }();
+    if constexpr (M == 8) {
+      if (!fc1) {
+        constexpr int bytes2 = Fc2Cfg<M>::SMEM;
+        ensure_smem(reinterpret_cast<const void*>(chain_fc2_kernel<M, STORE_T, WITH_F>), bytes2);
+        const int ctas2 = (int)((P[0] + Fc2Cfg<M>::CPC - 1) / Fc2Cfg<M>::CPC);
+        chain_fc2_kernel<M, STORE_T, WITH_F><<<ctas2, Fc2Cfg<M>::NW * 32, bytes2, s>>>(args(f, nullptr, nullptr), tree());
+        LAUNCH_CHECK();
+        ++launches;
+        return;
+      }
+    }
     constexpr int bytes = FcCfg<M>::SMEM;
     ensure_smem(reinterpret_cast<const void*>(chain_fc_kernel<M, STORE_T, WITH_F>), bytes);
     const int ctas = (int)((P[0] + FcCfg<M>::CPC - 1) / FcCfg<M>::CPC);
