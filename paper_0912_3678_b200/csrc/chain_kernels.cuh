@@ -1228,8 +1228,23 @@ __global__ void __launch_bounds__(32) chain_down_kernel(ChainLevelArgs g, ChainT
   if (lane < MB && kChainC0 * w + len2 == t.P[1]) out[(long)t.P[1] * MB + i] = hi;
 }
 
+// -DPSG_PROF: %globaltimer stamps of every CTA's phases (tools/prof_cs.py)
+#ifdef PSG_PROF
+__device__ long long g_prof[2][1024][6];
+__device__ __forceinline__ long long gtime() {
+  long long v;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+  return v;
+}
+#define PSG_STAMP(k) \
+  if (threadIdx.x == 0 && blockIdx.x < 1024) g_prof[KM - 1][blockIdx.x][k] = gtime()
+#else
+#define PSG_STAMP(k)
+#endif
+
 template <int MB, int KM>
 __global__ void __launch_bounds__(16 * MB) chain_solve_kernel(ChainLevelArgs g, ChainTree t) {
+  PSG_STAMP(0);
   pdl_trigger();  // the next down sweep waits for this grid before reading anything it writes
   constexpr int NT = 16 * MB, MAPS = ChainReg<MB>::MAPS, MM = MB * MB;
   extern __shared__ __align__(16) double ssm[];
@@ -1257,6 +1272,7 @@ __global__ void __launch_bounds__(16 * MB) chain_solve_kernel(ChainLevelArgs g, 
     if (KM == 2)
       for (int e = tid; e < (len1 + 1) * MB; e += NT) s_x[e] = __ldg(t.x1 + kChainC0 * c * MB + e);
     __syncthreads();
+    PSG_STAMP(1);
     if (tid < 32) {  // this CTA's level-1 values from the down sweep's level-2 values
       pdl_wait();  // launched programmatically after the down sweep: its values from here on
       const double* xl = t.xlev[SEL];
@@ -1275,6 +1291,7 @@ __global__ void __launch_bounds__(16 * MB) chain_solve_kernel(ChainLevelArgs g, 
       }
     }
     __syncthreads();
+    PSG_STAMP(2);
     const int PT = t.P[T - 1];
     if constexpr (KM == 1) {
       ps.run(g, j, live, i, s_v[grp * MB + i], s_v[grp * MB + i], s_v[(grp + 1) * MB + i], s_v[(grp + 1) * MB + i],
@@ -1301,7 +1318,9 @@ __global__ void __launch_bounds__(16 * MB) chain_solve_kernel(ChainLevelArgs g, 
       }
       if (T < 2) return;
       __syncthreads();
+      PSG_STAMP(3);
       if (tid < 32) chain_up<MB>(t, t.cfl, reg1, c, len1, lane);
+      PSG_STAMP(4);
     } else {
       // x += the homogeneous chain of d; certificate
       const double d0 = s_v[grp * MB + i], d1 = s_v[(grp + 1) * MB + i];
@@ -1323,8 +1342,10 @@ __global__ void __launch_bounds__(16 * MB) chain_solve_kernel(ChainLevelArgs g, 
           den = od;
         }
       }
+      PSG_STAMP(3);
       if (!finite) num = __longlong_as_double(0x7ff0000000000000ll), den = 1.0;
       if (g.status) cert_push(g.status, num, den);
+      PSG_STAMP(4);
     }
   }
 }

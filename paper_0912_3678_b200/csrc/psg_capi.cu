@@ -3430,3 +3430,10 @@ int psg_residual(const psg_desc* A, const double* x, const double* f, int on_dev
 }
 
 }  // extern "C"
+
+#ifdef PSG_PROF
+// chain_solve_kernel phase stamps (a -DPSG_PROF build only; tools/prof_cs.py)
+extern "C" int psg_prof_dump(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, psg::g_prof, sizeof(long long) * 2 * 1024 * 6);
+}
+#endif
