@@ -142,3 +142,48 @@ def test_chain_hierarchy_depths(cuda, m, nb):
     F.refactor()
     x2 = psg.solve(F, _dev(cuda, f)).cpu().numpy()
     assert np.array_equal(x, x2)
+
+
+_FC_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+sys.path.insert(0, sys.argv[1] + "/tests")
+import paper_0912_3678_b200 as psg
+from test_chain_gpu import random_bvp, _gpu
+out = {}
+for nb in (9, 16, 17, 18, 33, 255, 256, 257, 258, 4099, 65537):
+    A, f = random_bvp(8, nb, 100 + nb)
+    x, st, F, GA = _gpu(torch, A, 2 if nb < 64 else 16, f)
+    assert st.speculative, nb  # the chain path, not the exact fallback
+    out[str(nb)] = x
+    F.close()
+np.savez(sys.argv[2], **out)
+"""
+
+
+def test_fc2_bit_identical_to_row_per_lane(cuda, tmp_path):
+    """chain_fc2_kernel (m = 8: two rows per lane, pivot rows by shuffles) keeps
+    chain_fc_kernel's arithmetic element by element: the same solutions bit for
+    bit as the row-per-lane kernel (PSG_CHAIN_FC1 = 1, read once per process,
+    hence the two subprocesses), over ragged chain lengths -- a partial first
+    chunk, 16 k + 1 / 16 k + 2 blocks, partial level-1 and level-2 chunks -- and every x within the usual bound of the oracle."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for tag, env in (("fc2", "0"), ("fc1", "1")):
+        path = str(tmp_path / f"{tag}.npz")
+        e = dict(os.environ, PSG_CHAIN_FC1=env)
+        r = subprocess.run([sys.executable, "-c", _FC_SCRIPT, root, path], env=e, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[tag] = np.load(path)
+    for k in res["fc2"].files:
+        a, b = res["fc2"][k], res["fc1"][k]
+        assert np.isfinite(a).all()
+        assert np.array_equal(a, b), f"nb={k}: max diff {np.abs(a - b).max():.3e}"
+    A, f = random_bvp(8, 257, 100 + 257)
+    want = O.solve_sequential(A, f)
+    assert O.rel_err(res["fc2"]["257"], want) <= 1e-12
