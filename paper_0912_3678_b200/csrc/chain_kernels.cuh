@@ -942,7 +942,21 @@ __global__ void __launch_bounds__(Fc2Cfg<MB>::NW * 32) chain_fc2_kernel(ChainLev
 // group is one contiguous run) and f, kPre steps ahead in a register ring inside a fully
 // unrolled kChainC0-step chain.
 // ---------------------------------------------------------------------------
-constexpr int kPre = 3;
+#ifndef PSG_CS_PRE1
+#define PSG_CS_PRE1 3
+#endif
+#ifndef PSG_CS_PRE2
+#define PSG_CS_PRE2 3
+#endif
+#ifndef PSG_CS_MINB1
+#define PSG_CS_MINB1 5
+#endif
+#ifndef PSG_CS_MINB2
+#define PSG_CS_MINB2 5
+#endif
+// ring depth / resident CTAs per SM asked for, per pass (MODE 0 condense, 1 final, 2 correction)
+constexpr int chain_pre(int mode) { return mode == 2 ? PSG_CS_PRE2 : PSG_CS_PRE1; }
+constexpr int chain_minb(int mode) { return mode == 2 ? PSG_CS_MINB2 : PSG_CS_MINB1; }
 
 template <int MB>
 struct ChainReg {  // staged maps (padded rows: conflict-free) + rhs slots of one <= 16-step chain
@@ -951,19 +965,41 @@ struct ChainReg {  // staged maps (padded rows: conflict-free) + rhs slots of on
   static constexpr int SIZE = MAPS + (kChainC0 + 1) * MB;
 };
 
-// maps[first + s] (s < len) and rhs[rfirst + s] (s < nr); cooperative over nthr threads
+// maps[first + s] (s < len) and rhs[rfirst + s] (s < nr); cooperative over nthr threads.
+// Every element goes global -> shared by an 8-byte cp.async (no register round
+// trip: all of a thread's copies are in flight at once; the plain load + store
+// loop waited for each batch of loads, and the long-scoreboard stalls were most of
+// the down sweep's life); the coherent rhs (values another CTA of this grid
+// wrote) keeps its ld.cg.  chain_stage_wait() before the barrier that
+// publishes the region.
+template <int MB>
+__device__ __forceinline__ void chain_stage_maps(double* reg, const double* maps, long first, int len, int tid,
+                                                 int nthr) {
+  constexpr int MM = MB * MB, MP = MB + 1;
+  const double* src = maps + first * MM;
+  for (int e = tid; e < len * MM; e += nthr) {
+    const int s = e / MM, r = e % MM;
+    cp_async8(reg + s * MB * MP + (r / MB) * MP + r % MB, src + e);
+  }
+}
+template <int MB, bool COHERENT_RHS>
+__device__ __forceinline__ void chain_stage_rhs(double* reg, const double* rhs, long rfirst, int nr, int tid,
+                                                int nthr) {
+  double* rr = reg + ChainReg<MB>::MAPS;
+  for (int e = tid; e < nr * MB; e += nthr) {
+    if (COHERENT_RHS)
+      rr[e] = __ldcg(rhs + rfirst * MB + e);
+    else
+      cp_async8(rr + e, rhs + rfirst * MB + e);
+  }
+}
 template <int MB, bool COHERENT_RHS>
 __device__ __forceinline__ void chain_stage(double* reg, const double* maps, long first, int len, const double* rhs,
                                             long rfirst, int nr, int tid, int nthr) {
-  constexpr int MM = MB * MB, MP = MB + 1;
-  for (int e = tid; e < len * MM; e += nthr) {
-    const int s = e / MM, r = e % MM;
-    reg[s * MB * MP + (r / MB) * MP + r % MB] = __ldg(maps + (first + s) * MM + r);
-  }
-  double* rr = reg + ChainReg<MB>::MAPS;
-  for (int e = tid; e < nr * MB; e += nthr)
-    rr[e] = COHERENT_RHS ? __ldcg(rhs + rfirst * MB + e) : __ldg(rhs + rfirst * MB + e);
+  chain_stage_maps<MB>(reg, maps, first, len, tid, nthr);
+  chain_stage_rhs<MB, COHERENT_RHS>(reg, rhs, rfirst, nr, tid, nthr);
 }
+__device__ __forceinline__ void chain_stage_wait() { cp_async_wait_all(); }
 
 // y <- map_s y + fi (row i)
 template <int MB>
@@ -992,6 +1028,7 @@ __device__ __forceinline__ double chain_condense(const double* reg, int len, int
 // serial prologue so the loads are in flight meanwhile).
 template <int MB, int MODE>
 struct Pass0 {
+  static constexpr int kPre = chain_pre(MODE);
   long b0 = 0;
   int len = 0;
   double Tq[kPre][MB], Cq[kPre], Xq[kPre];  // row i of T_b, c_b[i] (final) or x_b[i] (correction)
@@ -1025,6 +1062,7 @@ struct Pass0 {
                                         double ye, double yte, double& corr, double& num, double& den,
                                         bool& finite) {
     double y = ys, yt = yts;
+    double ytp = yts;  // MODE 2: the corrected x one block before the separator row
     if (MODE != 0 && live && j == 0) g.x[i] = yt;
 #pragma unroll
     for (int t = 0; t < kChainC0; ++t) {
@@ -1034,24 +1072,9 @@ struct Pass0 {
 #pragma unroll
       for (int l = 0; l < MB; ++l) a = fma(Tq[sl][l], gshfl<MB>(y, l), a);
       const double xold = MODE == 2 ? Xq[sl] : 0.0;
-      // correction: certificate of the corrected separator row r = f - S x_prev - R x_sep
-      double S[MB], R[MB];
-      const bool cert_here = MODE == 2 && act && last;
-      if (cert_here) load_row<MB>(g.data, b0 + t, i, S, R);
-      double sg = 0.0, ab = 0.0;
-      if (MODE == 2) {
-#pragma unroll
-        for (int l = 0; l < MB; ++l) {
-          const double pl = gshfl<MB>(yt, l);
-          if (cert_here) {
-            const double p1 = S[l] * pl;
-            sg += p1;
-            ab += fabs(p1);
-          }
-        }
-      }
       if (act) {
         const long os = (b0 + t) * MB + i;
+        if (MODE == 2) ytp = yt;
         if (!last) {
           y = a;
           yt = MODE == 2 ? xold + y : y;
@@ -1070,23 +1093,38 @@ struct Pass0 {
         }
       }
       if (t + kPre < kChainC0) fetch(g, i, t + kPre, sl);
-      if (MODE == 2) {
+    }
+    if (MODE == 2) {
+      // certificate of the corrected separator row (the chunk's last block row):
+      // r = f - S x_prev - R x_sep, S terms first, then R terms (every group runs the shuffles)
+      const bool cert_here = len > 0;
+      double S[MB], R[MB];
+      if (cert_here) load_row<MB>(g.data, b0 + len - 1, i, S, R);
+      double sg = 0.0, ab = 0.0;
 #pragma unroll
-        for (int l = 0; l < MB; ++l) {
-          const double xl = gshfl<MB>(yt, l);
-          if (cert_here) {
-            const double p2 = R[l] * xl;
-            sg += p2;
-            ab += fabs(p2);
-          }
-        }
+      for (int l = 0; l < MB; ++l) {
+        const double pl = gshfl<MB>(ytp, l);
         if (cert_here) {
-          const double fv = __ldg(g.f + (b0 + t) * MB + i);
-          const double on = fabs(fv - sg), od = fabs(fv) + ab;
-          if (on * den > num * od || (den == 0.0 && on > 0)) {
-            num = on;
-            den = od;
-          }
+          const double p1 = S[l] * pl;
+          sg += p1;
+          ab += fabs(p1);
+        }
+      }
+#pragma unroll
+      for (int l = 0; l < MB; ++l) {
+        const double xl = gshfl<MB>(yt, l);
+        if (cert_here) {
+          const double p2 = R[l] * xl;
+          sg += p2;
+          ab += fabs(p2);
+        }
+      }
+      if (cert_here) {
+        const double fv = __ldg(g.f + (b0 + len - 1) * MB + i);
+        const double on = fabs(fv - sg), od = fabs(fv) + ab;
+        if (on * den > num * od || (den == 0.0 && on > 0)) {
+          num = on;
+          den = od;
         }
       }
     }
@@ -1111,6 +1149,7 @@ __device__ void chain_up(const ChainTree& t, double* const* Fu, double* reg1, lo
     const int len = (int)min((long)kChainC0, t.P[l - 1] - kChainC0 * cc);
     if (!warp_last_arrive(t.cnt + t.coff[l] + cc, len, lane)) return;
     chain_stage<MB, true>(reg1, t.phi[l - 1], kChainC0 * cc, len, Fu[l], kChainC0 * cc, len + 1, lane, 32);
+    chain_stage_wait();
     __syncwarp();
     y = chain_condense<MB>(reg1, len, i);
     if (lane < MB) {
@@ -1179,20 +1218,31 @@ __global__ void __launch_bounds__(32) chain_down_kernel(ChainLevelArgs g, ChainT
   const int lane = threadIdx.x, i = lane % MB, T = t.T, PT = t.P[T - 1];
   const long w = blockIdx.x;
   double* const* F = sel ? t.cfl : t.fl;
-  // launched programmatically: wait for the producer of F (and of the maps),
-  // then let the next level-0 pass start its prologue (it waits on this grid
-  // before reading the values written here)
+  // launched programmatically: wait for the producer of F (and, sel 0, of the
+  // maps), then let the next level-0 pass start its prologue (it waits on this
+  // grid before reading the values written here).  The correction sweep
+  // (sel 1) follows the final pass: its maps and the top LU date from the
+  // factor launch, complete before the final pass started, so they are staged
+  // while the final pass drains.
+  // regions: top at ssm, level l (2 <= l < T) at ssm + (T - l) * REG
+  auto stage = [&](bool maps, bool rhs) {
+    if (maps) chain_stage_maps<MB>(ssm, t.phi[T - 1], 0, PT, lane, 32);
+    if (rhs) chain_stage_rhs<MB, false>(ssm, F[T], 0, PT + 1, lane, 32);
+    for (int l = 2; l < T; ++l) {
+      const long cc = w >> (4 * (l - 2));
+      const int len = (int)min((long)kChainC0, t.P[l - 1] - kChainC0 * cc);
+      double* reg = ssm + (T - l) * REG;
+      if (maps) chain_stage_maps<MB>(reg, t.phi[l - 1], kChainC0 * cc, len, lane, 32);
+      if (rhs) chain_stage_rhs<MB, false>(reg, F[l], kChainC0 * cc, len + 1, lane, 32);
+    }
+    if (maps)
+      for (int e = lane; e < MM + MB; e += 32) cp_async8(s_glu + e, t.glu + e);
+  };
+  if (sel) stage(true, false);
   pdl_wait();
   pdl_trigger();
-  // regions: top at ssm, level l (2 <= l < T) at ssm + (T - l) * REG
-  chain_stage<MB, false>(ssm, t.phi[T - 1], 0, PT, F[T], 0, PT + 1, lane, 32);
-  for (int l = 2; l < T; ++l) {
-    const long cc = w >> (4 * (l - 2));
-    const int len = (int)min((long)kChainC0, t.P[l - 1] - kChainC0 * cc);
-    chain_stage<MB, false>(ssm + (T - l) * REG, t.phi[l - 1], kChainC0 * cc, len, F[l], kChainC0 * cc, len + 1, lane,
-                           32);
-  }
-  for (int e = lane; e < MM + MB; e += 32) s_glu[e] = __ldg(t.glu + e);
+  stage(!sel, true);
+  chain_stage_wait();
   __syncwarp();
   chain_top_solve<MB>(g, t, ssm, s_glu, s_r, s_top, lane);
   double* out = t.xlev[sel];
@@ -1243,7 +1293,7 @@ __device__ __forceinline__ long long gtime() {
 #endif
 
 template <int MB, int KM>
-__global__ void __launch_bounds__(16 * MB) chain_solve_kernel(ChainLevelArgs g, ChainTree t) {
+__global__ void __launch_bounds__(16 * MB, chain_minb(KM)) chain_solve_kernel(ChainLevelArgs g, ChainTree t) {
   PSG_STAMP(0);
   pdl_trigger();  // the next down sweep waits for this grid before reading anything it writes
   constexpr int NT = 16 * MB, MAPS = ChainReg<MB>::MAPS, MM = MB * MB;
@@ -1271,6 +1321,7 @@ __global__ void __launch_bounds__(16 * MB) chain_solve_kernel(ChainLevelArgs g, 
     if (T >= 2) chain_stage<MB, false>(reg1, t.phi[0], kChainC0 * c, len1, Fd[1], kChainC0 * c, len1 + 1, tid, NT);
     if (KM == 2)
       for (int e = tid; e < (len1 + 1) * MB; e += NT) s_x[e] = __ldg(t.x1 + kChainC0 * c * MB + e);
+    chain_stage_wait();
     __syncthreads();
     PSG_STAMP(1);
     if (tid < 32) {  // this CTA's level-1 values from the down sweep's level-2 values
