@@ -1676,7 +1676,8 @@ __global__ void __launch_bounds__(64) blktri_spec_kernel(BlkSpecArgs g) {
 template <int K>
 __global__ void blk_cert_kernel(const double* __restrict__ Tdiag, const int* __restrict__ sep, int nsep,
                                 const double* __restrict__ f, const double* __restrict__ xsep,
-                                const double* __restrict__ rec, DevStatus* st) {
+                                const double* __restrict__ rec, DevStatus* st, DevStatus* host_out,
+                                unsigned* done_ctr) {
   pdl_wait();
   double worst = 0.0;
   for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < (long)nsep * K; t += (long)gridDim.x * blockDim.x) {
@@ -1702,6 +1703,7 @@ __global__ void blk_cert_kernel(const double* __restrict__ Tdiag, const int* __r
   }
   for (int o = 16; o > 0; o >>= 1) worst = fmax(worst, __shfl_xor_sync(0xffffffffu, worst, o));
   if ((threadIdx.x & 31) == 0 && worst > 0) status_cert(st, worst);
+  if (host_out) status_publish_last(st, host_out, done_ctr);  // pinned host slot: no copy in the stream
 }
 
 }  // namespace psg

@@ -42,6 +42,8 @@ struct ChainLevelArgs {
   double* tm;            // per block T_b = -R_b^-1 S_b (MB x MB, double2 (row i, columns 2q, 2q+1) at q MB + i)
   double* cv;            // condense output: per block c_b = R_b^-1 f_b (nb x MB, block 0 unused)
   DevStatus* status;
+  DevStatus* host_out;  // pinned host slot the correction pass publishes the status to (NULL: none)
+  unsigned* done_ctr;   // its arrival counter
 };
 
 template <int MB>
@@ -1240,6 +1242,9 @@ __global__ void __launch_bounds__(32) chain_down_kernel(ChainLevelArgs g, ChainT
   };
   if (sel) stage(true, false);
   pdl_wait();
+  // the correction sweep resets the status slot its successor (the correction
+  // pass, the only kernel of a solve that reports) accumulates into
+  if (sel && g.status && w == 0 && lane == 0) status_reset(g.status);
   pdl_trigger();
   stage(!sel, true);
   chain_stage_wait();
@@ -1396,6 +1401,7 @@ __global__ void __launch_bounds__(16 * MB, chain_minb(KM)) chain_solve_kernel(Ch
       PSG_STAMP(3);
       if (!finite) num = __longlong_as_double(0x7ff0000000000000ll), den = 1.0;
       if (g.status) cert_push(g.status, num, den);
+      if (g.status && g.host_out) status_publish_last(g.status, g.host_out, g.done_ctr);
       PSG_STAMP(4);
     }
   }

@@ -936,6 +936,7 @@ struct BlkSolver {
   DevBuf<GPart> part;
   DevBuf<int> sep;
   DevBuf<double> Tdiag, xsep, rec;
+  DevBuf<unsigned> cctr;  // certificate kernel: finished-block counter (last block publishes the status)
   int nseg = 0, nsep = 0, launches = 0;
 
   void init(const psg_desc& A, const Plan& P) {
@@ -1020,6 +1021,8 @@ struct BlkSolver {
     Tdiag.alloc((size_t)nsep * K * K);
     xsep.alloc((size_t)nsep * K);
     rec.alloc((size_t)nseg * 4 * K);
+    cctr.alloc(1);
+    CUDA_TRY(cudaMemset(cctr.p, 0, sizeof(unsigned)));
     base.n = A.n;
     base.s = A.s;
     base.r = A.r;
@@ -1067,7 +1070,8 @@ struct BlkSolver {
   void spec_factor(cudaStream_t) {}
 
   // fused factor + separators -> bodies -> certificate; the first kernel resets the status slot.
-  void spec_solve(const double* f, double* x, DevStatus* st, cudaStream_t s, cudaEvent_t* ev) {
+  void spec_solve(const double* f, double* x, DevStatus* st, cudaStream_t s, cudaEvent_t* ev,
+                  DevStatus* host_out = nullptr) {
     BlkSpecArgs g{};
     g.data = base.data;
     g.n = base.n;
@@ -1133,12 +1137,13 @@ struct BlkSolver {
     const int* sp = sep.p;
     const double* xs = xsep.p;
     const double* rc = rec.p;
+    unsigned* dc = cctr.p;
     if (K == 4)
-      launch_pdl(blk_cert_kernel<4>, dim3(cg), dim3(256), 0, s, Td, sp, nsep, f, xs, rc, st);
+      launch_pdl(blk_cert_kernel<4>, dim3(cg), dim3(256), 0, s, Td, sp, nsep, f, xs, rc, st, host_out, dc);
     else if (K == 3)
-      launch_pdl(blk_cert_kernel<3>, dim3(cg), dim3(256), 0, s, Td, sp, nsep, f, xs, rc, st);
+      launch_pdl(blk_cert_kernel<3>, dim3(cg), dim3(256), 0, s, Td, sp, nsep, f, xs, rc, st, host_out, dc);
     else
-      launch_pdl(blk_cert_kernel<2>, dim3(cg), dim3(256), 0, s, Td, sp, nsep, f, xs, rc, st);
+      launch_pdl(blk_cert_kernel<2>, dim3(cg), dim3(256), 0, s, Td, sp, nsep, f, xs, rc, st, host_out, dc);
     LAUNCH_CHECK();
     launches += 3;
   }
@@ -1158,6 +1163,8 @@ struct ChainSolver {
   bool factor_pending = false;  // lazy factor: fused into the next solve's condense pass
   std::vector<std::unique_ptr<DevBuf<double>>> phi, fl, cfl;
   DevBuf<int> cnt;
+  DevBuf<unsigned> cctr;          // arrival counter of the status publish (self-resetting)
+  DevStatus* host_out = nullptr;  // this solve's pinned host status slot
   int coff[kChainMaxLev + 1] = {};
   DevBuf<double> falign;
   int launches = 0;
@@ -1206,6 +1213,8 @@ struct ChainSolver {
     coff[T] = tot++;
     cnt.alloc(tot);
     CUDA_TRY(cudaMemset(cnt.p, 0, sizeof(int) * tot));
+    cctr.alloc(1);
+    CUDA_TRY(cudaMemset(cctr.p, 0, sizeof(unsigned)));
     possible = true;
   }
 
@@ -1224,6 +1233,8 @@ struct ChainSolver {
     g.tm = tm.p;
     g.cv = cv.p;
     g.status = st;
+    g.host_out = st ? host_out : nullptr;
+    g.done_ctr = cctr.p;
     return g;
   }
 
@@ -1307,7 +1318,7 @@ struct ChainSolver {
       CUDA_TRY(cudaEventRecord(ev[2], s));
     }
     solve_launch<M, 1>(args(f, x, nullptr), t, s);  // x through every block, separator residuals up
-    down_launch<M>(args(f, x, nullptr), t, 1, s);   // the correction down
+    down_launch<M>(args(f, x, st), t, 1, s);        // the correction down (resets the status slot)
     solve_launch<M, 2>(args(f, x, st), t, s);       // x += d, certificate
   }
 
@@ -1321,8 +1332,10 @@ struct ChainSolver {
     else fc_launch<2, true, false>(nullptr, s);
     factor_pending = false;
   }
-  // status slot must be reset by the caller
-  void solve(const double* f, double* x, DevStatus* st, cudaStream_t s, cudaEvent_t* ev) {
+  // the correction sweep resets the status slot, the correction pass publishes
+  // it to the pinned host slot hout (NULL: the caller copies it)
+  void solve(const double* f, double* x, DevStatus* st, cudaStream_t s, cudaEvent_t* ev, DevStatus* hout = nullptr) {
+    host_out = hout;
     if (reinterpret_cast<uintptr_t>(f) & 15) {  // the passes read f by 16-byte loads
       falign.alloc((size_t)(N + 1) * MB);
       CUDA_TRY(cudaMemcpyAsync(falign.p, f, sizeof(double) * (N + 1) * MB, cudaMemcpyDeviceToDevice, s));
@@ -2380,26 +2393,21 @@ void ensure_reduced_gen(psg_handle* h, cudaStream_t s) {
 // slot `st`, copied to host slot `hst` and marked by event `done`.
 int blk_enqueue(psg_handle* h, const double* df, double* dx, cudaStream_t s, DevStatus* st, DevStatus* hst,
                 cudaEvent_t done, cudaEvent_t* ev) {
+  // the status slot is reset by a kernel of the solve and published to the
+  // pinned host slot by its last one: no copy operation in the stream
   int launches;
   if (h->use_blk()) {
     h->blk.launches = 0;
     if (ev) CUDA_TRY(cudaEventRecord(ev[0], s));
-    h->blk.spec_solve(df, dx, st, s, ev);  // its first kernel resets the status slot
+    h->blk.spec_solve(df, dx, st, s, ev, hst);  // its first kernel resets the status slot
     launches = h->blk.launches;
   } else {
-    DevStatus init{};
-    for (int i = 0; i < kCertSlots; ++i) init.cert_bits[i] = 0ull;
-    init.bad_seg = INT_MAX;
-    init.pivot_seg = INT_MAX;
-    *hst = init;
-    CUDA_TRY(cudaMemcpyAsync(st, hst, sizeof(DevStatus), cudaMemcpyHostToDevice, s));
     h->chain.launches = 0;
     if (ev) CUDA_TRY(cudaEventRecord(ev[0], s));
-    h->chain.solve(df, dx, st, s, ev);
+    h->chain.solve(df, dx, st, s, ev, hst);
     launches = h->chain.launches;
   }
   if (ev) CUDA_TRY(cudaEventRecord(ev[3], s));
-  CUDA_TRY(cudaMemcpyAsync(hst, st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaEventRecord(done, s));
   return launches;
 }

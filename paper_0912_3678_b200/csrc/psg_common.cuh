@@ -2,6 +2,7 @@
 // kernels: row-array views of the reference storage, TMA bulk staging with
 // mbarriers (cp.async.bulk, sm_90+/sm_100a), status words.
 #pragma once
+#include <climits>
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -48,6 +49,34 @@ __device__ __forceinline__ void status_pivot(DevStatus* st, int seg) { atomicMin
 __device__ __forceinline__ void status_cert(DevStatus* st, double w) {
   if (!(w <= 1.0e300)) w = __longlong_as_double(0x7ff0000000000000ll);  // NaN/huge -> +inf
   atomicMax(&st->cert_bits[blockIdx.x % kCertSlots], (unsigned long long)__double_as_longlong(w));
+}
+
+__device__ __forceinline__ void status_reset(DevStatus* st) {
+  for (int k = 0; k < kCertSlots; ++k) st->cert_bits[k] = 0ull;
+  st->bad_seg = INT_MAX;
+  st->pivot_seg = INT_MAX;
+}
+
+// The last block of the grid to get here publishes the solve's status straight
+// into the caller's pinned host slot (no device-to-host copy in the stream);
+// every thread of every block calls it after its last status update, done_ctr
+// (zero before the launch) resets itself.
+__device__ __forceinline__ void status_publish_last(DevStatus* st, DevStatus* host_out, unsigned* done_ctr) {
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(done_ctr, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(st);
+  volatile unsigned long long* dst = reinterpret_cast<volatile unsigned long long*>(host_out);
+  for (int i = threadIdx.x; i < (int)(sizeof(DevStatus) / 8); i += blockDim.x)
+    dst[i] = atomicAdd(const_cast<unsigned long long*>(src + i), 0ull);  // coherent read of the atomically-updated words
+  if (threadIdx.x == 0) *done_ctr = 0u;
+  __threadfence_system();
 }
 
 // cp.async (LDGSTS) 8-byte copy global -> shared, no register staging.

@@ -595,24 +595,7 @@ __global__ void tri_cert_kernel(int nsep, const double4* __restrict__ crec, DevS
   if (j < nsep) w = tri_omega(crec[j], crec[j + 1]);
   for (int o = 16; o > 0; o >>= 1) w = fmax(w, __shfl_xor_sync(0xffffffffu, w, o));
   if ((threadIdx.x & 31) == 0 && w > 0.0) status_cert(st, w);
-  if (!host_out) return;
-  // the last block to finish publishes the solve's status straight into the
-  // caller's pinned host slot (no device-to-host copy in the stream)
-  __shared__ bool last;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    last = atomicAdd(done_ctr, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(st);
-  volatile unsigned long long* dst = reinterpret_cast<volatile unsigned long long*>(host_out);
-  for (int i = threadIdx.x; i < (int)(sizeof(DevStatus) / 8); i += blockDim.x) dst[i] = atomicAdd(
-      const_cast<unsigned long long*>(src + i), 0ull);  // coherent read of the atomically-updated words
-  if (threadIdx.x == 0) *done_ctr = 0u;
-  __threadfence_system();
+  if (host_out) status_publish_last(st, host_out, done_ctr);
 }
 
 }  // namespace psg
