@@ -945,18 +945,21 @@ __global__ void __launch_bounds__(Fc2Cfg<MB>::NW * 32) chain_fc2_kernel(ChainLev
 // unrolled kChainC0-step chain.
 // ---------------------------------------------------------------------------
 #ifndef PSG_CS_PRE1
-#define PSG_CS_PRE1 3
+#define PSG_CS_PRE1 2
 #endif
 #ifndef PSG_CS_PRE2
-#define PSG_CS_PRE2 3
+#define PSG_CS_PRE2 2
 #endif
 #ifndef PSG_CS_MINB1
-#define PSG_CS_MINB1 5
+#define PSG_CS_MINB1 7
 #endif
 #ifndef PSG_CS_MINB2
-#define PSG_CS_MINB2 5
+#define PSG_CS_MINB2 7
 #endif
-// ring depth / resident CTAs per SM asked for, per pass (MODE 0 condense, 1 final, 2 correction)
+// ring depth / resident CTAs per SM asked for, per pass (MODE 0 condense, 1 final, 2 correction).
+// 2 deep at 72 registers = 7 CTAs of 128 threads per SM: all 1024 CTAs of config 4
+// resident in one wave (3 deep at 96 registers = 5 per SM left a second wave of
+// 284 CTAs running at a fraction of the bandwidth).
 constexpr int chain_pre(int mode) { return mode == 2 ? PSG_CS_PRE2 : PSG_CS_PRE1; }
 constexpr int chain_minb(int mode) { return mode == 2 ? PSG_CS_MINB2 : PSG_CS_MINB1; }
 
@@ -979,6 +982,18 @@ __device__ __forceinline__ void chain_stage_maps(double* reg, const double* maps
                                                  int nthr) {
   constexpr int MM = MB * MB, MP = MB + 1;
   const double* src = maps + first * MM;
+  if (nthr % MM == 0 || MM % nthr == 0) {
+    // a thread's elements sit at fixed (row, column) positions: no per-element division
+    if (nthr >= MM) {  // nthr / MM maps per round, one element each
+      const int r = tid % MM, ds = nthr / MM;
+      double* dst = reg + (r / MB) * MP + r % MB;
+      for (int s = tid / MM; s < len; s += ds) cp_async8(dst + s * MB * MP, src + s * MM + r);
+    } else {           // MM / nthr elements of every map
+      for (int s = 0; s < len; ++s)
+        for (int r = tid; r < MM; r += nthr) cp_async8(reg + s * MB * MP + (r / MB) * MP + r % MB, src + s * MM + r);
+    }
+    return;
+  }
   for (int e = tid; e < len * MM; e += nthr) {
     const int s = e / MM, r = e % MM;
     cp_async8(reg + s * MB * MP + (r / MB) * MP + r % MB, src + e);
@@ -1166,36 +1181,44 @@ __device__ void chain_up(const ChainTree& t, double* const* Fu, double* reg1, lo
 // top level of a sweep: phi_total, x_0 from G x_0 = F_T[0] - Bb phi_total
 // (stored LU, pivots), the top chain; values into s_top (whole warp)
 template <int MB>
-__device__ void chain_top_solve(const ChainLevelArgs& g, const ChainTree& t, const double* regT, const double* s_glu,
-                                double* s_r, double* s_top, int lane) {
+__device__ void chain_top_solve(const ChainTree& t, const double (&bb)[MB], const double* regT,
+                                const double* s_glu, double* s_r, double* s_top, int lane) {
   constexpr int MM = MB * MB;
   const int i = lane % MB, PT = t.P[t.T - 1];
   const double* rT = regT + ChainReg<MB>::MAPS;
   double y = chain_condense<MB>(regT, PT, i);
   double r = rT[i];
 #pragma unroll
-  for (int l = 0; l < MB; ++l) r = fma(-__ldg(g.corner + i * MB + l), gshfl<MB>(y, l), r);
-  if (lane < MB) s_r[i] = r;
-  __syncwarp();
-  if (lane == 0) {
-    for (int k = 0; k < MB; ++k) {
-      const int p = (int)s_glu[MM + k];
-      if (p != k) {
-        const double tmp = s_r[k];
-        s_r[k] = s_r[p];
-        s_r[p] = tmp;
-      }
-    }
-    for (int k = 0; k < MB; ++k)
-      for (int rr = k + 1; rr < MB; ++rr) s_r[rr] = fma(-s_glu[rr * MB + k], s_r[k], s_r[rr]);
-    for (int k = MB - 1; k >= 0; --k) {
-      double sv = s_r[k];
-      for (int cc = k + 1; cc < MB; ++cc) sv = fma(-s_glu[k * MB + cc], s_r[cc], sv);
-      s_r[k] = sv / s_glu[k * MB + k];
-    }
+  for (int l = 0; l < MB; ++l) r = fma(-bb[l], gshfl<MB>(y, l), r);
+  // stored LU of G (row interchanges, unit lower, upper): lane i = row i, the
+  // right-hand side one component per lane, pivot values by shuffles (8
+  // dependent steps per sweep; one lane working through shared memory took
+  // ~2.5 us of each down sweep).  Forward sweep in the serial order; the
+  // backward sweep is column-oriented (row i accumulates from column MB-1 down).
+  double lu[MB];
+#pragma unroll
+  for (int l = 0; l < MB; ++l) lu[l] = s_glu[i * MB + l];
+  const double dg = pick<MB>(lu, i);
+#pragma unroll
+  for (int k = 0; k < MB; ++k) {
+    const int p = (int)s_glu[MM + k];
+    const double rk = gshfl<MB>(r, k), rp = gshfl<MB>(r, p);
+    r = i == k ? rp : (i == p ? rk : r);
   }
-  __syncwarp();
-  y = s_r[i];
+#pragma unroll
+  for (int k = 0; k < MB; ++k) {
+    const double rk = gshfl<MB>(r, k);
+    if (i > k) r = fma(-lu[k], rk, r);
+  }
+  y = r;
+#pragma unroll
+  for (int k = MB - 1; k >= 0; --k) {
+    const double q = r / dg;
+    const double xk = gshfl<MB>(q, k);
+    if (i == k) y = q;
+    if (i < k) r = fma(-lu[k], xk, r);
+  }
+  (void)s_r;
   if (lane < MB) s_top[i] = y;
   for (int s = 1; s <= PT; ++s) {
     y = chain_step<MB>(regT, s - 1, i, y, rT[s * MB + i]);
@@ -1240,16 +1263,24 @@ __global__ void __launch_bounds__(32) chain_down_kernel(ChainLevelArgs g, ChainT
     if (maps)
       for (int e = lane; e < MM + MB; e += 32) cp_async8(s_glu + e, t.glu + e);
   };
+  double bb[MB];  // row i of Bb (user input: loaded ahead of the dependency wait)
+#pragma unroll
+  for (int l = 0; l < MB; ++l) bb[l] = __ldg(g.corner + i * MB + l);
   if (sel) stage(true, false);
   pdl_wait();
   // the correction sweep resets the status slot its successor (the correction
   // pass, the only kernel of a solve that reports) accumulates into
   if (sel && g.status && w == 0 && lane == 0) status_reset(g.status);
-  pdl_trigger();
+  // No early trigger: the next level-0 pass launches when this grid has
+  // completed.  Letting its ~740 CTAs start their prologue (maps and ring
+  // prefetch, ~25 MB of requests at once) beside the sweep filled the SMs'
+  // load/store queues, and this latency-bound warp's shared loads and shuffles
+  // waited behind them: 13-17 us per sweep against ~6 us alone (%globaltimer
+  // stamps), config 4 0.261 -> 0.253 ms/step without the overlap.
   stage(!sel, true);
   chain_stage_wait();
   __syncwarp();
-  chain_top_solve<MB>(g, t, ssm, s_glu, s_r, s_top, lane);
+  chain_top_solve<MB>(t, bb, ssm, s_glu, s_r, s_top, lane);
   double* out = t.xlev[sel];
   if (w == 0 && lane < MB)
     for (int s = 0; s <= PT; ++s) t.xtop[sel][s * MB + i] = s_top[s * MB + i];

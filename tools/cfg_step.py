@@ -26,6 +26,19 @@ for _ in range(3):
     F.solve_async(f, x)
     F.sync()
 torch.cuda.synchronize()
+if os.environ.get("ALONE"):  # bench.py's small-config mode: L2 flushed, each step's device time alone
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=f.device)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for a, b in evs:
+        flush.random_(0, 255)
+        a.record()
+        F.refactor(A)
+        F.solve_async(f, x)
+        b.record()
+        F.sync()
+    torch.cuda.synchronize()
+    print(json.dumps({"cfg": cfg, "alone_ms": round(sum(a.elapsed_time(b) for a, b in evs) / steps, 4)}))
+    sys.exit(0)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 st = psg.SolveStats()
 e0.record()
