@@ -585,7 +585,13 @@ __device__ __forceinline__ void fc2_tree16(double* fsm, int gsub, int i, double 
   }
 }
 
-// chain_fc_top for the two-columns-per-lane layout (lanes 0..MB/2-1 of warp 0)
+// chain_fc_top for the two-columns-per-lane layout: the whole of warp 0 calls
+// it (pa / pb valid in lanes 0..MB/2-1).  G = Ba + Bb Phi_total is built in
+// shared memory, then factored with lane i = row i (lanes >= MB replicate row
+// lane % MB): every lane sees the pivot column by shuffles and runs the same
+// first-maximum scan, the two rows change lanes by shuffles, the update is the
+// serial algorithm's element by element (bit-identical LU; one lane working
+// through shared memory took 9.3 us at the end of the factor launch).
 template <int MB>
 __device__ void chain_fc2_top(const ChainLevelArgs& g, const ChainTree& t, double* buf, int lane, const double (&pa)[MB],
                               const double (&pb)[MB]) {
@@ -605,27 +611,42 @@ __device__ void chain_fc2_top(const ChainLevelArgs& g, const ChainTree& t, doubl
     }
   }
   __syncwarp();
-  if (lane == 0) {
-    double* G = buf;
-    for (int k = 0; k < MB; ++k) {
-      int p = k;
-      for (int r = k + 1; r < MB; ++r)
-        if (fabs(G[r * GP + k]) > fabs(G[p * GP + k])) p = r;
-      if (p != k)
-        for (int c = 0; c < MB; ++c) {
-          const double tmp = G[k * GP + c];
-          G[k * GP + c] = G[p * GP + c];
-          G[p * GP + c] = tmp;
-        }
-      t.glu[MM + k] = (double)p;
-      for (int r = k + 1; r < MB; ++r) {
-        const double l = G[r * GP + k] / G[k * GP + k];
-        G[r * GP + k] = l;
-        for (int c = k + 1; c < MB; ++c) G[r * GP + c] = fma(-l, G[k * GP + c], G[r * GP + c]);
+  const int i = lane % MB;
+  double gr[MB];
+#pragma unroll
+  for (int c = 0; c < MB; ++c) gr[c] = buf[i * GP + c];
+#pragma unroll
+  for (int k = 0; k < MB; ++k) {
+    // partial pivoting: the first row >= k with the largest |G[r][k]|
+    const double mine = fabs(gr[k]);
+    int p = k;
+    double best = gshfl<MB>(mine, k);
+#pragma unroll
+    for (int r = k + 1; r < MB; ++r) {
+      const double v = gshfl<MB>(mine, r);
+      if (v > best) {
+        best = v;
+        p = r;
       }
     }
-    for (int e = 0; e < MM; ++e) t.glu[e] = G[(e / MB) * GP + e % MB];
+    double pr[MB];
+#pragma unroll
+    for (int c = 0; c < MB; ++c) {
+      const double rk = gshfl<MB>(gr[c], k), rp = gshfl<MB>(gr[c], p);
+      pr[c] = rp;  // the pivot row after the interchange
+      gr[c] = i == k ? rp : (i == p ? rk : gr[c]);
+    }
+    if (lane == 0) t.glu[MM + k] = (double)p;
+    if (i > k) {
+      const double l = gr[k] / pr[k];
+      gr[k] = l;
+#pragma unroll
+      for (int c = k + 1; c < MB; ++c) gr[c] = fma(-l, pr[c], gr[c]);
+    }
   }
+  if (lane < MB)
+#pragma unroll
+    for (int c = 0; c < MB; ++c) t.glu[i * MB + c] = gr[c];
   __syncwarp();
 }
 
@@ -847,7 +868,7 @@ __global__ void __launch_bounds__(Fc2Cfg<MB>::NW * 32) chain_fc2_kernel(ChainLev
   __syncthreads();
   fc2_tree16<MB, WITH_F>(fsm, gsub, i, pa, pq, ph);
   if (T == 1) {  // the level-0 maps were the top (one CTA)
-    if (STORE_T && gsub == 0) chain_fc2_top<MB>(g, t, fsm, lane, pa, pq);
+    if (STORE_T && threadIdx.x < 32) chain_fc2_top<MB>(g, t, fsm, lane, pa, pq);
     return;
   }
   {
@@ -902,7 +923,7 @@ __global__ void __launch_bounds__(Fc2Cfg<MB>::NW * 32) chain_fc2_kernel(ChainLev
     }
     fc2_tree16<MB, WITH_F>(fsm, gsub, i, pa, pq, ph);
     if (top) {
-      if (STORE_T && gsub == 0) chain_fc2_top<MB>(g, t, fsm, lane, pa, pq);
+      if (STORE_T && threadIdx.x < 32) chain_fc2_top<MB>(g, t, fsm, lane, pa, pq);
       return;
     }
     if (gsub == 0) {
