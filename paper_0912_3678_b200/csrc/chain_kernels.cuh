@@ -32,6 +32,25 @@
 
 namespace psg {
 
+// -DPSG_PROF: %globaltimer stamps per kernel of a solve (tools/tl_probe.py):
+// g_tl[id][k], id 0 factor, 1 / 3 down sweeps, 2 / 4 level-0 passes, 6 / 7
+// inside the sweeps, 9.. the factor's upper levels, 12 its top LU.
+#ifdef PSG_PROF
+__device__ unsigned long long g_tl[16][4];
+__device__ __forceinline__ unsigned long long tl_now() {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+  return v;
+}
+#define TL_MAX(id, k) \
+  if (threadIdx.x == 0) atomicMax(&g_tl[id][k], tl_now())
+#define TL_MIN(id, k) \
+  if (threadIdx.x == 0) atomicMin(&g_tl[id][k], tl_now())
+#else
+#define TL_MAX(id, k)
+#define TL_MIN(id, k)
+#endif
+
 // level 0: data = [Ba (MB*MB) | rows b = 1..nb-1: S_b | R_b (MB x 2MB, row-major)]
 struct ChainLevelArgs {
   const double* data;
@@ -611,6 +630,7 @@ __device__ void chain_fc2_top(const ChainLevelArgs& g, const ChainTree& t, doubl
     }
   }
   __syncwarp();
+  TL_MAX(12, 0);
   const int i = lane % MB;
   double gr[MB];
 #pragma unroll
@@ -644,6 +664,7 @@ __device__ void chain_fc2_top(const ChainLevelArgs& g, const ChainTree& t, doubl
       for (int c = k + 1; c < MB; ++c) gr[c] = fma(-l, pr[c], gr[c]);
     }
   }
+  TL_MAX(12, 1);
   if (lane < MB)
 #pragma unroll
     for (int c = 0; c < MB; ++c) t.glu[i * MB + c] = gr[c];
@@ -652,6 +673,7 @@ __device__ void chain_fc2_top(const ChainLevelArgs& g, const ChainTree& t, doubl
 
 template <int MB, bool STORE_T, bool WITH_F>
 __global__ void __launch_bounds__(Fc2Cfg<MB>::NW * 32) chain_fc2_kernel(ChainLevelArgs g, ChainTree t) {
+  TL_MIN(0, 0);
   pdl_trigger();  // the down sweep may launch (it waits for this grid before reading anything)
   using C = Fc2Cfg<MB>;
   constexpr int MM = MB * MB, RW = 2 * MB, H = C::LPB, NP = RW / 2;  // NP 16-byte pieces per row
@@ -890,6 +912,7 @@ __global__ void __launch_bounds__(Fc2Cfg<MB>::NW * 32) chain_fc2_kernel(ChainLev
       }
     }
   }
+  TL_MAX(8, 0);
   // ---- levels >= 2 and the top: the last arriving CTA composes (16 subgroups)
   long cprev = (long)blockIdx.x;  // arrival unit at level 2: this CTA
   for (int l = 2;; ++l) {
@@ -912,6 +935,7 @@ __global__ void __launch_bounds__(Fc2Cfg<MB>::NW * 32) chain_fc2_kernel(ChainLev
       len2 = (int)min((long)kChainC0, (long)t.P[l - 1] - kChainC0 * cc);
     }
     if (!cta_last_arrive(t.cnt + t.coff[l] + cc, expected)) return;
+    TL_MAX(7 + l, 1);
     const double* maps = t.phi[l - 1] + cc * kChainC0 * MM;
     const double* vecs = t.fl[l] + (cc * kChainC0 + 1) * MB;
 #pragma unroll
@@ -922,8 +946,10 @@ __global__ void __launch_bounds__(Fc2Cfg<MB>::NW * 32) chain_fc2_kernel(ChainLev
       ph[r] = have && WITH_F ? __ldcg(vecs + (long)gsub * MB + r) : 0.0;
     }
     fc2_tree16<MB, WITH_F>(fsm, gsub, i, pa, pq, ph);
+    TL_MAX(7 + l, 3);
     if (top) {
       if (STORE_T && threadIdx.x < 32) chain_fc2_top<MB>(g, t, fsm, lane, pa, pq);
+      TL_MAX(0, 1);
       return;
     }
     if (gsub == 0) {
@@ -1289,6 +1315,7 @@ __global__ void __launch_bounds__(32) chain_down_kernel(ChainLevelArgs g, ChainT
   for (int l = 0; l < MB; ++l) bb[l] = __ldg(g.corner + i * MB + l);
   if (sel) stage(true, false);
   pdl_wait();
+  TL_MIN(1 + 2 * sel, 0);
   // the correction sweep resets the status slot its successor (the correction
   // pass, the only kernel of a solve that reports) accumulates into
   if (sel && g.status && w == 0 && lane == 0) status_reset(g.status);
@@ -1301,7 +1328,9 @@ __global__ void __launch_bounds__(32) chain_down_kernel(ChainLevelArgs g, ChainT
   stage(!sel, true);
   chain_stage_wait();
   __syncwarp();
+  TL_MAX(6 + sel, 0);
   chain_top_solve<MB>(t, bb, ssm, s_glu, s_r, s_top, lane);
+  TL_MAX(6 + sel, 1);
   double* out = t.xlev[sel];
   if (w == 0 && lane < MB)
     for (int s = 0; s <= PT; ++s) t.xtop[sel][s * MB + i] = s_top[s * MB + i];
@@ -1322,6 +1351,7 @@ __global__ void __launch_bounds__(32) chain_down_kernel(ChainLevelArgs g, ChainT
     hi = t0 + 1 == len ? hi : chain_step<MB>(R, t0, i, yy, Rr[(t0 + 1) * MB + i]);
     lo = yy;
   }
+  TL_MAX(6 + sel, 2);
   // level-2 chunk w
   const double* R = ssm + (T - 2) * REG;
   const double* Rr = R + MAPS;
@@ -1333,6 +1363,7 @@ __global__ void __launch_bounds__(32) chain_down_kernel(ChainLevelArgs g, ChainT
     if (lane < MB) out[(kChainC0 * w + s) * MB + i] = yy;
   }
   if (lane < MB && kChainC0 * w + len2 == t.P[1]) out[(long)t.P[1] * MB + i] = hi;
+  TL_MAX(1 + 2 * sel, 1);
 }
 
 // -DPSG_PROF: %globaltimer stamps of every CTA's phases (tools/prof_cs.py)
@@ -1352,6 +1383,7 @@ __device__ __forceinline__ long long gtime() {
 template <int MB, int KM>
 __global__ void __launch_bounds__(16 * MB, chain_minb(KM)) chain_solve_kernel(ChainLevelArgs g, ChainTree t) {
   PSG_STAMP(0);
+  TL_MIN(2 * KM, 0);
   pdl_trigger();  // the next down sweep waits for this grid before reading anything it writes
   constexpr int NT = 16 * MB, MAPS = ChainReg<MB>::MAPS, MM = MB * MB;
   extern __shared__ __align__(16) double ssm[];
@@ -1383,6 +1415,7 @@ __global__ void __launch_bounds__(16 * MB, chain_minb(KM)) chain_solve_kernel(Ch
     PSG_STAMP(1);
     if (tid < 32) {  // this CTA's level-1 values from the down sweep's level-2 values
       pdl_wait();  // launched programmatically after the down sweep: its values from here on
+      TL_MIN(2 * KM, 2);
       const double* xl = t.xlev[SEL];
       if (T == 1) {
         if (lane < MB)
@@ -1429,6 +1462,7 @@ __global__ void __launch_bounds__(16 * MB, chain_minb(KM)) chain_solve_kernel(Ch
       PSG_STAMP(3);
       if (tid < 32) chain_up<MB>(t, t.cfl, reg1, c, len1, lane);
       PSG_STAMP(4);
+      TL_MAX(2 * KM, 1);
     } else {
       // x += the homogeneous chain of d; certificate
       const double d0 = s_v[grp * MB + i], d1 = s_v[(grp + 1) * MB + i];
@@ -1455,6 +1489,7 @@ __global__ void __launch_bounds__(16 * MB, chain_minb(KM)) chain_solve_kernel(Ch
       if (g.status) cert_push(g.status, num, den);
       if (g.status && g.host_out) status_publish_last(g.status, g.host_out, g.done_ctr);
       PSG_STAMP(4);
+      TL_MAX(2 * KM, 1);
     }
   }
 }

@@ -3444,4 +3444,20 @@ int psg_residual(const psg_desc* A, const double* x, const double* f, int on_dev
 extern "C" int psg_prof_dump(long long* out) {
   return (int)cudaMemcpyFromSymbol(out, psg::g_prof, sizeof(long long) * 2 * 1024 * 6);
 }
+// per-kernel timeline stamps (tools/tl_probe.py): out = 16 x 4 words; reset re-arms the minima / maxima
+extern "C" int psg_tl_dump(unsigned long long* out, int reset) {
+  const int rc = (int)cudaMemcpyFromSymbol(out, psg::g_tl, sizeof(unsigned long long) * 64);
+  if (reset) {
+    unsigned long long init[64];
+    for (int k = 0; k < 16; ++k) {
+      init[4 * k] = ~0ull;  // TL_MIN slots: [id][0] and, for the passes, [id][2]
+      init[4 * k + 1] = 0;
+      init[4 * k + 2] = (k == 2 || k == 4) ? ~0ull : 0;
+      init[4 * k + 3] = 0;
+    }
+    for (int k = 6; k < 16; ++k) init[4 * k] = 0;  // TL_MAX only
+    cudaMemcpyToSymbol(psg::g_tl, init, sizeof(init));
+  }
+  return rc;
+}
 #endif
